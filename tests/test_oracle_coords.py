@@ -1,0 +1,118 @@
+"""Pins for the oracle's coordinate functions (O1-O3) against the paper, SPEC worked
+examples, brute force and invariants.  No GPU."""
+import numpy as np
+import pytest
+
+from conftest import golden_lines
+
+
+def test_quantize_worked_examples(orc):
+    # tests/golden/quantize_example.txt: S:77 and reading R6.
+    for line in golden_lines("quantize_example.txt"):
+        lhs, rhs = line.split("->")
+        v, *p = [float(x) for x in lhs.split()]
+        want = [int(x) for x in rhs.split()]
+        coords, p2r, first = orc.quantize(np.array([p], np.float32), v)
+        assert coords.tolist() == [want + [0]]
+        assert p2r.tolist() == [0] and first.tolist() == [0]
+
+
+def _brute_voxels(points, voxel, batch):
+    """Independent dedup: Python dict keyed by the tuple of floors, first occurrence wins."""
+    q = np.floor(points.astype(np.float32) / np.float32(voxel)).astype(np.int64)
+    rows, first, p2r = {}, [], []
+    for p in range(points.shape[0]):
+        key = tuple(q[p].tolist()) + (int(batch[p]),)
+        if key not in rows:
+            rows[key] = len(rows)
+            first.append(p)
+        p2r.append(rows[key])
+    coords = np.array(list(rows.keys()), np.int64).reshape(-1, points.shape[1] + 1)
+    return coords, np.array(p2r), np.array(first)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_quantize_matches_brute_force(orc, seed):
+    # voxel count equals the brute-force set of floors; R8/R9 first-occurrence order.
+    g = np.random.default_rng(seed)
+    pts = g.uniform(-1.0, 1.0, (3000, 3)).astype(np.float32)
+    batch = g.integers(0, 3, 3000).astype(np.int32)
+    coords, p2r, first = orc.quantize(pts, 0.1, batch)
+    bc, bp, bf = _brute_voxels(pts, 0.1, batch)
+    assert np.array_equal(coords, bc)
+    assert np.array_equal(p2r, bp)
+    assert np.array_equal(first, bf)
+    # invariants: first point maps to its row; first_point is increasing (first occurrence)
+    assert np.array_equal(p2r[first], np.arange(coords.shape[0]))
+    assert np.all(np.diff(first) > 0)
+
+
+def test_quantize_batch_isolation(orc):
+    # Eq. 1: identical spatial coordinates in different batches stay distinct.
+    pts = np.array([[0.05, 0.05, 0.05]] * 4, np.float32)
+    coords, p2r, _ = orc.quantize(pts, 0.1, np.array([0, 1, 0, 1], np.int32))
+    assert coords.tolist() == [[0, 0, 0, 0], [0, 0, 0, 1]]
+    assert p2r.tolist() == [0, 1, 0, 1]
+
+
+def test_quantize_errors_and_empty(orc):
+    pts = np.array([[0.0, 0.0], [np.nan, 0.0], [np.inf, 1.0]], np.float32)
+    with pytest.raises(orc.OracleError) as e:
+        orc.quantize(pts, 0.1)
+    assert e.value.status == orc.NONFINITE_INPUT and e.value.row == 1
+    with pytest.raises(orc.OracleError) as e:
+        orc.quantize(np.array([[0.0], [3e9]], np.float32), 1.0)
+    assert e.value.status == orc.COORD_RANGE and e.value.row == 1
+    coords, p2r, first = orc.quantize(np.zeros((0, 3), np.float32), 0.1)
+    assert coords.shape == (0, 4) and p2r.shape == (0,)
+
+
+def test_create_identity_and_inverse(orc):
+    g = np.random.default_rng(5)
+    c = np.unique(g.integers(-50, 50, (500, 3)), axis=0)
+    c = g.permutation(c)
+    rows = np.concatenate([c, np.zeros((c.shape[0], 1), int)], axis=1).astype(np.int32)
+    out, inv = orc.create(rows)
+    assert np.array_equal(out, rows)  # already-unique input keeps its order
+    assert np.array_equal(inv, np.arange(rows.shape[0]))
+    dup = np.concatenate([rows, rows[::-1]])
+    out2, inv2 = orc.create(dup)
+    assert np.array_equal(out2, rows)
+    assert np.array_equal(out2[inv2], dup)
+
+
+def test_create_stride_check(orc):
+    rows = np.array([[0, 2, 0], [2, 3, 0]], np.int32)
+    with pytest.raises(orc.OracleError) as e:
+        orc.create(rows, tensor_stride=[2, 2])
+    assert e.value.status == orc.STRIDE and e.value.row == 1
+    out, _ = orc.create(np.array([[0, 2, 0], [-2, 4, 0]], np.int32), tensor_stride=[2, 2])
+    assert out.shape == (2, 3)
+
+
+def test_stride_worked_examples(orc):
+    # tests/golden/stride_example.txt: S:87-88.
+    for line in golden_lines("stride_example.txt"):
+        lhs, rhs = line.split("->")
+        cin, ts, cs = [x.strip() for x in lhs.split("|")]
+        c = np.array([[int(x), 0] for x in cin.split(",")], np.int32)
+        out = orc.stride(c, [int(cs)], [int(ts)])
+        assert out[:, 0].tolist() == [int(x) for x in rhs.split(",")]
+
+
+@pytest.mark.parametrize("sigma,ts", [(2, 1), (3, 2), (4, 4)])
+def test_stride_brute_force(orc, sigma, ts):
+    g = np.random.default_rng(sigma)
+    c = g.integers(-40, 40, (800, 3)) * ts
+    rows = np.concatenate([c, g.integers(0, 2, (800, 1))], axis=1).astype(np.int32)
+    rows, _ = orc.create(rows, tensor_stride=[ts] * 3)
+    out = orc.stride(rows, [sigma] * 3, [ts] * 3)
+    s = ts * sigma
+    seen, want = set(), []
+    for r in rows.tolist():  # Python // is floor division: a separate implementation
+        k = tuple(x // s * s for x in r[:3]) + (r[3],)
+        if k not in seen:
+            seen.add(k)
+            want.append(k)
+    assert out.tolist() == [list(k) for k in want]
+    assert out.shape[0] <= rows.shape[0]
