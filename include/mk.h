@@ -1,0 +1,210 @@
+/*
+ * mk.h — C ABI of the B200-native generalized sparse convolution library (libmk.so).
+ *
+ * Implements the data-parallel hot path of Choy, Gwak, Savarese, "4D Spatio-Temporal
+ * ConvNets: Minkowski Convolutional Neural Networks" (arXiv 1904.08755).  Citations:
+ * "P:n" = line n of the paper's text, "S:n" = line n of SPEC.md, "Rk" = the
+ * reading k of an ambiguous passage, listed in DESIGN.md §3.
+ *
+ * Conventions shared by every call
+ *  - Plain C types only.  Device pointers are prefixed d_, host pointers h_.  A stream is
+ *    a cudaStream_t passed as void* (NULL = legacy default stream).  All device work is
+ *    enqueued on that stream; the caller owns ordering with other streams.
+ *  - Coordinates are int32 rows [n][D+1]: D spatial components, then the batch index
+ *    (Eq. 1).  D is 1..4 on this implementation.  Batch indices are >= 0.
+ *  - Features are row-major [n][C] (row i = f_i^T, Eq. 1).  Weights are [K][C_out][C_in]
+ *    row-major: the K matrices W_i of size N_out x N_in (R17).
+ *  - Handles (mk_coords, mk_kmap) are immutable once created ("build then freeze",
+ *    S:113/S:173): any number of streams may read them concurrently.  They own their
+ *    device memory and release it (stream-ordered, on the stream they were created on)
+ *    in *_destroy.  Feature/weight/gradient buffers are caller-owned; outputs are
+ *    overwritten, never accumulated into.
+ *  - Calls that must report a size (coords_*, kmap_build) synchronize their stream once.
+ *    Every other call is asynchronous.
+ *  - Every call returns mk_status.  On failure mk_last_error_message() (thread-local)
+ *    describes it and mk_last_error_row() gives the first offending input row, or -1.
+ *    No C++ exception crosses this boundary.  On failure no handle is returned and
+ *    caller buffers may have been partially written.
+ */
+#ifndef MK_H
+#define MK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MK_MAX_DIM 4        /* spatial dimensions supported on the GPU path (D <= 4) */
+#define MK_MAX_REGION 8     /* entries of mk_region.size / .dilation */
+
+typedef enum {
+  MK_OK = 0,
+  MK_ERR_INVALID_ARGUMENT = 1,   /* null pointer, bad size, negative batch index, ...  */
+  MK_ERR_DIMENSION_MISMATCH = 2, /* coordinate sets / regions of different D    */
+  MK_ERR_SHAPE_MISMATCH = 3,     /* channel counts inconsistent with the map    */
+  MK_ERR_NONFINITE_INPUT = 4,    /* NaN / Inf point coordinate                   */
+  MK_ERR_COORD_RANGE = 5,        /* coordinate outside the representable domain (R19)   */
+  MK_ERR_STRIDE = 6,             /* coordinate not a multiple of the tensor stride*/
+  MK_ERR_UNSUPPORTED = 7,        /* D > 4, channel count not a multiple of 8, ...       */
+  MK_ERR_OUT_OF_MEMORY = 8,
+  MK_ERR_CUDA = 9                /* a CUDA runtime error; message carries its text      */
+} mk_status;
+
+typedef enum { MK_F32 = 0, MK_BF16 = 1 } mk_dtype;
+
+/* Kernel shapes N^D (P:154 hypercube V^D(K); Fig. 3 P:250-282 cross / hypercross / hybrid). */
+typedef enum { MK_HYPERCUBE = 0, MK_HYPERCROSS = 1, MK_HYBRID = 2, MK_CUSTOM = 3 } mk_region_type;
+
+/* A kernel region.  Per-axis index range R(K) = {-(K-1)/2 .. (K-1)/2} for odd K
+ * (V^1(3) = {-1,0,1}) and {0 .. K-1} for even K (R3); each component is scaled by
+ * dilation[d] ("dilated convolution").  Built-in shapes are enumerated in
+ * lexicographic order, axis 0 most significant (R2):
+ *   HYPERCUBE  = prod_d R(size[d])
+ *   HYPERCROSS = {0} U { i e_d : i in R(size[d]) \ {0} }
+ *   HYBRID     = (cube over the spatial axes at temporal offset 0) U
+ *                { i e_t : i in R(size[t]) \ {0} },  t = temporal_axis (R4)
+ *   CUSTOM     = offsets[n_offsets][D] (host), distinct, caller's order, taken literally.
+ * dilation entries of 0 are read as 1; temporal_axis < 0 means D-1. */
+typedef struct {
+  int32_t type;                    /* mk_region_type */
+  int32_t D;
+  int32_t size[MK_MAX_REGION];
+  int32_t dilation[MK_MAX_REGION];
+  int32_t temporal_axis;
+  const int32_t* offsets;          /* CUSTOM only: host [n_offsets][D] */
+  int32_t n_offsets;
+} mk_region;
+
+typedef struct mk_context mk_context;
+typedef struct mk_coords mk_coords;
+typedef struct mk_kmap mk_kmap;
+
+/* Optional device allocator (e.g. a framework caching allocator).  NULL callbacks select
+ * cudaMallocAsync / cudaFreeAsync on the call's stream. */
+typedef void* (*mk_alloc_fn)(size_t bytes, void* stream, void* user);
+typedef void (*mk_free_fn)(void* ptr, void* stream, void* user);
+
+/* ---------------------------------------------------------------- context ---------- */
+/* Binds the library to a CUDA device.  Fails with MK_ERR_UNSUPPORTED on devices older
+ * than sm_100 (the kernels are compiled for sm_100a only). */
+mk_status mk_context_create(int device, mk_alloc_fn alloc, mk_free_fn free_fn, void* user,
+                            mk_context** out);
+void mk_context_destroy(mk_context* ctx);
+
+/* ---------------------------------------------------------------- coordinates ------ */
+/* Sparse tensor quantization, Alg. 1: C' = floor(C_p / v) per axis, computed
+ * as IEEE fp32 division then floor (R6), unique by exact key (R5), rows numbered in
+ * first-occurrence order of the input points (R8); the first point of each voxel is its
+ * representative (R9: i_x of the reduction f).
+ *   d_points      device float32 [n][D]          point coordinates
+ *   d_batch       device int32 [n] or NULL (all 0) batch index per point, >= 0
+ *   voxel         quantization step v_l > 0
+ *   d_point_to_row  device int32 [n] or NULL: row of each point's voxel
+ *   d_first_point   device int32 [n] (capacity n) or NULL: first point of each row
+ * Errors: NONFINITE_INPUT / COORD_RANGE / INVALID_ARGUMENT (negative batch) with the first
+ * offending point row; for D = 4 COORD_RANGE also flags t outside [-2^15, 2^15) or a batch
+ * index above 65534 (packed-key limit of this implementation).  n = 0 is
+ * valid and yields an empty set. */
+mk_status mk_coords_quantize(mk_context* ctx, const float* d_points, const int32_t* d_batch,
+                             int64_t n, int32_t D, float voxel, void* stream, mk_coords** out,
+                             int32_t* d_point_to_row, int32_t* d_first_point);
+
+/* A coordinate set from integer rows (Eq. 1), duplicates merged, first occurrence wins.
+ *   d_coords        device int32 [n][D+1], batch last
+ *   h_tensor_stride host int32 [D] or NULL (all 1): every spatial component must be a
+ *                   multiple of it ("minimum distance between coordinates")
+ *   d_inverse       device int32 [n] or NULL: row of each input row
+ * Errors: STRIDE, INVALID_ARGUMENT (negative batch), COORD_RANGE (D = 4 packing) with the
+ * first offending row. */
+mk_status mk_coords_create(mk_context* ctx, const int32_t* d_coords, int64_t n, int32_t D,
+                           const int32_t* h_tensor_stride, void* stream, mk_coords** out,
+                           int32_t* d_inverse);
+
+/* Size, dimension and per-axis tensor stride (h_tensor_stride host [D], may be NULL). */
+mk_status mk_coords_info(const mk_coords* c, int64_t* n, int32_t* D, int32_t* h_tensor_stride);
+
+/* Copies the rows to d_out (device int32 [n][D+1]). */
+mk_status mk_coords_export(const mk_coords* c, int32_t* d_out, void* stream);
+
+/* Exact membership: d_rows[i] = row of d_queries[i] ([q][D+1]) or -1. */
+mk_status mk_coords_lookup(const mk_coords* c, const int32_t* d_queries, int64_t q,
+                           int32_t* d_rows, void* stream);
+
+/* Output coordinates of a strided convolution (rule R11 from S:84):
+ * s_out = s_in * conv_stride per axis; rows u' = floor_div(u, s_out) * s_out (floor toward
+ * -inf, R7), batch unchanged, first occurrence in input row order. h_conv_stride host [D]. */
+mk_status mk_coords_stride(mk_context* ctx, const mk_coords* in, const int32_t* h_conv_stride,
+                           void* stream, mk_coords** out);
+
+void mk_coords_destroy(mk_coords* c);
+
+/* ---------------------------------------------------------------- kernel region ---- */
+/* Enumerates N^D.  *K receives the count; h_offsets (host int32 [K][D]) may be NULL. */
+mk_status mk_region_offsets(const mk_region* region, int32_t* K, int32_t* h_offsets);
+
+/* ---------------------------------------------------------------- kernel map ------- */
+/* Kernel map M = {(I_i, O_i)}_i for the generalized sparse convolution Eq. 3
+ * (P:155-159): for every output u in C_out and offset i in N^D, the pair (row of u + i*s,
+ * row of u) when u + i*s is in C_in; s = the input tensor stride (R14).  With transposed
+ * != 0 the roles of input and output are reversed (R13): pairs (row of v - i*s,
+ * row of v) for v in C_out with s = the OUTPUT (fine) tensor stride — the map of the
+ * transposed convolution from a coarse set back to a fine one.  Batch indices are never
+ * offset (R18).  Within each offset pairs are sorted by output row.  Requires
+ * in and out of equal D (DIMENSION_MISMATCH) and region->D == D. */
+mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* out,
+                        const mk_region* region, int32_t transposed, void* stream,
+                        mk_kmap** out_map);
+
+mk_status mk_kmap_info(const mk_kmap* m, int32_t* K, int64_t* n_pairs, int64_t* n_in,
+                       int64_t* n_out);
+
+/* CSR export: d_ptr device int64 [K+1], d_in / d_out device int32 [n_pairs]. */
+mk_status mk_kmap_export(const mk_kmap* m, int64_t* d_ptr, int32_t* d_in, int32_t* d_out,
+                         void* stream);
+
+void mk_kmap_destroy(mk_kmap* m);
+
+/* ---------------------------------------------------------------- convolution ------ */
+/* Generalized sparse convolution, Alg. 2:
+ *   F_out[o] = sum over pairs (a, o) of offset k of W_k F_in[a];  rows without any pair
+ *   are 0 ("F^o <- 0"; R15).  No bias (R16).
+ *   d_fin   [n_in][c_in] of in_dt;  d_w [K][c_out][c_in] of in_dt;  d_fout [n_out][c_out]
+ *   of out_dt.  Accumulation is fp32.  MK_BF16 inputs run on the tcgen05 tensor cores;
+ *   MK_F32 inputs run exact fp32 FFMA.  c_in, c_out: multiples of 8, <= 256.
+ * Works on any map; mk_conv_transpose_forward additionally requires a transposed map. */
+mk_status mk_conv_forward(mk_context* ctx, const mk_kmap* m, const void* d_fin, int32_t c_in,
+                          const void* d_w, void* d_fout, int32_t c_out, mk_dtype in_dt,
+                          mk_dtype out_dt, void* stream);
+
+/* Reverse mode of mk_conv_forward (not in the paper, which covers forward only):
+ *   d_gin[a]  = sum over pairs (a, o) of offset k of W_k^T G_out[o]       (NULL: skip)
+ *   d_gw[k]   = sum over pairs (a, o) of offset k of G_out[o] F_in[a]^T   (NULL: skip),
+ *               float32 [K][c_out][c_in], reduced in a fixed order (deterministic).
+ * d_gout [n_out][c_out], d_fin [n_in][c_in], d_w [K][c_out][c_in] and d_gin are of dt. */
+mk_status mk_conv_backward(mk_context* ctx, const mk_kmap* m, const void* d_gout,
+                           const void* d_fin, const void* d_w, int32_t c_in, int32_t c_out,
+                           mk_dtype dt, void* d_gin, float* d_gw, void* stream);
+
+/* Transposed convolution: the same operations on a map built with transposed=1
+ * (fails with INVALID_ARGUMENT otherwise).  W is the transposed conv's own weights
+ * [K][c_out][c_in]; passing W_k^T of a forward conv gives its adjoint. */
+mk_status mk_conv_transpose_forward(mk_context* ctx, const mk_kmap* m, const void* d_fin,
+                                    int32_t c_in, const void* d_w, void* d_fout, int32_t c_out,
+                                    mk_dtype in_dt, mk_dtype out_dt, void* stream);
+mk_status mk_conv_transpose_backward(mk_context* ctx, const mk_kmap* m, const void* d_gout,
+                                     const void* d_fin, const void* d_w, int32_t c_in,
+                                     int32_t c_out, mk_dtype dt, void* d_gin, float* d_gw,
+                                     void* stream);
+
+/* ---------------------------------------------------------------- diagnostics ------ */
+const char* mk_last_error_message(void);
+int64_t mk_last_error_row(void);
+/* Number of library kernels launched by this process so far (bench "gpu_launches"). */
+int64_t mk_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MK_H */

@@ -1,0 +1,297 @@
+"""B200-native generalized sparse convolution (Choy et al., arXiv 1904.08755) — Python binding.
+
+Thin marshalling layer over the C ABI in ``include/mk.h`` (libmk.so): every step of the
+hot path runs in the library's sm_100a kernels; torch provides device memory, streams
+and (in ``dist``) process groups.  Function names mirror the C entry points without the
+``mk_`` prefix.  There is no CPU or eager fallback: without a CUDA device and libmk.so
+the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import BF16, CUSTOM, F32, HYBRID, HYPERCROSS, HYPERCUBE
+
+__all__ = [
+    "MkError", "Coords", "KernelMap", "Region", "context",
+    "coords_quantize", "coords_create", "coords_stride", "coords_lookup", "coords_export",
+    "region_offsets", "kmap_build", "kmap_export",
+    "conv_forward", "conv_backward", "conv_transpose_forward", "conv_transpose_backward",
+    "kernel_launch_count", "HYPERCUBE", "HYPERCROSS", "HYBRID", "CUSTOM", "F32", "BF16",
+]
+
+_L = _lib.load()
+
+
+class MkError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        self.status = status
+        self.name = _lib.STATUS.get(status, str(status))
+        self.row = int(_L.mk_last_error_row())
+        msg = _L.mk_last_error_message().decode(errors="replace")
+        super().__init__(f"{where}: {self.name}: {msg}")
+
+
+def _check(st: int, where: str):
+    if st != 0:
+        raise MkError(st, where)
+
+
+_ctx = {}
+
+
+def context(device: Optional[int] = None) -> ctypes.c_void_p:
+    """The library context of a CUDA device (created once per device)."""
+    if device is None:
+        device = torch.cuda.current_device()
+    if device not in _ctx:
+        h = ctypes.c_void_p()
+        _check(_L.mk_context_create(device, None, None, None, ctypes.byref(h)), "mk_context_create")
+        _ctx[device] = h
+    return _ctx[device]
+
+
+def _stream(t: Optional[torch.Tensor] = None) -> ctypes.c_void_p:
+    dev = t.device if t is not None else None
+    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _cuda(t: torch.Tensor, dtype: torch.dtype, what: str) -> torch.Tensor:
+    if not t.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor (no CPU path)")
+    return t.to(dtype).contiguous()
+
+
+def kernel_launch_count() -> int:
+    return int(_L.mk_kernel_launch_count())
+
+
+# ------------------------------------------------------------------------------ coords
+class Coords:
+    """Immutable coordinate set C (Eq. 1) with its GPU hash table (``mk_coords``)."""
+
+    def __init__(self, handle: ctypes.c_void_p, device: torch.device):
+        self._h = handle
+        self.device = device
+        n, D = ctypes.c_int64(), ctypes.c_int32()
+        ts = (ctypes.c_int32 * 4)()
+        _check(_L.mk_coords_info(handle, ctypes.byref(n), ctypes.byref(D), ts), "mk_coords_info")
+        self.n, self.D = int(n.value), int(D.value)
+        self.tensor_stride = [int(ts[d]) for d in range(self.D)]
+
+    def __len__(self):
+        return self.n
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _L.mk_coords_destroy(self._h)
+            self._h = None
+
+    def export(self) -> torch.Tensor:
+        return coords_export(self)
+
+    def lookup(self, queries: torch.Tensor) -> torch.Tensor:
+        return coords_lookup(self, queries)
+
+
+def coords_quantize(points: torch.Tensor, voxel: float, batch: Optional[torch.Tensor] = None,
+                    return_maps: bool = True):
+    """Alg. 1 -> (Coords, point_to_row int32 [N_p], first_point int32 [N])."""
+    pts = _cuda(points, torch.float32, "points")
+    n, D = pts.shape
+    b = None if batch is None else _cuda(batch, torch.int32, "batch")
+    p2r = torch.empty(n, dtype=torch.int32, device=pts.device) if return_maps else None
+    first = torch.empty(max(n, 1), dtype=torch.int32, device=pts.device) if return_maps else None
+    h = ctypes.c_void_p()
+    with torch.cuda.device(pts.device):
+        _check(_L.mk_coords_quantize(context(pts.device.index), _ptr(pts), _ptr(b), n, D, ctypes.c_float(voxel),
+                                     _stream(pts), ctypes.byref(h), _ptr(p2r), _ptr(first)), "mk_coords_quantize")
+    c = Coords(h, pts.device)
+    if not return_maps:
+        return c
+    return c, p2r, first[:c.n]
+
+
+def coords_create(coords: torch.Tensor, tensor_stride: Optional[Sequence[int]] = None, return_inverse: bool = False):
+    """Coordinate set from integer rows [n][D+1] (batch last); first occurrence wins."""
+    c = _cuda(coords, torch.int32, "coords")
+    n, Dp1 = c.shape
+    D = Dp1 - 1
+    ts = None if tensor_stride is None else (ctypes.c_int32 * D)(*tensor_stride)
+    inv = torch.empty(n, dtype=torch.int32, device=c.device) if return_inverse else None
+    h = ctypes.c_void_p()
+    with torch.cuda.device(c.device):
+        _check(_L.mk_coords_create(context(c.device.index), _ptr(c), n, D, ts, _stream(c), ctypes.byref(h), _ptr(inv)),
+               "mk_coords_create")
+    out = Coords(h, c.device)
+    return (out, inv) if return_inverse else out
+
+
+def coords_stride(cin: Coords, conv_stride: Sequence[int]) -> Coords:
+    """Strided output coordinates (R11)."""
+    cs = (ctypes.c_int32 * cin.D)(*conv_stride)
+    h = ctypes.c_void_p()
+    with torch.cuda.device(cin.device):
+        _check(_L.mk_coords_stride(context(cin.device.index), cin._h, cs, _stream(), ctypes.byref(h)),
+               "mk_coords_stride")
+    return Coords(h, cin.device)
+
+
+def coords_export(c: Coords) -> torch.Tensor:
+    out = torch.empty((c.n, c.D + 1), dtype=torch.int32, device=c.device)
+    with torch.cuda.device(c.device):
+        _check(_L.mk_coords_export(c._h, _ptr(out), _stream()), "mk_coords_export")
+    return out
+
+
+def coords_lookup(c: Coords, queries: torch.Tensor) -> torch.Tensor:
+    q = _cuda(queries, torch.int32, "queries")
+    rows = torch.empty(q.shape[0], dtype=torch.int32, device=q.device)
+    with torch.cuda.device(c.device):
+        _check(_L.mk_coords_lookup(c._h, _ptr(q), q.shape[0], _ptr(rows), _stream()), "mk_coords_lookup")
+    return rows
+
+
+# ------------------------------------------------------------------------------ regions
+class Region:
+    """Kernel offset set N^D description (``mk_region``)."""
+
+    def __init__(self, kind: int, D: int, size=3, dilation=1, temporal_axis: int = -1, offsets=None):
+        self.kind, self.D = kind, D
+        self.size = list(size) if np.ndim(size) else [size] * D
+        self.dilation = list(dilation) if np.ndim(dilation) else [dilation] * D
+        self.temporal_axis = temporal_axis
+        self.offsets = None if offsets is None else np.ascontiguousarray(offsets, np.int32).reshape(-1, D)
+
+    def _struct(self) -> _lib.MkRegion:
+        r = _lib.MkRegion()
+        r.type, r.D, r.temporal_axis = self.kind, self.D, self.temporal_axis
+        for d in range(self.D):
+            r.size[d] = self.size[d]
+            r.dilation[d] = self.dilation[d]
+        if self.offsets is not None:
+            r.offsets = self.offsets.ctypes.data_as(ctypes.POINTER(ctypes.c_int32))
+            r.n_offsets = self.offsets.shape[0]
+        return r
+
+
+def region_offsets(region: Region) -> np.ndarray:
+    r = region._struct()
+    K = ctypes.c_int32()
+    _check(_L.mk_region_offsets(ctypes.byref(r), ctypes.byref(K), None), "mk_region_offsets")
+    out = np.zeros((K.value, region.D), np.int32)
+    _check(_L.mk_region_offsets(ctypes.byref(r), ctypes.byref(K), out.ctypes.data_as(ctypes.c_void_p)),
+           "mk_region_offsets")
+    return out
+
+
+# ------------------------------------------------------------------------------ kernel maps
+class KernelMap:
+    """Immutable kernel map M = {(I_i, O_i)} with its conv-side neighbour tables."""
+
+    def __init__(self, handle, device, cin: Coords, cout: Coords, transposed: bool):
+        self._h = handle
+        self.device = device
+        self.transposed = transposed
+        self._keep = (cin, cout)  # a map never outlives the coordinate sets it indexes
+        K, npairs, nin, nout = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        _check(_L.mk_kmap_info(handle, ctypes.byref(K), ctypes.byref(npairs), ctypes.byref(nin), ctypes.byref(nout)),
+               "mk_kmap_info")
+        self.K, self.n_pairs, self.n_in, self.n_out = K.value, npairs.value, nin.value, nout.value
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            _L.mk_kmap_destroy(self._h)
+            self._h = None
+
+    def export(self):
+        return kmap_export(self)
+
+
+def kmap_build(cin: Coords, cout: Coords, region: Region, transposed: bool = False) -> KernelMap:
+    r = region._struct()
+    h = ctypes.c_void_p()
+    with torch.cuda.device(cin.device):
+        _check(_L.mk_kmap_build(context(cin.device.index), cin._h, cout._h, ctypes.byref(r), int(transposed),
+                                _stream(), ctypes.byref(h)), "mk_kmap_build")
+    return KernelMap(h, cin.device, cin, cout, transposed)
+
+
+def kmap_export(m: KernelMap):
+    """CSR (ptr int64 [K+1], in int32 [|M|], out int32 [|M|]) on the device."""
+    ptr = torch.empty(m.K + 1, dtype=torch.int64, device=m.device)
+    ins = torch.empty(m.n_pairs, dtype=torch.int32, device=m.device)
+    outs = torch.empty(m.n_pairs, dtype=torch.int32, device=m.device)
+    with torch.cuda.device(m.device):
+        _check(_L.mk_kmap_export(m._h, _ptr(ptr), _ptr(ins), _ptr(outs), _stream()), "mk_kmap_export")
+    return ptr, ins, outs
+
+
+# ------------------------------------------------------------------------------ convolution
+_DT = {torch.float32: F32, torch.bfloat16: BF16}
+
+
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype not in _DT:
+        raise TypeError(f"features must be float32 or bfloat16, got {t.dtype}")
+    return _DT[t.dtype]
+
+
+def _conv(fn, name, m: KernelMap, f_in, W, out_dtype, out=None):
+    if not (f_in.is_cuda and W.is_cuda):
+        raise ValueError("conv inputs must be CUDA tensors (no CPU path)")
+    K, c_out, c_in = W.shape
+    if K != m.K or f_in.shape[-1] != c_in or f_in.shape[0] != m.n_in or W.dtype != f_in.dtype:
+        raise ValueError(f"{name}: shape/dtype mismatch (K={m.K}, n_in={m.n_in})")
+    out_dtype = out_dtype or f_in.dtype
+    y = out if out is not None else torch.empty((m.n_out, c_out), dtype=out_dtype, device=f_in.device)
+    with torch.cuda.device(f_in.device):
+        _check(fn(context(f_in.device.index), m._h, _ptr(f_in.contiguous()), c_in, _ptr(W.contiguous()), _ptr(y),
+                  c_out, _dt(f_in), _DT[out_dtype], _stream(f_in)), name)
+    return y
+
+
+def conv_forward(m: KernelMap, f_in: torch.Tensor, W: torch.Tensor, out_dtype=None, out=None) -> torch.Tensor:
+    """Alg. 2: F_out[o] = sum_k W_k F_in[I_k] scattered to O_k.  W [K][C_out][C_in]."""
+    return _conv(_L.mk_conv_forward, "mk_conv_forward", m, f_in, W, out_dtype, out)
+
+
+def conv_transpose_forward(m: KernelMap, f_in: torch.Tensor, W: torch.Tensor, out_dtype=None, out=None):
+    """Transposed conv on a map built with transposed=True."""
+    return _conv(_L.mk_conv_transpose_forward, "mk_conv_transpose_forward", m, f_in, W, out_dtype, out)
+
+
+def _backward(fn, name, m: KernelMap, g_out, f_in, W, need_gin=True, need_gw=True, gin=None, gw=None):
+    K, c_out, c_in = W.shape
+    if g_out.shape != (m.n_out, c_out) or f_in.shape != (m.n_in, c_in) or K != m.K:
+        raise ValueError(f"{name}: shape mismatch")
+    if not (g_out.dtype == f_in.dtype == W.dtype):
+        raise TypeError(f"{name}: g_out, f_in and W must share a dtype")
+    if need_gin and gin is None:
+        gin = torch.empty((m.n_in, c_in), dtype=f_in.dtype, device=f_in.device)
+    if need_gw and gw is None:
+        gw = torch.empty((K, c_out, c_in), dtype=torch.float32, device=f_in.device)
+    with torch.cuda.device(f_in.device):
+        _check(fn(context(f_in.device.index), m._h, _ptr(g_out.contiguous()), _ptr(f_in.contiguous()),
+                  _ptr(W.contiguous()), c_in, c_out, _dt(f_in), _ptr(gin if need_gin else None),
+                  _ptr(gw if need_gw else None), _stream(f_in)), name)
+    return (gin if need_gin else None), (gw if need_gw else None)
+
+
+def conv_backward(m: KernelMap, g_out, f_in, W, need_gin=True, need_gw=True, gin=None, gw=None):
+    """(G_in, dW) of conv_forward; dW is float32 [K][C_out][C_in]."""
+    return _backward(_L.mk_conv_backward, "mk_conv_backward", m, g_out, f_in, W, need_gin, need_gw, gin, gw)
+
+
+def conv_transpose_backward(m: KernelMap, g_out, f_in, W, need_gin=True, need_gw=True, gin=None, gw=None):
+    return _backward(_L.mk_conv_transpose_backward, "mk_conv_transpose_backward", m, g_out, f_in, W, need_gin,
+                     need_gw, gin, gw)

@@ -1,0 +1,61 @@
+"""Builds libmk.so (the C-ABI library) in-tree with nvcc for sm_100a.
+
+No fast-math anywhere: quantization must be IEEE fp32 division + floor (reading R6).
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+SO = PKG / "libmk.so"
+SOURCES = ["context.cu", "region.cu", "coords.cu", "kmap.cu", "conv.cu", "conv_simt.cu", "conv_umma.cu"]
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+         "-I", str(ROOT / "include"), "-I", str(CSRC)]
+
+
+def _stale(obj: Path, src: Path) -> bool:
+    if not obj.exists():
+        return True
+    deps = [src, *CSRC.glob("*.cuh"), ROOT / "include" / "mk.h"]
+    return obj.stat().st_mtime < max(d.stat().st_mtime for d in deps)
+
+
+def build(verbose: bool = False, jobs: int = 8) -> Path:
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
+    procs, objs = [], []
+    for s in SOURCES:
+        src, obj = CSRC / s, objdir / (Path(s).stem + ".o")
+        objs.append(obj)
+        if _stale(obj, src):
+            cmd = ["nvcc", *ARCH, *FLAGS, "-Xptxas", "-v" if verbose else "-O3", "-c", str(src), "-o", str(obj)]
+            procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+            if len(procs) >= jobs:
+                _drain(procs, verbose)
+    _drain(procs, verbose)
+    if not SO.exists() or SO.stat().st_mtime < max(o.stat().st_mtime for o in objs):
+        tmp = SO.with_suffix(f".so.{os.getpid()}")
+        subprocess.check_call(["nvcc", *ARCH, "-shared", "-o", str(tmp), *map(str, objs)])
+        os.replace(tmp, SO)
+    return SO
+
+
+def _drain(procs, verbose):
+    while procs:
+        cmd, p = procs.pop(0)
+        out, _ = p.communicate()
+        if p.returncode != 0:
+            sys.stderr.write(out)
+            raise RuntimeError("nvcc failed: " + " ".join(cmd))
+        if verbose and out.strip():
+            print(out)
+
+
+if __name__ == "__main__":
+    print(build(verbose="-v" in sys.argv))

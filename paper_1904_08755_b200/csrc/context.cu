@@ -1,0 +1,91 @@
+// context.cu — device binding, allocator plumbing and the thread-local error channel.
+#include <cstdio>
+
+#include "mk_internal.cuh"
+
+namespace mk {
+
+namespace {
+thread_local std::string t_msg;
+thread_local int64_t t_row = -1;
+}  // namespace
+
+std::atomic<int64_t> g_launches{0};
+
+void set_error(mk_status s, const std::string& msg, int64_t row) {
+  (void)s;
+  t_msg = msg;
+  t_row = row;
+}
+void clear_error() {
+  t_msg.clear();
+  t_row = -1;
+}
+
+void* dev_alloc(const Alloc& a, size_t bytes, cudaStream_t s) {
+  if (bytes == 0) bytes = 16;
+  if (a.alloc) return a.alloc(bytes, s, a.user);
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void dev_free(const Alloc& a, void* p, cudaStream_t s) {
+  if (!p) return;
+  if (a.free_fn) {
+    a.free_fn(p, s, a.user);
+    return;
+  }
+  cudaFreeAsync(p, s);
+}
+
+uint32_t next_pow2(uint64_t v) {
+  uint64_t p = 1;
+  while (p < v) p <<= 1;
+  return (uint32_t)p;
+}
+
+}  // namespace mk
+
+extern "C" {
+
+mk_status mk_context_create(int device, mk_alloc_fn alloc, mk_free_fn free_fn, void* user,
+                            mk_context** out) {
+  mk::clear_error();
+  if (!out) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_context_create: out is NULL");
+  if ((alloc == nullptr) != (free_fn == nullptr))
+    MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_context_create: alloc and free must both be set or both NULL");
+  int count = 0;
+  MK_CUDA_TRY(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_context_create: no such device");
+  cudaDeviceProp prop;
+  MK_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  if (prop.major < 10)
+    MK_FAIL(MK_ERR_UNSUPPORTED, "mk_context_create: libmk is built for sm_100a (B200) only");
+  MK_CUDA_TRY(cudaSetDevice(device));
+  // Keep freed blocks in the stream-ordered pool (no release to the OS on every sync).
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  mk_context* c = new mk_context();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  c->alloc.alloc = alloc;
+  c->alloc.free_fn = free_fn;
+  c->alloc.user = user;
+  *out = c;
+  return MK_OK;
+}
+
+void mk_context_destroy(mk_context* ctx) { delete ctx; }
+
+const char* mk_last_error_message(void) { return mk::t_msg.c_str(); }
+int64_t mk_last_error_row(void) { return mk::t_row; }
+int64_t mk_kernel_launch_count(void) { return mk::g_launches.load(); }
+
+}  // extern "C"

@@ -1,0 +1,154 @@
+// conv.cu — entry points of the generalized sparse convolution (Alg. 2), its
+// reverse mode, and the transposed convolution.  Validation and dispatch only:
+// fp32 -> exact FFMA kernels (conv_simt.cu); bf16 -> tcgen05 tensor cores (conv_umma.cu).
+#include <algorithm>
+
+#include "conv.cuh"
+
+namespace mk {
+namespace {
+
+mk_status check_common(mk_context* ctx, const mk_kmap* m, int32_t c_in, int32_t c_out, mk_dtype dt) {
+  if (!ctx || !m) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv: null context or map");
+  if (c_in < 1 || c_out < 1) MK_FAIL(MK_ERR_SHAPE_MISMATCH, "conv: channel counts must be >= 1");
+  if (dt != MK_F32 && dt != MK_BF16) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv: unknown dtype");
+  if (c_in > 256 || c_out > 256) MK_FAIL(MK_ERR_UNSUPPORTED, "conv: channel counts above 256");
+  if (dt == MK_BF16 && (c_in % 16 != 0 || c_out % 16 != 0))
+    MK_FAIL(MK_ERR_UNSUPPORTED, "conv: bf16 tensor-core path needs channel counts that are multiples of 16");
+  return MK_OK;
+}
+
+NbrView forward_view(const mk_kmap* m) {
+  NbrView v;
+  v.tab = m->nbr;
+  v.mask = m->tile_mask;
+  v.n = m->n_out;
+  v.K = m->K;
+  v.mw = m->mask_words;
+  return v;
+}
+
+NbrView dgrad_view(const mk_kmap* m) {
+  NbrView v;
+  v.K = m->K;
+  v.mw = m->mask_words;
+  v.n = m->n_in;
+  if (m->nbrT) {
+    v.tab = m->nbrT;
+    v.mask = m->tile_maskT;
+  } else {  // symmetric submanifold map: nbrT[k] = nbr[mirror[k]]
+    v.tab = m->nbr;
+    v.mirror = m->d_mirror;
+    v.mask = m->tile_mask;
+  }
+  return v;
+}
+
+mk_status forward_impl(mk_context* ctx, const mk_kmap* m, const void* d_fin, int32_t c_in, const void* d_w,
+                       void* d_fout, int32_t c_out, mk_dtype in_dt, mk_dtype out_dt, cudaStream_t s) {
+  mk_status st = check_common(ctx, m, c_in, c_out, in_dt);
+  if (st != MK_OK) return st;
+  if (out_dt != MK_F32 && out_dt != MK_BF16) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv: unknown output dtype");
+  if (m->n_out > 0 && !d_fout) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv: null output");
+  if (m->n_pairs > 0 && (!d_fin || !d_w)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv: null input or weights");
+  if (m->n_out == 0) return MK_OK;
+  const NbrView v = forward_view(m);
+  if (in_dt == MK_F32)
+    return launch_conv_f32(v, (const float*)d_fin, c_in, (const float*)d_w, c_in, c_out, d_fout, c_out, out_dt,
+                           m->n_out, false, s);
+  return launch_conv_bf16(ctx, v, d_fin, c_in, d_w, c_in, c_out, d_fout, c_out, out_dt, m->n_out, false, s);
+}
+
+mk_status backward_impl(mk_context* ctx, const mk_kmap* m, const void* d_gout, const void* d_fin, const void* d_w,
+                        int32_t c_in, int32_t c_out, mk_dtype dt, void* d_gin, float* d_gw, cudaStream_t s) {
+  mk_status st = check_common(ctx, m, c_in, c_out, dt);
+  if (st != MK_OK) return st;
+  if (m->n_out > 0 && m->n_pairs > 0 && !d_gout) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv backward: null grad_out");
+  if (d_gin && m->n_in > 0) {
+    if (m->n_pairs > 0 && !d_w) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv backward: null weights");
+    const NbrView v = dgrad_view(m);
+    if (dt == MK_F32)
+      st = launch_conv_f32(v, (const float*)d_gout, c_out, (const float*)d_w, c_in, c_out, d_gin, c_in, MK_F32,
+                           m->n_in, true, s);
+    else
+      st = launch_conv_bf16(ctx, v, d_gout, c_out, d_w, c_in, c_out, d_gin, c_in, MK_BF16, m->n_in, true, s);
+    if (st != MK_OK) return st;
+  }
+  if (d_gw) {
+    if (m->n_pairs > 0 && !d_fin) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv backward: null input features");
+    if (dt == MK_F32) {
+      // split-K plan: chunks of <= 4096 pairs per offset
+      const int64_t P = 4096;
+      std::vector<int4> chunks;
+      std::vector<int32_t> begin(m->K + 1, 0);
+      for (int k = 0; k < m->K; ++k) {
+        begin[k] = (int32_t)chunks.size();
+        for (int64_t b = m->h_ptr[k]; b < m->h_ptr[k + 1]; b += P)
+          chunks.push_back(make_int4(k, (int)b, (int)std::min(b + P, m->h_ptr[k + 1]), (int)chunks.size()));
+      }
+      begin[m->K] = (int32_t)chunks.size();
+      WgradPlan plan;
+      plan.n_chunks = (int64_t)chunks.size();
+      const size_t part_bytes = sizeof(float) * std::max<int64_t>(1, plan.n_chunks) * c_out * c_in;
+      char* ws = (char*)dev_alloc(ctx->alloc, part_bytes + sizeof(int4) * (chunks.size() + 1) + 256 +
+                                                sizeof(int32_t) * (m->K + 1), s);
+      if (!ws) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "conv backward: workspace allocation failed");
+      plan.part = (float*)ws;
+      plan.chunks = (int4*)(ws + ((part_bytes + 255) & ~size_t(255)));
+      plan.chunk_begin = (int32_t*)(plan.chunks + chunks.size() + 1);
+      cudaError_t e = cudaSuccess;
+      if (!chunks.empty())
+        e = cudaMemcpyAsync(plan.chunks, chunks.data(), sizeof(int4) * chunks.size(), cudaMemcpyHostToDevice, s);
+      if (e == cudaSuccess)
+        e = cudaMemcpyAsync(plan.chunk_begin, begin.data(), sizeof(int32_t) * (m->K + 1), cudaMemcpyHostToDevice, s);
+      if (e != cudaSuccess) {
+        dev_free(ctx->alloc, ws, s);
+        MK_FAIL(MK_ERR_CUDA, std::string("conv backward: ") + cudaGetErrorString(e));
+      }
+      st = launch_wgrad_f32(m, plan, (const float*)d_gout, c_out, (const float*)d_fin, c_in, d_gw, s);
+      // pageable H2D copies above are staged synchronously, so host vectors may go out of scope
+      dev_free(ctx->alloc, ws, s);
+    } else {
+      st = launch_wgrad_bf16(ctx, m, d_gout, c_out, d_fin, c_in, d_gw, s);
+    }
+  }
+  return st;
+}
+
+}  // namespace
+}  // namespace mk
+
+using namespace mk;
+
+extern "C" {
+
+mk_status mk_conv_forward(mk_context* ctx, const mk_kmap* m, const void* d_fin, int32_t c_in, const void* d_w,
+                          void* d_fout, int32_t c_out, mk_dtype in_dt, mk_dtype out_dt, void* stream) {
+  clear_error();
+  return forward_impl(ctx, m, d_fin, c_in, d_w, d_fout, c_out, in_dt, out_dt, (cudaStream_t)stream);
+}
+
+mk_status mk_conv_backward(mk_context* ctx, const mk_kmap* m, const void* d_gout, const void* d_fin,
+                           const void* d_w, int32_t c_in, int32_t c_out, mk_dtype dt, void* d_gin, float* d_gw,
+                           void* stream) {
+  clear_error();
+  return backward_impl(ctx, m, d_gout, d_fin, d_w, c_in, c_out, dt, d_gin, d_gw, (cudaStream_t)stream);
+}
+
+mk_status mk_conv_transpose_forward(mk_context* ctx, const mk_kmap* m, const void* d_fin, int32_t c_in,
+                                    const void* d_w, void* d_fout, int32_t c_out, mk_dtype in_dt, mk_dtype out_dt,
+                                    void* stream) {
+  clear_error();
+  if (m && !m->transposed) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_conv_transpose_forward: map is not transposed");
+  return forward_impl(ctx, m, d_fin, c_in, d_w, d_fout, c_out, in_dt, out_dt, (cudaStream_t)stream);
+}
+
+mk_status mk_conv_transpose_backward(mk_context* ctx, const mk_kmap* m, const void* d_gout, const void* d_fin,
+                                     const void* d_w, int32_t c_in, int32_t c_out, mk_dtype dt, void* d_gin,
+                                     float* d_gw, void* stream) {
+  clear_error();
+  if (m && !m->transposed) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_conv_transpose_backward: map is not transposed");
+  return backward_impl(ctx, m, d_gout, d_fin, d_w, c_in, c_out, dt, d_gin, d_gw, (cudaStream_t)stream);
+}
+
+}  // extern "C"

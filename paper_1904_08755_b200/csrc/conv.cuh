@@ -1,0 +1,49 @@
+// conv.cuh — internal interface between the conv entry points (conv.cu) and the kernels
+// (conv_simt.cu: fp32 FFMA; conv_umma.cu: bf16 tcgen05).
+#pragma once
+#include "mk_internal.cuh"
+
+namespace mk {
+
+// Read-only view of a dense neighbour table for an output-stationary gather-GEMM:
+// at(k, r) = source row feeding row r at offset k (or -1).  With `mirror` set, the table
+// is the forward nbr of a symmetric submanifold map read at the mirrored offset
+// (nbrT[k] == nbr[mirror[k]]), so dgrad needs no second table.
+struct NbrView {
+  const int32_t* tab = nullptr;     // [K][n]
+  const int32_t* mirror = nullptr;  // [K] or null
+  const uint32_t* mask = nullptr;   // [ceil(n/128)][mw]
+  int64_t n = 0;
+  int K = 0;
+  int mw = 1;
+  __device__ __forceinline__ int kk(int k) const { return mirror ? __ldg(mirror + k) : k; }
+  __device__ __forceinline__ int32_t at(int k, int64_t r) const { return __ldg(tab + (int64_t)kk(k) * n + r); }
+  __device__ __forceinline__ bool active(int64_t tile128, int k) const {
+    const int q = kk(k);
+    return (__ldg(mask + tile128 * mw + (q >> 5)) >> (q & 31)) & 1u;
+  }
+};
+
+// Split-K plan for the weight gradient: the pairs of offset k are cut into chunks of at
+// most `chunk` pairs; chunks[c] = (k, begin, end, c); chunk_begin[k] = first chunk of k.
+struct WgradPlan {
+  int4* chunks = nullptr;
+  int32_t* chunk_begin = nullptr;
+  float* part = nullptr;  // [n_chunks][c_out][c_in]
+  int64_t n_chunks = 0;
+};
+
+mk_status launch_conv_f32(const NbrView& nb, const float* x, int c_x, const float* W, int c_in_w, int c_out_w,
+                          void* y, int c_y, mk_dtype out_dt, int64_t n_rows, bool trans, cudaStream_t s);
+mk_status launch_wgrad_f32(const mk_kmap* m, const WgradPlan& plan, const float* g, int c_out, const float* x,
+                           int c_in, float* dW, cudaStream_t s);
+
+// bf16 tensor-core path (conv_umma.cu)
+mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, int c_x, const void* W, int c_in_w,
+                           int c_out_w, void* y, int c_y, mk_dtype out_dt, int64_t n_rows, bool trans, cudaStream_t s);
+mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, int c_out, const void* x, int c_in,
+                            float* dW, cudaStream_t s);
+__global__ void k_reduce_partials(const int32_t* __restrict__ chunk_begin, const float* __restrict__ part,
+                                  int64_t tile_elems, float* __restrict__ dW);
+
+}  // namespace mk

@@ -1,0 +1,477 @@
+// coords.cu — coordinate manager: quantization (Alg. 1), creation from integer
+// rows (Eq. 1), strided output coordinates (R11), exact lookup and export.
+//
+// One sort-free pipeline serves all three constructors (a "key source" supplies row p's
+// packed key and validation):
+//   k_insert  one thread per input row: build the key, claim a slot of an open-addressing
+//             table (linear probing, power-of-two capacity >= 2n) by 32-bit atomicCAS of
+//             the row index; equal keys resolve to the smallest row via atomicMin.  Keys are
+//             compared by recomputing the occupant's key from the immutable input, so no
+//             128-bit atomics are needed and no thread ever reads a half-written key.
+//   k_rank    winners (claim[slot] == p) are ranked by a single-pass decoupled look-back
+//             scan in input order => rows in first-occurrence order (R8), first point of a
+//             voxel is its representative (R9).  Writes the row keys and finalises the
+//             table slot (key, row).
+//   k_p2r     optional inverse map point_to_row[p] = table value of its slot.
+// The host then reads the error word and the row count (the one sync of the call).
+#include <cuda/atomic>
+
+#include <climits>
+#include <cstring>
+
+#include "mk_internal.cuh"
+
+namespace mk {
+
+namespace {
+
+constexpr int kBlock = 256;
+constexpr int kItems = 4;
+constexpr int kTile = kBlock * kItems;
+
+enum : uint32_t { E_NONE = 0, E_NONFINITE = 1, E_RANGE = 2, E_BATCH = 3, E_STRIDE = 4 };
+
+__device__ __forceinline__ void report(unsigned long long* err, int64_t row, uint32_t code) {
+  atomicMin(err, ((unsigned long long)row << 8) | code);
+}
+
+// ---------------------------------------------------------------- key sources
+struct QuantSrc {  // Alg. 1 line 1: C_p' <- floor(C_p / v_l)   (R6: fp32 division, floor)
+  const float* pts;
+  const int32_t* batch;
+  int D;
+  float voxel;
+  __device__ __forceinline__ uint32_t key(int64_t p, int4* k) const {
+    int64_t c[4] = {0, 0, 0, 0};
+    bool nonfinite = false, range = false;
+    for (int d = 0; d < D; ++d) {
+      const float x = pts[p * D + d];
+      if (!isfinite(x)) {
+        nonfinite = true;
+        continue;
+      }
+      const float q = floorf(__fdiv_rn(x, voxel));
+      if (!(q >= -2147483648.0f && q < 2147483648.0f)) range = true;
+      else c[d] = (int64_t)q;
+    }
+    if (nonfinite) return E_NONFINITE;
+    if (range) return E_RANGE;
+    const int64_t b = batch ? batch[p] : 0;
+    if (b < 0) return E_BATCH;
+    return pack_key(c, D, b, k) ? E_NONE : E_RANGE;
+  }
+};
+
+struct IntSrc {  // integer rows [n][D+1], batch last (Eq. 1); multiples of the tensor stride
+  const int32_t* rows;
+  int D;
+  int32_t ts[4];
+  __device__ __forceinline__ uint32_t key(int64_t p, int4* k) const {
+    int64_t c[4] = {0, 0, 0, 0};
+    const int32_t* r = rows + p * (D + 1);
+    for (int d = 0; d < D; ++d) {
+      const int32_t v = r[d];
+      if (v % ts[d] != 0) return E_STRIDE;
+      c[d] = v;
+    }
+    const int64_t b = r[D];
+    if (b < 0) return E_BATCH;
+    return pack_key(c, D, b, k) ? E_NONE : E_RANGE;
+  }
+};
+
+struct StrideSrc {  // u' = floor_div(u, s_out) * s_out per spatial axis (R7, R11)
+  const int4* keys;
+  int D;
+  int64_t s[4];
+  __device__ __forceinline__ uint32_t key(int64_t p, int4* k) const {
+    const int4 in = keys[p];
+    int64_t c[4] = {0, 0, 0, 0};
+    for (int d = 0; d < D; ++d) {
+      const int64_t u = key_axis(in, D, d);
+      int64_t q = u / s[d];
+      if (q * s[d] != u && u < 0) q -= 1;
+      const int64_t v = q * s[d];
+      if (v < INT32_MIN || v > INT32_MAX) return E_RANGE;
+      c[d] = v;
+    }
+    return pack_key(c, D, key_batch(in, D), k) ? E_NONE : E_RANGE;
+  }
+};
+
+// ---------------------------------------------------------------- kernels
+template <class Src>
+__global__ void __launch_bounds__(kBlock) k_insert(Src src, int64_t n, int32_t* __restrict__ claim,
+                                                   uint32_t mask, int32_t* __restrict__ slot_of,
+                                                   unsigned long long* err) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    int4 k;
+    const uint32_t code = src.key(p, &k);
+    if (code != E_NONE) {
+      report(err, p, code);
+      continue;
+    }
+    uint32_t h = hash_key(k) & mask;
+    while (true) {
+      int32_t cur = __ldcg(claim + h);
+      if (cur == -1) {
+        cur = atomicCAS(claim + h, -1, (int32_t)p);
+        if (cur == -1) {
+          slot_of[p] = (int32_t)h;
+          break;
+        }
+      }
+      int4 occ;
+      src.key(cur, &occ);  // occupant keys are recomputed from the immutable input
+      if (key_eq(occ, k)) {
+        if (cur > p) atomicMin(claim + h, (int32_t)p);
+        slot_of[p] = (int32_t)h;
+        break;
+      }
+      h = (h + 1) & mask;
+    }
+  }
+}
+
+__device__ __forceinline__ int64_t warp_sum64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Decoupled look-back (single pass): called by all 32 lanes of warp 0; returns the
+// exclusive prefix of `tile` given its aggregate.
+__device__ int64_t lookback(unsigned long long* status, int64_t tile, int64_t agg) {
+  using Ref = cuda::atomic_ref<unsigned long long, cuda::thread_scope_device>;
+  constexpr unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kVal = (1ull << 62) - 1;
+  const int lane = threadIdx.x & 31;
+  if (tile == 0) {
+    if (lane == 0) Ref(status[0]).store(kInc | (unsigned long long)agg, cuda::memory_order_relaxed);
+    return 0;
+  }
+  if (lane == 0) Ref(status[tile]).store(kAgg | (unsigned long long)agg, cuda::memory_order_relaxed);
+  int64_t excl = 0;
+  int64_t top = tile - 1;
+  while (true) {
+    const int64_t idx = top - lane;
+    unsigned long long v = kInc;
+    if (idx >= 0) {
+      v = Ref(status[idx]).load(cuda::memory_order_relaxed);
+      while ((v >> 62) == 0) v = Ref(status[idx]).load(cuda::memory_order_relaxed);
+    }
+    const unsigned inc = __ballot_sync(0xffffffffu, (v >> 62) == 2);
+    const int first = inc ? __ffs(inc) - 1 : 32;
+    excl += warp_sum64(lane <= first ? (int64_t)(v & kVal) : 0);
+    if (inc) break;
+    top -= 32;
+  }
+  if (lane == 0)
+    Ref(status[tile]).store(kInc | (unsigned long long)(excl + agg), cuda::memory_order_relaxed);
+  return excl;
+}
+
+template <class Src>
+__global__ void __launch_bounds__(kBlock) k_rank(Src src, int64_t n, const int32_t* __restrict__ claim,
+                                                 const int32_t* __restrict__ slot_of, int4* __restrict__ tkeys,
+                                                 int32_t* __restrict__ tvals, int4* __restrict__ out_keys,
+                                                 int32_t* __restrict__ first_point,
+                                                 unsigned long long* status, unsigned int* ticket,
+                                                 int64_t* count) {
+  __shared__ int64_t s_tile;
+  __shared__ int32_t s_warp[kBlock / 32];
+  __shared__ int64_t s_prefix;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int64_t base = tile * kTile + (int64_t)threadIdx.x * kItems;
+  bool win[kItems];
+  int32_t slot[kItems];
+  int cnt = 0;
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const int64_t p = base + i;
+    win[i] = false;
+    if (p < n) {
+      slot[i] = slot_of[p];
+      win[i] = claim[slot[i]] == (int32_t)p;
+    }
+    cnt += win[i];
+  }
+  // block-exclusive scan of per-thread counts
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  int warp_off = 0, agg = 0;
+#pragma unroll
+  for (int w = 0; w < kBlock / 32; ++w) {
+    if (w < warp) warp_off += s_warp[w];
+    agg += s_warp[w];
+  }
+  if (warp == 0) {
+    const int64_t pre = lookback(status, tile, agg);
+    if (lane == 0) {
+      s_prefix = pre;
+      if ((tile + 1) * kTile >= n) *count = pre + agg;
+    }
+  }
+  __syncthreads();
+  int64_t row = s_prefix + warp_off + incl - cnt;
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    if (!win[i]) continue;
+    const int64_t p = base + i;
+    int4 k;
+    src.key(p, &k);
+    out_keys[row] = k;
+    tkeys[slot[i]] = k;
+    tvals[slot[i]] = (int32_t)row;
+    if (first_point) first_point[row] = (int32_t)p;
+    ++row;
+  }
+}
+
+__global__ void k_p2r(int64_t n, const int32_t* __restrict__ slot_of, const int32_t* __restrict__ tvals,
+                      int32_t* __restrict__ p2r) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
+    p2r[p] = tvals[slot_of[p]];
+}
+
+__global__ void k_lookup(const int32_t* __restrict__ q, int64_t nq, int D, const int4* __restrict__ tkeys,
+                         const int32_t* __restrict__ tvals, uint32_t mask, int32_t* __restrict__ rows) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t c[4] = {0, 0, 0, 0};
+    for (int d = 0; d < D; ++d) c[d] = q[i * (D + 1) + d];
+    int4 k;
+    rows[i] = pack_key(c, D, q[i * (D + 1) + D], &k) ? probe(tkeys, tvals, mask, k) : -1;
+  }
+}
+
+__global__ void k_export(const int4* __restrict__ keys, int64_t n, int D, int32_t* __restrict__ out) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n; r += (int64_t)gridDim.x * blockDim.x) {
+    const int4 k = keys[r];
+    for (int d = 0; d < D; ++d) out[r * (D + 1) + d] = key_axis(k, D, d);
+    out[r * (D + 1) + D] = key_batch(k, D);
+  }
+}
+
+int grid_for(int64_t n, int block, int sms) {
+  int64_t g = ceil_div(n, block);
+  int64_t cap = (int64_t)sms * 16;
+  return (int)std::max<int64_t>(1, std::min(g, cap));
+}
+
+// Carves one device allocation into 256-byte aligned pieces.
+struct Carver {
+  size_t off = 0;
+  template <class T>
+  size_t take(size_t count) {
+    size_t o = off;
+    off += (count * sizeof(T) + 255) & ~size_t(255);
+    return o;
+  }
+};
+
+template <class Src>
+mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const int32_t* ts,
+                       cudaStream_t s, mk_coords** out, int32_t* d_p2r, int32_t* d_first) {
+  if (n < 0 || n > INT32_MAX) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "row count out of range [0, 2^31)");
+  const uint32_t cap = next_pow2(std::max<int64_t>(2 * n, 64));
+  const int64_t ntiles = std::max<int64_t>(1, ceil_div(n, kTile));
+
+  mk_coords* c = new mk_coords();
+  c->alloc = ctx->alloc;
+  c->stream = s;
+  c->D = D;
+  for (int d = 0; d < D; ++d) c->tensor_stride[d] = ts[d];
+
+  // persistent: table keys, table values, row keys
+  Carver pc;
+  const size_t o_tk = pc.take<int4>(cap), o_tv = pc.take<int32_t>(cap), o_rk = pc.take<int4>(std::max<int64_t>(n, 1));
+  char* pbase = (char*)dev_alloc(c->alloc, pc.off, s);
+  if (!pbase) {
+    delete c;
+    MK_FAIL(MK_ERR_OUT_OF_MEMORY, "coords: device allocation failed");
+  }
+  c->owned.push_back(pbase);
+  c->table.keys = (int4*)(pbase + o_tk);
+  c->table.vals = (int32_t*)(pbase + o_tv);
+  c->table.mask = cap - 1;
+  c->keys = (int4*)(pbase + o_rk);
+
+  // scratch: claims, slot per row, look-back status, ticket, error word, count
+  Carver sc;
+  const size_t o_cl = sc.take<int32_t>(cap), o_sl = sc.take<int32_t>(std::max<int64_t>(n, 1)),
+               o_st = sc.take<unsigned long long>(ntiles), o_ti = sc.take<unsigned int>(1),
+               o_er = sc.take<unsigned long long>(1), o_ct = sc.take<int64_t>(1);
+  char* sbase = (char*)dev_alloc(c->alloc, sc.off, s);
+  if (!sbase) {
+    mk_coords_destroy(c);
+    MK_FAIL(MK_ERR_OUT_OF_MEMORY, "coords: scratch allocation failed");
+  }
+  auto fail_cuda = [&](cudaError_t e, const char* what) {
+    dev_free(c->alloc, sbase, s);
+    mk_coords_destroy(c);
+    set_error(MK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    return MK_ERR_CUDA;
+  };
+  int32_t* claim = (int32_t*)(sbase + o_cl);
+  int32_t* slot_of = (int32_t*)(sbase + o_sl);
+  unsigned long long* status = (unsigned long long*)(sbase + o_st);
+  unsigned int* ticket = (unsigned int*)(sbase + o_ti);
+  unsigned long long* err = (unsigned long long*)(sbase + o_er);
+  int64_t* count = (int64_t*)(sbase + o_ct);
+
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(c->table.keys, 0xFF, sizeof(int4) * (size_t)cap, s)) != cudaSuccess) return fail_cuda(e, "memset");
+  if ((e = cudaMemsetAsync(claim, 0xFF, sizeof(int32_t) * (size_t)cap, s)) != cudaSuccess) return fail_cuda(e, "memset");
+  // status[], ticket, err(=all ones after the next memset), count: contiguous from o_st
+  if ((e = cudaMemsetAsync(sbase + o_st, 0, o_er - o_st, s)) != cudaSuccess) return fail_cuda(e, "memset");
+  if ((e = cudaMemsetAsync(err, 0xFF, sizeof(unsigned long long), s)) != cudaSuccess) return fail_cuda(e, "memset");
+  if ((e = cudaMemsetAsync(count, 0, sizeof(int64_t), s)) != cudaSuccess) return fail_cuda(e, "memset");
+  if (n > 0) {
+    k_insert<Src><<<grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s>>>(src, n, claim, cap - 1, slot_of, err);
+    g_launches++;
+    k_rank<Src><<<(int)ntiles, kBlock, 0, s>>>(src, n, claim, slot_of, c->table.keys, c->table.vals, c->keys,
+                                                 d_first, status, ticket, count);
+    g_launches++;
+    if (d_p2r) {
+      k_p2r<<<grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s>>>(n, slot_of, c->table.vals, d_p2r);
+      g_launches++;
+    }
+    if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "launch");
+  }
+  struct {
+    unsigned long long err;
+    int64_t count;
+  } h;
+  if ((e = cudaMemcpyAsync(&h.err, err, sizeof(h.err), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail_cuda(e, "D2H");
+  if ((e = cudaMemcpyAsync(&h.count, count, sizeof(h.count), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail_cuda(e, "D2H");
+  dev_free(c->alloc, sbase, s);
+  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) {
+    mk_coords_destroy(c);
+    set_error(MK_ERR_CUDA, std::string("coords: ") + cudaGetErrorString(e));
+    return MK_ERR_CUDA;
+  }
+  if (h.err != ~0ull) {
+    const int64_t row = (int64_t)(h.err >> 8);
+    const uint32_t code = (uint32_t)(h.err & 0xFF);
+    mk_coords_destroy(c);
+    mk_status st = code == E_NONFINITE ? MK_ERR_NONFINITE_INPUT
+                 : code == E_RANGE     ? MK_ERR_COORD_RANGE
+                 : code == E_STRIDE    ? MK_ERR_STRIDE
+                                       : MK_ERR_INVALID_ARGUMENT;
+    const char* what = code == E_NONFINITE ? "non-finite coordinate"
+                     : code == E_RANGE     ? "coordinate outside the representable range"
+                     : code == E_STRIDE    ? "coordinate not a multiple of the tensor stride"
+                                           : "negative batch index";
+    set_error(st, std::string("coords: ") + what + " at row " + std::to_string(row), row);
+    return st;
+  }
+  c->n = n > 0 ? h.count : 0;
+  *out = c;
+  return MK_OK;
+}
+
+bool valid_stream_dim(int32_t D) { return D >= 1 && D <= MK_MAX_DIM; }
+
+}  // namespace
+}  // namespace mk
+
+using namespace mk;
+
+extern "C" {
+
+mk_status mk_coords_quantize(mk_context* ctx, const float* d_points, const int32_t* d_batch, int64_t n,
+                             int32_t D, float voxel, void* stream, mk_coords** out, int32_t* d_point_to_row,
+                             int32_t* d_first_point) {
+  clear_error();
+  if (!ctx || !out || (n > 0 && !d_points)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_quantize: null argument");
+  if (!valid_stream_dim(D)) MK_FAIL(D > MK_MAX_DIM ? MK_ERR_UNSUPPORTED : MK_ERR_INVALID_ARGUMENT,
+                                    "mk_coords_quantize: D must be in 1..4");
+  if (!(voxel > 0.0f) || !isfinite(voxel)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_quantize: voxel must be > 0");
+  QuantSrc src{d_points, d_batch, D, voxel};
+  const int32_t ts[4] = {1, 1, 1, 1};
+  return build_coords(ctx, src, n, D, ts, (cudaStream_t)stream, out, d_point_to_row, d_first_point);
+}
+
+mk_status mk_coords_create(mk_context* ctx, const int32_t* d_coords, int64_t n, int32_t D,
+                           const int32_t* h_tensor_stride, void* stream, mk_coords** out, int32_t* d_inverse) {
+  clear_error();
+  if (!ctx || !out || (n > 0 && !d_coords)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_create: null argument");
+  if (!valid_stream_dim(D)) MK_FAIL(D > MK_MAX_DIM ? MK_ERR_UNSUPPORTED : MK_ERR_INVALID_ARGUMENT,
+                                    "mk_coords_create: D must be in 1..4");
+  IntSrc src;
+  src.rows = d_coords;
+  src.D = D;
+  int32_t ts[4] = {1, 1, 1, 1};
+  for (int d = 0; d < D; ++d) {
+    ts[d] = h_tensor_stride ? h_tensor_stride[d] : 1;
+    if (ts[d] < 1) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_create: tensor stride must be >= 1");
+  }
+  for (int d = 0; d < 4; ++d) src.ts[d] = ts[d];
+  return build_coords(ctx, src, n, D, ts, (cudaStream_t)stream, out, d_inverse, nullptr);
+}
+
+mk_status mk_coords_stride(mk_context* ctx, const mk_coords* in, const int32_t* h_conv_stride, void* stream,
+                           mk_coords** out) {
+  clear_error();
+  if (!ctx || !in || !out || !h_conv_stride) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_stride: null argument");
+  StrideSrc src;
+  src.keys = in->keys;
+  src.D = in->D;
+  int32_t ts[4] = {1, 1, 1, 1};
+  for (int d = 0; d < in->D; ++d) {
+    if (h_conv_stride[d] < 1) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_stride: stride must be >= 1");
+    const int64_t s = (int64_t)in->tensor_stride[d] * h_conv_stride[d];
+    if (s > INT32_MAX) MK_FAIL(MK_ERR_COORD_RANGE, "mk_coords_stride: tensor stride overflows int32");
+    ts[d] = (int32_t)s;
+    src.s[d] = s;
+  }
+  for (int d = in->D; d < 4; ++d) src.s[d] = 1;
+  return build_coords(ctx, src, in->n, in->D, ts, (cudaStream_t)stream, out, nullptr, nullptr);
+}
+
+mk_status mk_coords_info(const mk_coords* c, int64_t* n, int32_t* D, int32_t* h_tensor_stride) {
+  clear_error();
+  if (!c) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_info: null handle");
+  if (n) *n = c->n;
+  if (D) *D = c->D;
+  if (h_tensor_stride)
+    for (int d = 0; d < c->D; ++d) h_tensor_stride[d] = c->tensor_stride[d];
+  return MK_OK;
+}
+
+mk_status mk_coords_export(const mk_coords* c, int32_t* d_out, void* stream) {
+  clear_error();
+  if (!c || (c->n > 0 && !d_out)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_export: null argument");
+  if (c->n == 0) return MK_OK;
+  k_export<<<grid_for(c->n, 256, 148), 256, 0, (cudaStream_t)stream>>>(c->keys, c->n, c->D, d_out);
+  MK_LAUNCH_CHECK();
+  return MK_OK;
+}
+
+mk_status mk_coords_lookup(const mk_coords* c, const int32_t* d_queries, int64_t q, int32_t* d_rows, void* stream) {
+  clear_error();
+  if (!c || q < 0 || (q > 0 && (!d_queries || !d_rows))) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_lookup: bad argument");
+  if (q == 0) return MK_OK;
+  k_lookup<<<grid_for(q, 256, 148), 256, 0, (cudaStream_t)stream>>>(d_queries, q, c->D, c->table.keys,
+                                                                      c->table.vals, c->table.mask, d_rows);
+  MK_LAUNCH_CHECK();
+  return MK_OK;
+}
+
+void mk_coords_destroy(mk_coords* c) {
+  if (!c) return;
+  for (void* p : c->owned) dev_free(c->alloc, p, c->stream);
+  delete c;
+}
+
+}  // extern "C"
+

@@ -1,0 +1,184 @@
+// mk_internal.cuh — shared internals of libmk (device key layout, hash table, handles,
+// error plumbing).  Not part of the ABI; see include/mk.h for the public contract.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+#include <vector>
+
+#include "mk.h"
+
+namespace mk {
+
+// ------------------------------------------------------------------ errors
+struct Error {
+  mk_status status;
+  std::string msg;
+  int64_t row;
+};
+
+void set_error(mk_status s, const std::string& msg, int64_t row = -1);
+void clear_error();
+extern std::atomic<int64_t> g_launches;
+
+#define MK_CUDA_TRY(expr)                                                                  \
+  do {                                                                                     \
+    cudaError_t _e = (expr);                                                               \
+    if (_e != cudaSuccess) {                                                               \
+      ::mk::set_error(_e == cudaErrorMemoryAllocation ? MK_ERR_OUT_OF_MEMORY : MK_ERR_CUDA, \
+                      std::string(#expr ": ") + cudaGetErrorString(_e));                   \
+      return _e == cudaErrorMemoryAllocation ? MK_ERR_OUT_OF_MEMORY : MK_ERR_CUDA;         \
+    }                                                                                      \
+  } while (0)
+
+#define MK_LAUNCH_CHECK()                                                                  \
+  do {                                                                                     \
+    ::mk::g_launches.fetch_add(1, std::memory_order_relaxed);                              \
+    MK_CUDA_TRY(cudaGetLastError());                                                       \
+  } while (0)
+
+#define MK_FAIL(status, msg)                 \
+  do {                                       \
+    ::mk::set_error((status), (msg));        \
+    return (status);                         \
+  } while (0)
+
+// ------------------------------------------------------------------ keys
+// A coordinate row (u_1..u_D, b) is packed into one 128-bit key (int4) so that a table
+// slot is a single 16-byte load (coalesced 128-bit coordinate access):
+//   D <= 3 : (u_1, u_2, u_3, b)  with missing axes 0
+//   D == 4 : (u_1, u_2, u_3, (u_4 << 16) | b)  with u_4 in [-2^15, 2^15), b <= 65534
+// The empty sentinel is all ones; no valid key has w == -1 (b >= 0, and b != 0xFFFF
+// for D == 4).
+constexpr int32_t kEmptyWord = -1;
+
+__host__ __device__ __forceinline__ uint32_t hash_key(int4 k) {
+  uint32_t h = (uint32_t)k.x * 0x9E3779B1u;
+  h ^= (uint32_t)k.y * 0x85EBCA77u;
+  h = (h << 13) | (h >> 19);
+  h ^= (uint32_t)k.z * 0xC2B2AE3Du;
+  h ^= (uint32_t)k.w * 0x27D4EB2Fu;
+  h ^= h >> 16;
+  h *= 0x7FEB352Du;
+  h ^= h >> 15;
+  h *= 0x846CA68Bu;
+  h ^= h >> 16;
+  return h;
+}
+
+__host__ __device__ __forceinline__ bool key_eq(int4 a, int4 b) {
+  return a.x == b.x && a.y == b.y && a.z == b.z && a.w == b.w;
+}
+
+// Spatial component d of a packed key.
+__host__ __device__ __forceinline__ int32_t key_axis(int4 k, int D, int d) {
+  if (d == 0) return k.x;
+  if (d == 1) return k.y;
+  if (d == 2) return k.z;
+  return (int32_t)(int16_t)((uint32_t)k.w >> 16);  // d == 3, D == 4
+}
+__host__ __device__ __forceinline__ int32_t key_batch(int4 k, int D) {
+  return D == 4 ? (int32_t)((uint32_t)k.w & 0xFFFFu) : k.w;
+}
+// Packs spatial components c[0..D) (int64, already range-checked by the caller for
+// int32) and batch b.  Returns false when D == 4 and the packed-key limits are violated.
+__host__ __device__ __forceinline__ bool pack_key(const int64_t* c, int D, int64_t b, int4* out) {
+  int4 k;
+  k.x = D > 0 ? (int32_t)c[0] : 0;
+  k.y = D > 1 ? (int32_t)c[1] : 0;
+  k.z = D > 2 ? (int32_t)c[2] : 0;
+  if (D == 4) {
+    if (c[3] < -32768 || c[3] > 32767 || b < 0 || b > 65534) return false;
+    k.w = (int32_t)(((uint32_t)(uint16_t)(int16_t)c[3] << 16) | (uint32_t)b);
+  } else {
+    if (b < 0 || b > INT32_MAX) return false;
+    k.w = (int32_t)b;
+  }
+  *out = k;
+  return true;
+}
+
+// Linear-probing lookup of key q; row or -1.  One 16-byte load per probed slot.
+__device__ __forceinline__ int32_t probe(const int4* __restrict__ tkeys, const int32_t* __restrict__ tvals,
+                                         uint32_t mask, int4 q) {
+  uint32_t h = hash_key(q) & mask;
+  while (true) {
+    const int4 k = __ldg(tkeys + h);
+    if (key_eq(k, q)) return __ldg(tvals + h);
+    if (k.w == kEmptyWord) return -1;
+    h = (h + 1) & mask;
+  }
+}
+
+// ------------------------------------------------------------------ handles
+struct Table {
+  int4* keys = nullptr;     // [cap]
+  int32_t* vals = nullptr;  // [cap] row of the key
+  uint32_t mask = 0;        // cap - 1 (cap is a power of two >= 2n)
+};
+
+struct Alloc {
+  mk_alloc_fn alloc = nullptr;
+  mk_free_fn free_fn = nullptr;
+  void* user = nullptr;
+};
+
+}  // namespace mk
+
+struct mk_context {
+  int device = 0;
+  int num_sms = 148;
+  mk::Alloc alloc;
+};
+
+struct mk_coords {
+  mk::Alloc alloc;
+  cudaStream_t stream = nullptr;  // stream the handle was created on (frees are ordered there)
+  int64_t n = 0;
+  int32_t D = 0;
+  int32_t tensor_stride[MK_MAX_DIM] = {1, 1, 1, 1};
+  int4* keys = nullptr;  // [n] packed rows, row order = first occurrence
+  mk::Table table;
+  std::vector<void*> owned;
+};
+
+struct mk_kmap {
+  mk::Alloc alloc;
+  cudaStream_t stream = nullptr;
+  int32_t K = 0;
+  int32_t D = 0;
+  int32_t transposed = 0;
+  int64_t n_in = 0, n_out = 0, n_pairs = 0;
+  std::vector<int64_t> h_ptr;       // [K+1] host copy of the CSR offsets
+  int64_t* ptr = nullptr;           // [K+1]
+  int32_t* in_idx = nullptr;        // [n_pairs]
+  int32_t* out_idx = nullptr;       // [n_pairs]
+  // Dense neighbour tables used by the output-stationary convolution kernels:
+  //   nbr[k][o]  = input row paired with output o at offset k, or -1       (forward)
+  //   nbrT[k][a] = output row paired with input a at offset k, or -1        (dgrad)
+  // When in == out (submanifold) and N^D is closed under negation, nbrT[k] == nbr[mirror[k]]
+  // and nbrT is not stored (nbrT == nullptr).
+  int32_t* nbr = nullptr;
+  int32_t* nbrT = nullptr;
+  std::vector<int32_t> mirror;      // [K] index of -offset_k, or -1
+  int32_t* d_mirror = nullptr;      // [K]
+  // Per 128-row tile bitmasks of non-empty offsets (mask words = ceil(K/32)):
+  uint32_t* tile_mask = nullptr;    // [ceil(n_out/128)][mw]  forward tiles
+  uint32_t* tile_maskT = nullptr;   // [ceil(n_in/128)][mw]   dgrad tiles
+  int32_t mask_words = 1;
+  std::vector<void*> owned;
+};
+
+namespace mk {
+void* dev_alloc(const Alloc& a, size_t bytes, cudaStream_t s);
+void dev_free(const Alloc& a, void* p, cudaStream_t s);
+inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+uint32_t next_pow2(uint64_t v);
+
+// Table-building pipeline shared by quantize / create / stride (coords.cu).
+// Region enumeration (region.cu):
+mk_status region_enumerate(const mk_region* r, std::vector<int32_t>* offsets, int32_t* K);
+}  // namespace mk

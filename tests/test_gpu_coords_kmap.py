@@ -1,0 +1,198 @@
+"""GPU <-> oracle parity of the integer path: coordinates, hash lookups and kernel maps
+must be byte-identical (BASELINE.json north_star; DESIGN.md §3 R22)."""
+import numpy as np
+import pytest
+import torch
+
+import synthetic
+from conftest import full_grid
+from gpu_util import csr_np
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mk():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_1904_08755_b200 as m
+    return m
+
+
+def dev(a, dtype=None):
+    t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    return t if dtype is None else t.to(dtype)
+
+
+# ------------------------------------------------------------------ quantize / create
+@pytest.mark.parametrize("seed,n,D,span,voxel", [(0, 1, 3, 1.0, 0.1), (1, 3000, 3, 1.0, 0.1), (2, 50000, 3, 3.0, 0.05),
+                                                 (3, 20000, 2, 1.0, 0.01), (4, 7000, 1, 5.0, 0.3), (5, 40000, 4, 2.0, 0.25)])
+def test_quantize_matches_oracle(mk, orc, seed, n, D, span, voxel):
+    g = np.random.default_rng(seed)
+    pts = g.uniform(-span, span, (n, D)).astype(np.float32)
+    batch = g.integers(0, 4, n).astype(np.int32)
+    c, p2r, first = mk.coords_quantize(dev(pts), voxel, dev(batch))
+    oc, op2r, ofirst = orc.quantize(pts, voxel, batch)
+    assert np.array_equal(c.export().cpu().numpy(), oc)
+    assert np.array_equal(p2r.cpu().numpy(), op2r)
+    assert np.array_equal(first.cpu().numpy(), ofirst)
+
+
+def test_quantize_room_full_size(mk, orc):
+    # cfg2 shape: ~1M raw points -> ~150k voxels at 2 cm (BASELINE configs[1])
+    pts = synthetic.room_points(2001)
+    c, p2r, first = mk.coords_quantize(dev(pts), synthetic.ROOM_VOXEL)
+    oc, op2r, ofirst = orc.quantize(pts, synthetic.ROOM_VOXEL)
+    assert np.array_equal(c.export().cpu().numpy(), oc)
+    assert np.array_equal(p2r.cpu().numpy(), op2r)
+    assert np.array_equal(first.cpu().numpy(), ofirst)
+
+
+def test_quantize_worked_example_and_r6(mk):
+    pts = np.array([[0.12, 0.34, 0.56], [0.3, 0.3, 0.3], [0.58, 0.58, 0.58]], np.float32)
+    c, _, _ = mk.coords_quantize(dev(pts[:1]), 0.1)
+    assert c.export().cpu().tolist() == [[1, 3, 5, 0]]
+    c, _, _ = mk.coords_quantize(dev(pts[1:2]), 0.1)
+    assert c.export().cpu().tolist() == [[3, 3, 3, 0]]  # R6: fp32 division
+    c, _, _ = mk.coords_quantize(dev(pts[2:3]), 0.02)
+    assert c.export().cpu().tolist() == [[29, 29, 29, 0]]
+
+
+def test_quantize_errors(mk):
+    pts = np.zeros((5000, 3), np.float32)
+    pts[3001, 1] = np.nan
+    pts[4000, 0] = np.inf
+    with pytest.raises(mk.MkError) as e:
+        mk.coords_quantize(dev(pts), 0.1)
+    assert e.value.name == "MK_ERR_NONFINITE_INPUT" and e.value.row == 3001
+    pts = np.zeros((100, 2), np.float32)
+    pts[77, 0] = 3e9
+    with pytest.raises(mk.MkError) as e:
+        mk.coords_quantize(dev(pts), 1.0)
+    assert e.value.name == "MK_ERR_COORD_RANGE" and e.value.row == 77
+    b = np.zeros(100, np.int32)
+    b[12] = -1
+    with pytest.raises(mk.MkError) as e:
+        mk.coords_quantize(dev(np.zeros((100, 3), np.float32)), 1.0, dev(b))
+    assert e.value.name == "MK_ERR_INVALID_ARGUMENT" and e.value.row == 12
+
+
+def test_empty_inputs(mk):
+    c, p2r, first = mk.coords_quantize(torch.zeros((0, 3), device="cuda"), 0.1)
+    assert c.n == 0 and p2r.numel() == 0
+    m = mk.kmap_build(c, c, mk.Region(mk.HYPERCUBE, 3, 3))
+    assert m.n_pairs == 0 and m.K == 27
+    W = torch.randn(27, 16, 16, device="cuda")
+    y = mk.conv_forward(m, torch.zeros((0, 16), device="cuda"), W)
+    assert y.shape == (0, 16)
+
+
+@pytest.mark.parametrize("D,ts", [(3, 1), (3, 2), (4, 1), (2, 3)])
+def test_create_matches_oracle(mk, orc, D, ts):
+    g = np.random.default_rng(D * 7 + ts)
+    rows = np.concatenate([g.integers(-60, 60, (30000, D)) * ts, g.integers(0, 3, (30000, 1))], axis=1).astype(np.int32)
+    c, inv = mk.coords_create(dev(rows), [ts] * D, return_inverse=True)
+    oc, oinv = orc.create(rows, [ts] * D)
+    assert np.array_equal(c.export().cpu().numpy(), oc)
+    assert np.array_equal(inv.cpu().numpy(), oinv)
+    assert c.tensor_stride == [ts] * D
+
+
+def test_create_errors(mk):
+    rows = np.zeros((300, 4), np.int32)
+    rows[:, :3] = 2
+    rows[123, 1] = 3
+    with pytest.raises(mk.MkError) as e:
+        mk.coords_create(dev(rows), [2, 2, 2])
+    assert e.value.name == "MK_ERR_STRIDE" and e.value.row == 123
+    r4 = np.zeros((10, 5), np.int32)
+    r4[4, 3] = 40000  # t outside the packed 4D key domain
+    with pytest.raises(mk.MkError) as e:
+        mk.coords_create(dev(r4))
+    assert e.value.name == "MK_ERR_COORD_RANGE" and e.value.row == 4
+
+
+@pytest.mark.parametrize("sigma,ts,D", [(2, 1, 3), (2, 2, 3), (3, 1, 3), (2, 1, 4), (4, 1, 2)])
+def test_stride_matches_oracle(mk, orc, sigma, ts, D):
+    g = np.random.default_rng(sigma * 10 + ts)
+    rows = np.concatenate([g.integers(-80, 80, (20000, D)) * ts, g.integers(0, 2, (20000, 1))], axis=1).astype(np.int32)
+    c = mk.coords_create(dev(rows), [ts] * D)
+    s = mk.coords_stride(c, [sigma] * D)
+    oc, _ = orc.create(rows, [ts] * D)
+    assert np.array_equal(s.export().cpu().numpy(), orc.stride(oc, [sigma] * D, [ts] * D))
+    assert s.tensor_stride == [ts * sigma] * D
+
+
+def test_lookup_matches_oracle(mk, orc):
+    g = np.random.default_rng(9)
+    rows = np.concatenate([g.integers(-30, 30, (20000, 3)), g.integers(0, 2, (20000, 1))], axis=1).astype(np.int32)
+    q = np.concatenate([g.integers(-31, 31, (50000, 3)), g.integers(0, 3, (50000, 1))], axis=1).astype(np.int32)
+    c = mk.coords_create(dev(rows))
+    oc, _ = orc.create(rows)
+    assert np.array_equal(c.lookup(dev(q)).cpu().numpy(), orc.lookup(oc, q))
+
+
+# ------------------------------------------------------------------ kernel maps
+def _check_map(mk, orc, cin_np, cout_np, region, scale, transposed, ci, co):
+    m = mk.kmap_build(ci, co, region, transposed=transposed)
+    offs = mk.region_offsets(region)
+    optr, oin, oout = orc.kmap(cin_np, cout_np, offs, scale, transposed)
+    ptr, ins, outs = csr_np(m)
+    assert np.array_equal(ptr, optr)
+    assert np.array_equal(ins, oin) and np.array_equal(outs, oout)
+    return m
+
+
+@pytest.mark.parametrize("kind,D,size,dil", [(0, 3, 3, 1), (0, 3, 5, 1), (1, 3, 3, 1), (2, 4, 3, 1), (0, 4, 3, 1),
+                                             (0, 3, 3, 2), (0, 3, 2, 1), (0, 2, 7, 1)])
+def test_kmap_submanifold_matches_oracle(mk, orc, kind, D, size, dil):
+    g = np.random.default_rng(kind * 100 + D * 10 + size)
+    rows = np.concatenate([g.integers(-25, 25, (40000, D)), g.integers(0, 2, (40000, 1))], axis=1).astype(np.int32)
+    c = mk.coords_create(dev(rows))
+    oc, _ = orc.create(rows)
+    _check_map(mk, orc, oc, oc, mk.Region(kind, D, size, dil), [1] * D, False, c, c)
+
+
+def test_kmap_worked_examples(mk):
+    c = mk.coords_create(dev(full_grid(4, 2)))
+    assert mk.kmap_build(c, c, mk.Region(mk.HYPERCUBE, 2, 3)).n_pairs == 100
+    c1 = mk.coords_create(dev(np.array([[5, 5, 5, 0]], np.int32)))
+    m = mk.kmap_build(c1, c1, mk.Region(mk.HYPERCUBE, 3, 3))
+    ptr, ins, outs = csr_np(m)
+    assert m.n_pairs == 1 and ptr[14] - ptr[13] == 1  # one pair at offset 0
+
+
+@pytest.mark.parametrize("K,ts", [(2, 1), (3, 1), (2, 2)])
+def test_kmap_strided_and_transposed_match_oracle(mk, orc, K, ts):
+    g = np.random.default_rng(K * 10 + ts)
+    rows = np.concatenate([g.integers(-40, 40, (30000, 3)) * ts, g.integers(0, 2, (30000, 1))], axis=1).astype(np.int32)
+    fine = mk.coords_create(dev(rows), [ts] * 3)
+    coarse = mk.coords_stride(fine, [2, 2, 2])
+    ofine, _ = orc.create(rows, [ts] * 3)
+    ocoarse = orc.stride(ofine, [2, 2, 2], [ts] * 3)
+    r = mk.Region(mk.HYPERCUBE, 3, K)
+    m = _check_map(mk, orc, ofine, ocoarse, r, [ts] * 3, False, fine, coarse)
+    if K == 2:
+        assert m.n_pairs == fine.n  # R3 partition pin
+    _check_map(mk, orc, ocoarse, ofine, r, [ts] * 3, True, coarse, fine)
+
+
+def test_kmap_room_full_size(mk, orc):
+    # BASELINE configs[1]: ScanNet-shaped room, 3x3x3, full size — maps bit-exact
+    pts = synthetic.room_points(2002)
+    c, _, _ = mk.coords_quantize(dev(pts), synthetic.ROOM_VOXEL)
+    oc, _, _ = orc.quantize(pts, synthetic.ROOM_VOXEL)
+    _check_map(mk, orc, oc, oc, mk.Region(mk.HYPERCUBE, 3, 3), [1, 1, 1], False, c, c)
+
+
+def test_kmap_video_hybrid_full_size(mk, orc):
+    # BASELINE configs[2]: 3 frames x ~100k voxels, hybrid kernel (29 offsets)
+    pts, fr = synthetic.video_points(3001)
+    c3, _, _ = mk.coords_quantize(dev(pts), synthetic.VIDEO_VOXEL, dev(fr))
+    rows4 = c3.export()
+    rows4 = torch.cat([rows4[:, :3], rows4[:, 3:4], torch.zeros_like(rows4[:, :1])], dim=1)  # frame -> t, b = 0
+    c4 = mk.coords_create(rows4)
+    o3, _, _ = orc.quantize(pts, synthetic.VIDEO_VOXEL, fr)
+    o4 = np.concatenate([o3, np.zeros((o3.shape[0], 1), np.int32)], axis=1)
+    assert np.array_equal(c4.export().cpu().numpy(), o4)
+    m = _check_map(mk, orc, o4, o4, mk.Region(mk.HYBRID, 4, 3), [1] * 4, False, c4, c4)
+    assert m.K == 29
