@@ -1,12 +1,525 @@
-// conv_umma.cu — bf16 tcgen05 gather-GEMM kernels (placeholder until the tensor-core path lands).
+// conv_umma.cu — bf16 tcgen05 (UMMA) kernels of the generalized sparse convolution.
+//
+// k_conv_umma<CH>: output-stationary gather-GEMM for forward, dgrad and the transposed conv
+//   (Alg. 2 P:189-201 reorganised per output tile).  Persistent, one CTA per SM,
+//   warp-specialised:
+//     warps 0-3  producers: for every (tile of 128 output rows, non-empty offset k,
+//                channel chunk c) gather the 128 neighbour rows x[nb(k,row)][c*CH..] into a
+//                swizzled K-major smem stage with 16-byte cp.async (absent neighbours are
+//                zero-filled, no global read), and bulk-copy (TMA engine) the pre-swizzled
+//                weight chunk W_k[:, c] into the same stage.
+//     warp 8     one elected thread issues tcgen05.mma (M=128, N=C_out, K=16) into a TMEM
+//                accumulator; tcgen05.commit frees the stage / publishes the tile.
+//     warps 4-7  epilogue: tcgen05.ld the 128 x C_out fp32 accumulator (double-buffered in
+//                TMEM so it overlaps the next tile's MMAs), convert, store whole rows.
+//   Every output row is produced by exactly one CTA from all its offsets: no atomics, fixed
+//   summation order, rows without neighbours are written as 0.
+// k_wgrad_umma: dW_k = sum_p G[o_p] x X[a_p]^T over the pairs of offset k (split-K).  The
+//   concatenated pair list is cut into per-CTA ranges; each (CTA, offset) segment is an
+//   accumulation unit: gathered G rows form the MN-major A operand (M = C_out padded to
+//   128), gathered X rows the MN-major B operand (N = C_in), K = pairs.  Segment partials
+//   go to a workspace and are summed per offset in a fixed order (deterministic).
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <mutex>
+
 #include "conv.cuh"
+#include "sm100.cuh"
 
 namespace mk {
-mk_status launch_conv_bf16(mk_context*, const NbrView&, const void*, int, const void*, int, int, void*, int, mk_dtype,
-                           int64_t, bool, cudaStream_t) {
-  MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 tensor-core conv not built yet");
+namespace {
+
+using namespace sm100;
+
+constexpr int kTileM = 128;
+constexpr int kProdWarps = 4;
+constexpr int kEpiWarps = 4;
+constexpr int kMmaWarp = kProdWarps + kEpiWarps;  // warp 8
+constexpr int kThreads = (kProdWarps + kEpiWarps + 1) * 32;
+constexpr int kMaxSmem = 227 * 1024;
+
+__device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
+  return (uint8_t*)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
 }
-mk_status launch_wgrad_bf16(mk_context*, const mk_kmap*, const void*, int, const void*, int, float*, cudaStream_t) {
-  MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 tensor-core wgrad not built yet");
+
+// ------------------------------------------------------------------ weight packing
+// Writes W_k chunk images in the exact swizzled K-major smem layout of the B operand:
+// image(k, c) = rows n in [0, c_y), channels [c*CH, c*CH+CH) of the reduction dimension.
+//   forward: B(n, kx) = W[k][n][kx]   (n = c_out, kx = c_in)
+//   dgrad  : B(n, kx) = W[k][kx][n]   (n = c_in,  kx = c_out)  i.e. W_k^T
+__global__ void k_pack_w(const __nv_bfloat16* __restrict__ W, int K, int c_out, int c_in, int trans, int CH,
+                         uint8_t* __restrict__ out) {
+  const int c_y = trans ? c_in : c_out, c_x = trans ? c_out : c_in;
+  const int nch = c_x / CH, J = CH / 8, RB = CH * 2;
+  const int64_t total = (int64_t)K * nch * c_y * J;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    const int j = (int)(idx % J);
+    const int n = (int)((idx / J) % c_y);
+    const int c = (int)((idx / ((int64_t)J * c_y)) % nch);
+    const int k = (int)(idx / ((int64_t)J * c_y * nch));
+    __align__(16) __nv_bfloat16 v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int kx = c * CH + j * 8 + e;
+      v[e] = trans ? W[((int64_t)k * c_out + kx) * c_in + n] : W[((int64_t)k * c_out + n) * c_in + kx];
+    }
+    uint8_t* dst = out + ((int64_t)k * nch + c) * c_y * RB + swz(n, j, RB);
+    *(uint4*)dst = *(const uint4*)v;
+  }
 }
+
+// ------------------------------------------------------------------ forward / dgrad
+struct FwdParams {
+  const __nv_bfloat16* x;  // [n_src][c_x]
+  const uint8_t* wpack;    // [K][nch] images of c_y * CH bf16
+  void* y;                 // [n_rows][c_y]
+  NbrView nb;
+  int64_t n_rows, ntiles;
+  int c_x, c_y, nch, out_f32, stages;
+  uint32_t a_bytes, b_bytes, stage_bytes, tmem_cols;
+};
+
+__device__ __forceinline__ int tile_active_count(const NbrView& nb, int64_t tile) {
+  if (!nb.mirror) {
+    int n = 0;
+    for (int w = 0; w < nb.mw; ++w) n += __popc(__ldg(nb.mask + tile * nb.mw + w));
+    return n;
+  }
+  int n = 0;
+  for (int k = 0; k < nb.K; ++k) n += nb.active(tile, k);
+  return n;
+}
+
+template <int CH>
+__global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant__ FwdParams p) {
+  constexpr int J = CH / 8;    // 16-byte chunks per gathered row
+  constexpr int RB = CH * 2;   // bytes per gathered row (= swizzle span)
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const int S = p.stages;
+  uint64_t* full = (uint64_t*)(smem + (size_t)S * p.stage_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, kProdWarps * 32 + 1);
+      mbar_init(empty + s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(tfull + b, 1);
+      mbar_init(tempty + b, kEpiWarps * 32);
+    }
+    fence_mbar_init();
+  }
+  if (warp == kMmaWarp) tmem_alloc_dyn(tmem_slot, p.tmem_cols);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const int K = p.nb.K;
+
+  if (warp < kProdWarps) {
+    // ---------------------------------------------------------------- producers
+    const int t = threadIdx.x;
+    uint32_t g = 0;
+    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+      const int64_t row0 = tile * kTileM;
+      for (int k = 0; k < K; ++k) {
+        if (!p.nb.active(tile, k)) continue;
+        int32_t src[J];
+#pragma unroll
+        for (int i = 0; i < J; ++i) {
+          const int r = (i * 128 + t) / J;
+          const int64_t row = row0 + r;
+          src[i] = row < p.n_rows ? p.nb.at(k, row) : -1;
+        }
+        for (int c = 0; c < p.nch; ++c) {
+          const uint32_t s = g % S, ph = (g / S) & 1;
+          mbar_wait(empty + s, ph ^ 1);
+          uint8_t* stage = smem + (size_t)s * p.stage_bytes;
+          const uint32_t a_s = smem_u32(stage);
+#pragma unroll
+          for (int i = 0; i < J; ++i) {
+            const int idx = i * 128 + t;
+            const int r = idx / J, j = idx % J;
+            const bool ok = src[i] >= 0;
+            const __nv_bfloat16* gp = ok ? p.x + (int64_t)src[i] * p.c_x + c * CH + j * 8 : p.x;
+            cp_async16(a_s + swz(r, j, RB), gp, ok ? 16u : 0u);
+          }
+          if (t == 0) {
+            mbar_arrive_expect_tx(full + s, p.b_bytes);
+            bulk_g2s(stage + p.a_bytes, p.wpack + ((int64_t)k * p.nch + c) * p.b_bytes, p.b_bytes, full + s);
+          }
+          cp_async_arrive_noinc(full + s);
+          ++g;
+        }
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (warp == kMmaWarp) {
+    // ---------------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16(kTileM, p.c_y, 0, 0);
+      const uint32_t lay = layout_code(RB);
+      uint32_t g = 0, tl = 0;
+      for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+        if (tile_active_count(p.nb, tile) == 0) continue;
+        const uint32_t b = tl & 1, tph = (tl >> 1) & 1;
+        mbar_wait(tempty + b, tph ^ 1);
+        tc_fence_after();
+        const uint32_t d = tbase + b * (uint32_t)p.c_y;
+        uint32_t acc = 0;
+        for (int k = 0; k < K; ++k) {
+          if (!p.nb.active(tile, k)) continue;
+          for (int c = 0; c < p.nch; ++c) {
+            const uint32_t s = g % S, ph = (g / S) & 1;
+            mbar_wait(full + s, ph);
+            tc_fence_after();
+            fence_proxy_async_smem();
+            const uint32_t a_s = smem_u32(smem + (size_t)s * p.stage_bytes);
+            const uint32_t b_s = a_s + p.a_bytes;
+#pragma unroll
+            for (int kk = 0; kk < CH / 16; ++kk) {
+              const uint64_t ad = smem_desc(a_s + kk * 32, 16, 8 * RB, lay);
+              const uint64_t bd = smem_desc(b_s + kk * 32, 16, 8 * RB, lay);
+              umma_f16(d, ad, bd, idesc, acc);
+              acc = 1;
+            }
+            umma_commit(empty + s);
+            ++g;
+          }
+        }
+        umma_commit(tfull + b);
+        ++tl;
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    const int q = warp & 3;  // TMEM lane quarter owned by this warp
+    uint32_t tl = 0;
+    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+      const int64_t row = tile * kTileM + q * 32 + lane;
+      const bool valid = row < p.n_rows;
+      if (tile_active_count(p.nb, tile) == 0) {
+        if (valid) {
+          if (p.out_f32) {
+            float4* yr = (float4*)((float*)p.y + row * p.c_y);
+            for (int c = 0; c < p.c_y / 4; ++c) yr[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+          } else {
+            uint4* yr = (uint4*)((__nv_bfloat16*)p.y + row * p.c_y);
+            for (int c = 0; c < p.c_y / 8; ++c) yr[c] = make_uint4(0, 0, 0, 0);
+          }
+        }
+        continue;
+      }
+      const uint32_t b = tl & 1, tph = (tl >> 1) & 1;
+      mbar_wait(tfull + b, tph);
+      tc_fence_after();
+      const uint32_t tl_addr = tbase + ((uint32_t)(q * 32) << 16) + b * (uint32_t)p.c_y;
+      for (int col0 = 0; col0 < p.c_y; col0 += 16) {
+        uint32_t v[16];
+        tmem_ld16(tl_addr + col0, v);
+        tmem_ld_wait();
+        if (valid) {
+          if (p.out_f32) {
+            float4* yr = (float4*)((float*)p.y + row * p.c_y + col0);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              yr[e] = make_float4(__uint_as_float(v[4 * e]), __uint_as_float(v[4 * e + 1]),
+                                  __uint_as_float(v[4 * e + 2]), __uint_as_float(v[4 * e + 3]));
+          } else {
+            uint32_t h[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+              __nv_bfloat162 t2 = __floats2bfloat162_rn(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+              h[e] = *(uint32_t*)&t2;
+            }
+            uint4* yr = (uint4*)((__nv_bfloat16*)p.y + row * p.c_y + col0);
+            yr[0] = make_uint4(h[0], h[1], h[2], h[3]);
+            yr[1] = make_uint4(h[4], h[5], h[6], h[7]);
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty + b);
+      ++tl;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kMmaWarp) tmem_dealloc(tbase, p.tmem_cols);
+}
+
+// ------------------------------------------------------------------ weight gradient
+struct WgradParams {
+  const __nv_bfloat16* g;  // [n_out][c_out]
+  const __nv_bfloat16* x;  // [n_in][c_in]
+  const int32_t* in_idx;
+  const int32_t* out_idx;
+  const int4* segs;          // (k, begin, end, slot), grouped by CTA
+  const int32_t* seg_begin;  // [n_cta + 1]
+  float* part;               // [n_slots][c_out][c_in]
+  int c_out, c_in, stages, halves;
+  int pwa, pwb;              // panel widths (channels) of A (G) and B (X)
+  uint32_t a_bytes, b_bytes, stage_bytes, tmem_cols;
+};
+
+constexpr int kPairsPerStage = 64;
+
+__global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constant__ WgradParams p) {
+  constexpr int PS = kPairsPerStage;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = align1024(smem_raw);
+  const int S = p.stages;
+  uint64_t* full = (uint64_t*)(smem + (size_t)S * p.stage_bytes);
+  uint64_t* empty = full + S;
+  uint64_t* tfull = empty + S;
+  uint64_t* tempty = tfull + 1;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rba = p.pwa * 2, rbb = p.pwb * 2;              // panel row bytes
+  const int npa = p.c_out / p.pwa, npb = p.c_in / p.pwb;   // real panels
+  const uint32_t panel_a = PS * rba, panel_b = PS * rbb;   // panel strides (LBO)
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(full + s, kProdWarps * 32);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(tfull, 1);
+    mbar_init(tempty, kEpiWarps * 32);
+    fence_mbar_init();
+  }
+  // zero the padding panels of A (M padded to 128 per half) once; never overwritten
+  {
+    const int tot_pa = (int)(p.a_bytes / panel_a);
+    for (int s = 0; s < S; ++s)
+      for (int pa = npa; pa < tot_pa; ++pa) {
+        uint4* z = (uint4*)(smem + (size_t)s * p.stage_bytes + (size_t)pa * panel_a);
+        for (int i = threadIdx.x; i < (int)(panel_a / 16); i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
+      }
+  }
+  if (warp == kMmaWarp) tmem_alloc_dyn(tmem_slot, p.tmem_cols);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_slot;
+  const int sb = p.seg_begin[blockIdx.x], se = p.seg_begin[blockIdx.x + 1];
+
+  if (warp < kProdWarps) {
+    const int t = threadIdx.x;
+    const int ja = rba / 16, jb = rbb / 16;  // 16-byte chunks per panel row
+    const int per_pair = npa * ja + npb * jb;
+    uint32_t g = 0;
+    for (int si = sb; si < se; ++si) {
+      const int4 sg = p.segs[si];
+      for (int b0 = sg.y; b0 < sg.z; b0 += PS) {
+        const uint32_t s = g % S, ph = (g / S) & 1;
+        mbar_wait(empty + s, ph ^ 1);
+        uint8_t* stage = smem + (size_t)s * p.stage_bytes;
+        const uint32_t a_s = smem_u32(stage), b_s = a_s + p.a_bytes;
+        for (int idx = t; idx < PS * per_pair; idx += kProdWarps * 32) {
+          const int pr = idx / per_pair, rem = idx % per_pair;
+          const int pi = b0 + pr;
+          const bool ok = pi < sg.z;
+          if (rem < npa * ja) {  // G row chunk -> A panel
+            const int pa = rem / ja, j = rem % ja;
+            const __nv_bfloat16* src = ok ? p.g + (int64_t)__ldg(p.out_idx + pi) * p.c_out + pa * p.pwa + j * 8 : p.g;
+            cp_async16(a_s + pa * panel_a + swz(pr, j, rba), src, ok ? 16u : 0u);
+          } else {  // X row chunk -> B panel
+            const int r2 = rem - npa * ja;
+            const int pb = r2 / jb, j = r2 % jb;
+            const __nv_bfloat16* src = ok ? p.x + (int64_t)__ldg(p.in_idx + pi) * p.c_in + pb * p.pwb + j * 8 : p.x;
+            cp_async16(b_s + pb * panel_b + swz(pr, j, rbb), src, ok ? 16u : 0u);
+          }
+        }
+        cp_async_arrive_noinc(full + s);
+        ++g;
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (warp == kMmaWarp) {
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16(kTileM, p.c_in, 1, 1);
+      const uint32_t la = layout_code(rba), lb = layout_code(rbb);
+      uint32_t g = 0, n_seg = 0;
+      for (int si = sb; si < se; ++si, ++n_seg) {
+        const int4 sg = p.segs[si];
+        mbar_wait(tempty, (n_seg & 1) ^ 1);
+        tc_fence_after();
+        uint32_t acc = 0;
+        for (int b0 = sg.y; b0 < sg.z; b0 += PS) {
+          const uint32_t s = g % S, ph = (g / S) & 1;
+          mbar_wait(full + s, ph);
+          tc_fence_after();
+          fence_proxy_async_smem();
+          const uint32_t a_s = smem_u32(smem + (size_t)s * p.stage_bytes), b_s = a_s + p.a_bytes;
+#pragma unroll
+          for (int kk = 0; kk < PS / 16; ++kk) {
+            const uint64_t bd = smem_desc(b_s + kk * 16 * rbb, panel_b, 8 * rbb, lb);
+            for (int h = 0; h < p.halves; ++h) {
+              const uint32_t a_half = a_s + h * (128 / p.pwa) * panel_a;
+              const uint64_t ad = smem_desc(a_half + kk * 16 * rba, panel_a, 8 * rba, la);
+              umma_f16(tbase + h * (uint32_t)p.c_in, ad, bd, idesc, acc);
+            }
+            acc = 1;
+          }
+          umma_commit(empty + s);
+          ++g;
+        }
+        umma_commit(tfull);
+      }
+    }
+    __syncwarp();
+  } else {
+    const int q = warp & 3;
+    uint32_t n_seg = 0;
+    for (int si = sb; si < se; ++si, ++n_seg) {
+      const int4 sg = p.segs[si];
+      mbar_wait(tfull, n_seg & 1);
+      tc_fence_after();
+      for (int h = 0; h < p.halves; ++h) {
+        const int co = h * 128 + q * 32 + lane;
+        float* dst = p.part + ((int64_t)sg.w * p.c_out + co) * p.c_in;
+        const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + h * (uint32_t)p.c_in;
+        for (int col0 = 0; col0 < p.c_in; col0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(ta + col0, v);
+          tmem_ld_wait();
+          if (co < p.c_out) {
+            float4* d4 = (float4*)(dst + col0);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              d4[e] = make_float4(__uint_as_float(v[4 * e]), __uint_as_float(v[4 * e + 1]),
+                                  __uint_as_float(v[4 * e + 2]), __uint_as_float(v[4 * e + 3]));
+          }
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(tempty);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == kMmaWarp) tmem_dealloc(tbase, p.tmem_cols);
+}
+
+uint32_t pow2_cols(uint32_t c) {
+  uint32_t r = 32;
+  while (r < c) r <<= 1;
+  return r;
+}
+
+template <class F>
+void set_smem_once(F* f, int bytes) {
+  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+
+}  // namespace
+
+mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, int c_x, const void* W, int c_in_w,
+                            int c_out_w, void* y, int c_y, mk_dtype out_dt, int64_t n_rows, bool trans,
+                            cudaStream_t s) {
+  if (n_rows == 0) return MK_OK;
+  const int CH = c_x % 64 == 0 ? 64 : c_x % 32 == 0 ? 32 : 16;
+  const int nch = c_x / CH;
+  FwdParams p;
+  p.x = (const __nv_bfloat16*)x;
+  p.y = y;
+  p.nb = nb;
+  p.n_rows = n_rows;
+  p.ntiles = ceil_div(n_rows, kTileM);
+  p.c_x = c_x;
+  p.c_y = c_y;
+  p.nch = nch;
+  p.out_f32 = out_dt == MK_F32;
+  p.a_bytes = kTileM * CH * 2;
+  p.b_bytes = (uint32_t)c_y * CH * 2;
+  p.stage_bytes = (p.a_bytes + p.b_bytes + 1023) & ~1023u;
+  const int reserve = 1024 + 256;
+  p.stages = std::min<int>(8, (kMaxSmem - reserve) / (int)p.stage_bytes);
+  if (p.stages < 2) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: channel counts too large for the smem pipeline");
+  p.tmem_cols = pow2_cols(2 * c_y);
+  if (p.tmem_cols > 512) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: C_out above 256");
+  const size_t wbytes = (size_t)nb.K * nch * p.b_bytes;
+  uint8_t* wpack = (uint8_t*)dev_alloc(ctx->alloc, wbytes, s);
+  if (!wpack) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 conv: weight pack allocation failed");
+  {
+    const int64_t chunks = (int64_t)nb.K * nch * c_y * (CH / 8);
+    const int grid = (int)std::min<int64_t>(ceil_div(chunks, 256), 4 * ctx->num_sms);
+    k_pack_w<<<grid, 256, 0, s>>>((const __nv_bfloat16*)W, nb.K, c_out_w, c_in_w, trans ? 1 : 0, CH, wpack);
+    g_launches++;
+  }
+  p.wpack = wpack;
+  const int smem = p.stages * (int)p.stage_bytes + reserve;
+  const int grid = (int)std::min<int64_t>(p.ntiles, ctx->num_sms);
+  if (CH == 64) {
+    set_smem_once(k_conv_umma<64>, smem);
+    k_conv_umma<64><<<grid, kThreads, smem, s>>>(p);
+  } else if (CH == 32) {
+    set_smem_once(k_conv_umma<32>, smem);
+    k_conv_umma<32><<<grid, kThreads, smem, s>>>(p);
+  } else {
+    set_smem_once(k_conv_umma<16>, smem);
+    k_conv_umma<16><<<grid, kThreads, smem, s>>>(p);
+  }
+  g_launches++;
+  cudaError_t e = cudaGetLastError();
+  dev_free(ctx->alloc, wpack, s);
+  if (e != cudaSuccess) MK_FAIL(MK_ERR_CUDA, std::string("bf16 conv launch: ") + cudaGetErrorString(e));
+  return MK_OK;
+}
+
+mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, int c_out, const void* x, int c_in,
+                            float* dW, cudaStream_t s) {
+  const int64_t te = (int64_t)c_out * c_in;
+  WgradParams p;
+  p.g = (const __nv_bfloat16*)g;
+  p.x = (const __nv_bfloat16*)x;
+  p.in_idx = m->in_idx;
+  p.out_idx = m->out_idx;
+  p.segs = m->wseg;
+  p.seg_begin = m->wseg_begin;
+  p.c_out = c_out;
+  p.c_in = c_in;
+  p.pwa = c_out % 64 == 0 ? 64 : c_out % 32 == 0 ? 32 : 16;
+  p.pwb = c_in % 64 == 0 ? 64 : c_in % 32 == 0 ? 32 : 16;
+  p.halves = c_out > 128 ? 2 : 1;
+  if (c_out > 256) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: C_out above 256");
+  p.a_bytes = (uint32_t)(p.halves * 128) * kPairsPerStage * 2;  // M padded to 128 per half
+  p.b_bytes = (uint32_t)c_in * kPairsPerStage * 2;
+  p.stage_bytes = (p.a_bytes + p.b_bytes + 1023) & ~1023u;
+  const int reserve = 1024 + 256;
+  p.stages = std::min<int>(6, (kMaxSmem - reserve) / (int)p.stage_bytes);
+  p.tmem_cols = pow2_cols((uint32_t)(p.halves * c_in));
+  if (p.stages < 2 || p.tmem_cols > 512) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: channel counts too large");
+  float* part = nullptr;
+  if (m->n_wslots > 0) {
+    part = (float*)dev_alloc(ctx->alloc, sizeof(float) * m->n_wslots * te, s);
+    if (!part) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 wgrad: workspace allocation failed");
+    p.part = part;
+    const int smem = p.stages * (int)p.stage_bytes + reserve;
+    set_smem_once(k_wgrad_umma, smem);
+    k_wgrad_umma<<<m->n_wcta, kThreads, smem, s>>>(p);
+    g_launches++;
+  }
+  dim3 rg((unsigned)ceil_div(te, 256), (unsigned)m->K);
+  k_reduce_partials<<<rg, 256, 0, s>>>(m->wslot_begin, part, te, dW);
+  g_launches++;
+  cudaError_t e = cudaGetLastError();
+  if (part) dev_free(ctx->alloc, part, s);
+  if (e != cudaSuccess) MK_FAIL(MK_ERR_CUDA, std::string("bf16 wgrad launch: ") + cudaGetErrorString(e));
+  return MK_OK;
+}
+
 }  // namespace mk

@@ -278,6 +278,38 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: device allocation failed");
   }
   ck(cudaMemcpyAsync(m->ptr, m->h_ptr.data(), sizeof(int64_t) * (K + 1), cudaMemcpyHostToDevice, s));
+  {  // weight-gradient split-K plan (deterministic: depends only on the map and the SM count)
+    std::vector<int4> segs;
+    std::vector<int32_t> seg_begin, slot_begin(K + 1, 0);
+    const int64_t P = m->n_pairs;
+    int64_t L = std::max<int64_t>(64, ceil_div(ceil_div(std::max<int64_t>(P, 1), ctx->num_sms), 64) * 64);
+    const int64_t ncta = P > 0 ? ceil_div(P, L) : 0;
+    for (int64_t c = 0; c < ncta; ++c) {
+      seg_begin.push_back((int32_t)segs.size());
+      const int64_t cb = c * L, ce = std::min(P, cb + L);
+      for (int k = 0; k < K; ++k) {
+        const int64_t b = std::max(cb, m->h_ptr[k]), e2 = std::min(ce, m->h_ptr[k + 1]);
+        if (b < e2) segs.push_back(make_int4(k, (int)b, (int)e2, (int)segs.size()));
+      }
+    }
+    seg_begin.push_back((int32_t)segs.size());
+    for (int k = 0, i = 0; k <= K; ++k) {
+      while (i < (int)segs.size() && segs[i].x < k) ++i;
+      slot_begin[k] = i;
+    }
+    m->n_wcta = (int32_t)ncta;
+    m->n_wslots = (int64_t)segs.size();
+    m->wseg = (int4*)alloc(sizeof(int4) * std::max<size_t>(1, segs.size()));
+    m->wseg_begin = (int32_t*)alloc(sizeof(int32_t) * seg_begin.size());
+    m->wslot_begin = (int32_t*)alloc(sizeof(int32_t) * (K + 1));
+    if (!m->wseg || !m->wseg_begin || !m->wslot_begin) {
+      dev_free(m->alloc, scratch, s);
+      return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: device allocation failed");
+    }
+    if (!segs.empty()) ck(cudaMemcpyAsync(m->wseg, segs.data(), sizeof(int4) * segs.size(), cudaMemcpyHostToDevice, s));
+    ck(cudaMemcpyAsync(m->wseg_begin, seg_begin.data(), sizeof(int32_t) * seg_begin.size(), cudaMemcpyHostToDevice, s));
+    ck(cudaMemcpyAsync(m->wslot_begin, slot_begin.data(), sizeof(int32_t) * (K + 1), cudaMemcpyHostToDevice, s));
+  }
   if (n_out > 0) {
     k_emit<<<(unsigned)ntiles, kThreads, sizeof(int32_t) * K * 4, s>>>(m->nbr, n_out, K, m->ptr, tile_off, ntiles,
                                                                         m->in_idx, m->out_idx, m->nbrT, n_in,

@@ -169,6 +169,15 @@ struct mk_kmap {
   uint32_t* tile_mask = nullptr;    // [ceil(n_out/128)][mw]  forward tiles
   uint32_t* tile_maskT = nullptr;   // [ceil(n_in/128)][mw]   dgrad tiles
   int32_t mask_words = 1;
+  // Split-K plan of the weight gradient (tensor-core path): the concatenated pair list is
+  // cut into n_wcta contiguous ranges; wseg = (k, begin, end, slot) for every non-empty
+  // (range, offset) intersection, grouped by range (wseg_begin[n_wcta+1]); slots are in
+  // offset order, wslot_begin[k] = first slot of offset k ([K+1]).
+  int4* wseg = nullptr;
+  int32_t* wseg_begin = nullptr;
+  int32_t* wslot_begin = nullptr;
+  int64_t n_wslots = 0;
+  int32_t n_wcta = 0;
   std::vector<void*> owned;
 };
 
