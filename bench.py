@@ -1,0 +1,362 @@
+"""bench.py — measures the generalized sparse convolution hot path (arXiv 1904.08755) on B200.
+
+One step = one pass of every §8(a) row of SURVEY.md over one ScanNet-shaped scan
+(BASELINE.json configs[1]): quantize ~1M float points at 2 cm into a coordinate hash table
+(a1, a2), build the 3x3x3 kernel map (a4, a5), then conv forward, input gradient and weight
+gradient at C = 64 -> 64 in bf16 on the tcgen05 tensor cores (a6-a8).  Inputs are resident
+in HBM when the timed region starts; L2 is flushed (256 MiB write, untimed) before every
+timed step; each step is timed with CUDA events on the launching stream.
+
+Usage:  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl mk|reference]
+Under torchrun (N > 1) every rank runs its own scan (weak scaling, batch-index sharding,
+SURVEY §8(e)); the only collective is the NCCL all-reduce of dW (data-parallel gradient sum).
+`--impl reference` times the CPU oracle (oracle/, the only other place bench.py runs it).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = json.loads((ROOT / "BASELINE.json").read_text())["metric"]
+UNIT = "TFLOP/s"
+C_IN = C_OUT = 64
+K_OFF = 27
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="mk", choices=["mk", "reference"])
+    ap.add_argument("--seed", type=int, default=2000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained"), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "source": "fallback"}
+
+
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append((time.time(), parts))
+
+    def stop(self, t0, t1):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.12)
+        self.proc.terminate()
+        rows = [r for (t, r) in self.rows if t0 - 0.06 <= t <= t1 + 0.06] or [r for (_, r) in self.rows[-3:]]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[2 + i].lower() == "active"})
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def workload(seed):
+    import synthetic
+    pts = synthetic.room_points(seed)
+    return pts
+
+
+# ---------------------------------------------------------------------------- GPU arm
+def run_mk(args, ws, rank, local):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1904_08755_b200 as mk
+    import synthetic
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    stream = torch.cuda.current_stream()
+    region = mk.Region(mk.HYPERCUBE, 3, 3)
+
+    # ---- synthetic inputs (each rank its own scan: weak scaling by batch-index sharding)
+    pts_h = workload(args.seed + rank)
+    pts = torch.from_numpy(pts_h).to(dev)
+    c0, _, _ = mk.coords_quantize(pts, synthetic.ROOM_VOXEL)
+    N = c0.n
+    m0 = mk.kmap_build(c0, c0, region)
+    M = m0.n_pairs
+    del m0, c0
+    X = torch.from_numpy(synthetic.features(1, N, C_IN)).to(dev).to(torch.bfloat16)
+    W = torch.from_numpy(synthetic.weights(2, K_OFF, C_OUT, C_IN)).to(dev).to(torch.bfloat16)
+    G = torch.from_numpy(synthetic.features(3, N, C_OUT)).to(dev).to(torch.bfloat16)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+    flops_pass = 2.0 * C_IN * C_OUT * M  # one of fwd / dgrad / wgrad
+    flops_step = 3.0 * flops_pass
+
+    def step(ev=None):
+        def mark(i):
+            if ev is not None:
+                ev[i].record(stream)
+        mark(0)
+        c, _, _ = mk.coords_quantize(pts, synthetic.ROOM_VOXEL, return_maps=True)  # a1, a2
+        mark(1)
+        m = mk.kmap_build(c, c, region)                                             # a4, a5
+        mark(2)
+        y = mk.conv_forward(m, X, W)                                                # a6
+        mark(3)
+        gin, _ = mk.conv_backward(m, G, X, W, need_gin=True, need_gw=False)          # a7
+        mark(4)
+        _, gw = mk.conv_backward(m, G, X, W, need_gin=False, need_gw=True)           # a8
+        mark(5)
+        if ws > 1:
+            dist.all_reduce(gw)  # data-parallel weight-gradient sum over NVLink (NCCL)
+        mark(6)
+        return y, gin, gw
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+
+    n_ev = 7
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    launches0 = mk.kernel_launch_count()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.time()
+    for i in range(args.steps):
+        flush.zero_()  # L2 flush (untimed: outside the step's events)
+        step(evs[i])
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    t1 = time.time()
+    launches = mk.kernel_launch_count() - launches0
+    clocks = sampler.stop(t0, t1)
+
+    ph = np.array([[evs[i][j].elapsed_time(evs[i][j + 1]) for j in range(n_ev - 1)] for i in range(args.steps)])
+    step_ms = ph.sum(axis=1)
+    total_ms = float(step_ms.sum())
+    if ws > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = ws * flops_step / (ms_per_step * 1e-3) / 1e12
+    mean_ph = ph.mean(axis=0)
+    names = ["quantize", "kmap", "conv_fwd", "conv_dgrad", "conv_wgrad", "allreduce_dW"]
+    phases = {n: round(float(v) * 1e3, 2) for n, v in zip(names, mean_ph)}  # microseconds
+
+    # ---- end to end through the public API with host buffers (pinned), per step:
+    #      H2D of points, features, grad, weights; D2H of y, grad_in, dW
+    pts_p = torch.from_numpy(pts_h).pin_memory()
+    X_p, W_p, G_p = X.cpu().pin_memory(), W.cpu().pin_memory(), G.cpu().pin_memory()
+    y_p = torch.empty((N, C_OUT), dtype=torch.bfloat16).pin_memory()
+    gi_p = torch.empty((N, C_IN), dtype=torch.bfloat16).pin_memory()
+    gw_p = torch.empty((K_OFF, C_OUT, C_IN), dtype=torch.float32).pin_memory()
+    h2d = pts_p.numel() * 4 + (X_p.numel() + W_p.numel() + G_p.numel()) * 2
+    d2h = (y_p.numel() + gi_p.numel()) * 2 + gw_p.numel() * 4
+
+    def e2e_step():
+        p = pts_p.to(dev, non_blocking=True)
+        x, w, g = (t.to(dev, non_blocking=True) for t in (X_p, W_p, G_p))
+        c, _, _ = mk.coords_quantize(p, synthetic.ROOM_VOXEL)
+        m = mk.kmap_build(c, c, region)
+        y = mk.conv_forward(m, x, w)
+        gin, gw = mk.conv_backward(m, g, x, w)
+        if ws > 1:
+            dist.all_reduce(gw)
+        y_p.copy_(y, non_blocking=True)
+        gi_p.copy_(gin, non_blocking=True)
+        gw_p.copy_(gw, non_blocking=True)
+
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        e_ev[i][0].record(stream)
+        e2e_step()
+        e_ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = float(sum(a.elapsed_time(b) for a, b in e_ev))
+    if ws > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = ws * flops_step / (e2e_ms / args.steps * 1e-3) / 1e12
+
+    # ---- roofline of the dominant kernel (largest phase among the conv kernels / map build)
+    pk = peaks()
+    conv_ph = {"conv_fwd": mean_ph[2], "conv_dgrad": mean_ph[3], "conv_wgrad": mean_ph[4]}
+    dom = max(conv_ph, key=conv_ph.get)
+    dom_ms = float(conv_ph[dom])
+    bytes_alg = N * C_IN * 2 + N * C_OUT * 2 + 8 * M + K_OFF * C_IN * C_OUT * 2
+    ai = flops_pass / bytes_alg
+    ridge = pk["bf16_tflops"] * 1e12 / (pk["hbm_gbs"] * 1e9)
+    traffic = None
+    summ = ROOT / "profiles" / "ncu_summary.json"
+    if summ.exists():
+        try:
+            traffic = json.loads(summ.read_text()).get("dram_bytes_per_launch", {}).get(dom)
+        except (ValueError, AttributeError):
+            traffic = None
+    if ai >= ridge:
+        achieved = flops_pass / (dom_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": pk["bf16_tflops"], "unit": "TFLOP/s"}
+    else:
+        achieved = bytes_alg / (dom_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s"}
+    roof.update({"frac": round(roof["achieved"] / roof["peak"], 4), "traffic": traffic, "kernel": dom,
+                 "kernel_us": round(dom_ms * 1e3, 2), "algorithmic_flops": flops_pass,
+                 "algorithmic_bytes": bytes_alg, "arith_intensity": round(ai, 1), "peak_source": pk["source"]})
+
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": "configs[1]: ScanNet-shaped room, 2 cm voxels, 3x3x3 hypercube, C 64->64, "
+                               "quantize + hash + kernel map + fwd + dgrad + wgrad",
+                   "voxels_per_gpu": N, "pairs_per_gpu": M, "points_per_gpu": int(pts_h.shape[0]),
+                   "seed": args.seed, "parallelism": f"batch-index dp{ws}",
+                   "l2": "flushed before every timed step (256 MiB write, outside the step events)"},
+        "phases_us": phases,
+        "conv_tflops": round(flops_step / ((mean_ph[2] + mean_ph[3] + mean_ph[4]) * 1e-3) / 1e12, 3),
+        "kmap_mpts": round(N / (mean_ph[1] * 1e-3) / 1e6, 2),
+        "quantize_mpts": round(pts_h.shape[0] / (mean_ph[0] * 1e-3) / 1e6, 2),
+        "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_ms / args.steps, 4)},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "clocks": clocks,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(pts_h, args.cpu_seconds)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------- CPU oracle
+def oracle_sample(pts_h, budget_s):
+    """The oracle, as it stands (single thread), on a bounded sample of the configs[1] step:
+    quantize + kernel map on the full scan, then fwd + dgrad + wgrad on the pairs of the
+    first k offsets, k grown until the budget is used.  Returns (flops, seconds, sample)."""
+    import oracle
+    import synthetic
+    t0 = time.perf_counter()
+    coords, _, _ = oracle.quantize(pts_h, synthetic.ROOM_VOXEL)
+    offs = oracle.region(0, 3, [3, 3, 3])
+    ptr, ins, outs = oracle.kmap(coords, coords, offs)
+    t_map = time.perf_counter() - t0
+    N = coords.shape[0]
+    X = synthetic.features(1, N, C_IN).astype(np.float64)
+    W = synthetic.weights(2, K_OFF, C_OUT, C_IN).astype(np.float64)
+    G = synthetic.features(3, N, C_OUT).astype(np.float64)
+    flops, t_conv, k = 0.0, 0.0, 0
+    while k < K_OFF and t_map + t_conv < budget_s:
+        sub = (np.array([0, ptr[k + 1] - ptr[k]], np.int64), ins[ptr[k]:ptr[k + 1]], outs[ptr[k]:ptr[k + 1]])
+        t1 = time.perf_counter()
+        oracle.conv_forward(sub, X, W[k:k + 1], N)
+        oracle.conv_dgrad(sub, G, W[k:k + 1], N)
+        oracle.conv_wgrad(sub, G, X, 1)
+        t_conv += time.perf_counter() - t1
+        flops += 3 * 2.0 * C_IN * C_OUT * (ptr[k + 1] - ptr[k])
+        k += 1
+    sample = (f"configs[1] room ({pts_h.shape[0]} points, {N} voxels): oracle quantize + kernel map on the full "
+              f"scan, fwd+dgrad+wgrad fp64 on the pairs of offsets 0..{k - 1} of 27")
+    return flops, t_map + t_conv, sample
+
+
+def cpu_baseline(pts_h, budget_s):
+    flops, secs, sample = oracle_sample(pts_h, budget_s)
+    return {"value": round(flops / secs / 1e12, 6), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample,
+            "seconds": round(secs, 2), "host_cpus": os.cpu_count()}
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    pts_h = workload(args.seed)
+    budget = max(2.0, min(args.cpu_seconds, 20.0))
+    for _ in range(min(args.warmup, 1)):
+        oracle_sample(pts_h, 1.0)
+    flops, secs = 0.0, 0.0
+    sample = ""
+    for _ in range(args.steps):
+        f, s, sample = oracle_sample(pts_h, budget / max(args.steps, 1))
+        flops += f
+        secs += s
+    v = flops / secs / 1e12
+    out = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": UNIT, "n_gpus": ws,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(secs / args.steps * 1e3, 3),
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "configs[1] (bounded sample per step, see cpu_baseline.sample)"},
+           "cpu_baseline": {"value": round(v, 6), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+           "e2e": {"value": round(v, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+    run_mk(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -22,7 +22,7 @@ NbrView forward_view(const mk_kmap* m) {
   NbrView v;
   v.tab = m->nbr;
   v.mask = m->tile_mask;
-  v.n = m->n_out;
+  v.n = m->nbr_stride;
   v.K = m->K;
   v.mw = m->mask_words;
   return v;
@@ -32,14 +32,13 @@ NbrView dgrad_view(const mk_kmap* m) {
   NbrView v;
   v.K = m->K;
   v.mw = m->mask_words;
-  v.n = m->n_in;
+  v.n = m->nbrT_stride;
+  v.mask = m->tile_maskT;
   if (m->nbrT) {
     v.tab = m->nbrT;
-    v.mask = m->tile_maskT;
   } else {  // symmetric submanifold map: nbrT[k] = nbr[mirror[k]]
     v.tab = m->nbr;
     v.mirror = m->d_mirror;
-    v.mask = m->tile_mask;
   }
   return v;
 }

@@ -82,14 +82,54 @@ struct FwdParams {
 };
 
 __device__ __forceinline__ int tile_active_count(const NbrView& nb, int64_t tile) {
-  if (!nb.mirror) {
-    int n = 0;
-    for (int w = 0; w < nb.mw; ++w) n += __popc(__ldg(nb.mask + tile * nb.mw + w));
-    return n;
-  }
   int n = 0;
-  for (int k = 0; k < nb.K; ++k) n += nb.active(tile, k);
+  for (int w = 0; w < nb.mw; ++w) n += __popc(__ldg(nb.mask + tile * nb.mw + w));
   return n;
+}
+
+__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// Enumerates the (tile, mask word) units of a CTA in processing order: tiles blockIdx.x,
+// blockIdx.x + gridDim.x, ...; inside a tile the words with at least one active offset.
+struct UnitIter {
+  const uint32_t* mask;
+  int64_t ntiles;
+  int mw;
+  int64_t tile;
+  int w;
+  uint32_t bits;
+  __device__ UnitIter(const NbrView& nb, int64_t ntiles_) : mask(nb.mask), ntiles(ntiles_), mw(nb.mw) {
+    tile = blockIdx.x;
+    w = -1;
+    bits = 0;
+  }
+  __device__ __forceinline__ bool next() {
+    while (true) {
+      if (++w >= mw) {
+        w = 0;
+        tile += gridDim.x;
+      }
+      if (tile >= ntiles) return false;
+      bits = __ldg(mask + tile * mw + w);
+      if (bits) return true;
+    }
+  }
+};
+
+constexpr int kNbrBuf = 32 * kTileM;  // int32 entries per staging buffer (32 offsets x 128 rows)
+
+// Bulk-copies (TMA engine) the neighbour indices of unit `u` — 128 rows per active offset,
+// one 512-byte row segment each — into a staging buffer; completion on `bar`.
+__device__ __forceinline__ void stage_nbr(const NbrView& nb, const UnitIter& u, int32_t* buf, uint64_t* bar) {
+  mbar_arrive_expect_tx(bar, (uint32_t)__popc(u.bits) * kTileM * 4);
+  uint32_t bits = u.bits;
+  for (int j = 0; bits; ++j) {
+    const int k = u.w * 32 + __ffs(bits) - 1;
+    bits &= bits - 1;
+    bulk_g2s(buf + j * kTileM, nb.tab + (int64_t)nb.kk(k) * nb.n + u.tile * kTileM, kTileM * 4, bar);
+  }
 }
 
 template <int CH>
@@ -99,11 +139,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const int S = p.stages;
-  uint64_t* full = (uint64_t*)(smem + (size_t)S * p.stage_bytes);
+  int32_t* nbr_s = (int32_t*)(smem + (size_t)S * p.stage_bytes);  // [2][32][128]
+  uint64_t* full = (uint64_t*)(nbr_s + 2 * kNbrBuf);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+  uint64_t* nfull = tempty + 2;
+  uint32_t* tmem_slot = (uint32_t*)(nfull + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
@@ -114,6 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
     for (int b = 0; b < 2; ++b) {
       mbar_init(tfull + b, 1);
       mbar_init(tempty + b, kEpiWarps * 32);
+      mbar_init(nfull + b, 1);
     }
     fence_mbar_init();
   }
@@ -122,44 +165,55 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const int K = p.nb.K;
 
   if (warp < kProdWarps) {
     // ---------------------------------------------------------------- producers
     const int t = threadIdx.x;
-    uint32_t g = 0;
-    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-      const int64_t row0 = tile * kTileM;
-      for (int k = 0; k < K; ++k) {
-        if (!p.nb.active(tile, k)) continue;
+    UnitIter cur(p.nb, p.ntiles), st(p.nb, p.ntiles);
+    if (t == 0)
+      for (int b = 0; b < 2; ++b)
+        if (st.next()) stage_nbr(p.nb, st, nbr_s + b * kNbrBuf, nfull + b);
+    uint32_t s = 0, ph = 0, ub = 0, nph = 0;
+    while (cur.next()) {
+      mbar_wait(nfull + ub, (nph >> ub) & 1u);
+      nph ^= 1u << ub;
+      const int32_t* nb_u = nbr_s + ub * kNbrBuf;
+      uint32_t bits = cur.bits;
+      for (int j = 0; bits; ++j) {
+        const int k = cur.w * 32 + __ffs(bits) - 1;
+        bits &= bits - 1;
         int32_t src[J];
 #pragma unroll
-        for (int i = 0; i < J; ++i) {
-          const int r = (i * 128 + t) / J;
-          const int64_t row = row0 + r;
-          src[i] = row < p.n_rows ? p.nb.at(k, row) : -1;
-        }
+        for (int i = 0; i < J; ++i) src[i] = nb_u[j * kTileM + (i * 128 + t) / J];
         for (int c = 0; c < p.nch; ++c) {
-          const uint32_t s = g % S, ph = (g / S) & 1;
           mbar_wait(empty + s, ph ^ 1);
           uint8_t* stage = smem + (size_t)s * p.stage_bytes;
           const uint32_t a_s = smem_u32(stage);
 #pragma unroll
           for (int i = 0; i < J; ++i) {
             const int idx = i * 128 + t;
-            const int r = idx / J, j = idx % J;
+            const int r = idx / J, jj = idx % J;
             const bool ok = src[i] >= 0;
-            const __nv_bfloat16* gp = ok ? p.x + (int64_t)src[i] * p.c_x + c * CH + j * 8 : p.x;
-            cp_async16(a_s + swz(r, j, RB), gp, ok ? 16u : 0u);
+            const __nv_bfloat16* gp = ok ? p.x + (int64_t)src[i] * p.c_x + c * CH + jj * 8 : p.x;
+            cp_async16(a_s + swz(r, jj, RB), gp, ok ? 16u : 0u);
           }
           if (t == 0) {
             mbar_arrive_expect_tx(full + s, p.b_bytes);
             bulk_g2s(stage + p.a_bytes, p.wpack + ((int64_t)k * p.nch + c) * p.b_bytes, p.b_bytes, full + s);
           }
           cp_async_arrive_noinc(full + s);
-          ++g;
+          if (++s == (uint32_t)S) {
+            s = 0;
+            ph ^= 1;
+          }
         }
       }
+      named_bar_sync(1, kProdWarps * 32);  // every producer is done reading buffer ub
+      if (t == 0 && st.next()) {
+        fence_proxy_async_smem();
+        stage_nbr(p.nb, st, nbr_s + ub * kNbrBuf, nfull + ub);
+      }
+      ub ^= 1;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp == kMmaWarp) {
@@ -167,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16(kTileM, p.c_y, 0, 0);
       const uint32_t lay = layout_code(RB);
-      uint32_t g = 0, tl = 0;
+      uint32_t s = 0, ph = 0, tl = 0;
       for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
         if (tile_active_count(p.nb, tile) == 0) continue;
         const uint32_t b = tl & 1, tph = (tl >> 1) & 1;
@@ -175,10 +229,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
         tc_fence_after();
         const uint32_t d = tbase + b * (uint32_t)p.c_y;
         uint32_t acc = 0;
-        for (int k = 0; k < K; ++k) {
-          if (!p.nb.active(tile, k)) continue;
-          for (int c = 0; c < p.nch; ++c) {
-            const uint32_t s = g % S, ph = (g / S) & 1;
+        for (int w = 0; w < p.nb.mw; ++w) {
+          const int nk = __popc(__ldg(p.nb.mask + tile * p.nb.mw + w));
+          for (int q = 0; q < nk * p.nch; ++q) {
             mbar_wait(full + s, ph);
             tc_fence_after();
             fence_proxy_async_smem();
@@ -192,7 +245,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
               acc = 1;
             }
             umma_commit(empty + s);
-            ++g;
+            if (++s == (uint32_t)S) {
+              s = 0;
+              ph ^= 1;
+            }
           }
         }
         umma_commit(tfull + b);
@@ -273,17 +329,57 @@ struct WgradParams {
 };
 
 constexpr int kPairsPerStage = 64;
+constexpr int kUnitPairs = 1024;            // pairs per index-staging unit (16 stages)
+constexpr int kIdxBuf = kUnitPairs + 8;     // int32 entries per staged index array
+
+// Enumerates the index-staging units of a CTA: every segment (k, begin, end, slot) of the
+// CTA cut into runs of at most kUnitPairs pairs (multiples of the 64-pair stage).
+struct WUnitIter {
+  const int4* segs;
+  int si, se;
+  int4 sg;
+  int b, e;
+  __device__ WUnitIter(const int4* s, int sb, int se_) : segs(s), si(sb - 1), se(se_), b(0), e(0) { sg = make_int4(0, 0, 0, 0); }
+  __device__ __forceinline__ bool next() {
+    if (e < sg.z) {  // more of the current segment
+      b = e;
+      e = min(b + kUnitPairs, sg.z);
+      return true;
+    }
+    while (++si < se) {
+      sg = __ldg(segs + si);
+      if (sg.y < sg.z) {
+        b = sg.y;
+        e = min(b + kUnitPairs, sg.z);
+        return true;
+      }
+    }
+    return false;
+  }
+};
+
+// Bulk-copies out_idx / in_idx of the unit's pairs (16-byte aligned superset) into `buf`.
+__device__ __forceinline__ void stage_idx(const int32_t* out_idx, const int32_t* in_idx, const WUnitIter& u,
+                                          int32_t* buf, uint64_t* bar) {
+  const int b4 = u.b & ~3, e4 = (u.e + 3) & ~3;
+  const uint32_t bytes = (uint32_t)(e4 - b4) * 4;
+  mbar_arrive_expect_tx(bar, 2 * bytes);
+  bulk_g2s(buf, out_idx + b4, bytes, bar);
+  bulk_g2s(buf + kIdxBuf, in_idx + b4, bytes, bar);
+}
 
 __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constant__ WgradParams p) {
   constexpr int PS = kPairsPerStage;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   const int S = p.stages;
-  uint64_t* full = (uint64_t*)(smem + (size_t)S * p.stage_bytes);
+  int32_t* idx_s = (int32_t*)(smem + (size_t)S * p.stage_bytes);  // [2][out, in][kIdxBuf]
+  uint64_t* full = (uint64_t*)(idx_s + 4 * kIdxBuf);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;
   uint64_t* tempty = tfull + 1;
-  uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
+  uint64_t* nfull = tempty + 1;
+  uint32_t* tmem_slot = (uint32_t*)(nfull + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rba = p.pwa * 2, rbb = p.pwb * 2;              // panel row bytes
   const int npa = p.c_out / p.pwa, npb = p.c_in / p.pwb;   // real panels
@@ -296,6 +392,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, kEpiWarps * 32);
+    mbar_init(nfull, 1);
+    mbar_init(nfull + 1, 1);
     fence_mbar_init();
   }
   // zero the padding panels of A (M padded to 128 per half) once; never overwritten
@@ -319,46 +417,62 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
     const int t = threadIdx.x;
     const int ja = rba / 16, jb = rbb / 16;  // 16-byte chunks per panel row
     const int per_pair = npa * ja + npb * jb;
-    uint32_t g = 0;
-    for (int si = sb; si < se; ++si) {
-      const int4 sg = p.segs[si];
-      for (int b0 = sg.y; b0 < sg.z; b0 += PS) {
-        const uint32_t s = g % S, ph = (g / S) & 1;
+    WUnitIter cur(p.segs, sb, se), st(p.segs, sb, se);
+    if (t == 0)
+      for (int b = 0; b < 2; ++b)
+        if (st.next()) stage_idx(p.out_idx, p.in_idx, st, idx_s + b * 2 * kIdxBuf, nfull + b);
+    uint32_t s = 0, ph = 0, ub = 0, nph = 0;
+    while (cur.next()) {
+      mbar_wait(nfull + ub, (nph >> ub) & 1u);
+      nph ^= 1u << ub;
+      const int32_t* oi = idx_s + ub * 2 * kIdxBuf;
+      const int32_t* ii = oi + kIdxBuf;
+      const int b4 = cur.b & ~3;
+      for (int b0 = cur.b; b0 < cur.e; b0 += PS) {
         mbar_wait(empty + s, ph ^ 1);
         uint8_t* stage = smem + (size_t)s * p.stage_bytes;
         const uint32_t a_s = smem_u32(stage), b_s = a_s + p.a_bytes;
         for (int idx = t; idx < PS * per_pair; idx += kProdWarps * 32) {
           const int pr = idx / per_pair, rem = idx % per_pair;
           const int pi = b0 + pr;
-          const bool ok = pi < sg.z;
+          const bool ok = pi < cur.e;
           if (rem < npa * ja) {  // G row chunk -> A panel
             const int pa = rem / ja, j = rem % ja;
-            const __nv_bfloat16* src = ok ? p.g + (int64_t)__ldg(p.out_idx + pi) * p.c_out + pa * p.pwa + j * 8 : p.g;
+            const __nv_bfloat16* src = ok ? p.g + (int64_t)oi[pi - b4] * p.c_out + pa * p.pwa + j * 8 : p.g;
             cp_async16(a_s + pa * panel_a + swz(pr, j, rba), src, ok ? 16u : 0u);
           } else {  // X row chunk -> B panel
             const int r2 = rem - npa * ja;
             const int pb = r2 / jb, j = r2 % jb;
-            const __nv_bfloat16* src = ok ? p.x + (int64_t)__ldg(p.in_idx + pi) * p.c_in + pb * p.pwb + j * 8 : p.x;
+            const __nv_bfloat16* src = ok ? p.x + (int64_t)ii[pi - b4] * p.c_in + pb * p.pwb + j * 8 : p.x;
             cp_async16(b_s + pb * panel_b + swz(pr, j, rbb), src, ok ? 16u : 0u);
           }
         }
         cp_async_arrive_noinc(full + s);
-        ++g;
+        if (++s == (uint32_t)S) {
+          s = 0;
+          ph ^= 1;
+        }
       }
+      named_bar_sync(1, kProdWarps * 32);
+      if (t == 0 && st.next()) {
+        fence_proxy_async_smem();
+        stage_idx(p.out_idx, p.in_idx, st, idx_s + ub * 2 * kIdxBuf, nfull + ub);
+      }
+      ub ^= 1;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
   } else if (warp == kMmaWarp) {
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16(kTileM, p.c_in, 1, 1);
       const uint32_t la = layout_code(rba), lb = layout_code(rbb);
-      uint32_t g = 0, n_seg = 0;
-      for (int si = sb; si < se; ++si, ++n_seg) {
+      uint32_t s = 0, ph = 0, n_seg = 0;
+      for (int si = sb; si < se; ++si) {
         const int4 sg = p.segs[si];
+        if (sg.y >= sg.z) continue;
         mbar_wait(tempty, (n_seg & 1) ^ 1);
         tc_fence_after();
         uint32_t acc = 0;
         for (int b0 = sg.y; b0 < sg.z; b0 += PS) {
-          const uint32_t s = g % S, ph = (g / S) & 1;
           mbar_wait(full + s, ph);
           tc_fence_after();
           fence_proxy_async_smem();
@@ -374,17 +488,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
             acc = 1;
           }
           umma_commit(empty + s);
-          ++g;
+          if (++s == (uint32_t)S) {
+            s = 0;
+            ph ^= 1;
+          }
         }
         umma_commit(tfull);
+        ++n_seg;
       }
     }
     __syncwarp();
   } else {
     const int q = warp & 3;
     uint32_t n_seg = 0;
-    for (int si = sb; si < se; ++si, ++n_seg) {
+    for (int si = sb; si < se; ++si) {
       const int4 sg = p.segs[si];
+      if (sg.y >= sg.z) continue;
       mbar_wait(tfull, n_seg & 1);
       tc_fence_after();
       for (int h = 0; h < p.halves; ++h) {
@@ -406,6 +525,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
       }
       tc_fence_before();
       mbar_arrive(tempty);
+      ++n_seg;
     }
   }
   tc_fence_before();
@@ -446,7 +566,7 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   p.a_bytes = kTileM * CH * 2;
   p.b_bytes = (uint32_t)c_y * CH * 2;
   p.stage_bytes = (p.a_bytes + p.b_bytes + 1023) & ~1023u;
-  const int reserve = 1024 + 256;
+  const int reserve = 1024 + 256 + 2 * kNbrBuf * 4;
   p.stages = std::min<int>(8, (kMaxSmem - reserve) / (int)p.stage_bytes);
   if (p.stages < 2) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: channel counts too large for the smem pipeline");
   p.tmem_cols = pow2_cols(2 * c_y);
@@ -499,7 +619,7 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   p.a_bytes = (uint32_t)(p.halves * 128) * kPairsPerStage * 2;  // M padded to 128 per half
   p.b_bytes = (uint32_t)c_in * kPairsPerStage * 2;
   p.stage_bytes = (p.a_bytes + p.b_bytes + 1023) & ~1023u;
-  const int reserve = 1024 + 256;
+  const int reserve = 1024 + 256 + 4 * kIdxBuf * 4;
   p.stages = std::min<int>(6, (kMaxSmem - reserve) / (int)p.stage_bytes);
   p.tmem_cols = pow2_cols((uint32_t)(p.halves * c_in));
   if (p.stages < 2 || p.tmem_cols > 512) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: channel counts too large");

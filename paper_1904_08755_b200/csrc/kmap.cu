@@ -41,7 +41,7 @@ __device__ __forceinline__ bool shift_key(int4 u, int D, const int32_t* off, int
   return pack_key(c, D, key_batch(u, D), q);
 }
 
-__global__ void __launch_bounds__(kThreads) k_probe(const int4* __restrict__ okeys, int64_t n_out,
+__global__ void __launch_bounds__(kThreads) k_probe(const int4* __restrict__ okeys, int64_t n_out, int64_t n_pad,
                                                     const int4* __restrict__ tkeys, const int32_t* __restrict__ tvals,
                                                     uint32_t mask, const int32_t* __restrict__ offs, int K, int D,
                                                     int sign, int4 scale4, int32_t* __restrict__ nbr,
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(kThreads) k_probe(const int4* __restrict__ oke
     int32_t a = -1;
     int4 q;
     if (valid && shift_key(u, D, s_off + k * D, sign, scale, &q)) a = probe(tkeys, tvals, mask, q);
-    if (valid) nbr[(int64_t)k * n_out + o] = a;
+    nbr[(int64_t)k * n_pad + o] = a;  // rows padded to whole tiles (-1)
     const unsigned b = __ballot_sync(0xffffffffu, a >= 0);
     if ((threadIdx.x & 31) == 0 && b) atomicAdd(s_cnt + k, __popc(b));
   }
@@ -115,11 +115,11 @@ __global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ tile_
   if (threadIdx.x == 0) totals[k] = s_carry;
 }
 
-__global__ void __launch_bounds__(kThreads) k_emit(const int32_t* __restrict__ nbr, int64_t n_out, int K,
+__global__ void __launch_bounds__(kThreads) k_emit(const int32_t* __restrict__ nbr, int64_t n_out, int64_t n_pad, int K,
                                                    const int64_t* __restrict__ ptr, const int64_t* __restrict__ tile_off,
                                                    int64_t ntiles, int32_t* __restrict__ in_idx,
                                                    int32_t* __restrict__ out_idx, int32_t* __restrict__ nbrT,
-                                                   int64_t n_in, uint32_t* __restrict__ tile_maskT, int mw) {
+                                                   int64_t nT_pad, uint32_t* __restrict__ tile_maskT, int mw) {
   extern __shared__ int32_t s_wc[];  // [K][4] pairs per (offset, warp of the tile)
   const int64_t tile = blockIdx.x;
   const int r = threadIdx.x & (kTileRows - 1);
@@ -128,13 +128,13 @@ __global__ void __launch_bounds__(kThreads) k_emit(const int32_t* __restrict__ n
   const int lane = threadIdx.x & 31, wq = r >> 5;  // warp quarter of the 128-row tile
   const unsigned lt = (1u << lane) - 1u;
   for (int k = threadIdx.x / kTileRows; k < K; k += kThreads / kTileRows) {
-    const int32_t a = valid ? nbr[(int64_t)k * n_out + o] : -1;
+    const int32_t a = valid ? nbr[(int64_t)k * n_pad + o] : -1;
     const unsigned b = __ballot_sync(0xffffffffu, a >= 0);
     if (lane == 0) s_wc[k * 4 + wq] = __popc(b);
   }
   __syncthreads();
   for (int k = threadIdx.x / kTileRows; k < K; k += kThreads / kTileRows) {
-    const int32_t a = valid ? nbr[(int64_t)k * n_out + o] : -1;
+    const int32_t a = valid ? nbr[(int64_t)k * n_pad + o] : -1;
     const unsigned b = __ballot_sync(0xffffffffu, a >= 0);
     if (a < 0) continue;
     int64_t pos = ptr[k] + tile_off[(int64_t)k * ntiles + tile] + __popc(b & lt);
@@ -142,10 +142,24 @@ __global__ void __launch_bounds__(kThreads) k_emit(const int32_t* __restrict__ n
     in_idx[pos] = a;
     out_idx[pos] = (int32_t)o;
     if (nbrT) {
-      nbrT[(int64_t)k * n_in + a] = (int32_t)o;
+      nbrT[(int64_t)k * nT_pad + a] = (int32_t)o;
       atomicOr(tile_maskT + (int64_t)(a / kTileRows) * mw + (k >> 5), 1u << (k & 31));
     }
   }
+}
+
+// Dgrad tile masks of a symmetric map: bit k of tile t = bit mirror[k] of the forward mask.
+__global__ void k_mirror_mask(const uint32_t* __restrict__ mask, int64_t ntiles, int mw, const int32_t* __restrict__ mirror,
+                              int K, uint32_t* __restrict__ maskT) {
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x)
+    for (int w = 0; w < mw; ++w) {
+      uint32_t bits = 0;
+      for (int j = 0; j < 32 && w * 32 + j < K; ++j) {
+        const int q = mirror[w * 32 + j];
+        bits |= ((mask[t * mw + (q >> 5)] >> (q & 31)) & 1u) << j;
+      }
+      maskT[t * mw + w] = bits;
+    }
 }
 
 }  // namespace
@@ -201,6 +215,9 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   const int64_t n_out = out->n, n_in = in->n;
   const int64_t ntiles = std::max<int64_t>(1, ceil_div(n_out, kTileRows));
   const int64_t ntilesT = std::max<int64_t>(1, ceil_div(n_in, kTileRows));
+  const int64_t n_pad = ntiles * kTileRows, nT_pad = ntilesT * kTileRows;  // table rows padded to whole tiles
+  m->nbr_stride = n_pad;
+  m->nbrT_stride = symmetric ? n_pad : nT_pad;
 
   auto fail = [&](mk_status code, const std::string& msg) {
     mk_kmap_destroy(m);
@@ -217,16 +234,14 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   m->ptr = (int64_t*)alloc(sizeof(int64_t) * (K + 1));
   m->d_mirror = (int32_t*)alloc(sizeof(int32_t) * K);
   int32_t* d_offs = (int32_t*)alloc(sizeof(int32_t) * K * D);
-  m->nbr = (int32_t*)alloc(sizeof(int32_t) * std::max<int64_t>(1, (int64_t)K * n_out));
+  m->nbr = (int32_t*)alloc(sizeof(int32_t) * (int64_t)K * n_pad);
   m->tile_mask = (uint32_t*)alloc(sizeof(uint32_t) * ntiles * mw);
-  if (!symmetric) {
-    m->nbrT = (int32_t*)alloc(sizeof(int32_t) * std::max<int64_t>(1, (int64_t)K * n_in));
-    m->tile_maskT = (uint32_t*)alloc(sizeof(uint32_t) * ntilesT * mw);
-  }
+  m->tile_maskT = (uint32_t*)alloc(sizeof(uint32_t) * ntilesT * mw);
+  if (!symmetric) m->nbrT = (int32_t*)alloc(sizeof(int32_t) * (int64_t)K * nT_pad);
   // scratch: tile counts, tile offsets, totals
   void* scratch = dev_alloc(m->alloc, sizeof(int32_t) * K * ntiles + sizeof(int64_t) * K * ntiles + 256 +
                                           sizeof(int64_t) * K, s);
-  if (!m->ptr || !m->d_mirror || !d_offs || !m->nbr || !m->tile_mask || (!symmetric && (!m->nbrT || !m->tile_maskT)) ||
+  if (!m->ptr || !m->d_mirror || !d_offs || !m->nbr || !m->tile_mask || !m->tile_maskT || (!symmetric && !m->nbrT) ||
       !scratch) {
     if (scratch) dev_free(m->alloc, scratch, s);
     return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: device allocation failed");
@@ -242,18 +257,19 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   ck(cudaMemcpyAsync(d_offs, offs.data(), sizeof(int32_t) * K * D, cudaMemcpyHostToDevice, s));
   ck(cudaMemcpyAsync(m->d_mirror, m->mirror.data(), sizeof(int32_t) * K, cudaMemcpyHostToDevice, s));
   if (!symmetric) {
-    if (n_in > 0) ck(cudaMemsetAsync(m->nbrT, 0xFF, sizeof(int32_t) * K * n_in, s));
+    ck(cudaMemsetAsync(m->nbrT, 0xFF, sizeof(int32_t) * K * nT_pad, s));
     ck(cudaMemsetAsync(m->tile_maskT, 0, sizeof(uint32_t) * ntilesT * mw, s));
   }
   if (n_out > 0) {
     k_probe<<<(unsigned)ntiles, kThreads, sizeof(int32_t) * (K * D + K), s>>>(
-        out->keys, n_out, in->table.keys, in->table.vals, in->table.mask, d_offs, K, D, sign, scale4, m->nbr,
+        out->keys, n_out, n_pad, in->table.keys, in->table.vals, in->table.mask, d_offs, K, D, sign, scale4, m->nbr,
         tile_cnt, ntiles, m->tile_mask, mw);
     g_launches++;
     k_scan<<<K, 1024, 0, s>>>(tile_cnt, ntiles, tile_off, totals);
     g_launches++;
   } else {
     ck(cudaMemsetAsync(m->tile_mask, 0, sizeof(uint32_t) * ntiles * mw, s));
+    ck(cudaMemsetAsync(m->nbr, 0xFF, sizeof(int32_t) * K * n_pad, s));
     ck(cudaMemsetAsync(totals, 0, sizeof(int64_t) * K, s));
   }
   ck(cudaGetLastError());
@@ -271,8 +287,9 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     dev_free(m->alloc, scratch, s);
     return fail(MK_ERR_UNSUPPORTED, "mk_kmap_build: more than 2^31 pairs");
   }
-  m->in_idx = (int32_t*)alloc(sizeof(int32_t) * std::max<int64_t>(1, m->n_pairs));
-  m->out_idx = (int32_t*)alloc(sizeof(int32_t) * std::max<int64_t>(1, m->n_pairs));
+  // +4 entries of padding: the wgrad kernel bulk-copies 16-byte aligned supersets of ranges
+  m->in_idx = (int32_t*)alloc(sizeof(int32_t) * (m->n_pairs + 4));
+  m->out_idx = (int32_t*)alloc(sizeof(int32_t) * (m->n_pairs + 4));
   if (!m->in_idx || !m->out_idx) {
     dev_free(m->alloc, scratch, s);
     return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: device allocation failed");
@@ -311,9 +328,14 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     ck(cudaMemcpyAsync(m->wslot_begin, slot_begin.data(), sizeof(int32_t) * (K + 1), cudaMemcpyHostToDevice, s));
   }
   if (n_out > 0) {
-    k_emit<<<(unsigned)ntiles, kThreads, sizeof(int32_t) * K * 4, s>>>(m->nbr, n_out, K, m->ptr, tile_off, ntiles,
-                                                                        m->in_idx, m->out_idx, m->nbrT, n_in,
+    k_emit<<<(unsigned)ntiles, kThreads, sizeof(int32_t) * K * 4, s>>>(m->nbr, n_out, n_pad, K, m->ptr, tile_off,
+                                                                        ntiles, m->in_idx, m->out_idx, m->nbrT, nT_pad,
                                                                         m->tile_maskT, mw);
+    g_launches++;
+  }
+  if (symmetric) {
+    k_mirror_mask<<<(unsigned)std::min<int64_t>(ceil_div(ntiles, 256), 1024), 256, 0, s>>>(m->tile_mask, ntiles, mw,
+                                                                                          m->d_mirror, K, m->tile_maskT);
     g_launches++;
   }
   ck(cudaGetLastError());

@@ -163,11 +163,13 @@ struct mk_kmap {
   // and nbrT is not stored (nbrT == nullptr).
   int32_t* nbr = nullptr;
   int32_t* nbrT = nullptr;
+  int64_t nbr_stride = 0;   // rows of nbr, padded to a multiple of 128 (padding = -1)
+  int64_t nbrT_stride = 0;  // rows of the dgrad table (nbrT or, when symmetric, nbr)
   std::vector<int32_t> mirror;      // [K] index of -offset_k, or -1
   int32_t* d_mirror = nullptr;      // [K]
   // Per 128-row tile bitmasks of non-empty offsets (mask words = ceil(K/32)):
   uint32_t* tile_mask = nullptr;    // [ceil(n_out/128)][mw]  forward tiles
-  uint32_t* tile_maskT = nullptr;   // [ceil(n_in/128)][mw]   dgrad tiles
+  uint32_t* tile_maskT = nullptr;   // [ceil(n_in/128)][mw]   dgrad tiles (mirrored when symmetric)
   int32_t mask_words = 1;
   // Split-K plan of the weight gradient (tensor-core path): the concatenated pair list is
   // cut into n_wcta contiguous ranges; wseg = (k, begin, end, slot) for every non-empty
