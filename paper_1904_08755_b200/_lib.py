@@ -9,7 +9,10 @@ from __future__ import annotations
 import ctypes
 from pathlib import Path
 
-SO = Path(__file__).resolve().parent / "libmk.so"
+import os
+
+# MK_LIBRARY overrides the library path (development builds, e.g. the MK_TRACE variant).
+SO = Path(os.environ.get("MK_LIBRARY", Path(__file__).resolve().parent / "libmk.so"))
 
 MK_MAX_REGION = 8
 STATUS = {

@@ -55,7 +55,7 @@ mk_status forward_impl(mk_context* ctx, const mk_kmap* m, const void* d_fin, int
   if (in_dt == MK_F32)
     return launch_conv_f32(v, (const float*)d_fin, c_in, (const float*)d_w, c_in, c_out, d_fout, c_out, out_dt,
                            m->n_out, false, s);
-  return launch_conv_bf16(ctx, v, d_fin, c_in, d_w, c_in, c_out, d_fout, c_out, out_dt, m->n_out, false, s);
+  return launch_conv_bf16(ctx, v, d_fin, m->n_in, c_in, d_w, c_in, c_out, d_fout, c_out, out_dt, m->n_out, false, s);
 }
 
 mk_status backward_impl(mk_context* ctx, const mk_kmap* m, const void* d_gout, const void* d_fin, const void* d_w,
@@ -70,7 +70,7 @@ mk_status backward_impl(mk_context* ctx, const mk_kmap* m, const void* d_gout, c
       st = launch_conv_f32(v, (const float*)d_gout, c_out, (const float*)d_w, c_in, c_out, d_gin, c_in, MK_F32,
                            m->n_in, true, s);
     else
-      st = launch_conv_bf16(ctx, v, d_gout, c_out, d_w, c_in, c_out, d_gin, c_in, MK_BF16, m->n_in, true, s);
+      st = launch_conv_bf16(ctx, v, d_gout, m->n_out, c_out, d_w, c_in, c_out, d_gin, c_in, MK_BF16, m->n_in, true, s);
     if (st != MK_OK) return st;
   }
   if (d_gw) {

@@ -38,8 +38,9 @@ mk_status launch_wgrad_f32(const mk_kmap* m, const WgradPlan& plan, const float*
                            int c_in, float* dW, cudaStream_t s);
 
 // bf16 tensor-core path (conv_umma.cu)
-mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, int c_x, const void* W, int c_in_w,
-                           int c_out_w, void* y, int c_y, mk_dtype out_dt, int64_t n_rows, bool trans, cudaStream_t s);
+mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, int64_t n_src, int c_x, const void* W,
+                           int c_in_w, int c_out_w, void* y, int c_y, mk_dtype out_dt, int64_t n_rows, bool trans,
+                           cudaStream_t s);
 mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, int c_out, const void* x, int c_in,
                             float* dW, cudaStream_t s);
 __global__ void k_reduce_partials(const int32_t* __restrict__ chunk_begin, const float* __restrict__ part,

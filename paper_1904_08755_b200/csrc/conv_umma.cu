@@ -19,9 +19,11 @@
 //   accumulation unit: gathered G rows form the MN-major A operand (M = C_out padded to
 //   128), gathered X rows the MN-major B operand (N = C_in), K = pairs.  Segment partials
 //   go to a workspace and are summed per offset in a fixed order (deterministic).
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "conv.cuh"
@@ -72,12 +74,13 @@ __global__ void k_pack_w(const __nv_bfloat16* __restrict__ W, int K, int c_out, 
 
 // ------------------------------------------------------------------ forward / dgrad
 struct FwdParams {
+  CUtensorMap tmap_x;      // x as a 2-D [n_src][c_x] bf16 tensor, box {CH, 1}, swizzle = CH*2 bytes
   const __nv_bfloat16* x;  // [n_src][c_x]
   const uint8_t* wpack;    // [K][nch] images of c_y * CH bf16
   void* y;                 // [n_rows][c_y]
   NbrView nb;
   int64_t n_rows, ntiles;
-  int c_x, c_y, nch, out_f32, stages;
+  int c_x, c_y, nch, out_f32, stages, lag;
   uint32_t a_bytes, b_bytes, stage_bytes, tmem_cols;
 };
 
@@ -118,6 +121,51 @@ struct UnitIter {
   }
 };
 
+// Per-warp completion signalling for cp.async stages: every stage a warp issues is one
+// cp.async group; once `lag` newer groups exist, the oldest is waited for, made visible to
+// the async proxy (the tensor cores read it) and announced with ONE arrival per warp on the
+// stage's full barrier (instead of one arrival per thread).
+struct StageSignal {
+  int lag, pending;
+  uint32_t s, S;
+  __device__ StageSignal(int lag_, uint32_t S_) : lag(lag_), pending(0), s(0), S(S_) {}
+  __device__ __forceinline__ void arrive_oldest(uint64_t* full) {
+    fence_proxy_async_smem();
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(full + s);
+    if (++s == S) s = 0;
+    --pending;
+  }
+  __device__ __forceinline__ void issued(uint64_t* full) {
+    cp_async_commit();
+    if (++pending > lag) {
+      cp_async_wait_n(lag);
+      arrive_oldest(full);
+    }
+  }
+  __device__ __forceinline__ void drain(uint64_t* full) {
+    cp_async_wait_n(0);
+    while (pending > 0) arrive_oldest(full);
+  }
+};
+
+#ifdef MK_TRACE
+__device__ unsigned long long g_trace[4][4096];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(role, i, v) \
+  do {                    \
+    if (blockIdx.x == 0 && (i) < 4096) g_trace[role][i] = (v); \
+  } while (0)
+#else
+#define TRACE(role, i, v) \
+  do {                    \
+  } while (0)
+#endif
+
 constexpr int kNbrBuf = 32 * kTileM;  // int32 entries per staging buffer (32 offsets x 128 rows)
 
 // Bulk-copies (TMA engine) the neighbour indices of unit `u` — 128 rows per active offset,
@@ -150,7 +198,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(full + s, kProdWarps * 32 + 1);
+      mbar_init(full + s, kProdWarps + 1);  // one per producer warp + the weight bulk copy
       mbar_init(empty + s, 1);
     }
     for (int b = 0; b < 2; ++b) {
@@ -168,14 +216,28 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
 
   if (warp < kProdWarps) {
     // ---------------------------------------------------------------- producers
+    // 128 threads gather the 128 rows x CH channels of a stage with 16-byte cp.async (8
+    // threads per 128-byte row => coalesced), absent neighbours zero-filled; thread 0
+    // bulk-copies the weight chunk.  One barrier arrival per warp (StageSignal).
     const int t = threadIdx.x;
     UnitIter cur(p.nb, p.ntiles), st(p.nb, p.ntiles);
     if (t == 0)
       for (int b = 0; b < 2; ++b)
         if (st.next()) stage_nbr(p.nb, st, nbr_s + b * kNbrBuf, nfull + b);
+    StageSignal sig(p.lag, (uint32_t)S);
     uint32_t s = 0, ph = 0, ub = 0, nph = 0;
+#ifdef MK_TRACE
+    int tr_g = 0, tr_u = 0;
+#endif
     while (cur.next()) {
+#ifdef MK_TRACE
+      if (t == 0) TRACE(3, 2 * tr_u, gtime());
+#endif
       mbar_wait(nfull + ub, (nph >> ub) & 1u);
+#ifdef MK_TRACE
+      if (t == 0) TRACE(3, 2 * tr_u + 1, gtime());
+      ++tr_u;
+#endif
       nph ^= 1u << ub;
       const int32_t* nb_u = nbr_s + ub * kNbrBuf;
       uint32_t bits = cur.bits;
@@ -186,22 +248,29 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
 #pragma unroll
         for (int i = 0; i < J; ++i) src[i] = nb_u[j * kTileM + (i * 128 + t) / J];
         for (int c = 0; c < p.nch; ++c) {
+#ifdef MK_TRACE
+          if (t == 0) TRACE(0, 2 * tr_g, gtime());
+#endif
           mbar_wait(empty + s, ph ^ 1);
+#ifdef MK_TRACE
+          if (t == 0) TRACE(0, 2 * tr_g + 1, gtime());
+          ++tr_g;
+#endif
           uint8_t* stage = smem + (size_t)s * p.stage_bytes;
           const uint32_t a_s = smem_u32(stage);
 #pragma unroll
           for (int i = 0; i < J; ++i) {
             const int idx = i * 128 + t;
             const int r = idx / J, jj = idx % J;
-            const bool ok = src[i] >= 0;
-            const __nv_bfloat16* gp = ok ? p.x + (int64_t)src[i] * p.c_x + c * CH + jj * 8 : p.x;
-            cp_async16(a_s + swz(r, jj, RB), gp, ok ? 16u : 0u);
+            // absent neighbour: zero the row in smem (no global request at all)
+            if (src[i] >= 0) cp_async16(a_s + swz(r, jj, RB), p.x + (int64_t)src[i] * p.c_x + c * CH + jj * 8, 16u);
+            else st_shared_zero16(a_s + swz(r, jj, RB));
           }
           if (t == 0) {
             mbar_arrive_expect_tx(full + s, p.b_bytes);
             bulk_g2s(stage + p.a_bytes, p.wpack + ((int64_t)k * p.nch + c) * p.b_bytes, p.b_bytes, full + s);
           }
-          cp_async_arrive_noinc(full + s);
+          sig.issued(full);
           if (++s == (uint32_t)S) {
             s = 0;
             ph ^= 1;
@@ -215,13 +284,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
       }
       ub ^= 1;
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    sig.drain(full);
   } else if (warp == kMmaWarp) {
     // ---------------------------------------------------------------- MMA issuer
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16(kTileM, p.c_y, 0, 0);
       const uint32_t lay = layout_code(RB);
       uint32_t s = 0, ph = 0, tl = 0;
+#ifdef MK_TRACE
+      int tr_m = 0;
+#endif
       for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
         if (tile_active_count(p.nb, tile) == 0) continue;
         const uint32_t b = tl & 1, tph = (tl >> 1) & 1;
@@ -233,8 +305,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
           const int nk = __popc(__ldg(p.nb.mask + tile * p.nb.mw + w));
           for (int q = 0; q < nk * p.nch; ++q) {
             mbar_wait(full + s, ph);
+#ifdef MK_TRACE
+            TRACE(1, tr_m, gtime());
+            ++tr_m;
+#endif
             tc_fence_after();
-            fence_proxy_async_smem();
             const uint32_t a_s = smem_u32(smem + (size_t)s * p.stage_bytes);
             const uint32_t b_s = a_s + p.a_bytes;
 #pragma unroll
@@ -277,6 +352,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
       }
       const uint32_t b = tl & 1, tph = (tl >> 1) & 1;
       mbar_wait(tfull + b, tph);
+#ifdef MK_TRACE
+      if (q == 0 && lane == 0) TRACE(2, 2 * tl, gtime());
+#endif
       tc_fence_after();
       const uint32_t tl_addr = tbase + ((uint32_t)(q * 32) << 16) + b * (uint32_t)p.c_y;
       for (int col0 = 0; col0 < p.c_y; col0 += 16) {
@@ -304,6 +382,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
         }
       }
       tc_fence_before();
+#ifdef MK_TRACE
+      if (q == 0 && lane == 0) TRACE(2, 2 * tl + 1, gtime());
+#endif
       mbar_arrive(tempty + b);
       ++tl;
     }
@@ -316,6 +397,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
 
 // ------------------------------------------------------------------ weight gradient
 struct WgradParams {
+  CUtensorMap tmap_g;      // g as [n_out][c_out], box {pwa, 1}
+  CUtensorMap tmap_x;      // x as [n_in][c_in],  box {pwb, 1}
   const __nv_bfloat16* g;  // [n_out][c_out]
   const __nv_bfloat16* x;  // [n_in][c_in]
   const int32_t* in_idx;
@@ -323,7 +406,7 @@ struct WgradParams {
   const int4* segs;          // (k, begin, end, slot), grouped by CTA
   const int32_t* seg_begin;  // [n_cta + 1]
   float* part;               // [n_slots][c_out][c_in]
-  int c_out, c_in, stages, halves;
+  int c_out, c_in, stages, halves, lag;
   int pwa, pwb;              // panel widths (channels) of A (G) and B (X)
   uint32_t a_bytes, b_bytes, stage_bytes, tmem_cols;
 };
@@ -387,7 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(full + s, kProdWarps * 32);
+      mbar_init(full + s, kProdWarps);
       mbar_init(empty + s, 1);
     }
     mbar_init(tfull, 1);
@@ -414,13 +497,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
   const int sb = p.seg_begin[blockIdx.x], se = p.seg_begin[blockIdx.x + 1];
 
   if (warp < kProdWarps) {
+    // 128 threads gather, per 64-pair stage, the G rows (A panels) and X rows (B panels) of
+    // the pairs with 16-byte cp.async; pairs past the segment end are zero-filled.  One
+    // barrier arrival per warp (StageSignal).
     const int t = threadIdx.x;
-    const int ja = rba / 16, jb = rbb / 16;  // 16-byte chunks per panel row
-    const int per_pair = npa * ja + npb * jb;
+    const int ca = p.c_out / 8, cb = p.c_in / 8;  // 16-byte chunks per G row / X row
+    const int ja = rba / 16, jb = rbb / 16;       // chunks per panel row
     WUnitIter cur(p.segs, sb, se), st(p.segs, sb, se);
     if (t == 0)
       for (int b = 0; b < 2; ++b)
         if (st.next()) stage_idx(p.out_idx, p.in_idx, st, idx_s + b * 2 * kIdxBuf, nfull + b);
+    StageSignal sig(p.lag, (uint32_t)S);
     uint32_t s = 0, ph = 0, ub = 0, nph = 0;
     while (cur.next()) {
       mbar_wait(nfull + ub, (nph >> ub) & 1u);
@@ -430,24 +517,24 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
       const int b4 = cur.b & ~3;
       for (int b0 = cur.b; b0 < cur.e; b0 += PS) {
         mbar_wait(empty + s, ph ^ 1);
-        uint8_t* stage = smem + (size_t)s * p.stage_bytes;
-        const uint32_t a_s = smem_u32(stage), b_s = a_s + p.a_bytes;
-        for (int idx = t; idx < PS * per_pair; idx += kProdWarps * 32) {
-          const int pr = idx / per_pair, rem = idx % per_pair;
+        const uint32_t a_s = smem_u32(smem + (size_t)s * p.stage_bytes), b_s = a_s + p.a_bytes;
+        for (int idx = t; idx < PS * ca; idx += kProdWarps * 32) {  // G rows -> A panels
+          const int pr = idx / ca, ch = idx - pr * ca;
           const int pi = b0 + pr;
           const bool ok = pi < cur.e;
-          if (rem < npa * ja) {  // G row chunk -> A panel
-            const int pa = rem / ja, j = rem % ja;
-            const __nv_bfloat16* src = ok ? p.g + (int64_t)oi[pi - b4] * p.c_out + pa * p.pwa + j * 8 : p.g;
-            cp_async16(a_s + pa * panel_a + swz(pr, j, rba), src, ok ? 16u : 0u);
-          } else {  // X row chunk -> B panel
-            const int r2 = rem - npa * ja;
-            const int pb = r2 / jb, j = r2 % jb;
-            const __nv_bfloat16* src = ok ? p.x + (int64_t)ii[pi - b4] * p.c_in + pb * p.pwb + j * 8 : p.x;
-            cp_async16(b_s + pb * panel_b + swz(pr, j, rbb), src, ok ? 16u : 0u);
-          }
+          const int pa = ch / ja, j = ch - pa * ja;
+          if (ok) cp_async16(a_s + pa * panel_a + swz(pr, j, rba), p.g + (int64_t)oi[pi - b4] * p.c_out + ch * 8, 16u);
+          else st_shared_zero16(a_s + pa * panel_a + swz(pr, j, rba));
         }
-        cp_async_arrive_noinc(full + s);
+        for (int idx = t; idx < PS * cb; idx += kProdWarps * 32) {  // X rows -> B panels
+          const int pr = idx / cb, ch = idx - pr * cb;
+          const int pi = b0 + pr;
+          const bool ok = pi < cur.e;
+          const int pb = ch / jb, j = ch - pb * jb;
+          if (ok) cp_async16(b_s + pb * panel_b + swz(pr, j, rbb), p.x + (int64_t)ii[pi - b4] * p.c_in + ch * 8, 16u);
+          else st_shared_zero16(b_s + pb * panel_b + swz(pr, j, rbb));
+        }
+        sig.issued(full);
         if (++s == (uint32_t)S) {
           s = 0;
           ph ^= 1;
@@ -460,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
       }
       ub ^= 1;
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
+    sig.drain(full);
   } else if (warp == kMmaWarp) {
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16(kTileM, p.c_in, 1, 1);
@@ -475,7 +562,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
         for (int b0 = sg.y; b0 < sg.z; b0 += PS) {
           mbar_wait(full + s, ph);
           tc_fence_after();
-          fence_proxy_async_smem();
           const uint32_t a_s = smem_u32(smem + (size_t)s * p.stage_bytes), b_s = a_s + p.a_bytes;
 #pragma unroll
           for (int kk = 0; kk < PS / 16; ++kk) {
@@ -534,6 +620,42 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
   if (warp == kMmaWarp) tmem_dealloc(tbase, p.tmem_cols);
 }
 
+
+// ------------------------------------------------------------------ host: tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return (EncodeTiledFn)f;
+  }();
+  return fn;
+}
+
+// A [rows][cols] bf16 row-major tensor viewed for row gathers: box {box_cols, 1}, swizzle
+// matching a K-major / MN-major UMMA panel of box_cols * 2 bytes; out-of-range rows
+// (index -1) are zero-filled by the TMA unit.
+bool make_row_map(CUtensorMap* m, const void* base, int64_t rows, int cols, int box_cols) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn || ((uintptr_t)base & 15) || rows < 1) return false;
+  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  const cuuint32_t box[2] = {(cuuint32_t)box_cols, 1};
+  const cuuint32_t es[2] = {1, 1};
+  const CUtensorMapSwizzle sw = box_cols * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                : box_cols * 2 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                     : CU_TENSOR_MAP_SWIZZLE_32B;
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 uint32_t pow2_cols(uint32_t c) {
   uint32_t r = 32;
   while (r < c) r <<= 1;
@@ -547,8 +669,14 @@ void set_smem_once(F* f, int bytes) {
 
 }  // namespace
 
-mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, int c_x, const void* W, int c_in_w,
-                            int c_out_w, void* y, int c_y, mk_dtype out_dt, int64_t n_rows, bool trans,
+#ifdef MK_TRACE
+extern "C" int mk_debug_trace(unsigned long long* host_out) {
+  return (int)cudaMemcpyFromSymbol(host_out, g_trace, sizeof(g_trace));
+}
+#endif
+
+mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, int64_t n_src, int c_x, const void* W,
+                            int c_in_w, int c_out_w, void* y, int c_y, mk_dtype out_dt, int64_t n_rows, bool trans,
                             cudaStream_t s) {
   if (n_rows == 0) return MK_OK;
   const int CH = c_x % 64 == 0 ? 64 : c_x % 32 == 0 ? 32 : 16;
@@ -569,8 +697,10 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   const int reserve = 1024 + 256 + 2 * kNbrBuf * 4;
   p.stages = std::min<int>(8, (kMaxSmem - reserve) / (int)p.stage_bytes);
   if (p.stages < 2) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: channel counts too large for the smem pipeline");
+
   p.tmem_cols = pow2_cols(2 * c_y);
   if (p.tmem_cols > 512) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: C_out above 256");
+  p.lag = std::min(4, p.stages - 1);
   const size_t wbytes = (size_t)nb.K * nch * p.b_bytes;
   uint8_t* wpack = (uint8_t*)dev_alloc(ctx->alloc, wbytes, s);
   if (!wpack) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 conv: weight pack allocation failed");
@@ -581,6 +711,10 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
     g_launches++;
   }
   p.wpack = wpack;
+  if (!make_row_map(&p.tmap_x, n_src > 0 ? x : (const void*)wpack, std::max<int64_t>(n_src, 1), c_x, CH)) {
+    dev_free(ctx->alloc, wpack, s);
+    MK_FAIL(MK_ERR_CUDA, "bf16 conv: cuTensorMapEncodeTiled failed (features must be 16-byte aligned)");
+  }
   const int smem = p.stages * (int)p.stage_bytes + reserve;
   const int grid = (int)std::min<int64_t>(p.ntiles, ctx->num_sms);
   if (CH == 64) {
@@ -622,7 +756,12 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   const int reserve = 1024 + 256 + 4 * kIdxBuf * 4;
   p.stages = std::min<int>(6, (kMaxSmem - reserve) / (int)p.stage_bytes);
   p.tmem_cols = pow2_cols((uint32_t)(p.halves * c_in));
+  p.lag = std::min(4, p.stages - 1);
   if (p.stages < 2 || p.tmem_cols > 512) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: channel counts too large");
+  if (m->n_wslots > 0 &&
+      (!make_row_map(&p.tmap_g, g, std::max<int64_t>(m->n_out, 1), c_out, p.pwa) ||
+       !make_row_map(&p.tmap_x, x, std::max<int64_t>(m->n_in, 1), c_in, p.pwb)))
+    MK_FAIL(MK_ERR_CUDA, "bf16 wgrad: cuTensorMapEncodeTiled failed (features must be 16-byte aligned)");
   float* part = nullptr;
   if (m->n_wslots > 0) {
     part = (float*)dev_alloc(ctx->alloc, sizeof(float) * m->n_wslots * te, s);
