@@ -92,7 +92,7 @@ class Coords:
         return self.n
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _L is not None:
             _L.mk_coords_destroy(self._h)
             self._h = None
 
@@ -209,7 +209,7 @@ class KernelMap:
         self.K, self.n_pairs, self.n_in, self.n_out = K.value, npairs.value, nin.value, nout.value
 
     def __del__(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _L is not None:
             _L.mk_kmap_destroy(self._h)
             self._h = None
 

@@ -22,6 +22,7 @@ NbrView forward_view(const mk_kmap* m) {
   NbrView v;
   v.tab = m->nbr;
   v.mask = m->tile_mask;
+  v.perm = m->perm;
   v.n = m->nbr_stride;
   v.K = m->K;
   v.mw = m->mask_words;
@@ -34,6 +35,7 @@ NbrView dgrad_view(const mk_kmap* m) {
   v.mw = m->mask_words;
   v.n = m->nbrT_stride;
   v.mask = m->tile_maskT;
+  v.perm = m->permT;
   if (m->nbrT) {
     v.tab = m->nbrT;
   } else {  // symmetric submanifold map: nbrT[k] = nbr[mirror[k]]

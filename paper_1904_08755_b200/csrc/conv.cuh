@@ -13,11 +13,13 @@ struct NbrView {
   const int32_t* tab = nullptr;     // [K][n], n = rows padded to a multiple of 128 (padding -1)
   const int32_t* mirror = nullptr;  // [K] or null
   const uint32_t* mask = nullptr;   // [n/128][mw], already mirrored for dgrad views
+  const int32_t* perm = nullptr;    // [n] output row of table position i, or null (identity)
   int64_t n = 0;
   int K = 0;
   int mw = 1;
   __device__ __forceinline__ int kk(int k) const { return mirror ? __ldg(mirror + k) : k; }
   __device__ __forceinline__ int32_t at(int k, int64_t r) const { return __ldg(tab + (int64_t)kk(k) * n + r); }
+  __device__ __forceinline__ int64_t row_of(int64_t i) const { return perm ? (int64_t)__ldg(perm + i) : i; }
   __device__ __forceinline__ bool active(int64_t tile128, int k) const {
     return (__ldg(mask + tile128 * mw + (k >> 5)) >> (k & 31)) & 1u;
   }

@@ -82,8 +82,9 @@ __global__ void __launch_bounds__(kThreads) k_conv_f32(NbrView nb, const float* 
       }
     }
   }
-  const int64_t row = row0 + r;
-  if (row < n_rows) {
+  const int64_t pos = row0 + r;
+  if (pos < n_rows) {
+    const int64_t row = nb.row_of(pos);  // tables are stored in the map's internal row order
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       const int j = jg + 8 * i;

@@ -35,10 +35,22 @@ namespace {
 using namespace sm100;
 
 constexpr int kTileM = 128;
-constexpr int kProdWarps = 4;
+// Random 128-byte row gathers are latency bound per warp: B200 reaches ~5 TB/s with 8
+// issuing warps per SM and >12 TB/s with 32 (tools/ubench_gather.cu), so the gather
+// producers are 16 warps.
+constexpr int kProdWarps = 16;                    // wgrad producers
 constexpr int kEpiWarps = 4;
-constexpr int kMmaWarp = kProdWarps + kEpiWarps;  // warp 8
-constexpr int kThreads = (kProdWarps + kEpiWarps + 1) * 32;
+constexpr int kEpiWarp0 = 16;                     // epilogue warps 16-19 (TMEM lane quarters 0-3)
+constexpr int kMmaWarp = kEpiWarp0 + kEpiWarps;   // warp 20
+constexpr int kThreads = (kMmaWarp + 1) * 32;     // 672 (weight-gradient kernel)
+// Forward / dgrad kernel: small CTAs (2 per SM co-reside, the hardware scheduler balances
+// the bitmask-sorted tiles, whose work varies ~4x): 4 gather warps, 4 epilogue warps, the
+// MMA warp and the W stager.
+constexpr int kFwdProd = 4;
+constexpr int kFwdEpi0 = 4;                       // epilogue warps 4-7 (TMEM lane quarters)
+constexpr int kFwdMma = 8;
+constexpr int kFwdStage = 9;
+constexpr int kFwdThreads = 10 * 32;
 constexpr int kMaxSmem = 227 * 1024;
 
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
@@ -73,17 +85,6 @@ __global__ void k_pack_w(const __nv_bfloat16* __restrict__ W, int K, int c_out, 
 }
 
 // ------------------------------------------------------------------ forward / dgrad
-struct FwdParams {
-  CUtensorMap tmap_x;      // x as a 2-D [n_src][c_x] bf16 tensor, box {CH, 1}, swizzle = CH*2 bytes
-  const __nv_bfloat16* x;  // [n_src][c_x]
-  const uint8_t* wpack;    // [K][nch] images of c_y * CH bf16
-  void* y;                 // [n_rows][c_y]
-  NbrView nb;
-  int64_t n_rows, ntiles;
-  int c_x, c_y, nch, out_f32, stages, lag;
-  uint32_t a_bytes, b_bytes, stage_bytes, tmem_cols;
-};
-
 __device__ __forceinline__ int tile_active_count(const NbrView& nb, int64_t tile) {
   int n = 0;
   for (int w = 0; w < nb.mw; ++w) n += __popc(__ldg(nb.mask + tile * nb.mw + w));
@@ -150,7 +151,7 @@ struct StageSignal {
 };
 
 #ifdef MK_TRACE
-__device__ unsigned long long g_trace[4][4096];
+__device__ unsigned long long g_trace[4][8192];
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -158,9 +159,29 @@ __device__ __forceinline__ unsigned long long gtime() {
 }
 #define TRACE(role, i, v) \
   do {                    \
-    if (blockIdx.x == 0 && (i) < 4096) g_trace[role][i] = (v); \
+    if (blockIdx.x == 0 && (i) < 8192) g_trace[role][i] = (v); \
+  } while (0)
+__device__ unsigned long long g_acct[32][8];
+#define ACCT_WAIT(slot, bar, par)                              \
+  do {                                                         \
+    const long long _t0 = clock64();                           \
+    mbar_wait(bar, par);                                       \
+    acct[slot] += clock64() - _t0;                             \
+  } while (0)
+#define ACCT_DECL long long acct[8] = {0, 0, 0, 0, 0, 0, 0, 0}; const long long acct_t0 = clock64();
+#define ACCT_DUMP                                                                             \
+  do {                                                                                        \
+    if (blockIdx.x == 100 && lane == 0) {                                                     \
+      for (int _i = 0; _i < 7; ++_i) g_acct[warp][_i] = acct[_i];                             \
+      g_acct[warp][7] = clock64() - acct_t0;                                                  \
+    }                                                                                         \
   } while (0)
 #else
+#define ACCT_WAIT(slot, bar, par) mbar_wait(bar, par)
+#define ACCT_DECL
+#define ACCT_DUMP \
+  do {            \
+  } while (0)
 #define TRACE(role, i, v) \
   do {                    \
   } while (0)
@@ -180,165 +201,293 @@ __device__ __forceinline__ void stage_nbr(const NbrView& nb, const UnitIter& u, 
   }
 }
 
+struct FwdParams {
+  const __nv_bfloat16* x;  // [n_src][c_x]
+  const uint8_t* wpack;    // [K][nch] images of c_y * CH bf16 (swizzled K-major B operand)
+  void* y;                 // [n_rows][c_y]
+  NbrView nb;
+  int64_t n_rows, ntiles;
+  int c_x, c_y, nch, out_f32;
+  int sa;  // A stages == producer warps (warp w owns stage slot w)
+  int ga;  // stage slots released together by one tcgen05.commit (sa % ga == 0)
+  int sw;  // W chunk slots (a ring: W_k chunks are prefetched several offsets ahead)
+  int tb;  // tiles per CTA (one TMEM accumulator each: tb * c_y <= 512 columns)
+  uint32_t a_bytes, b_bytes, tmem_cols;
+};
+
+constexpr int kMaxK = 128;  // offsets supported by the tensor-core conv (4 mask words)
+
+// Per-CTA plan, built once in shared memory by warp 0: the CTA's tiles are
+// blockIdx.x * tb + i (adjacent in the map's bitmask-sorted row order, so they share most
+// offsets).  A unit is an offset k active in at least one of them: tw = bitmask of those
+// tiles.  Units are visited starting at offset blockIdx.x % K (concurrent CTAs then fetch
+// different W_k).  g0[u] = first global step of unit u, a step = (unit, tile, chunk).
+struct Plan {
+  int n_units;
+  int n_steps;
+  uint32_t active_tiles;  // tiles with at least one offset
+  uint8_t k[kMaxK];       // offset of unit u  (K <= 128 < 256)
+  uint8_t tw[kMaxK];      // tiles of unit u
+  int32_t g0[kMaxK + 1];
+};
+
+__device__ void build_plan(const FwdParams& p, Plan* pl) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t0 = (int64_t)blockIdx.x * p.tb;
+  const int nt = (int)min((int64_t)p.tb, p.ntiles - t0);
+  const int K = p.nb.K;
+  const int rot = (int)(blockIdx.x % (unsigned)K);
+  uint32_t act = 0;
+  int base_units = 0, base_steps = 0;
+  for (int kb = 0; kb < K; kb += 32) {
+    // lane handles offset k = (rot + kb + lane) % K in visiting order
+    const int v = kb + lane;
+    const int k = v < K ? (rot + v) % K : 0;
+    uint32_t tw = 0;
+    if (v < K)
+      for (int i = 0; i < nt; ++i) tw |= ((__ldg(p.nb.mask + (t0 + i) * p.nb.mw + (k >> 5)) >> (k & 31)) & 1u) << i;
+    act |= __reduce_or_sync(0xffffffffu, tw);
+    const bool has = tw != 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, has);
+    const int pos = base_units + __popc(bal & ((1u << lane) - 1u));
+    int steps = has ? __popc(tw) * p.nch : 0;
+    int incl = steps;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (has) {
+      pl->k[pos] = (uint8_t)k;
+      pl->tw[pos] = (uint8_t)tw;
+      pl->g0[pos] = base_steps + incl - steps;
+    }
+    base_units += __popc(bal);
+    base_steps += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) {
+    pl->n_units = base_units;
+    pl->n_steps = base_steps;
+    pl->g0[base_units] = base_steps;
+    pl->active_tiles = act;
+  }
+}
+
+// Output-stationary gather-GEMM over the CTA's tb tiles, offset-outer (see file header).
 template <int CH>
-__global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant__ FwdParams p) {
+__global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_constant__ FwdParams p) {
   constexpr int J = CH / 8;    // 16-byte chunks per gathered row
   constexpr int RB = CH * 2;   // bytes per gathered row (= swizzle span)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  const int S = p.stages;
-  int32_t* nbr_s = (int32_t*)(smem + (size_t)S * p.stage_bytes);  // [2][32][128]
-  uint64_t* full = (uint64_t*)(nbr_s + 2 * kNbrBuf);
-  uint64_t* empty = full + S;
-  uint64_t* tfull = empty + S;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* nfull = tempty + 2;
-  uint32_t* tmem_slot = (uint32_t*)(nfull + 2);
+  uint8_t* a_base = smem;
+  uint8_t* w_base = a_base + (size_t)p.sa * p.a_bytes;
+  int32_t* nbr_s = (int32_t*)(w_base + (size_t)p.sw * p.b_bytes);  // [kFwdProd][2][128] index buffers
+  Plan* pl = (Plan*)(nbr_s + kFwdProd * 2 * kTileM);
+  uint64_t* a_full = (uint64_t*)(((uintptr_t)(pl + 1) + 15) & ~(uintptr_t)15);
+  uint64_t* a_empty = a_full + p.sa;
+  uint64_t* w_full = a_empty + p.sa;
+  uint64_t* w_empty = w_full + p.sw;
+  uint64_t* tfull = w_empty + p.sw;
+  uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t tile0 = (int64_t)blockIdx.x * p.tb;
 
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(full + s, kProdWarps + 1);  // one per producer warp + the weight bulk copy
-      mbar_init(empty + s, 1);
+  if (warp == 0) build_plan(p, pl);
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < p.sa; ++s) {
+      mbar_init(a_full + s, 1);
+      mbar_init(a_empty + s, 1);  // only a_empty[0 .. sa/ga) are used: one per group of ga slots
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(tfull + b, 1);
-      mbar_init(tempty + b, kEpiWarps * 32);
-      mbar_init(nfull + b, 1);
+    for (int s = 0; s < p.sw; ++s) {
+      mbar_init(w_full + s, 1);
+      mbar_init(w_empty + s, 1);
     }
+    mbar_init(tfull, 1);
     fence_mbar_init();
   }
-  if (warp == kMmaWarp) tmem_alloc_dyn(tmem_slot, p.tmem_cols);
+  if (warp == kFwdMma) tmem_alloc_dyn(tmem_slot, p.tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  const int n_units = pl->n_units, n_steps = pl->n_steps;
+  ACCT_DECL
 
-  if (warp < kProdWarps) {
-    // ---------------------------------------------------------------- producers
-    // 128 threads gather the 128 rows x CH channels of a stage with 16-byte cp.async (8
-    // threads per 128-byte row => coalesced), absent neighbours zero-filled; thread 0
-    // bulk-copies the weight chunk.  One barrier arrival per warp (StageSignal).
-    const int t = threadIdx.x;
-    UnitIter cur(p.nb, p.ntiles), st(p.nb, p.ntiles);
-    if (t == 0)
-      for (int b = 0; b < 2; ++b)
-        if (st.next()) stage_nbr(p.nb, st, nbr_s + b * kNbrBuf, nfull + b);
-    StageSignal sig(p.lag, (uint32_t)S);
-    uint32_t s = 0, ph = 0, ub = 0, nph = 0;
-#ifdef MK_TRACE
-    int tr_g = 0, tr_u = 0;
-#endif
-    while (cur.next()) {
-#ifdef MK_TRACE
-      if (t == 0) TRACE(3, 2 * tr_u, gtime());
-#endif
-      mbar_wait(nfull + ub, (nph >> ub) & 1u);
-#ifdef MK_TRACE
-      if (t == 0) TRACE(3, 2 * tr_u + 1, gtime());
-      ++tr_u;
-#endif
-      nph ^= 1u << ub;
-      const int32_t* nb_u = nbr_s + ub * kNbrBuf;
-      uint32_t bits = cur.bits;
-      for (int j = 0; bits; ++j) {
-        const int k = cur.w * 32 + __ffs(bits) - 1;
-        bits &= bits - 1;
-        int32_t src[J];
+  if (warp < p.sa) {
+    // ------------------------------------------------------------ gather producers
+    // Step g belongs to warp g % sa and uses its stage slot: 128 rows x CH channels; lane
+    // group q4 = lane/8 owns rows [32 q4, 32 q4 + 32), 8 lanes per 128-byte row (4 full lines
+    // per instruction); absent neighbours are zero-filled in smem.  The next step's 128
+    // neighbour indices are prefetched into a private double buffer by one 16-byte cp.async
+    // per lane, in the same cp.async group.  Then: wait for the group, publish to the async
+    // proxy, one arrival on the slot's full barrier.
+    int32_t* ibuf = nbr_s + warp * 2 * kTileM;
+    int u = 0;
+    auto locate = [&](int g, int* k, int64_t* tile, int* c) {
+      while (pl->g0[u + 1] <= g) ++u;
+      const int q = g - pl->g0[u];
+      const int j = q / p.nch;
+      *c = q - j * p.nch;
+      uint32_t tw = pl->tw[u];
+      for (int t = 0; t < j; ++t) tw &= tw - 1;
+      *tile = tile0 + (__ffs(tw) - 1);
+      *k = pl->k[u];
+    };
+    int g = warp;
+    int k, c, kn = 0, cn = 0;
+    int64_t tile, tilen = 0;
+    if (g < n_steps) {
+      locate(g, &k, &tile, &c);
+      cp_async16(smem_u32(ibuf) + lane * 16, p.nb.tab + (int64_t)p.nb.kk(k) * p.nb.n + tile * kTileM + lane * 4, 16u);
+      cp_async_commit();
+      cp_async_wait_n(0);
+      __syncwarp();
+    }
+    uint32_t my = 0, ib = 0;
+    const int q4 = lane >> 3, jj = lane & (J - 1);
+    for (; g < n_steps; g += p.sa) {
+      const bool have_n = g + p.sa < n_steps;
+      bool same = false;
+      if (have_n) {
+        locate(g + p.sa, &kn, &tilen, &cn);
+        same = kn == k && tilen == tile;  // further chunks of the same rows: indices reused
+        if (!same)
+          cp_async16(smem_u32(ibuf + (ib ^ 1) * kTileM) + lane * 16,
+                     p.nb.tab + (int64_t)p.nb.kk(kn) * p.nb.n + tilen * kTileM + lane * 4, 16u);
+      }
+      ACCT_WAIT(0, a_empty + warp / p.ga, (my & 1) ^ 1);
+      const uint32_t a_s = smem_u32(a_base + (size_t)warp * p.a_bytes);
+      const int32_t* ix = ibuf + ib * kTileM;
+      const __nv_bfloat16* xc = p.x + c * CH;
+      if (J == 8) {
+#pragma unroll 2
+        for (int i = 0; i < 32; i += 4) {
+          const int4 a4 = *(const int4*)(ix + q4 * 32 + i);
+          const int av[4] = {a4.x, a4.y, a4.z, a4.w};
 #pragma unroll
-        for (int i = 0; i < J; ++i) src[i] = nb_u[j * kTileM + (i * 128 + t) / J];
-        for (int c = 0; c < p.nch; ++c) {
-#ifdef MK_TRACE
-          if (t == 0) TRACE(0, 2 * tr_g, gtime());
-#endif
-          mbar_wait(empty + s, ph ^ 1);
-#ifdef MK_TRACE
-          if (t == 0) TRACE(0, 2 * tr_g + 1, gtime());
-          ++tr_g;
-#endif
-          uint8_t* stage = smem + (size_t)s * p.stage_bytes;
-          const uint32_t a_s = smem_u32(stage);
-#pragma unroll
-          for (int i = 0; i < J; ++i) {
-            const int idx = i * 128 + t;
-            const int r = idx / J, jj = idx % J;
-            // absent neighbour: zero the row in smem (no global request at all)
-            if (src[i] >= 0) cp_async16(a_s + swz(r, jj, RB), p.x + (int64_t)src[i] * p.c_x + c * CH + jj * 8, 16u);
+          for (int e = 0; e < 4; ++e) {
+            const int r = q4 * 32 + i + e;
+            if (av[e] >= 0) cp_async16(a_s + swz(r, jj, RB), xc + (int64_t)av[e] * p.c_x + jj * 8, 16u);
             else st_shared_zero16(a_s + swz(r, jj, RB));
           }
-          if (t == 0) {
-            mbar_arrive_expect_tx(full + s, p.b_bytes);
-            bulk_g2s(stage + p.a_bytes, p.wpack + ((int64_t)k * p.nch + c) * p.b_bytes, p.b_bytes, full + s);
-          }
-          sig.issued(full);
-          if (++s == (uint32_t)S) {
-            s = 0;
-            ph ^= 1;
-          }
+        }
+      } else {
+#pragma unroll 4
+        for (int slot = lane; slot < 128 * J; slot += 32) {
+          const int r = slot / J, j2 = slot % J;
+          const int32_t av = ix[r];
+          if (av >= 0) cp_async16(a_s + swz(r, j2, RB), xc + (int64_t)av * p.c_x + j2 * 8, 16u);
+          else st_shared_zero16(a_s + swz(r, j2, RB));
         }
       }
-      named_bar_sync(1, kProdWarps * 32);  // every producer is done reading buffer ub
-      if (t == 0 && st.next()) {
-        fence_proxy_async_smem();
-        stage_nbr(p.nb, st, nbr_s + ub * kNbrBuf, nfull + ub);
-      }
-      ub ^= 1;
+      cp_async_commit();
+      cp_async_wait_n(0);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full + warp);
+      ++my;
+      if (have_n && !same) ib ^= 1;
+      k = kn;
+      tile = tilen;
+      c = cn;
     }
-    sig.drain(full);
-  } else if (warp == kMmaWarp) {
-    // ---------------------------------------------------------------- MMA issuer
+  } else if (warp == kFwdStage) {
+    // ------------------------------------------------------------ W stager (one thread)
+    // Bulk copies (TMA engine) of the W_k chunks of every unit into a ring of sw slots.
     if (lane == 0) {
-      const uint32_t idesc = idesc_bf16(kTileM, p.c_y, 0, 0);
-      const uint32_t lay = layout_code(RB);
-      uint32_t s = 0, ph = 0, tl = 0;
-#ifdef MK_TRACE
-      int tr_m = 0;
-#endif
-      for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-        if (tile_active_count(p.nb, tile) == 0) continue;
-        const uint32_t b = tl & 1, tph = (tl >> 1) & 1;
-        mbar_wait(tempty + b, tph ^ 1);
-        tc_fence_after();
-        const uint32_t d = tbase + b * (uint32_t)p.c_y;
-        uint32_t acc = 0;
-        for (int w = 0; w < p.nb.mw; ++w) {
-          const int nk = __popc(__ldg(p.nb.mask + tile * p.nb.mw + w));
-          for (int q = 0; q < nk * p.nch; ++q) {
-            mbar_wait(full + s, ph);
-#ifdef MK_TRACE
-            TRACE(1, tr_m, gtime());
-            ++tr_m;
-#endif
-            tc_fence_after();
-            const uint32_t a_s = smem_u32(smem + (size_t)s * p.stage_bytes);
-            const uint32_t b_s = a_s + p.a_bytes;
-#pragma unroll
-            for (int kk = 0; kk < CH / 16; ++kk) {
-              const uint64_t ad = smem_desc(a_s + kk * 32, 16, 8 * RB, lay);
-              const uint64_t bd = smem_desc(b_s + kk * 32, 16, 8 * RB, lay);
-              umma_f16(d, ad, bd, idesc, acc);
-              acc = 1;
-            }
-            umma_commit(empty + s);
-            if (++s == (uint32_t)S) {
-              s = 0;
-              ph ^= 1;
-            }
+      uint32_t ws = 0, wph = 0;
+      for (int u = 0; u < n_units; ++u)
+        for (int c = 0; c < p.nch; ++c) {
+          ACCT_WAIT(0, w_empty + ws, wph ^ 1);
+          mbar_arrive_expect_tx(w_full + ws, p.b_bytes);
+          bulk_g2s(w_base + (size_t)ws * p.b_bytes, p.wpack + ((int64_t)pl->k[u] * p.nch + c) * p.b_bytes, p.b_bytes,
+                   w_full + ws);
+          if (++ws == (uint32_t)p.sw) {
+            ws = 0;
+            wph ^= 1;
           }
         }
-        umma_commit(tfull + b);
-        ++tl;
-      }
     }
     __syncwarp();
-  } else {
-    // ---------------------------------------------------------------- epilogue
+  } else if (warp == kFwdMma) {
+    // ------------------------------------------------------------ MMA issuer (one thread)
+    // Lean loop: descriptors are a constant high part | (smem address >> 4); slot / phase
+    // counters are incremental (no divisions); one commit per group of ga stage slots.
+    if (lane == 0) {
+      const uint32_t idesc = idesc_bf16(kTileM, p.c_y, 0, 0);
+      const uint64_t dhi = smem_desc(0, 16, 8 * RB, layout_code(RB));
+      const uint32_t a0 = smem_u32(a_base) >> 4, astep = p.a_bytes >> 4;
+      const uint32_t w0 = smem_u32(w_base) >> 4, wstep = p.b_bytes >> 4;
+      uint32_t s = 0, sph = 0, gq = 0;     // A slot, its phase, position inside the commit group
+      uint32_t ws = 0, wph = 0;            // W ring position of the unit's first chunk
+      uint32_t init = 0;                   // tiles whose accumulator holds data
+      for (int u = 0; u < n_units; ++u) {
+        const uint32_t tw = pl->tw[u];
+        {  // wait for the unit's W chunks
+          uint32_t x = ws, xph = wph;
+          for (int c = 0; c < p.nch; ++c) {
+            ACCT_WAIT(1, w_full + x, xph);
+            if (++x == (uint32_t)p.sw) {
+              x = 0;
+              xph ^= 1;
+            }
+          }
+        }
+        tc_fence_after();
+        for (uint32_t b = tw; b; b &= b - 1) {
+          const int i = __ffs(b) - 1;
+          const uint32_t d = tbase + (uint32_t)(i * p.c_y);
+          uint32_t acc = (init >> i) & 1u;
+          uint32_t x = ws;
+          for (int c = 0; c < p.nch; ++c) {
+            ACCT_WAIT(2, a_full + s, sph);
+            tc_fence_after();
+            const uint32_t alo = a0 + s * astep, blo = w0 + x * wstep;
+#pragma unroll
+            for (int kk = 0; kk < CH / 16; ++kk) {
+              umma_f16(d, dhi | (uint64_t)(alo + kk * 2), dhi | (uint64_t)(blo + kk * 2), idesc, acc);
+              acc = 1;
+            }
+            // tcgen05.commit costs ~400+ issue cycles: release stage slots in groups of ga
+            if (++gq == (uint32_t)p.ga) {
+              umma_commit(a_empty + s / p.ga);
+              gq = 0;
+            }
+            if (++s == (uint32_t)p.sa) {
+              s = 0;
+              sph ^= 1;
+            }
+            if (++x == (uint32_t)p.sw) x = 0;
+          }
+          init |= 1u << i;
+        }
+        for (int c = 0; c < p.nch; ++c) {
+          umma_commit(w_empty + ws);
+          if (++ws == (uint32_t)p.sw) {
+            ws = 0;
+            wph ^= 1;
+          }
+        }
+      }
+      if (n_steps > 0) umma_commit(tfull);
+    }
+    __syncwarp();
+  } else if (warp >= kFwdEpi0 && warp < kFwdEpi0 + 4) {
+    // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quarter owned by this warp
-    uint32_t tl = 0;
-    for (int64_t tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
-      const int64_t row = tile * kTileM + q * 32 + lane;
-      const bool valid = row < p.n_rows;
-      if (tile_active_count(p.nb, tile) == 0) {
+    if (n_steps > 0) {
+      ACCT_WAIT(0, tfull, 0);
+      tc_fence_after();
+    }
+    const uint32_t act = pl->active_tiles;
+    for (int i = 0; i < p.tb; ++i) {
+      const int64_t tile = tile0 + i;
+      if (tile >= p.ntiles) break;
+      const int64_t pos = tile * kTileM + q * 32 + lane;  // position in the map's row order
+      const bool valid = pos < p.n_rows;
+      const int64_t row = valid ? p.nb.row_of(pos) : 0;
+      if (!((act >> i) & 1u)) {
         if (valid) {
           if (p.out_f32) {
             float4* yr = (float4*)((float*)p.y + row * p.c_y);
@@ -350,13 +499,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
         }
         continue;
       }
-      const uint32_t b = tl & 1, tph = (tl >> 1) & 1;
-      mbar_wait(tfull + b, tph);
-#ifdef MK_TRACE
-      if (q == 0 && lane == 0) TRACE(2, 2 * tl, gtime());
-#endif
-      tc_fence_after();
-      const uint32_t tl_addr = tbase + ((uint32_t)(q * 32) << 16) + b * (uint32_t)p.c_y;
+      const uint32_t tl_addr = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(i * p.c_y);
       for (int col0 = 0; col0 < p.c_y; col0 += 16) {
         uint32_t v[16];
         tmem_ld16(tl_addr + col0, v);
@@ -381,24 +524,17 @@ __global__ void __launch_bounds__(kThreads, 1) k_conv_umma(const __grid_constant
           }
         }
       }
-      tc_fence_before();
-#ifdef MK_TRACE
-      if (q == 0 && lane == 0) TRACE(2, 2 * tl + 1, gtime());
-#endif
-      mbar_arrive(tempty + b);
-      ++tl;
     }
   }
+  ACCT_DUMP;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == kMmaWarp) tmem_dealloc(tbase, p.tmem_cols);
+  if (warp == kFwdMma) tmem_dealloc(tbase, p.tmem_cols);
 }
 
 // ------------------------------------------------------------------ weight gradient
 struct WgradParams {
-  CUtensorMap tmap_g;      // g as [n_out][c_out], box {pwa, 1}
-  CUtensorMap tmap_x;      // x as [n_in][c_in],  box {pwb, 1}
   const __nv_bfloat16* g;  // [n_out][c_out]
   const __nv_bfloat16* x;  // [n_in][c_in]
   const int32_t* in_idx;
@@ -406,85 +542,74 @@ struct WgradParams {
   const int4* segs;          // (k, begin, end, slot), grouped by CTA
   const int32_t* seg_begin;  // [n_cta + 1]
   float* part;               // [n_slots][c_out][c_in]
-  int c_out, c_in, stages, halves, lag;
+  int c_out, c_in, halves;
+  int sa, ga;                // stage slots (== producer warps), slots per commit group
   int pwa, pwb;              // panel widths (channels) of A (G) and B (X)
-  uint32_t a_bytes, b_bytes, stage_bytes, tmem_cols;
+  uint32_t a_bytes, b_bytes, slot_bytes, tmem_cols;
 };
 
 constexpr int kPairsPerStage = 64;
-constexpr int kUnitPairs = 1024;            // pairs per index-staging unit (16 stages)
-constexpr int kIdxBuf = kUnitPairs + 8;     // int32 entries per staged index array
+constexpr int kMaxSegs = 64;  // segments per CTA (<= 1 + K)
 
-// Enumerates the index-staging units of a CTA: every segment (k, begin, end, slot) of the
-// CTA cut into runs of at most kUnitPairs pairs (multiples of the 64-pair stage).
-struct WUnitIter {
-  const int4* segs;
-  int si, se;
-  int4 sg;
-  int b, e;
-  __device__ WUnitIter(const int4* s, int sb, int se_) : segs(s), si(sb - 1), se(se_), b(0), e(0) { sg = make_int4(0, 0, 0, 0); }
-  __device__ __forceinline__ bool next() {
-    if (e < sg.z) {  // more of the current segment
-      b = e;
-      e = min(b + kUnitPairs, sg.z);
-      return true;
-    }
-    while (++si < se) {
-      sg = __ldg(segs + si);
-      if (sg.y < sg.z) {
-        b = sg.y;
-        e = min(b + kUnitPairs, sg.z);
-        return true;
-      }
-    }
-    return false;
-  }
-};
-
-// Bulk-copies out_idx / in_idx of the unit's pairs (16-byte aligned superset) into `buf`.
-__device__ __forceinline__ void stage_idx(const int32_t* out_idx, const int32_t* in_idx, const WUnitIter& u,
-                                          int32_t* buf, uint64_t* bar) {
-  const int b4 = u.b & ~3, e4 = (u.e + 3) & ~3;
-  const uint32_t bytes = (uint32_t)(e4 - b4) * 4;
-  mbar_arrive_expect_tx(bar, 2 * bytes);
-  bulk_g2s(buf, out_idx + b4, bytes, bar);
-  bulk_g2s(buf + kIdxBuf, in_idx + b4, bytes, bar);
-}
-
+// Weight gradient: split-K over the pairs.  Step g = 64 pairs of one segment (k, range) of
+// this CTA, done by producer warp g % sa in its own stage slot (warp-per-stage, as in the
+// forward kernel): the warp prefetches the next step's 64 out/in indices (4-byte cp.async,
+// private double buffer), gathers the 64 G rows into the MN-major A panels and the 64 X
+// rows into the MN-major B panels (16-byte cp.async, zero-fill past the segment end),
+// waits for its group and arrives once.  The MMA thread accumulates a segment in TMEM
+// (M = C_out padded to 128 with a constant zero panel, N = C_in, K = 16 pairs), commits
+// stage slots in groups, and publishes the segment to the epilogue, which writes the fp32
+// partial dW_k tile of the segment's slot.
 __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constant__ WgradParams p) {
   constexpr int PS = kPairsPerStage;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  const int S = p.stages;
-  int32_t* idx_s = (int32_t*)(smem + (size_t)S * p.stage_bytes);  // [2][out, in][kIdxBuf]
-  uint64_t* full = (uint64_t*)(idx_s + 4 * kIdxBuf);
-  uint64_t* empty = full + S;
-  uint64_t* tfull = empty + S;
+  int32_t* ibuf_all = (int32_t*)(smem + (size_t)p.sa * p.slot_bytes);  // [sa][2][2][64]
+  int32_t* seg_g0 = ibuf_all + p.sa * 4 * PS;                          // [kMaxSegs + 1]
+  uint64_t* a_full = (uint64_t*)(seg_g0 + kMaxSegs + 2);
+  uint64_t* a_empty = a_full + p.sa;
+  uint64_t* tfull = a_empty + p.sa;
   uint64_t* tempty = tfull + 1;
-  uint64_t* nfull = tempty + 1;
-  uint32_t* tmem_slot = (uint32_t*)(nfull + 2);
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rba = p.pwa * 2, rbb = p.pwb * 2;              // panel row bytes
-  const int npa = p.c_out / p.pwa, npb = p.c_in / p.pwb;   // real panels
-  const uint32_t panel_a = PS * rba, panel_b = PS * rbb;   // panel strides (LBO)
+  const int rba = p.pwa * 2, rbb = p.pwb * 2;             // panel row bytes
+  const int npa = p.c_out / p.pwa, npb = p.c_in / p.pwb;  // real panels
+  const uint32_t panel_a = PS * rba, panel_b = PS * rbb;  // panel strides (LBO)
+  const int sb = p.seg_begin[blockIdx.x], se = min(p.seg_begin[blockIdx.x + 1], sb + kMaxSegs);
+  const int nseg = se - sb;
 
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < S; ++s) {
-      mbar_init(full + s, kProdWarps);
-      mbar_init(empty + s, 1);
+  if (warp == 0) {  // plan: first step of every segment
+    int base = 0;
+    for (int i0 = 0; i0 < nseg; i0 += 32) {
+      const int i = i0 + lane;
+      const int4 sg = i < nseg ? p.segs[sb + i] : make_int4(0, 0, 0, 0);
+      const int st = i < nseg ? (sg.z - sg.y + PS - 1) / PS : 0;
+      int incl = st;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (i < nseg) seg_g0[i] = base + incl - st;
+      base += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) seg_g0[nseg] = base;
+  }
+  if (threadIdx.x == 32) {
+    for (int s = 0; s < p.sa; ++s) {
+      mbar_init(a_full + s, 1);
+      mbar_init(a_empty + s, 1);
     }
     mbar_init(tfull, 1);
     mbar_init(tempty, kEpiWarps * 32);
-    mbar_init(nfull, 1);
-    mbar_init(nfull + 1, 1);
     fence_mbar_init();
   }
   // zero the padding panels of A (M padded to 128 per half) once; never overwritten
   {
     const int tot_pa = (int)(p.a_bytes / panel_a);
-    for (int s = 0; s < S; ++s)
+    for (int s = 0; s < p.sa; ++s)
       for (int pa = npa; pa < tot_pa; ++pa) {
-        uint4* z = (uint4*)(smem + (size_t)s * p.stage_bytes + (size_t)pa * panel_a);
+        uint4* z = (uint4*)(smem + (size_t)s * p.slot_bytes + (size_t)pa * panel_a);
         for (int i = threadIdx.x; i < (int)(panel_a / 16); i += kThreads) z[i] = make_uint4(0, 0, 0, 0);
       }
   }
@@ -494,103 +619,143 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
-  const int sb = p.seg_begin[blockIdx.x], se = p.seg_begin[blockIdx.x + 1];
+  const int n_steps = seg_g0[nseg];
+  ACCT_DECL
 
-  if (warp < kProdWarps) {
-    // 128 threads gather, per 64-pair stage, the G rows (A panels) and X rows (B panels) of
-    // the pairs with 16-byte cp.async; pairs past the segment end are zero-filled.  One
-    // barrier arrival per warp (StageSignal).
-    const int t = threadIdx.x;
+  if (warp < p.sa) {
+    // ------------------------------------------------------------ gather producers
+    int32_t* ib_w = ibuf_all + warp * 4 * PS;  // [2][out, in][64]
+    int si = 0;
+    auto locate = [&](int g, int* b0, int* e) {
+      while (seg_g0[si + 1] <= g) ++si;
+      const int4 sg = p.segs[sb + si];
+      *b0 = sg.y + (g - seg_g0[si]) * PS;
+      *e = sg.z;
+    };
+    auto fetch_idx = [&](int b0, int e, int buf) {
+      int32_t* d = ib_w + buf * 2 * PS;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = lane + 32 * h;
+        if (b0 + i < e) {
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(d + i)), "l"(p.out_idx + b0 + i) : "memory");
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(d + PS + i)), "l"(p.in_idx + b0 + i)
+                       : "memory");
+        }
+      }
+    };
+    int g = warp, b0 = 0, e = 0, b0n = 0, en = 0;
+    if (g < n_steps) {
+      locate(g, &b0, &e);
+      fetch_idx(b0, e, 0);
+      cp_async_commit();
+      cp_async_wait_n(0);
+      __syncwarp();
+    }
+    uint32_t my = 0, ib = 0;
     const int ca = p.c_out / 8, cb = p.c_in / 8;  // 16-byte chunks per G row / X row
     const int ja = rba / 16, jb = rbb / 16;       // chunks per panel row
-    WUnitIter cur(p.segs, sb, se), st(p.segs, sb, se);
-    if (t == 0)
-      for (int b = 0; b < 2; ++b)
-        if (st.next()) stage_idx(p.out_idx, p.in_idx, st, idx_s + b * 2 * kIdxBuf, nfull + b);
-    StageSignal sig(p.lag, (uint32_t)S);
-    uint32_t s = 0, ph = 0, ub = 0, nph = 0;
-    while (cur.next()) {
-      mbar_wait(nfull + ub, (nph >> ub) & 1u);
-      nph ^= 1u << ub;
-      const int32_t* oi = idx_s + ub * 2 * kIdxBuf;
-      const int32_t* ii = oi + kIdxBuf;
-      const int b4 = cur.b & ~3;
-      for (int b0 = cur.b; b0 < cur.e; b0 += PS) {
-        mbar_wait(empty + s, ph ^ 1);
-        const uint32_t a_s = smem_u32(smem + (size_t)s * p.stage_bytes), b_s = a_s + p.a_bytes;
-        for (int idx = t; idx < PS * ca; idx += kProdWarps * 32) {  // G rows -> A panels
+    for (; g < n_steps; g += p.sa) {
+      const bool have_n = g + p.sa < n_steps;
+      if (have_n) {
+        locate(g + p.sa, &b0n, &en);
+        fetch_idx(b0n, en, ib ^ 1);
+      }
+      ACCT_WAIT(0, a_empty + warp / p.ga, (my & 1) ^ 1);
+      const uint32_t a_s = smem_u32(smem + (size_t)warp * p.slot_bytes), b_s = a_s + p.a_bytes;
+      const int32_t* oi = ib_w + ib * 2 * PS;
+      const int32_t* ii = oi + PS;
+      // G rows -> A panels, X rows -> B panels.  Fast path when a row's chunk count divides
+      // the warp: each lane keeps one chunk column (no per-element divisions).
+      if ((32 % ca) == 0) {
+        const int ch = lane % ca, pa = ch / ja, j = ch - pa * ja;
+        const __nv_bfloat16* src = p.g + ch * 8;
+        const uint32_t dst0 = a_s + pa * panel_a;
+#pragma unroll 4
+        for (int pr = lane / ca; pr < PS; pr += 32 / ca) {
+          const uint32_t dst = dst0 + swz(pr, j, rba);
+          if (b0 + pr < e) cp_async16(dst, src + (int64_t)oi[pr] * p.c_out, 16u);
+          else st_shared_zero16(dst);
+        }
+      } else {
+        for (int idx = lane; idx < PS * ca; idx += 32) {
           const int pr = idx / ca, ch = idx - pr * ca;
-          const int pi = b0 + pr;
-          const bool ok = pi < cur.e;
           const int pa = ch / ja, j = ch - pa * ja;
-          if (ok) cp_async16(a_s + pa * panel_a + swz(pr, j, rba), p.g + (int64_t)oi[pi - b4] * p.c_out + ch * 8, 16u);
-          else st_shared_zero16(a_s + pa * panel_a + swz(pr, j, rba));
+          const uint32_t dst = a_s + pa * panel_a + swz(pr, j, rba);
+          if (b0 + pr < e) cp_async16(dst, p.g + (int64_t)oi[pr] * p.c_out + ch * 8, 16u);
+          else st_shared_zero16(dst);
         }
-        for (int idx = t; idx < PS * cb; idx += kProdWarps * 32) {  // X rows -> B panels
+      }
+      if ((32 % cb) == 0) {
+        const int ch = lane % cb, pb = ch / jb, j = ch - pb * jb;
+        const __nv_bfloat16* src = p.x + ch * 8;
+        const uint32_t dst0 = b_s + pb * panel_b;
+#pragma unroll 4
+        for (int pr = lane / cb; pr < PS; pr += 32 / cb) {
+          const uint32_t dst = dst0 + swz(pr, j, rbb);
+          if (b0 + pr < e) cp_async16(dst, src + (int64_t)ii[pr] * p.c_in, 16u);
+          else st_shared_zero16(dst);
+        }
+      } else {
+        for (int idx = lane; idx < PS * cb; idx += 32) {
           const int pr = idx / cb, ch = idx - pr * cb;
-          const int pi = b0 + pr;
-          const bool ok = pi < cur.e;
           const int pb = ch / jb, j = ch - pb * jb;
-          if (ok) cp_async16(b_s + pb * panel_b + swz(pr, j, rbb), p.x + (int64_t)ii[pi - b4] * p.c_in + ch * 8, 16u);
-          else st_shared_zero16(b_s + pb * panel_b + swz(pr, j, rbb));
-        }
-        sig.issued(full);
-        if (++s == (uint32_t)S) {
-          s = 0;
-          ph ^= 1;
+          const uint32_t dst = b_s + pb * panel_b + swz(pr, j, rbb);
+          if (b0 + pr < e) cp_async16(dst, p.x + (int64_t)ii[pr] * p.c_in + ch * 8, 16u);
+          else st_shared_zero16(dst);
         }
       }
-      named_bar_sync(1, kProdWarps * 32);
-      if (t == 0 && st.next()) {
-        fence_proxy_async_smem();
-        stage_idx(p.out_idx, p.in_idx, st, idx_s + ub * 2 * kIdxBuf, nfull + ub);
-      }
-      ub ^= 1;
+      cp_async_commit();
+      cp_async_wait_n(0);
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a_full + warp);
+      ++my;
+      ib ^= 1;
+      b0 = b0n;
+      e = en;
     }
-    sig.drain(full);
   } else if (warp == kMmaWarp) {
     if (lane == 0) {
       const uint32_t idesc = idesc_bf16(kTileM, p.c_in, 1, 1);
-      const uint32_t la = layout_code(rba), lb = layout_code(rbb);
-      uint32_t s = 0, ph = 0, n_seg = 0;
-      for (int si = sb; si < se; ++si) {
-        const int4 sg = p.segs[si];
-        if (sg.y >= sg.z) continue;
-        mbar_wait(tempty, (n_seg & 1) ^ 1);
+      const uint64_t ahi = smem_desc(0, panel_a, 8 * rba, layout_code(rba));
+      const uint64_t bhi = smem_desc(0, panel_b, 8 * rbb, layout_code(rbb));
+      const uint32_t s0 = smem_u32(smem) >> 4, sstep = p.slot_bytes >> 4, boff = p.a_bytes >> 4;
+      const uint32_t ka = (16 * rba) >> 4, kb = (16 * rbb) >> 4, hstep = ((128 / p.pwa) * panel_a) >> 4;
+      uint32_t s = 0, sph = 0, gq = 0;
+      for (int i = 0; i < nseg; ++i) {
+        mbar_wait(tempty, (i & 1) ^ 1);
         tc_fence_after();
         uint32_t acc = 0;
-        for (int b0 = sg.y; b0 < sg.z; b0 += PS) {
-          mbar_wait(full + s, ph);
+        for (int q = seg_g0[i]; q < seg_g0[i + 1]; ++q) {
+          ACCT_WAIT(2, a_full + s, sph);
           tc_fence_after();
-          const uint32_t a_s = smem_u32(smem + (size_t)s * p.stage_bytes), b_s = a_s + p.a_bytes;
+          const uint32_t alo = s0 + s * sstep, blo = alo + boff;
 #pragma unroll
           for (int kk = 0; kk < PS / 16; ++kk) {
-            const uint64_t bd = smem_desc(b_s + kk * 16 * rbb, panel_b, 8 * rbb, lb);
-            for (int h = 0; h < p.halves; ++h) {
-              const uint32_t a_half = a_s + h * (128 / p.pwa) * panel_a;
-              const uint64_t ad = smem_desc(a_half + kk * 16 * rba, panel_a, 8 * rba, la);
-              umma_f16(tbase + h * (uint32_t)p.c_in, ad, bd, idesc, acc);
-            }
+            for (int h = 0; h < p.halves; ++h)
+              umma_f16(tbase + h * (uint32_t)p.c_in, ahi | (uint64_t)(alo + h * hstep + kk * ka),
+                       bhi | (uint64_t)(blo + kk * kb), idesc, acc);
             acc = 1;
           }
-          umma_commit(empty + s);
-          if (++s == (uint32_t)S) {
+          if (++gq == (uint32_t)p.ga) {
+            umma_commit(a_empty + s / p.ga);
+            gq = 0;
+          }
+          if (++s == (uint32_t)p.sa) {
             s = 0;
-            ph ^= 1;
+            sph ^= 1;
           }
         }
         umma_commit(tfull);
-        ++n_seg;
       }
     }
     __syncwarp();
-  } else {
+  } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
     const int q = warp & 3;
-    uint32_t n_seg = 0;
-    for (int si = sb; si < se; ++si) {
-      const int4 sg = p.segs[si];
-      if (sg.y >= sg.z) continue;
-      mbar_wait(tfull, n_seg & 1);
+    for (int i = 0; i < nseg; ++i) {
+      const int4 sg = p.segs[sb + i];
+      ACCT_WAIT(0, tfull, i & 1);
       tc_fence_after();
       for (int h = 0; h < p.halves; ++h) {
         const int co = h * 128 + q * 32 + lane;
@@ -603,23 +768,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
           if (co < p.c_out) {
             float4* d4 = (float4*)(dst + col0);
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
-              d4[e] = make_float4(__uint_as_float(v[4 * e]), __uint_as_float(v[4 * e + 1]),
-                                  __uint_as_float(v[4 * e + 2]), __uint_as_float(v[4 * e + 3]));
+            for (int e4 = 0; e4 < 4; ++e4)
+              d4[e4] = make_float4(__uint_as_float(v[4 * e4]), __uint_as_float(v[4 * e4 + 1]),
+                                   __uint_as_float(v[4 * e4 + 2]), __uint_as_float(v[4 * e4 + 3]));
           }
         }
       }
       tc_fence_before();
       mbar_arrive(tempty);
-      ++n_seg;
     }
   }
+  ACCT_DUMP;
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == kMmaWarp) tmem_dealloc(tbase, p.tmem_cols);
 }
-
 
 // ------------------------------------------------------------------ host: tensor maps
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -673,12 +837,17 @@ void set_smem_once(F* f, int bytes) {
 extern "C" int mk_debug_trace(unsigned long long* host_out) {
   return (int)cudaMemcpyFromSymbol(host_out, g_trace, sizeof(g_trace));
 }
+extern "C" int mk_debug_acct(unsigned long long* host_out) {
+  return (int)cudaMemcpyFromSymbol(host_out, g_acct, sizeof(g_acct));
+}
 #endif
 
 mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, int64_t n_src, int c_x, const void* W,
                             int c_in_w, int c_out_w, void* y, int c_y, mk_dtype out_dt, int64_t n_rows, bool trans,
                             cudaStream_t s) {
   if (n_rows == 0) return MK_OK;
+  (void)n_src;
+  if (nb.K > kMaxK) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: more than 128 kernel offsets");
   const int CH = c_x % 64 == 0 ? 64 : c_x % 32 == 0 ? 32 : 16;
   const int nch = c_x / CH;
   FwdParams p;
@@ -693,14 +862,20 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   p.out_f32 = out_dt == MK_F32;
   p.a_bytes = kTileM * CH * 2;
   p.b_bytes = (uint32_t)c_y * CH * 2;
-  p.stage_bytes = (p.a_bytes + p.b_bytes + 1023) & ~1023u;
-  const int reserve = 1024 + 256 + 2 * kNbrBuf * 4;
-  p.stages = std::min<int>(8, (kMaxSmem - reserve) / (int)p.stage_bytes);
-  if (p.stages < 2) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: channel counts too large for the smem pipeline");
-
-  p.tmem_cols = pow2_cols(2 * c_y);
-  if (p.tmem_cols > 512) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: C_out above 256");
-  p.lag = std::min(4, p.stages - 1);
+  // Two tiles per CTA (one TMEM accumulator each, <= 256 columns so two CTAs share an SM);
+  // smem ~100 KB per CTA: 4 A stages (16 KB each at CH=64), a ring of 4 W chunks, per-warp
+  // index buffers and the plan (B200 gathers ~9 TB/s at 8 warps/SM, ubench_gather.cu).
+  p.tb = std::max(1, std::min(2, 256 / c_y));
+  p.tmem_cols = pow2_cols((uint32_t)(p.tb * c_y));
+  const int base = 1024 + 512 + kFwdProd * 2 * kTileM * 4 + (int)sizeof(Plan);
+  p.sw = nch * 2;
+  if (base + p.sw * (int)p.b_bytes + kFwdProd * (int)p.a_bytes <= kMaxSmem / 2 - 1024 - 2 * nch * (int)p.b_bytes)
+    p.sw = nch * 4;
+  const int fixed = base + p.sw * (int)p.b_bytes;
+  p.sa = std::min(kFwdProd, (kMaxSmem - fixed) / (int)p.a_bytes);
+  p.ga = p.sa % 2 == 0 ? 2 : 1;
+  if (p.sa < 2 || p.tmem_cols > 512)
+    MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: channel counts too large for the smem pipeline");
   const size_t wbytes = (size_t)nb.K * nch * p.b_bytes;
   uint8_t* wpack = (uint8_t*)dev_alloc(ctx->alloc, wbytes, s);
   if (!wpack) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 conv: weight pack allocation failed");
@@ -711,21 +886,17 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
     g_launches++;
   }
   p.wpack = wpack;
-  if (!make_row_map(&p.tmap_x, n_src > 0 ? x : (const void*)wpack, std::max<int64_t>(n_src, 1), c_x, CH)) {
-    dev_free(ctx->alloc, wpack, s);
-    MK_FAIL(MK_ERR_CUDA, "bf16 conv: cuTensorMapEncodeTiled failed (features must be 16-byte aligned)");
-  }
-  const int smem = p.stages * (int)p.stage_bytes + reserve;
-  const int grid = (int)std::min<int64_t>(p.ntiles, ctx->num_sms);
+  const int smem = fixed + p.sa * (int)p.a_bytes;
+  const int64_t grid = ceil_div(p.ntiles, p.tb);  // one CTA per tb adjacent tiles
   if (CH == 64) {
     set_smem_once(k_conv_umma<64>, smem);
-    k_conv_umma<64><<<grid, kThreads, smem, s>>>(p);
+    k_conv_umma<64><<<(unsigned)grid, kFwdThreads, smem, s>>>(p);
   } else if (CH == 32) {
     set_smem_once(k_conv_umma<32>, smem);
-    k_conv_umma<32><<<grid, kThreads, smem, s>>>(p);
+    k_conv_umma<32><<<(unsigned)grid, kFwdThreads, smem, s>>>(p);
   } else {
     set_smem_once(k_conv_umma<16>, smem);
-    k_conv_umma<16><<<grid, kThreads, smem, s>>>(p);
+    k_conv_umma<16><<<(unsigned)grid, kFwdThreads, smem, s>>>(p);
   }
   g_launches++;
   cudaError_t e = cudaGetLastError();
@@ -750,24 +921,22 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   p.pwb = c_in % 64 == 0 ? 64 : c_in % 32 == 0 ? 32 : 16;
   p.halves = c_out > 128 ? 2 : 1;
   if (c_out > 256) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: C_out above 256");
+  if (m->K + 1 > kMaxSegs) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: more than 63 kernel offsets");
   p.a_bytes = (uint32_t)(p.halves * 128) * kPairsPerStage * 2;  // M padded to 128 per half
   p.b_bytes = (uint32_t)c_in * kPairsPerStage * 2;
-  p.stage_bytes = (p.a_bytes + p.b_bytes + 1023) & ~1023u;
-  const int reserve = 1024 + 256 + 4 * kIdxBuf * 4;
-  p.stages = std::min<int>(6, (kMaxSmem - reserve) / (int)p.stage_bytes);
+  p.slot_bytes = (p.a_bytes + p.b_bytes + 1023) & ~1023u;
+  const int reserve = 1024 + 1024 + kProdWarps * 4 * kPairsPerStage * 4 + (kMaxSegs + 2) * 4;
+  p.sa = std::min(kProdWarps, (kMaxSmem - reserve) / (int)p.slot_bytes);
+  if (p.sa >= 8) p.sa -= p.sa % 4;
+  p.ga = p.sa % 4 == 0 ? 4 : p.sa % 2 == 0 ? 2 : 1;
   p.tmem_cols = pow2_cols((uint32_t)(p.halves * c_in));
-  p.lag = std::min(4, p.stages - 1);
-  if (p.stages < 2 || p.tmem_cols > 512) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: channel counts too large");
-  if (m->n_wslots > 0 &&
-      (!make_row_map(&p.tmap_g, g, std::max<int64_t>(m->n_out, 1), c_out, p.pwa) ||
-       !make_row_map(&p.tmap_x, x, std::max<int64_t>(m->n_in, 1), c_in, p.pwb)))
-    MK_FAIL(MK_ERR_CUDA, "bf16 wgrad: cuTensorMapEncodeTiled failed (features must be 16-byte aligned)");
+  if (p.sa < 2 || p.tmem_cols > 512) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: channel counts too large");
   float* part = nullptr;
   if (m->n_wslots > 0) {
     part = (float*)dev_alloc(ctx->alloc, sizeof(float) * m->n_wslots * te, s);
     if (!part) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 wgrad: workspace allocation failed");
     p.part = part;
-    const int smem = p.stages * (int)p.stage_bytes + reserve;
+    const int smem = p.sa * (int)p.slot_bytes + reserve;
     set_smem_once(k_wgrad_umma, smem);
     k_wgrad_umma<<<m->n_wcta, kThreads, smem, s>>>(p);
     g_launches++;

@@ -46,12 +46,15 @@ __global__ void __launch_bounds__(kThreads) k_probe(const int4* __restrict__ oke
                                                     uint32_t mask, const int32_t* __restrict__ offs, int K, int D,
                                                     int sign, int4 scale4, int32_t* __restrict__ nbr,
                                                     int32_t* __restrict__ tile_cnt, int64_t ntiles,
-                                                    uint32_t* __restrict__ tile_mask, int mw) {
+                                                    uint32_t* __restrict__ tile_mask, int mw,
+                                                    uint32_t* __restrict__ rowmask) {
   extern __shared__ int32_t sm[];
   int32_t* s_off = sm;              // [K*D]
   int32_t* s_cnt = sm + K * D;      // [K]
+  uint32_t* s_rm = (uint32_t*)(s_cnt + K);  // [128] row masks (K <= 32)
   for (int i = threadIdx.x; i < K * D; i += kThreads) s_off[i] = offs[i];
   for (int i = threadIdx.x; i < K; i += kThreads) s_cnt[i] = 0;
+  if (threadIdx.x < kTileRows) s_rm[threadIdx.x] = 0;
   __syncthreads();
   const int32_t scale[4] = {scale4.x, scale4.y, scale4.z, scale4.w};
   const int64_t tile = blockIdx.x;
@@ -59,15 +62,19 @@ __global__ void __launch_bounds__(kThreads) k_probe(const int4* __restrict__ oke
   const bool valid = o < n_out;
   int4 u = make_int4(0, 0, 0, 0);
   if (valid) u = okeys[o];
+  uint32_t rm = 0;
   for (int k = threadIdx.x / kTileRows; k < K; k += kThreads / kTileRows) {
     int32_t a = -1;
     int4 q;
     if (valid && shift_key(u, D, s_off + k * D, sign, scale, &q)) a = probe(tkeys, tvals, mask, q);
     nbr[(int64_t)k * n_pad + o] = a;  // rows padded to whole tiles (-1)
+    if (a >= 0 && k < 32) rm |= 1u << k;
     const unsigned b = __ballot_sync(0xffffffffu, a >= 0);
     if ((threadIdx.x & 31) == 0 && b) atomicAdd(s_cnt + k, __popc(b));
   }
+  if (rowmask) atomicOr(s_rm + (threadIdx.x & (kTileRows - 1)), rm);
   __syncthreads();
+  if (rowmask && threadIdx.x < kTileRows && valid) rowmask[o] = s_rm[threadIdx.x];
   for (int k = threadIdx.x; k < K; k += kThreads) tile_cnt[(int64_t)k * ntiles + tile] = s_cnt[k];
   for (int w = threadIdx.x; w < mw; w += kThreads) {
     uint32_t bits = 0;
@@ -146,6 +153,37 @@ __global__ void __launch_bounds__(kThreads) k_emit(const int32_t* __restrict__ n
       atomicOr(tile_maskT + (int64_t)(a / kTileRows) * mw + (k >> 5), 1u << (k & 31));
     }
   }
+}
+
+// Row masks of the dgrad table: bit k set when nbrT[k][a] >= 0 (K <= 32).
+__global__ void k_rowmask_T(const int32_t* __restrict__ nbrT, int64_t stride, int64_t n, int K,
+                            uint32_t* __restrict__ rowmask) {
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n; a += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t rm = 0;
+    for (int k = 0; k < K; ++k) rm |= (nbrT[(int64_t)k * stride + a] >= 0 ? 1u : 0u) << k;
+    rowmask[a] = rm;
+  }
+}
+
+// Neighbour table in permuted row order: out[k][i] = tab[k][perm[i]] (padding rows -1), and
+// the active-offset mask of every permuted 128-row tile (K <= 32: one word).
+__global__ void __launch_bounds__(kTileRows) k_permute(const int32_t* __restrict__ tab, int64_t stride, int64_t n,
+                                                       int K, const int32_t* __restrict__ perm,
+                                                       int32_t* __restrict__ out, uint32_t* __restrict__ tmask) {
+  __shared__ uint32_t s_bits;
+  if (threadIdx.x == 0) s_bits = 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * kTileRows + threadIdx.x;
+  const int32_t r = i < n ? perm[i] : -1;
+  uint32_t bits = 0;
+  for (int k = 0; k < K; ++k) {
+    const int32_t a = r >= 0 ? tab[(int64_t)k * stride + r] : -1;
+    out[(int64_t)k * stride + i] = a;
+    if (__any_sync(0xffffffffu, a >= 0)) bits |= 1u << k;
+  }
+  if ((threadIdx.x & 31) == 0) atomicOr(&s_bits, bits);
+  __syncthreads();
+  if (threadIdx.x == 0) tmask[blockIdx.x] = s_bits;
 }
 
 // Dgrad tile masks of a symmetric map: bit k of tile t = bit mirror[k] of the forward mask.
@@ -246,6 +284,13 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     if (scratch) dev_free(m->alloc, scratch, s);
     return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: device allocation failed");
   }
+  // Row masks for the bitmask ordering of the conv tiles (K <= 32 offsets only).
+  const bool sort_rows = K <= 32;
+  uint32_t* rowmask = sort_rows ? (uint32_t*)dev_alloc(m->alloc, sizeof(uint32_t) * std::max<int64_t>(1, std::max(n_out, n_in)), s) : nullptr;
+  if (sort_rows && !rowmask) {
+    dev_free(m->alloc, scratch, s);
+    return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: device allocation failed");
+  }
   int64_t* tile_off = (int64_t*)scratch;
   int64_t* totals = tile_off + K * ntiles;
   int32_t* tile_cnt = (int32_t*)(totals + K);
@@ -261,9 +306,9 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     ck(cudaMemsetAsync(m->tile_maskT, 0, sizeof(uint32_t) * ntilesT * mw, s));
   }
   if (n_out > 0) {
-    k_probe<<<(unsigned)ntiles, kThreads, sizeof(int32_t) * (K * D + K), s>>>(
+    k_probe<<<(unsigned)ntiles, kThreads, sizeof(int32_t) * (K * D + K + kTileRows), s>>>(
         out->keys, n_out, n_pad, in->table.keys, in->table.vals, in->table.mask, d_offs, K, D, sign, scale4, m->nbr,
-        tile_cnt, ntiles, m->tile_mask, mw);
+        tile_cnt, ntiles, m->tile_mask, mw, rowmask);
     g_launches++;
     k_scan<<<K, 1024, 0, s>>>(tile_cnt, ntiles, tile_off, totals);
     g_launches++;
@@ -333,10 +378,40 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
                                                                         m->tile_maskT, mw);
     g_launches++;
   }
+  // Order the conv tiles' rows by neighbour bitmask (stable radix sort of the row masks):
+  // rows sharing offsets share tiles, so the tensor-core kernels skip empty (tile, k) units.
+  // The permutation is internal; the CSR above and all exported row orders are unchanged.
+  if (sort_rows && n_out > 0) {
+    auto permute = [&](int32_t*& tab, int64_t stride, int64_t n, int64_t nt, uint32_t* tmask, int32_t*& perm_out) {
+      int32_t* perm = (int32_t*)alloc(sizeof(int32_t) * stride);
+      int32_t* tabP = (int32_t*)alloc(sizeof(int32_t) * (int64_t)K * stride);
+      if (!perm || !tabP) return MK_ERR_OUT_OF_MEMORY;
+      mk_status st2 = radix_sort_perm(m->alloc, rowmask, n, K, perm, s);
+      if (st2 != MK_OK) return st2;
+      k_permute<<<(unsigned)nt, kTileRows, 0, s>>>(tab, stride, n, K, perm, tabP, tmask);
+      g_launches++;
+      tab = tabP;  // the unpermuted table stays owned (freed with the map) but is no longer read
+      perm_out = perm;
+      return MK_OK;
+    };
+    mk_status st2 = permute(m->nbr, n_pad, n_out, ntiles, m->tile_mask, m->perm);
+    if (st2 == MK_OK && !symmetric && n_in > 0) {
+      k_rowmask_T<<<(unsigned)std::min<int64_t>(ceil_div(n_in, 256), 4096), 256, 0, s>>>(m->nbrT, nT_pad, n_in, K, rowmask);
+      g_launches++;
+      st2 = permute(m->nbrT, nT_pad, n_in, ntilesT, m->tile_maskT, m->permT);
+    }
+    if (st2 != MK_OK) {
+      dev_free(m->alloc, rowmask, s);
+      dev_free(m->alloc, scratch, s);
+      return fail(st2, "mk_kmap_build: row ordering failed");
+    }
+  }
+  if (rowmask) dev_free(m->alloc, rowmask, s);
   if (symmetric) {
     k_mirror_mask<<<(unsigned)std::min<int64_t>(ceil_div(ntiles, 256), 1024), 256, 0, s>>>(m->tile_mask, ntiles, mw,
                                                                                           m->d_mirror, K, m->tile_maskT);
     g_launches++;
+    m->permT = m->perm;  // same row set, mirrored masks: same ordering
   }
   ck(cudaGetLastError());
   dev_free(m->alloc, scratch, s);

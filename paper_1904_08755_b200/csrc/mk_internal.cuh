@@ -164,6 +164,10 @@ struct mk_kmap {
   int32_t* nbr = nullptr;
   int32_t* nbrT = nullptr;
   int64_t nbr_stride = 0;   // rows of nbr, padded to a multiple of 128 (padding = -1)
+  // Internal row order of the conv tiles (bitmask-sorted when K <= 32, else NULL = identity):
+  // nbr / nbrT / the tile masks are stored in this order; position i holds row perm[i].
+  int32_t* perm = nullptr;
+  int32_t* permT = nullptr;
   int64_t nbrT_stride = 0;  // rows of the dgrad table (nbrT or, when symmetric, nbr)
   std::vector<int32_t> mirror;      // [K] index of -offset_k, or -1
   int32_t* d_mirror = nullptr;      // [K]
@@ -192,4 +196,6 @@ uint32_t next_pow2(uint64_t v);
 // Table-building pipeline shared by quantize / create / stride (coords.cu).
 // Region enumeration (region.cu):
 mk_status region_enumerate(const mk_region* r, std::vector<int32_t>* offsets, int32_t* K);
+// Stable radix sort of keys (low `bits` bits) -> permutation (sort.cu).  Clobbers keys.
+mk_status radix_sort_perm(const Alloc& a, uint32_t* keys, int64_t n, int bits, int32_t* perm, cudaStream_t s);
 }  // namespace mk

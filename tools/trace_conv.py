@@ -22,19 +22,26 @@ W = (torch.randn(27, 64, 64, device="cuda") * 0.02).bfloat16()
 for _ in range(3):
     mk.conv_forward(m, X, W)
 torch.cuda.synchronize()
-tr = np.zeros((4, 4096), np.uint64)
+tr = np.zeros((4, 8192), np.uint64)
 mk._L.mk_debug_trace.argtypes = [ctypes.c_void_p]
 mk._L.mk_debug_trace(tr.ctypes.data)
-t0 = int(tr[0][0])
-prod = tr[0].astype(np.int64) - t0
-mma = tr[1].astype(np.int64) - t0
-epi = tr[2].astype(np.int64) - t0
-unit = tr[3].astype(np.int64) - t0
-n = 216
-print("producer step: [t_before_empty_wait, t_after] (ns)")
-for g in list(range(0, 12)) + list(range(100, 106)) + list(range(n - 4, n)):
-    print(g, prod[2 * g], prod[2 * g + 1], " mma_full_ok", mma[g])
-print("units (nbr wait start/end):", [(unit[2 * i], unit[2 * i + 1]) for i in range(9)])
-print("epilogue tfull ok / done:", [(epi[2 * i], epi[2 * i + 1]) for i in range(9)])
-d = np.diff(mma[:n])
-print("mma step interval ns: median", np.median(d), "mean", d.mean(), "max", d.max())
+t0 = int(tr[3][0])
+P = (tr[0].astype(np.int64) - t0).reshape(-1, 4)
+M = (tr[1].astype(np.int64) - t0).reshape(-1, 2)
+U = (tr[3].astype(np.int64) - t0).reshape(-1, 4)
+n = 90
+print("step: prod[before_empty, empty_ok, issued, data_ok]  mma[wait, full_ok]")
+for g in list(range(0, 20)) + list(range(100, 106)) + list(range(n - 3, n)):
+    print(g, P[g].tolist(), M[g].tolist())
+print("units: [start, n_empty_ok, staged]")
+for u in range(0, 30):
+    print(u, U[u, :3].tolist())
+for name, arr in (("prod empty wait", P[:n, 1] - P[:n, 0]), ("prod issue", P[:n, 2] - P[:n, 1]),
+                  ("prod data wait", P[:n, 3] - P[:n, 2]), ("mma full wait", M[:n, 1] - M[:n, 0])):
+    print(f"{name:18s} median {np.median(arr):8.0f} ns  mean {arr.mean():8.0f}  max {arr.max():8.0f}")
+Q = (tr[2][2000:2000 + 2 * n].astype(np.int64) - t0).reshape(-1, 2)
+iss = Q[:, 0] - M[:n, 1]
+com = Q[:, 1] - Q[:, 0]
+nxt = M[1:n, 0] - Q[:n - 1, 1]
+for name, arr in (("mma issue (after full_ok -> UMMAs issued)", iss), ("mma commit", com), ("mma loop to next wait", nxt)):
+    print(f"{name:42s} median {np.median(arr):8.0f} ns  mean {arr.mean():8.0f}  max {arr.max():8.0f}")

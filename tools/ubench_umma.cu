@@ -1,0 +1,174 @@
+// ubench_umma.cu — cost of issuing tcgen05.mma (kind::f16, M=128, K=16) from one thread for
+// several N, with a commit + mbarrier round trip every `per` MMAs.  Development tool.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_1904_08755_b200/csrc ubench_umma.cu
+#include <cuda_runtime.h>
+
+#include <cstdio>
+
+#include "sm100.cuh"
+
+using namespace mk::sm100;
+
+__global__ void __launch_bounds__(128, 1) k_umma(int N, int iters, int per, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 65536 / 4; i += 128) ((uint32_t*)sm)[i] = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc_dyn(&tslot, 256);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tslot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_bf16(128, N, 0, 0);
+    const uint32_t a = smem_u32(sm), b = a + 16384;
+    long long t0 = clock64();
+    uint32_t ph = 0;
+    for (int it = 0; it < iters; ++it) {
+      for (int q = 0; q < per; ++q) {
+        const uint64_t ad = smem_desc(a + (q & 3) * 32, 16, 1024, 2);
+        const uint64_t bd = smem_desc(b + (q & 3) * 32, 16, 1024, 2);
+        umma_f16(tbase, ad, bd, idesc, (it | q) ? 1u : 0u);
+      }
+      umma_commit(&bar);
+      mbar_wait(&bar, ph);
+      ph ^= 1;
+    }
+    long long t1 = clock64();
+    out[blockIdx.x] = (t1 - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tbase, 256);
+}
+
+// same, but the commit does not wait (fire-and-forget pipeline, wait only at the end)
+__global__ void __launch_bounds__(128, 1) k_umma_nowait(int N, int iters, int per, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar[8];
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 65536 / 4; i += 128) ((uint32_t*)sm)[i] = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 8; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc_dyn(&tslot, 256);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tslot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_bf16(128, N, 0, 0);
+    const uint32_t a = smem_u32(sm), b = a + 16384;
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      if (it >= 8) mbar_wait(&bar[it & 7], ((it >> 3) - 1) & 1);
+      for (int q = 0; q < per; ++q) {
+        const uint64_t ad = smem_desc(a + (q & 3) * 32, 16, 1024, 2);
+        const uint64_t bd = smem_desc(b + (q & 3) * 32, 16, 1024, 2);
+        umma_f16(tbase, ad, bd, idesc, (it | q) ? 1u : 0u);
+      }
+      umma_commit(&bar[it & 7]);
+    }
+    for (int it = iters > 8 ? iters - 8 : 0; it < iters; ++it) mbar_wait(&bar[it & 7], (it >> 3) & 1);
+    long long t1 = clock64();
+    out[blockIdx.x] = (t1 - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tbase, 256);
+}
+
+// step = [wait on an already-complete mbarrier] [tcgen05 fence] 4 MMAs, commit every 4 steps
+__global__ void __launch_bounds__(128, 1) k_steps(int N, int steps, int fence, int waitbar, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar[3];
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 65536 / 4; i += 128) ((uint32_t*)sm)[i] = 0;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_init(&bar[2], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc_dyn(&tslot, 512);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tslot;
+  if (threadIdx.x == 0) {
+    mbar_arrive(&bar[1]);  // phase 0 of bar[1] complete: waits on it return at once
+    const uint32_t idesc = idesc_bf16(128, N, 0, 0);
+    const uint64_t dhi = smem_desc(0, 16, 1024, 2);
+    const uint32_t a0 = smem_u32(sm) >> 4, b0 = a0 + 1024;
+    long long t0 = clock64();
+    uint32_t ph = 0;
+    for (int st = 0; st < steps; ++st) {
+      if (waitbar) mbar_wait(&bar[1], 0);
+      if (fence) tc_fence_after();
+      const uint32_t d = tbase + (st & 7) * 64;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) umma_f16(d, dhi | (uint64_t)(a0 + kk * 2), dhi | (uint64_t)(b0 + kk * 2), idesc, 1u);
+      if ((st & 3) == 3) {
+        umma_commit(&bar[0]);
+      }
+    }
+    umma_commit(&bar[2]);  // tracks every prior MMA
+    mbar_wait(&bar[2], 0);
+    (void)ph;
+    long long t1 = clock64();
+    out[blockIdx.x] = (t1 - t0);
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tbase, 512);
+}
+
+int main() {
+  long long* d;
+  cudaMalloc(&d, 148 * 8);
+  long long h[148];
+  cudaFuncSetAttribute(k_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  cudaFuncSetAttribute(k_umma_nowait, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  for (int nowait = 0; nowait < 2; ++nowait)
+    for (int N : {64, 128, 256})
+      for (int per : {1, 4, 16}) {
+        const int iters = 2048 / per;
+        if (nowait) k_umma_nowait<<<148, 128, 65536>>>(N, iters, per, d);
+        else k_umma<<<148, 128, 65536>>>(N, iters, per, d);
+        cudaDeviceSynchronize();
+        cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+        double mean = 0;
+        for (int i = 0; i < 148; ++i) mean += h[i];
+        mean /= 148;
+        printf("%s N=%3d per=%2d: %7.1f cycles per MMA  (%s)\n", nowait ? "pipelined" : "wait-each", N, per,
+               mean / (iters * per), cudaGetErrorString(cudaGetLastError()));
+      }
+  cudaFuncSetAttribute(k_steps, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+  for (int fence = 0; fence < 2; ++fence)
+    for (int wb = 0; wb < 2; ++wb) {
+      const int steps = 512;
+      k_steps<<<148, 128, 65536>>>(64, steps, fence, wb, d);
+      cudaDeviceSynchronize();
+      cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+      double mean = 0;
+      for (int i = 0; i < 148; ++i) mean += h[i];
+      mean /= 148;
+      printf("steps N=64 fence=%d waitbar=%d: %7.1f cycles per 4-MMA step (%s)\n", fence, wb, mean / steps,
+             cudaGetErrorString(cudaGetLastError()));
+    }
+  return 0;
+}
