@@ -117,6 +117,7 @@ def run_mk(args, ws, rank, local):
 
     import paper_1904_08755_b200 as mk
     import synthetic
+    from paper_1904_08755_b200.dist import allreduce_grad
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
@@ -156,7 +157,7 @@ def run_mk(args, ws, rank, local):
         _, gw = mk.conv_backward(m, G, X, W, need_gin=False, need_gw=True)           # a8
         mark(5)
         if ws > 1:
-            dist.all_reduce(gw)  # data-parallel weight-gradient sum over NVLink (NCCL)
+            allreduce_grad(gw)  # data-parallel weight-gradient sum over NVLink (NCCL)
         mark(6)
         return y, gin, gw
 
@@ -215,7 +216,7 @@ def run_mk(args, ws, rank, local):
         y = mk.conv_forward(m, x, w)
         gin, gw = mk.conv_backward(m, g, x, w)
         if ws > 1:
-            dist.all_reduce(gw)
+            allreduce_grad(gw)
         y_p.copy_(y, non_blocking=True)
         gi_p.copy_(gin, non_blocking=True)
         gw_p.copy_(gw, non_blocking=True)
