@@ -42,6 +42,44 @@ void dev_free(const Alloc& a, void* p, cudaStream_t s) {
   cudaFreeAsync(p, s);
 }
 
+// Thread-local pinned staging buffer for the few small host<->device copies of a call:
+// pageable cudaMemcpyAsync is synchronous (and slow); pinned copies are true async DMA.
+namespace {
+struct PinnedStage {
+  void* p = nullptr;
+  size_t cap = 0;
+  cudaEvent_t ev = nullptr;
+  bool pending = false;
+  ~PinnedStage() {
+    if (p) cudaFreeHost(p);
+    if (ev) cudaEventDestroy(ev);
+  }
+};
+thread_local PinnedStage t_pin;
+}  // namespace
+
+void* pinned_stage(size_t bytes) {
+  if (t_pin.pending) {  // a previous async copy may still read / write the buffer
+    cudaEventSynchronize(t_pin.ev);
+    t_pin.pending = false;
+  }
+  if (!t_pin.ev && cudaEventCreateWithFlags(&t_pin.ev, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  if (bytes > t_pin.cap) {
+    if (t_pin.p) cudaFreeHost(t_pin.p);
+    t_pin.p = nullptr;
+    t_pin.cap = 0;
+    size_t c = 4096;
+    while (c < bytes) c <<= 1;
+    if (cudaMallocHost(&t_pin.p, c) != cudaSuccess) return nullptr;
+    t_pin.cap = c;
+  }
+  return t_pin.p;
+}
+
+void pinned_in_flight(cudaStream_t s) {
+  if (t_pin.ev && cudaEventRecord(t_pin.ev, s) == cudaSuccess) t_pin.pending = true;
+}
+
 uint32_t next_pow2(uint64_t v) {
   uint64_t p = 1;
   while (p < v) p <<= 1;

@@ -44,15 +44,18 @@ struct QuantSrc {  // Alg. 1 line 1: C_p' <- floor(C_p / v_l)   (R6: fp32 divisi
   __device__ __forceinline__ uint32_t key(int64_t p, int4* k) const {
     int64_t c[4] = {0, 0, 0, 0};
     bool nonfinite = false, range = false;
-    for (int d = 0; d < D; ++d) {
-      const float x = pts[p * D + d];
-      if (!isfinite(x)) {
-        nonfinite = true;
-        continue;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {  // fully unrolled: c[] stays in registers
+      if (d < D) {
+        const float x = pts[p * D + d];
+        if (!isfinite(x)) {
+          nonfinite = true;
+        } else {
+          const float q = floorf(__fdiv_rn(x, voxel));
+          if (!(q >= -2147483648.0f && q < 2147483648.0f)) range = true;
+          else c[d] = (int64_t)q;
+        }
       }
-      const float q = floorf(__fdiv_rn(x, voxel));
-      if (!(q >= -2147483648.0f && q < 2147483648.0f)) range = true;
-      else c[d] = (int64_t)q;
     }
     if (nonfinite) return E_NONFINITE;
     if (range) return E_RANGE;
@@ -69,10 +72,13 @@ struct IntSrc {  // integer rows [n][D+1], batch last (Eq. 1); multiples of the 
   __device__ __forceinline__ uint32_t key(int64_t p, int4* k) const {
     int64_t c[4] = {0, 0, 0, 0};
     const int32_t* r = rows + p * (D + 1);
-    for (int d = 0; d < D; ++d) {
-      const int32_t v = r[d];
-      if (v % ts[d] != 0) return E_STRIDE;
-      c[d] = v;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      if (d < D) {
+        const int32_t v = r[d];
+        if (v % ts[d] != 0) return E_STRIDE;
+        c[d] = v;
+      }
     }
     const int64_t b = r[D];
     if (b < 0) return E_BATCH;
@@ -87,13 +93,16 @@ struct StrideSrc {  // u' = floor_div(u, s_out) * s_out per spatial axis (R7, R1
   __device__ __forceinline__ uint32_t key(int64_t p, int4* k) const {
     const int4 in = keys[p];
     int64_t c[4] = {0, 0, 0, 0};
-    for (int d = 0; d < D; ++d) {
-      const int64_t u = key_axis(in, D, d);
-      int64_t q = u / s[d];
-      if (q * s[d] != u && u < 0) q -= 1;
-      const int64_t v = q * s[d];
-      if (v < INT32_MIN || v > INT32_MAX) return E_RANGE;
-      c[d] = v;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      if (d < D) {
+        const int64_t u = key_axis(in, D, d);
+        int64_t q = u / s[d];
+        if (q * s[d] != u && u < 0) q -= 1;
+        const int64_t v = q * s[d];
+        if (v < INT32_MIN || v > INT32_MAX) return E_RANGE;
+        c[d] = v;
+      }
     }
     return pack_key(c, D, key_batch(in, D), k) ? E_NONE : E_RANGE;
   }
@@ -237,6 +246,23 @@ __global__ void __launch_bounds__(kBlock) k_rank(Src src, int64_t n, const int32
   }
 }
 
+// Table init in one launch: keys and claims to the empty sentinel (all ones), look-back
+// status words / ticket / count to 0, the error word to all ones.
+__global__ void k_init(int4* __restrict__ keys, int32_t* __restrict__ claim, uint32_t cap,
+                       unsigned long long* __restrict__ small, int64_t n_small, unsigned long long* err) {
+  const int4 e = make_int4(-1, -1, -1, -1);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x) {
+    keys[i] = e;
+    claim[i] = -1;
+  }
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_small; i += (int64_t)gridDim.x * blockDim.x)
+    small[i] = 0ull;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    err[0] = ~0ull;  // no error
+    err[1] = 0ull;   // row count
+  }
+}
+
 __global__ void k_p2r(int64_t n, const int32_t* __restrict__ slot_of, const int32_t* __restrict__ tvals,
                       int32_t* __restrict__ p2r) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
@@ -247,7 +273,9 @@ __global__ void k_lookup(const int32_t* __restrict__ q, int64_t nq, int D, const
                          const int32_t* __restrict__ tvals, uint32_t mask, int32_t* __restrict__ rows) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t c[4] = {0, 0, 0, 0};
-    for (int d = 0; d < D; ++d) c[d] = q[i * (D + 1) + d];
+#pragma unroll
+    for (int d = 0; d < 4; ++d)
+      if (d < D) c[d] = q[i * (D + 1) + d];
     int4 k;
     rows[i] = pack_key(c, D, q[i * (D + 1) + D], &k) ? probe(tkeys, tvals, mask, k) : -1;
   }
@@ -309,7 +337,7 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
   Carver sc;
   const size_t o_cl = sc.take<int32_t>(cap), o_sl = sc.take<int32_t>(std::max<int64_t>(n, 1)),
                o_st = sc.take<unsigned long long>(ntiles), o_ti = sc.take<unsigned int>(1),
-               o_er = sc.take<unsigned long long>(1), o_ct = sc.take<int64_t>(1);
+               o_er = sc.take<unsigned long long>(2);  // error word, then the row count
   char* sbase = (char*)dev_alloc(c->alloc, sc.off, s);
   if (!sbase) {
     mk_coords_destroy(c);
@@ -326,15 +354,17 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
   unsigned long long* status = (unsigned long long*)(sbase + o_st);
   unsigned int* ticket = (unsigned int*)(sbase + o_ti);
   unsigned long long* err = (unsigned long long*)(sbase + o_er);
-  int64_t* count = (int64_t*)(sbase + o_ct);
+  int64_t* count = (int64_t*)(err + 1);
 
   cudaError_t e;
-  if ((e = cudaMemsetAsync(c->table.keys, 0xFF, sizeof(int4) * (size_t)cap, s)) != cudaSuccess) return fail_cuda(e, "memset");
-  if ((e = cudaMemsetAsync(claim, 0xFF, sizeof(int32_t) * (size_t)cap, s)) != cudaSuccess) return fail_cuda(e, "memset");
-  // status[], ticket, err(=all ones after the next memset), count: contiguous from o_st
-  if ((e = cudaMemsetAsync(sbase + o_st, 0, o_er - o_st, s)) != cudaSuccess) return fail_cuda(e, "memset");
-  if ((e = cudaMemsetAsync(err, 0xFF, sizeof(unsigned long long), s)) != cudaSuccess) return fail_cuda(e, "memset");
-  if ((e = cudaMemsetAsync(count, 0, sizeof(int64_t), s)) != cudaSuccess) return fail_cuda(e, "memset");
+  {
+    // status[ntiles], ticket, count are contiguous 8-byte words from o_st; err follows.
+    unsigned long long* small = (unsigned long long*)(sbase + o_st);
+    const int64_t n_small = (int64_t)((o_er - o_st) / 8);
+    k_init<<<grid_for(std::max<int64_t>(cap, n_small), 256, ctx->num_sms), 256, 0, s>>>(c->table.keys, claim, cap,
+                                                                                       small, n_small, err);
+    g_launches++;
+  }
   if (n > 0) {
     k_insert<Src><<<grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s>>>(src, n, claim, cap - 1, slot_of, err);
     g_launches++;
@@ -347,18 +377,21 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "launch");
   }
-  struct {
+  struct Result {
     unsigned long long err;
     int64_t count;
-  } h;
-  if ((e = cudaMemcpyAsync(&h.err, err, sizeof(h.err), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail_cuda(e, "D2H");
-  if ((e = cudaMemcpyAsync(&h.count, count, sizeof(h.count), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail_cuda(e, "D2H");
+  };
+  Result* hr = (Result*)pinned_stage(sizeof(Result));
+  if (!hr) return fail_cuda(cudaErrorMemoryAllocation, "pinned staging");
+  // err and count are adjacent device words: one 16-byte copy
+  if ((e = cudaMemcpyAsync(hr, err, sizeof(Result), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail_cuda(e, "D2H");
   dev_free(c->alloc, sbase, s);
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) {
     mk_coords_destroy(c);
     set_error(MK_ERR_CUDA, std::string("coords: ") + cudaGetErrorString(e));
     return MK_ERR_CUDA;
   }
+  const Result h = *hr;
   if (h.err != ~0ull) {
     const int64_t row = (int64_t)(h.err >> 8);
     const uint32_t code = (uint32_t)(h.err & 0xFF);

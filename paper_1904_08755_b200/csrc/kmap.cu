@@ -30,13 +30,16 @@ constexpr int kThreads = 256;
 
 // u + sign * off * scale, per spatial axis, batch unchanged (R18).  False when the
 // shifted coordinate cannot exist (outside int32 or the packed-key domain).
-__device__ __forceinline__ bool shift_key(int4 u, int D, const int32_t* off, int sign, const int32_t* scale,
-                                          int4* q) {
+__device__ __forceinline__ bool shift_key(int4 u, int D, const int32_t* off, int sign, int4 scale, int4* q) {
   int64_t c[4] = {0, 0, 0, 0};
-  for (int d = 0; d < D; ++d) {
-    const int64_t v = (int64_t)key_axis(u, D, d) + (int64_t)sign * off[d] * scale[d];
-    if (v < INT32_MIN || v > INT32_MAX) return false;
-    c[d] = v;
+  const int32_t sc[4] = {scale.x, scale.y, scale.z, scale.w};
+#pragma unroll
+  for (int d = 0; d < 4; ++d) {  // fully unrolled: c[] and sc[] stay in registers
+    if (d < D) {
+      const int64_t v = (int64_t)key_axis(u, D, d) + (int64_t)sign * off[d] * sc[d];
+      if (v < INT32_MIN || v > INT32_MAX) return false;
+      c[d] = v;
+    }
   }
   return pack_key(c, D, key_batch(u, D), q);
 }
@@ -56,7 +59,6 @@ __global__ void __launch_bounds__(kThreads) k_probe(const int4* __restrict__ oke
   for (int i = threadIdx.x; i < K; i += kThreads) s_cnt[i] = 0;
   if (threadIdx.x < kTileRows) s_rm[threadIdx.x] = 0;
   __syncthreads();
-  const int32_t scale[4] = {scale4.x, scale4.y, scale4.z, scale4.w};
   const int64_t tile = blockIdx.x;
   const int64_t o = tile * kTileRows + (threadIdx.x & (kTileRows - 1));
   const bool valid = o < n_out;
@@ -66,7 +68,7 @@ __global__ void __launch_bounds__(kThreads) k_probe(const int4* __restrict__ oke
   for (int k = threadIdx.x / kTileRows; k < K; k += kThreads / kTileRows) {
     int32_t a = -1;
     int4 q;
-    if (valid && shift_key(u, D, s_off + k * D, sign, scale, &q)) a = probe(tkeys, tvals, mask, q);
+    if (valid && shift_key(u, D, s_off + k * D, sign, scale4, &q)) a = probe(tkeys, tvals, mask, q);
     nbr[(int64_t)k * n_pad + o] = a;  // rows padded to whole tiles (-1)
     if (a >= 0 && k < 32) rm |= 1u << k;
     const unsigned b = __ballot_sync(0xffffffffu, a >= 0);
@@ -269,9 +271,8 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   };
 
   // persistent: offsets/mirror, ptr, nbr, tile masks (+ nbrT / maskT when not symmetric)
-  m->ptr = (int64_t*)alloc(sizeof(int64_t) * (K + 1));
-  m->d_mirror = (int32_t*)alloc(sizeof(int32_t) * K);
-  int32_t* d_offs = (int32_t*)alloc(sizeof(int32_t) * K * D);
+  int32_t* d_offs = (int32_t*)alloc(sizeof(int32_t) * (K * D + K));  // offsets, then mirror
+  m->d_mirror = d_offs ? d_offs + K * D : nullptr;
   m->nbr = (int32_t*)alloc(sizeof(int32_t) * (int64_t)K * n_pad);
   m->tile_mask = (uint32_t*)alloc(sizeof(uint32_t) * ntiles * mw);
   m->tile_maskT = (uint32_t*)alloc(sizeof(uint32_t) * ntilesT * mw);
@@ -279,7 +280,7 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   // scratch: tile counts, tile offsets, totals
   void* scratch = dev_alloc(m->alloc, sizeof(int32_t) * K * ntiles + sizeof(int64_t) * K * ntiles + 256 +
                                           sizeof(int64_t) * K, s);
-  if (!m->ptr || !m->d_mirror || !d_offs || !m->nbr || !m->tile_mask || !m->tile_maskT || (!symmetric && !m->nbrT) ||
+  if (!m->d_mirror || !d_offs || !m->nbr || !m->tile_mask || !m->tile_maskT || (!symmetric && !m->nbrT) ||
       !scratch) {
     if (scratch) dev_free(m->alloc, scratch, s);
     return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: device allocation failed");
@@ -299,8 +300,17 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   auto ck = [&](cudaError_t r) {
     if (e == cudaSuccess) e = r;
   };
-  ck(cudaMemcpyAsync(d_offs, offs.data(), sizeof(int32_t) * K * D, cudaMemcpyHostToDevice, s));
-  ck(cudaMemcpyAsync(m->d_mirror, m->mirror.data(), sizeof(int32_t) * K, cudaMemcpyHostToDevice, s));
+  {  // one pinned H2D copy of the offsets and their mirror indices
+    int32_t* h = (int32_t*)pinned_stage(sizeof(int32_t) * (K * D + K));
+    if (!h) {
+      dev_free(m->alloc, scratch, s);
+      return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: pinned staging failed");
+    }
+    std::copy(offs.begin(), offs.end(), h);
+    std::copy(m->mirror.begin(), m->mirror.end(), h + K * D);
+    ck(cudaMemcpyAsync(d_offs, h, sizeof(int32_t) * (K * D + K), cudaMemcpyHostToDevice, s));
+    pinned_in_flight(s);
+  }
   if (!symmetric) {
     ck(cudaMemsetAsync(m->nbrT, 0xFF, sizeof(int32_t) * K * nT_pad, s));
     ck(cudaMemsetAsync(m->tile_maskT, 0, sizeof(uint32_t) * ntilesT * mw, s));
@@ -318,8 +328,12 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     ck(cudaMemsetAsync(totals, 0, sizeof(int64_t) * K, s));
   }
   ck(cudaGetLastError());
-  std::vector<int64_t> h_tot(K);
-  ck(cudaMemcpyAsync(h_tot.data(), totals, sizeof(int64_t) * K, cudaMemcpyDeviceToHost, s));
+  int64_t* h_tot = (int64_t*)pinned_stage(sizeof(int64_t) * K);
+  if (!h_tot) {
+    dev_free(m->alloc, scratch, s);
+    return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: pinned staging failed");
+  }
+  ck(cudaMemcpyAsync(h_tot, totals, sizeof(int64_t) * K, cudaMemcpyDeviceToHost, s));
   ck(cudaStreamSynchronize(s));
   if (e != cudaSuccess) {
     dev_free(m->alloc, scratch, s);
@@ -339,8 +353,7 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     dev_free(m->alloc, scratch, s);
     return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: device allocation failed");
   }
-  ck(cudaMemcpyAsync(m->ptr, m->h_ptr.data(), sizeof(int64_t) * (K + 1), cudaMemcpyHostToDevice, s));
-  {  // weight-gradient split-K plan (deterministic: depends only on the map and the SM count)
+  {  // CSR offsets + weight-gradient split-K plan: one device block, one pinned H2D copy
     std::vector<int4> segs;
     std::vector<int32_t> seg_begin, slot_begin(K + 1, 0);
     const int64_t P = m->n_pairs;
@@ -361,16 +374,25 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     }
     m->n_wcta = (int32_t)ncta;
     m->n_wslots = (int64_t)segs.size();
-    m->wseg = (int4*)alloc(sizeof(int4) * std::max<size_t>(1, segs.size()));
-    m->wseg_begin = (int32_t*)alloc(sizeof(int32_t) * seg_begin.size());
-    m->wslot_begin = (int32_t*)alloc(sizeof(int32_t) * (K + 1));
-    if (!m->wseg || !m->wseg_begin || !m->wslot_begin) {
+    const size_t b_ptr = (sizeof(int64_t) * (K + 1) + 15) & ~size_t(15), b_seg = sizeof(int4) * std::max<size_t>(1, segs.size());
+    const size_t b_sb = sizeof(int32_t) * seg_begin.size(), b_kb = sizeof(int32_t) * (K + 1);
+    const size_t total = b_ptr + b_seg + b_sb + b_kb;
+    char* d = (char*)alloc(total);
+    char* h = (char*)pinned_stage(total);
+    if (!d || !h) {
       dev_free(m->alloc, scratch, s);
-      return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: device allocation failed");
+      return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: allocation failed");
     }
-    if (!segs.empty()) ck(cudaMemcpyAsync(m->wseg, segs.data(), sizeof(int4) * segs.size(), cudaMemcpyHostToDevice, s));
-    ck(cudaMemcpyAsync(m->wseg_begin, seg_begin.data(), sizeof(int32_t) * seg_begin.size(), cudaMemcpyHostToDevice, s));
-    ck(cudaMemcpyAsync(m->wslot_begin, slot_begin.data(), sizeof(int32_t) * (K + 1), cudaMemcpyHostToDevice, s));
+    std::memcpy(h, m->h_ptr.data(), sizeof(int64_t) * (K + 1));
+    if (!segs.empty()) std::memcpy(h + b_ptr, segs.data(), sizeof(int4) * segs.size());
+    std::memcpy(h + b_ptr + b_seg, seg_begin.data(), b_sb);
+    std::memcpy(h + b_ptr + b_seg + b_sb, slot_begin.data(), b_kb);
+    ck(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, s));
+    pinned_in_flight(s);
+    m->ptr = (int64_t*)d;  // b_ptr is padded to 16 bytes so the int4 plan stays aligned
+    m->wseg = (int4*)(d + b_ptr);
+    m->wseg_begin = (int32_t*)(d + b_ptr + b_seg);
+    m->wslot_begin = (int32_t*)(d + b_ptr + b_seg + b_sb);
   }
   if (n_out > 0) {
     k_emit<<<(unsigned)ntiles, kThreads, sizeof(int32_t) * K * 4, s>>>(m->nbr, n_out, n_pad, K, m->ptr, tile_off,

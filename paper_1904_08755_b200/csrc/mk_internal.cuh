@@ -86,6 +86,7 @@ __host__ __device__ __forceinline__ int32_t key_batch(int4 k, int D) {
 // Packs spatial components c[0..D) (int64, already range-checked by the caller for
 // int32) and batch b.  Returns false when D == 4 and the packed-key limits are violated.
 __host__ __device__ __forceinline__ bool pack_key(const int64_t* c, int D, int64_t b, int4* out) {
+  // c[] is indexed with compile-time constants only (keeps it in registers)
   int4 k;
   k.x = D > 0 ? (int32_t)c[0] : 0;
   k.y = D > 1 ? (int32_t)c[1] : 0;
@@ -99,6 +100,17 @@ __host__ __device__ __forceinline__ bool pack_key(const int64_t* c, int D, int64
   }
   *out = k;
   return true;
+}
+
+// Linear probing from slot h onward; row or -1.
+__device__ __forceinline__ int32_t probe_from(const int4* __restrict__ tkeys, const int32_t* __restrict__ tvals,
+                                              uint32_t mask, int4 q, uint32_t h) {
+  while (true) {
+    const int4 k = __ldg(tkeys + h);
+    if (key_eq(k, q)) return __ldg(tvals + h);
+    if (k.w == kEmptyWord) return -1;
+    h = (h + 1) & mask;
+  }
 }
 
 // Linear-probing lookup of key q; row or -1.  One 16-byte load per probed slot.
@@ -192,6 +204,11 @@ void* dev_alloc(const Alloc& a, size_t bytes, cudaStream_t s);
 void dev_free(const Alloc& a, void* p, cudaStream_t s);
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 uint32_t next_pow2(uint64_t v);
+// Thread-local pinned staging buffer (context.cu).  pinned_stage() waits until the previous
+// async copy that used it has completed; pinned_in_flight(s) marks it busy until `s`
+// reaches the current point.
+void* pinned_stage(size_t bytes);
+void pinned_in_flight(cudaStream_t s);
 
 // Table-building pipeline shared by quantize / create / stride (coords.cu).
 // Region enumeration (region.cu):

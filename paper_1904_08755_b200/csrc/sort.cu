@@ -3,9 +3,9 @@
 // Used by the kernel-map builder to order output rows by their neighbour bitmask (the set
 // of offsets k with a pair): rows with equal or similar masks land in the same 128-row
 // tile, so the tensor-core conv skips (tile, k) units that have no pair at all.
-// Per pass: k_radix_hist (per-block digit counts) -> k_radix_scan (digit-major exclusive
-// scan over blocks) -> k_radix_scatter (stable: elements are ranked in index order with a
-// warp match + per-warp digit prefix).  Blocks are 256 threads x 4 elements, striped.
+// Per pass: k_radix_hist (per-block digit counts) -> k_radix_offsets (one CTA per digit
+// scans the digit's block counts) -> k_radix_scatter (stable: elements are ranked in index
+// order with a warp match + per-warp digit prefix).  Blocks are 256 threads x 4 elements.
 #include "mk_internal.cuh"
 
 namespace mk {
@@ -16,8 +16,9 @@ constexpr int kItems = 4;
 constexpr int kTile = kThreads * kItems;
 constexpr int kWarps = kThreads / 32;
 
+// Per-block digit counts, layout [digit][block].
 __global__ void __launch_bounds__(kThreads) k_radix_hist(const uint32_t* __restrict__ keys, int64_t n, int shift,
-                                                         int64_t nblocks, uint32_t* __restrict__ hist) {
+                                                         int64_t nblocks, uint32_t* __restrict__ cnt_out) {
   __shared__ uint32_t cnt[256];
   cnt[threadIdx.x] = 0;
   __syncthreads();
@@ -28,28 +29,23 @@ __global__ void __launch_bounds__(kThreads) k_radix_hist(const uint32_t* __restr
     if (e < n) atomicAdd(&cnt[(keys[e] >> shift) & 255u], 1u);
   }
   __syncthreads();
-  hist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = cnt[threadIdx.x];
+  cnt_out[(int64_t)threadIdx.x * nblocks + blockIdx.x] = cnt[threadIdx.x];
 }
 
-// Exclusive scan of hist[0 .. len) in place: one CTA of 1024 threads, 16 consecutive
-// elements per thread per round (a 16K-element round costs one block-wide scan).
-__global__ void __launch_bounds__(1024) k_radix_scan(uint32_t* __restrict__ hist, int64_t len) {
-  constexpr int kPer = 16;
-  __shared__ uint32_t s_w[32];
+// One CTA per digit: exclusive scan of the digit's per-block counts (in place) and the
+// digit total.
+__global__ void __launch_bounds__(kThreads) k_radix_offsets(uint32_t* __restrict__ cnt, int64_t nblocks,
+                                                            uint32_t* __restrict__ totals) {
+  __shared__ uint32_t s_w[kWarps];
   __shared__ uint32_t s_carry;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t* c = cnt + (int64_t)blockIdx.x * nblocks;
   if (threadIdx.x == 0) s_carry = 0;
   __syncthreads();
-  for (int64_t b = 0; b < len; b += 1024 * kPer) {
-    const int64_t i0 = b + (int64_t)threadIdx.x * kPer;
-    uint32_t v[kPer];
-    uint32_t sum = 0;
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      v[j] = i0 + j < len ? hist[i0 + j] : 0u;
-      sum += v[j];
-    }
-    uint32_t x = sum;
+  for (int64_t b0 = 0; b0 < nblocks; b0 += kThreads) {
+    const int64_t i = b0 + threadIdx.x;
+    const uint32_t v = i < nblocks ? c[i] : 0u;
+    uint32_t x = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
@@ -57,38 +53,45 @@ __global__ void __launch_bounds__(1024) k_radix_scan(uint32_t* __restrict__ hist
     }
     if (lane == 31) s_w[warp] = x;
     __syncthreads();
-    if (warp == 0) {
-      uint32_t w = s_w[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) w += y;
-      }
-      s_w[lane] = w;
-    }
+    uint32_t wb = 0;
+    for (int w = 0; w < warp; ++w) wb += s_w[w];
+    const uint32_t excl = s_carry + wb + x - v;
+    if (i < nblocks) c[i] = excl;
     __syncthreads();
-    uint32_t run = s_carry + (warp ? s_w[warp - 1] : 0u) + x - sum;
-#pragma unroll
-    for (int j = 0; j < kPer; ++j) {
-      if (i0 + j < len) hist[i0 + j] = run;
-      run += v[j];
-    }
-    __syncthreads();
-    if (threadIdx.x == 1023) s_carry = run;
+    if (threadIdx.x == kThreads - 1) s_carry = excl + v;
     __syncthreads();
   }
+  if (threadIdx.x == 0) totals[blockIdx.x] = s_carry;
 }
 
+// Stable scatter: output offset of (digit, block) = exclusive scan of the digit totals +
+// the scanned per-block count (k_radix_offsets).
 __global__ void __launch_bounds__(kThreads) k_radix_scatter(const uint32_t* __restrict__ kin, const int32_t* __restrict__ vin,
                                                             uint32_t* __restrict__ kout, int32_t* __restrict__ vout,
                                                             int64_t n, int shift, int64_t nblocks,
-                                                            const uint32_t* __restrict__ offs) {
+                                                            const uint32_t* __restrict__ cnt,
+                                                            const uint32_t* __restrict__ totals) {
   __shared__ uint32_t wcnt[kWarps][256];
   __shared__ uint32_t wpre[kWarps][256];
   __shared__ uint32_t run[256];
+  __shared__ uint32_t s_w[kWarps];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   for (int w = 0; w < kWarps; ++w) wcnt[w][t] = 0;
-  run[t] = offs[(int64_t)t * nblocks + blockIdx.x];
+  {
+    // exclusive scan of the 256 digit totals + this block's offset within the digit
+    const uint32_t v = totals[t];
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    uint32_t wb = 0;
+    for (int w = 0; w < warp; ++w) wb += s_w[w];
+    run[t] = wb + x - v + cnt[(int64_t)t * nblocks + blockIdx.x];
+  }
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kTile;
   const unsigned lt = (1u << lane) - 1u;
@@ -133,34 +136,37 @@ mk_status radix_sort_perm(const Alloc& a, uint32_t* keys, int64_t n, int bits, i
   uint32_t* k2 = (uint32_t*)dev_alloc(a, sizeof(uint32_t) * n, s);
   int32_t* v2 = (int32_t*)dev_alloc(a, sizeof(int32_t) * n, s);
   int32_t* v1 = (int32_t*)dev_alloc(a, sizeof(int32_t) * n, s);
-  uint32_t* hist = (uint32_t*)dev_alloc(a, sizeof(uint32_t) * 256 * nblocks, s);
-  if (!k2 || !v2 || !v1 || !hist) {
+  uint32_t* cnt = (uint32_t*)dev_alloc(a, sizeof(uint32_t) * (256 * nblocks + 256 * passes), s);
+  if (!k2 || !v2 || !v1 || !cnt) {
     dev_free(a, k2, s);
     dev_free(a, v2, s);
     dev_free(a, v1, s);
-    dev_free(a, hist, s);
+    dev_free(a, cnt, s);
     MK_FAIL(MK_ERR_OUT_OF_MEMORY, "radix sort: allocation failed");
   }
+  uint32_t* totals = cnt + 256 * nblocks;  // [passes][256]
+  cudaError_t e = cudaSuccess;
   uint32_t* kin = keys;
   uint32_t* kout = k2;
   int32_t* vin = nullptr;  // first pass: values are the element indices
   int32_t* vout = passes == 1 ? perm : v1;
-  for (int p = 0; p < passes; ++p) {
+  for (int p = 0; p < passes && e == cudaSuccess; ++p) {
     const int shift = 8 * p;
-    k_radix_hist<<<(unsigned)nblocks, kThreads, 0, s>>>(kin, n, shift, nblocks, hist);
-    k_radix_scan<<<1, 1024, 0, s>>>(hist, 256 * nblocks);
-    k_radix_scatter<<<(unsigned)nblocks, kThreads, 0, s>>>(kin, vin, kout, vout, n, shift, nblocks, hist);
+    k_radix_hist<<<(unsigned)nblocks, kThreads, 0, s>>>(kin, n, shift, nblocks, cnt);
+    k_radix_offsets<<<256, kThreads, 0, s>>>(cnt, nblocks, totals + 256 * p);
+    k_radix_scatter<<<(unsigned)nblocks, kThreads, 0, s>>>(kin, vin, kout, vout, n, shift, nblocks, cnt,
+                                                           totals + 256 * p);
     g_launches += 3;
     std::swap(kin, kout);
     vin = vout;
     // ping-pong values, the last pass writes perm
     vout = (p + 2 == passes) ? perm : (vout == v1 ? v2 : v1);
   }
-  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
   dev_free(a, k2, s);
   dev_free(a, v2, s);
   dev_free(a, v1, s);
-  dev_free(a, hist, s);
+  dev_free(a, cnt, s);
   if (e != cudaSuccess) MK_FAIL(MK_ERR_CUDA, std::string("radix sort: ") + cudaGetErrorString(e));
   return MK_OK;
 }
