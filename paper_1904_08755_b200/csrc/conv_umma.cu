@@ -162,6 +162,7 @@ __device__ __forceinline__ unsigned long long gtime() {
     if (blockIdx.x == 0 && (i) < 8192) g_trace[role][i] = (v); \
   } while (0)
 __device__ unsigned long long g_acct[32][8];
+__device__ unsigned long long g_cta[4096][4];  // per-CTA [start ns, end ns, smid, steps]
 #define ACCT_WAIT(slot, bar, par)                              \
   do {                                                         \
     const long long _t0 = clock64();                           \
@@ -216,6 +217,11 @@ struct FwdParams {
 };
 
 constexpr int kMaxK = 128;  // offsets supported by the tensor-core conv (4 mask words)
+// Ring of commit barriers: the MMA thread's j-th group commit (covering steps up to
+// (j+1)*ga - 1) arrives on cb[j % kNCB]; anyone needing "all MMAs of step <= x done" waits
+// for commit x / ga at parity (j / kNCB) & 1.  kNCB >> the MMA's possible run-ahead, so a
+// waiter can never confuse phases.
+constexpr int kNCB = 16;
 
 // Per-CTA plan, built once in shared memory by warp 0: the CTA's tiles are
 // blockIdx.x * tb + i (adjacent in the map's bitmask-sorted row order, so they share most
@@ -231,9 +237,17 @@ struct Plan {
   int32_t g0[kMaxK + 1];
 };
 
+// First tile of this CTA.  Rows are bitmask-sorted ascending, which puts the densest
+// masks (most offsets per tile, up to ~4x the work) at the end; CTAs take batches from the
+// end first so the heaviest work is scheduled in the first wave (longest-first).
+__device__ __forceinline__ int64_t cta_tile0(const FwdParams& p) {
+  const int64_t nb = (p.ntiles + p.tb - 1) / p.tb;
+  return (nb - 1 - (int64_t)blockIdx.x) * p.tb;
+}
+
 __device__ void build_plan(const FwdParams& p, Plan* pl) {
   const int lane = threadIdx.x & 31;
-  const int64_t t0 = (int64_t)blockIdx.x * p.tb;
+  const int64_t t0 = cta_tile0(p);
   const int nt = (int)min((int64_t)p.tb, p.ntiles - t0);
   const int K = p.nb.K;
   const int rot = (int)(blockIdx.x % (unsigned)K);
@@ -285,24 +299,18 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
   int32_t* nbr_s = (int32_t*)(w_base + (size_t)p.sw * p.b_bytes);  // [kFwdProd][2][128] index buffers
   Plan* pl = (Plan*)(nbr_s + kFwdProd * 2 * kTileM);
   uint64_t* a_full = (uint64_t*)(((uintptr_t)(pl + 1) + 15) & ~(uintptr_t)15);
-  uint64_t* a_empty = a_full + p.sa;
-  uint64_t* w_full = a_empty + p.sa;
-  uint64_t* w_empty = w_full + p.sw;
-  uint64_t* tfull = w_empty + p.sw;
+  uint64_t* cb = a_full + p.sa;  // [kNCB] commit ring (stage slots and W slots are released by it)
+  uint64_t* w_full = cb + kNCB;
+  uint64_t* tfull = w_full + p.sw;
   uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t tile0 = (int64_t)blockIdx.x * p.tb;
+  const int64_t tile0 = cta_tile0(p);
 
   if (warp == 0) build_plan(p, pl);
   if (threadIdx.x == 32) {
-    for (int s = 0; s < p.sa; ++s) {
-      mbar_init(a_full + s, 1);
-      mbar_init(a_empty + s, 1);  // only a_empty[0 .. sa/ga) are used: one per group of ga slots
-    }
-    for (int s = 0; s < p.sw; ++s) {
-      mbar_init(w_full + s, 1);
-      mbar_init(w_empty + s, 1);
-    }
+    for (int s = 0; s < p.sa; ++s) mbar_init(a_full + s, 1);
+    for (int j = 0; j < kNCB; ++j) mbar_init(cb + j, 1);
+    for (int s = 0; s < p.sw; ++s) mbar_init(w_full + s, 1);
     mbar_init(tfull, 1);
     fence_mbar_init();
   }
@@ -313,6 +321,15 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
   const uint32_t tbase = *tmem_slot;
   const int n_units = pl->n_units, n_steps = pl->n_steps;
   ACCT_DECL
+#ifdef MK_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 4096) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_cta[blockIdx.x][0] = gtime();
+    g_cta[blockIdx.x][2] = smid;
+    g_cta[blockIdx.x][3] = (unsigned long long)n_steps;
+  }
+#endif
 
   if (warp < p.sa) {
     // ------------------------------------------------------------ gather producers
@@ -356,7 +373,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
           cp_async16(smem_u32(ibuf + (ib ^ 1) * kTileM) + lane * 16,
                      p.nb.tab + (int64_t)p.nb.kk(kn) * p.nb.n + tilen * kTileM + lane * 4, 16u);
       }
-      ACCT_WAIT(0, a_empty + warp / p.ga, (my & 1) ^ 1);
+      if (g >= p.sa) {  // slot reuse: all MMAs of step g - sa done
+        const int j = (g - p.sa) / p.ga;
+        ACCT_WAIT(0, cb + j % kNCB, (uint32_t)(j / kNCB) & 1u);
+      }
       const uint32_t a_s = smem_u32(a_base + (size_t)warp * p.a_bytes);
       const int32_t* ix = ibuf + ib * kTileM;
       const __nv_bfloat16* xc = p.x + c * CH;
@@ -394,36 +414,47 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
     }
   } else if (warp == kFwdStage) {
     // ------------------------------------------------------------ W stager (one thread)
-    // Bulk copies (TMA engine) of the W_k chunks of every unit into a ring of sw slots.
+    // Bulk copies (TMA engine) of the W_k chunks of every unit into a ring of sw slots.  A
+    // slot is free once every MMA of its previous unit uo completed; no extra commit is spent
+    // on that: the group commit covering uo's last step (commit ring cb) implies it.
+    // Deadlock-free because the ring holds >= ga units.
     if (lane == 0) {
-      uint32_t ws = 0, wph = 0;
-      for (int u = 0; u < n_units; ++u)
+      uint32_t ws = 0;
+      const int upr = p.sw / p.nch;  // units held by the ring
+      for (int u = 0; u < n_units; ++u) {
+        const int uo = u - upr;
+        if (uo >= 0) {
+          const int j = (pl->g0[uo + 1] - 1) / p.ga;  // commit covering uo's last step
+          ACCT_WAIT(0, cb + j % kNCB, (uint32_t)(j / kNCB) & 1u);
+        }
         for (int c = 0; c < p.nch; ++c) {
-          ACCT_WAIT(0, w_empty + ws, wph ^ 1);
           mbar_arrive_expect_tx(w_full + ws, p.b_bytes);
           bulk_g2s(w_base + (size_t)ws * p.b_bytes, p.wpack + ((int64_t)pl->k[u] * p.nch + c) * p.b_bytes, p.b_bytes,
                    w_full + ws);
-          if (++ws == (uint32_t)p.sw) {
-            ws = 0;
-            wph ^= 1;
-          }
+          if (++ws == (uint32_t)p.sw) ws = 0;
         }
+      }
     }
     __syncwarp();
   } else if (warp == kFwdMma) {
-    // ------------------------------------------------------------ MMA issuer (one thread)
-    // Lean loop: descriptors are a constant high part | (smem address >> 4); slot / phase
-    // counters are incremental (no divisions); one commit per group of ga stage slots.
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issuer
+    // The whole warp runs the loop with warp-uniform values (so descriptors live in uniform
+    // registers: no per-MMA R2UR); lane 0 issues the tcgen05 instructions.  Descriptors are
+    // a constant high part | (smem address >> 4); slot / phase counters are incremental;
+    // one commit per group of ga stage slots.
+    {
+      const bool leader = lane == 0;
       const uint32_t idesc = idesc_bf16(kTileM, p.c_y, 0, 0);
       const uint64_t dhi = smem_desc(0, 16, 8 * RB, layout_code(RB));
-      const uint32_t a0 = smem_u32(a_base) >> 4, astep = p.a_bytes >> 4;
-      const uint32_t w0 = smem_u32(w_base) >> 4, wstep = p.b_bytes >> 4;
+      const uint32_t a0 = __shfl_sync(0xffffffffu, smem_u32(a_base) >> 4, 0), astep = p.a_bytes >> 4;
+      const uint32_t w0 = __shfl_sync(0xffffffffu, smem_u32(w_base) >> 4, 0), wstep = p.b_bytes >> 4;
+      const uint32_t tb0 = __shfl_sync(0xffffffffu, tbase, 0);
       uint32_t s = 0, sph = 0, gq = 0;     // A slot, its phase, position inside the commit group
+      uint32_t ncommit = 0;                // group commits issued (commit ring index)
       uint32_t ws = 0, wph = 0;            // W ring position of the unit's first chunk
       uint32_t init = 0;                   // tiles whose accumulator holds data
       for (int u = 0; u < n_units; ++u) {
-        const uint32_t tw = pl->tw[u];
+        const uint32_t tw = __shfl_sync(0xffffffffu, (uint32_t)pl->tw[u], 0);
         {  // wait for the unit's W chunks
           uint32_t x = ws, xph = wph;
           for (int c = 0; c < p.nch; ++c) {
@@ -437,21 +468,24 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
         tc_fence_after();
         for (uint32_t b = tw; b; b &= b - 1) {
           const int i = __ffs(b) - 1;
-          const uint32_t d = tbase + (uint32_t)(i * p.c_y);
+          const uint32_t d = tb0 + (uint32_t)(i * p.c_y);
           uint32_t acc = (init >> i) & 1u;
           uint32_t x = ws;
           for (int c = 0; c < p.nch; ++c) {
             ACCT_WAIT(2, a_full + s, sph);
             tc_fence_after();
             const uint32_t alo = a0 + s * astep, blo = w0 + x * wstep;
+            if (leader) {
 #pragma unroll
-            for (int kk = 0; kk < CH / 16; ++kk) {
-              umma_f16(d, dhi | (uint64_t)(alo + kk * 2), dhi | (uint64_t)(blo + kk * 2), idesc, acc);
-              acc = 1;
+              for (int kk = 0; kk < CH / 16; ++kk)
+                umma_f16(d, dhi | (uint64_t)(alo + kk * 2), dhi | (uint64_t)(blo + kk * 2), idesc, acc | (uint32_t)kk);
             }
-            // tcgen05.commit costs ~400+ issue cycles: release stage slots in groups of ga
+            acc = 1;
+            __syncwarp();
+            // a commit stalls the next MMAs ~250 cycles (tools/ubench_umma.cu): one per ga steps
             if (++gq == (uint32_t)p.ga) {
-              umma_commit(a_empty + s / p.ga);
+              if (leader) umma_commit(cb + (ncommit % kNCB));
+              ++ncommit;
               gq = 0;
             }
             if (++s == (uint32_t)p.sa) {
@@ -462,17 +496,15 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
           }
           init |= 1u << i;
         }
-        for (int c = 0; c < p.nch; ++c) {
-          umma_commit(w_empty + ws);
+        for (int c = 0; c < p.nch; ++c)
           if (++ws == (uint32_t)p.sw) {
             ws = 0;
             wph ^= 1;
           }
-        }
       }
-      if (n_steps > 0) umma_commit(tfull);
+      if (leader && n_steps > 0) umma_commit(tfull);
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp >= kFwdEpi0 && warp < kFwdEpi0 + 4) {
     // ------------------------------------------------------------ epilogue
     const int q = warp & 3;  // TMEM lane quarter owned by this warp
@@ -526,6 +558,10 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
       }
     }
   }
+#ifdef MK_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0 && blockIdx.x < 4096) g_cta[blockIdx.x][1] = gtime();
+#endif
   ACCT_DUMP;
   tc_fence_before();
   __syncthreads();
@@ -716,30 +752,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
       e = en;
     }
   } else if (warp == kMmaWarp) {
-    if (lane == 0) {
+    {  // whole warp, warp-uniform values, lane 0 issues (see the forward kernel)
+      const bool leader = lane == 0;
       const uint32_t idesc = idesc_bf16(kTileM, p.c_in, 1, 1);
       const uint64_t ahi = smem_desc(0, panel_a, 8 * rba, layout_code(rba));
       const uint64_t bhi = smem_desc(0, panel_b, 8 * rbb, layout_code(rbb));
-      const uint32_t s0 = smem_u32(smem) >> 4, sstep = p.slot_bytes >> 4, boff = p.a_bytes >> 4;
+      const uint32_t s0 = __shfl_sync(0xffffffffu, smem_u32(smem) >> 4, 0), sstep = p.slot_bytes >> 4,
+                     boff = p.a_bytes >> 4;
+      const uint32_t tb0 = __shfl_sync(0xffffffffu, tbase, 0);
       const uint32_t ka = (16 * rba) >> 4, kb = (16 * rbb) >> 4, hstep = ((128 / p.pwa) * panel_a) >> 4;
       uint32_t s = 0, sph = 0, gq = 0;
       for (int i = 0; i < nseg; ++i) {
         mbar_wait(tempty, (i & 1) ^ 1);
         tc_fence_after();
         uint32_t acc = 0;
-        for (int q = seg_g0[i]; q < seg_g0[i + 1]; ++q) {
+        const int q0 = __shfl_sync(0xffffffffu, seg_g0[i], 0), q1 = __shfl_sync(0xffffffffu, seg_g0[i + 1], 0);
+        for (int q = q0; q < q1; ++q) {
           ACCT_WAIT(2, a_full + s, sph);
           tc_fence_after();
           const uint32_t alo = s0 + s * sstep, blo = alo + boff;
+          if (leader) {
 #pragma unroll
-          for (int kk = 0; kk < PS / 16; ++kk) {
-            for (int h = 0; h < p.halves; ++h)
-              umma_f16(tbase + h * (uint32_t)p.c_in, ahi | (uint64_t)(alo + h * hstep + kk * ka),
-                       bhi | (uint64_t)(blo + kk * kb), idesc, acc);
-            acc = 1;
+            for (int kk = 0; kk < PS / 16; ++kk)
+              for (int h = 0; h < p.halves; ++h)
+                umma_f16(tb0 + h * (uint32_t)p.c_in, ahi | (uint64_t)(alo + h * hstep + kk * ka),
+                         bhi | (uint64_t)(blo + kk * kb), idesc, acc | (uint32_t)kk);
           }
+          acc = 1;
+          __syncwarp();
           if (++gq == (uint32_t)p.ga) {
-            umma_commit(a_empty + s / p.ga);
+            if (leader) umma_commit(a_empty + s / p.ga);
             gq = 0;
           }
           if (++s == (uint32_t)p.sa) {
@@ -747,10 +789,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
             sph ^= 1;
           }
         }
-        umma_commit(tfull);
+        if (leader) umma_commit(tfull);
+        __syncwarp();
       }
     }
-    __syncwarp();
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
     const int q = warp & 3;
     for (int i = 0; i < nseg; ++i) {
@@ -840,6 +882,9 @@ extern "C" int mk_debug_trace(unsigned long long* host_out) {
 extern "C" int mk_debug_acct(unsigned long long* host_out) {
   return (int)cudaMemcpyFromSymbol(host_out, g_acct, sizeof(g_acct));
 }
+extern "C" int mk_debug_cta(unsigned long long* host_out) {
+  return (int)cudaMemcpyFromSymbol(host_out, g_cta, sizeof(g_cta));
+}
 #endif
 
 mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, int64_t n_src, int c_x, const void* W,
@@ -873,7 +918,7 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
     p.sw = nch * 4;
   const int fixed = base + p.sw * (int)p.b_bytes;
   p.sa = std::min(kFwdProd, (kMaxSmem - fixed) / (int)p.a_bytes);
-  p.ga = p.sa % 2 == 0 ? 2 : 1;
+  p.ga = p.sa % 2 == 0 ? 2 : 1;  // the W ring must hold >= ga units: sw / nch >= 2 >= ga
   if (p.sa < 2 || p.tmem_cols > 512)
     MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: channel counts too large for the smem pipeline");
   const size_t wbytes = (size_t)nb.K * nch * p.b_bytes;
