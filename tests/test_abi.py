@@ -12,11 +12,12 @@ ROOT = Path(__file__).resolve().parents[1]
 
 @pytest.fixture(scope="module")
 def libmk():
-    import sys
-    sys.path.insert(0, str(ROOT))
-    from paper_1904_08755_b200 import build
-    so = build.build()
-    return so
+    # by path: importing the package would load the library before it is built
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("_mk_build", ROOT / "paper_1904_08755_b200" / "build.py")
+    build = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(build)
+    return build.build()
 
 
 def _declared():
