@@ -26,24 +26,28 @@ def _stale(obj: Path, src: Path) -> bool:
     return obj.stat().st_mtime < max(d.stat().st_mtime for d in deps)
 
 
-def build(verbose: bool = False, jobs: int = 8) -> Path:
-    objdir = PKG / "build"
+def build(verbose: bool = False, jobs: int = 8, trace: bool = False) -> Path:
+    """trace=True builds the MK_TRACE instrumented variant as tools/libmk_trace.so
+    (development timelines; load it with MK_LIBRARY)."""
+    objdir = PKG / ("build_trace" if trace else "build")
+    so = ROOT / "tools" / "libmk_trace.so" if trace else SO
+    defs = ["-DMK_TRACE"] if trace else []
     objdir.mkdir(exist_ok=True)
     procs, objs = [], []
     for s in SOURCES:
         src, obj = CSRC / s, objdir / (Path(s).stem + ".o")
         objs.append(obj)
         if _stale(obj, src):
-            cmd = ["nvcc", *ARCH, *FLAGS, "-Xptxas", "-v" if verbose else "-O3", "-c", str(src), "-o", str(obj)]
+            cmd = ["nvcc", *ARCH, *FLAGS, *defs, "-Xptxas", "-v" if verbose else "-O3", "-c", str(src), "-o", str(obj)]
             procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
             if len(procs) >= jobs:
                 _drain(procs, verbose)
     _drain(procs, verbose)
-    if not SO.exists() or SO.stat().st_mtime < max(o.stat().st_mtime for o in objs):
-        tmp = SO.with_suffix(f".so.{os.getpid()}")
+    if not so.exists() or so.stat().st_mtime < max(o.stat().st_mtime for o in objs):
+        tmp = so.with_suffix(f".so.{os.getpid()}")
         subprocess.check_call(["nvcc", *ARCH, "-shared", "-o", str(tmp), *map(str, objs)])
-        os.replace(tmp, SO)
-    return SO
+        os.replace(tmp, so)
+    return so
 
 
 def _drain(procs, verbose):
@@ -58,4 +62,4 @@ def _drain(procs, verbose):
 
 
 if __name__ == "__main__":
-    print(build(verbose="-v" in sys.argv))
+    print(build(verbose="-v" in sys.argv, trace="--trace" in sys.argv))

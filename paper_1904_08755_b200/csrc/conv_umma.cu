@@ -209,6 +209,7 @@ struct FwdParams {
   NbrView nb;
   int64_t n_rows, ntiles;
   int c_x, c_y, nch, out_f32;
+  int dbg;  // development switch (env MK_DEBUG_CONV): bit 0 = no MMAs, bit 1 = no gathers; 0 in production
   int sa;  // A stages == producer warps (warp w owns stage slot w)
   int ga;  // stage slots released together by one tcgen05.commit (sa % ga == 0)
   int sw;  // W chunk slots (a ring: W_k chunks are prefetched several offsets ahead)
@@ -380,7 +381,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
       const uint32_t a_s = smem_u32(a_base + (size_t)warp * p.a_bytes);
       const int32_t* ix = ibuf + ib * kTileM;
       const __nv_bfloat16* xc = p.x + c * CH;
-      if (J == 8) {
+      if (p.dbg & 2) {
+      } else if (J == 8) {
 #pragma unroll 2
         for (int i = 0; i < 32; i += 4) {
           const int4 a4 = *(const int4*)(ix + q4 * 32 + i);
@@ -475,7 +477,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
             ACCT_WAIT(2, a_full + s, sph);
             tc_fence_after();
             const uint32_t alo = a0 + s * astep, blo = w0 + x * wstep;
-            if (leader) {
+            if (leader && !(p.dbg & 1)) {
 #pragma unroll
               for (int kk = 0; kk < CH / 16; ++kk)
                 umma_f16(d, dhi | (uint64_t)(alo + kk * 2), dhi | (uint64_t)(blo + kk * 2), idesc, acc | (uint32_t)kk);
@@ -905,6 +907,11 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   p.c_y = c_y;
   p.nch = nch;
   p.out_f32 = out_dt == MK_F32;
+  static const int dbg = [] {
+    const char* e = std::getenv("MK_DEBUG_CONV");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.dbg = dbg;
   p.a_bytes = kTileM * CH * 2;
   p.b_bytes = (uint32_t)c_y * CH * 2;
   // Two tiles per CTA (one TMEM accumulator each, <= 256 columns so two CTAs share an SM);
