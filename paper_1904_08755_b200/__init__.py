@@ -56,9 +56,30 @@ def context(device: Optional[int] = None) -> ctypes.c_void_p:
     return _ctx[device]
 
 
-def _stream(t: Optional[torch.Tensor] = None) -> ctypes.c_void_p:
-    dev = t.device if t is not None else None
-    return ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
+def _stream(t: Optional[torch.Tensor] = None) -> int:
+    """Raw handle of torch's current stream on the tensor's device (cheap accessor)."""
+    idx = t.device.index if t is not None else torch.cuda.current_device()
+    return torch._C._cuda_getCurrentRawStream(idx)
+
+
+class _on_device:
+    """Makes `device` current for the duration of a call, only when it is not already."""
+
+    __slots__ = ("idx", "prev")
+
+    def __init__(self, device):
+        self.idx = device.index if isinstance(device, torch.device) else int(device)
+        self.prev = None
+
+    def __enter__(self):
+        cur = torch.cuda.current_device()
+        if cur != self.idx:
+            self.prev = cur
+            torch.cuda.set_device(self.idx)
+
+    def __exit__(self, *exc):
+        if self.prev is not None:
+            torch.cuda.set_device(self.prev)
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -112,7 +133,7 @@ def coords_quantize(points: torch.Tensor, voxel: float, batch: Optional[torch.Te
     p2r = torch.empty(n, dtype=torch.int32, device=pts.device) if return_maps else None
     first = torch.empty(max(n, 1), dtype=torch.int32, device=pts.device) if return_maps else None
     h = ctypes.c_void_p()
-    with torch.cuda.device(pts.device):
+    with _on_device(pts.device):
         _check(_L.mk_coords_quantize(context(pts.device.index), _ptr(pts), _ptr(b), n, D, ctypes.c_float(voxel),
                                      _stream(pts), ctypes.byref(h), _ptr(p2r), _ptr(first)), "mk_coords_quantize")
     c = Coords(h, pts.device)
@@ -129,7 +150,7 @@ def coords_create(coords: torch.Tensor, tensor_stride: Optional[Sequence[int]] =
     ts = None if tensor_stride is None else (ctypes.c_int32 * D)(*tensor_stride)
     inv = torch.empty(n, dtype=torch.int32, device=c.device) if return_inverse else None
     h = ctypes.c_void_p()
-    with torch.cuda.device(c.device):
+    with _on_device(c.device):
         _check(_L.mk_coords_create(context(c.device.index), _ptr(c), n, D, ts, _stream(c), ctypes.byref(h), _ptr(inv)),
                "mk_coords_create")
     out = Coords(h, c.device)
@@ -140,7 +161,7 @@ def coords_stride(cin: Coords, conv_stride: Sequence[int]) -> Coords:
     """Strided output coordinates (R11)."""
     cs = (ctypes.c_int32 * cin.D)(*conv_stride)
     h = ctypes.c_void_p()
-    with torch.cuda.device(cin.device):
+    with _on_device(cin.device):
         _check(_L.mk_coords_stride(context(cin.device.index), cin._h, cs, _stream(), ctypes.byref(h)),
                "mk_coords_stride")
     return Coords(h, cin.device)
@@ -148,7 +169,7 @@ def coords_stride(cin: Coords, conv_stride: Sequence[int]) -> Coords:
 
 def coords_export(c: Coords) -> torch.Tensor:
     out = torch.empty((c.n, c.D + 1), dtype=torch.int32, device=c.device)
-    with torch.cuda.device(c.device):
+    with _on_device(c.device):
         _check(_L.mk_coords_export(c._h, _ptr(out), _stream()), "mk_coords_export")
     return out
 
@@ -156,7 +177,7 @@ def coords_export(c: Coords) -> torch.Tensor:
 def coords_lookup(c: Coords, queries: torch.Tensor) -> torch.Tensor:
     q = _cuda(queries, torch.int32, "queries")
     rows = torch.empty(q.shape[0], dtype=torch.int32, device=q.device)
-    with torch.cuda.device(c.device):
+    with _on_device(c.device):
         _check(_L.mk_coords_lookup(c._h, _ptr(q), q.shape[0], _ptr(rows), _stream()), "mk_coords_lookup")
     return rows
 
@@ -220,7 +241,7 @@ class KernelMap:
 def kmap_build(cin: Coords, cout: Coords, region: Region, transposed: bool = False) -> KernelMap:
     r = region._struct()
     h = ctypes.c_void_p()
-    with torch.cuda.device(cin.device):
+    with _on_device(cin.device):
         _check(_L.mk_kmap_build(context(cin.device.index), cin._h, cout._h, ctypes.byref(r), int(transposed),
                                 _stream(), ctypes.byref(h)), "mk_kmap_build")
     return KernelMap(h, cin.device, cin, cout, transposed)
@@ -231,7 +252,7 @@ def kmap_export(m: KernelMap):
     ptr = torch.empty(m.K + 1, dtype=torch.int64, device=m.device)
     ins = torch.empty(m.n_pairs, dtype=torch.int32, device=m.device)
     outs = torch.empty(m.n_pairs, dtype=torch.int32, device=m.device)
-    with torch.cuda.device(m.device):
+    with _on_device(m.device):
         _check(_L.mk_kmap_export(m._h, _ptr(ptr), _ptr(ins), _ptr(outs), _stream()), "mk_kmap_export")
     return ptr, ins, outs
 
@@ -254,7 +275,7 @@ def _conv(fn, name, m: KernelMap, f_in, W, out_dtype, out=None):
         raise ValueError(f"{name}: shape/dtype mismatch (K={m.K}, n_in={m.n_in})")
     out_dtype = out_dtype or f_in.dtype
     y = out if out is not None else torch.empty((m.n_out, c_out), dtype=out_dtype, device=f_in.device)
-    with torch.cuda.device(f_in.device):
+    with _on_device(f_in.device):
         _check(fn(context(f_in.device.index), m._h, _ptr(f_in.contiguous()), c_in, _ptr(W.contiguous()), _ptr(y),
                   c_out, _dt(f_in), _DT[out_dtype], _stream(f_in)), name)
     return y
@@ -280,7 +301,7 @@ def _backward(fn, name, m: KernelMap, g_out, f_in, W, need_gin=True, need_gw=Tru
         gin = torch.empty((m.n_in, c_in), dtype=f_in.dtype, device=f_in.device)
     if need_gw and gw is None:
         gw = torch.empty((K, c_out, c_in), dtype=torch.float32, device=f_in.device)
-    with torch.cuda.device(f_in.device):
+    with _on_device(f_in.device):
         _check(fn(context(f_in.device.index), m._h, _ptr(g_out.contiguous()), _ptr(f_in.contiguous()),
                   _ptr(W.contiguous()), c_in, c_out, _dt(f_in), _ptr(gin if need_gin else None),
                   _ptr(gw if need_gw else None), _stream(f_in)), name)

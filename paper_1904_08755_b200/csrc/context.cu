@@ -1,5 +1,7 @@
 // context.cu — device binding, allocator plumbing and the thread-local error channel.
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 
 #include "mk_internal.cuh"
 
@@ -78,6 +80,22 @@ void* pinned_stage(size_t bytes) {
 
 void pinned_in_flight(cudaStream_t s) {
   if (t_pin.ev && cudaEventRecord(t_pin.ev, s) == cudaSuccess) t_pin.pending = true;
+}
+
+double HostTimer::now() {
+  return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+HostTimer::HostTimer(const char* nm) : name(nm) {
+  static const bool enabled = std::getenv("MK_HOST_TIMING") != nullptr;
+  on = enabled;
+  mark("start");
+}
+HostTimer::~HostTimer() {
+  if (!on || n == 0) return;
+  mark("end");
+  std::fprintf(stderr, "[mk host] %s:", name);
+  for (int i = 1; i < n; ++i) std::fprintf(stderr, " %s=%.1f", lab[i], t[i] - t[0]);
+  std::fprintf(stderr, "\n");
 }
 
 uint32_t next_pow2(uint64_t v) {

@@ -111,7 +111,7 @@ struct StrideSrc {  // u' = floor_div(u, s_out) * s_out per spatial axis (R7, R1
 // ---------------------------------------------------------------- kernels
 template <class Src>
 __global__ void __launch_bounds__(kBlock) k_insert(Src src, int64_t n, int32_t* __restrict__ claim,
-                                                   uint32_t mask, int32_t* __restrict__ slot_of,
+                                                   uint32_t bmask, int32_t* __restrict__ slot_of,
                                                    unsigned long long* err) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
@@ -119,9 +119,11 @@ __global__ void __launch_bounds__(kBlock) k_insert(Src src, int64_t n, int32_t* 
     const uint32_t code = src.key(p, &k);
     if (code != E_NONE) {
       report(err, p, code);
+      slot_of[p] = -1;  // no slot: k_rank / k_p2r skip the row (the call fails anyway)
       continue;
     }
-    uint32_t h = hash_key(k) & mask;
+    const uint32_t nslots = (bmask + 1u) * kSlotsPerBucket;
+    uint32_t h = (hash_key(k) & bmask) * kSlotsPerBucket;  // first slot of the key's bucket
     while (true) {
       int32_t cur = __ldcg(claim + h);
       if (cur == -1) {
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(kBlock) k_insert(Src src, int64_t n, int32_t* 
         slot_of[p] = (int32_t)h;
         break;
       }
-      h = (h + 1) & mask;
+      h = h + 1 == nslots ? 0u : h + 1;
     }
   }
 }
@@ -182,8 +184,8 @@ __device__ int64_t lookback(unsigned long long* status, int64_t tile, int64_t ag
 
 template <class Src>
 __global__ void __launch_bounds__(kBlock) k_rank(Src src, int64_t n, const int32_t* __restrict__ claim,
-                                                 const int32_t* __restrict__ slot_of, int4* __restrict__ tkeys,
-                                                 int32_t* __restrict__ tvals, int4* __restrict__ out_keys,
+                                                 const int32_t* __restrict__ slot_of, int4* __restrict__ buckets,
+                                                 int4* __restrict__ out_keys,
                                                  int32_t* __restrict__ first_point,
                                                  unsigned long long* status, unsigned int* ticket,
                                                  int64_t* count) {
@@ -203,7 +205,7 @@ __global__ void __launch_bounds__(kBlock) k_rank(Src src, int64_t n, const int32
     win[i] = false;
     if (p < n) {
       slot[i] = slot_of[p];
-      win[i] = claim[slot[i]] == (int32_t)p;
+      win[i] = slot[i] >= 0 && claim[slot[i]] == (int32_t)p;
     }
     cnt += win[i];
   }
@@ -239,21 +241,22 @@ __global__ void __launch_bounds__(kBlock) k_rank(Src src, int64_t n, const int32
     int4 k;
     src.key(p, &k);
     out_keys[row] = k;
-    tkeys[slot[i]] = k;
-    tvals[slot[i]] = (int32_t)row;
+    *slot_key(buckets, (uint32_t)slot[i]) = k;
+    *slot_val(buckets, (uint32_t)slot[i]) = (int32_t)row;
     if (first_point) first_point[row] = (int32_t)p;
     ++row;
   }
 }
 
-// Table init in one launch: keys and claims to the empty sentinel (all ones), look-back
-// status words / ticket / count to 0, the error word to all ones.
-__global__ void k_init(int4* __restrict__ keys, int32_t* __restrict__ claim, uint32_t cap,
+// Table init in one launch: bucket words and claims to the empty sentinel (all ones),
+// look-back status words / ticket / count to 0, the error word to all ones.
+__global__ void k_init(int4* __restrict__ buckets, int32_t* __restrict__ claim, uint32_t nb,
                        unsigned long long* __restrict__ small, int64_t n_small, unsigned long long* err) {
   const int4 e = make_int4(-1, -1, -1, -1);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cap; i += (int64_t)gridDim.x * blockDim.x) {
-    keys[i] = e;
-    claim[i] = -1;
+  const int64_t words = (int64_t)nb * 4, slots = (int64_t)nb * kSlotsPerBucket;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x) {
+    buckets[i] = e;
+    if (i < slots) claim[i] = -1;
   }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_small; i += (int64_t)gridDim.x * blockDim.x)
     small[i] = 0ull;
@@ -263,21 +266,24 @@ __global__ void k_init(int4* __restrict__ keys, int32_t* __restrict__ claim, uin
   }
 }
 
-__global__ void k_p2r(int64_t n, const int32_t* __restrict__ slot_of, const int32_t* __restrict__ tvals,
+__global__ void k_p2r(int64_t n, const int32_t* __restrict__ slot_of, int4* __restrict__ buckets,
                       int32_t* __restrict__ p2r) {
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
-    p2r[p] = tvals[slot_of[p]];
+  {
+    const int32_t sl = slot_of[p];
+    p2r[p] = sl >= 0 ? *slot_val(buckets, (uint32_t)sl) : -1;
+  }
 }
 
-__global__ void k_lookup(const int32_t* __restrict__ q, int64_t nq, int D, const int4* __restrict__ tkeys,
-                         const int32_t* __restrict__ tvals, uint32_t mask, int32_t* __restrict__ rows) {
+__global__ void k_lookup(const int32_t* __restrict__ q, int64_t nq, int D, const int4* __restrict__ buckets,
+                         uint32_t bmask, int32_t* __restrict__ rows) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t c[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int d = 0; d < 4; ++d)
       if (d < D) c[d] = q[i * (D + 1) + d];
     int4 k;
-    rows[i] = pack_key(c, D, q[i * (D + 1) + D], &k) ? probe(tkeys, tvals, mask, k) : -1;
+    rows[i] = pack_key(c, D, q[i * (D + 1) + D], &k) ? probe(buckets, bmask, k) : -1;
   }
 }
 
@@ -309,8 +315,11 @@ struct Carver {
 template <class Src>
 mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const int32_t* ts,
                        cudaStream_t s, mk_coords** out, int32_t* d_p2r, int32_t* d_first) {
+  HostTimer ht("build_coords");
   if (n < 0 || n > INT32_MAX) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "row count out of range [0, 2^31)");
-  const uint32_t cap = next_pow2(std::max<int64_t>(2 * n, 64));
+  // buckets of 3 slots, >= 2n slots in total (load factor <= 1/2)
+  const uint32_t nb = next_pow2(std::max<int64_t>(ceil_div(2 * n, kSlotsPerBucket), 32));
+  const uint32_t nslots = nb * kSlotsPerBucket;
   const int64_t ntiles = std::max<int64_t>(1, ceil_div(n, kTile));
 
   mk_coords* c = new mk_coords();
@@ -321,21 +330,20 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
 
   // persistent: table keys, table values, row keys
   Carver pc;
-  const size_t o_tk = pc.take<int4>(cap), o_tv = pc.take<int32_t>(cap), o_rk = pc.take<int4>(std::max<int64_t>(n, 1));
+  const size_t o_tk = pc.take<int4>((size_t)nb * 4), o_rk = pc.take<int4>(std::max<int64_t>(n, 1));
   char* pbase = (char*)dev_alloc(c->alloc, pc.off, s);
   if (!pbase) {
     delete c;
     MK_FAIL(MK_ERR_OUT_OF_MEMORY, "coords: device allocation failed");
   }
   c->owned.push_back(pbase);
-  c->table.keys = (int4*)(pbase + o_tk);
-  c->table.vals = (int32_t*)(pbase + o_tv);
-  c->table.mask = cap - 1;
+  c->table.buckets = (int4*)(pbase + o_tk);
+  c->table.bmask = nb - 1;
   c->keys = (int4*)(pbase + o_rk);
 
   // scratch: claims, slot per row, look-back status, ticket, error word, count
   Carver sc;
-  const size_t o_cl = sc.take<int32_t>(cap), o_sl = sc.take<int32_t>(std::max<int64_t>(n, 1)),
+  const size_t o_cl = sc.take<int32_t>(nslots), o_sl = sc.take<int32_t>(std::max<int64_t>(n, 1)),
                o_st = sc.take<unsigned long long>(ntiles), o_ti = sc.take<unsigned int>(1),
                o_er = sc.take<unsigned long long>(2);  // error word, then the row count
   char* sbase = (char*)dev_alloc(c->alloc, sc.off, s);
@@ -361,18 +369,18 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
     // status[ntiles], ticket, count are contiguous 8-byte words from o_st; err follows.
     unsigned long long* small = (unsigned long long*)(sbase + o_st);
     const int64_t n_small = (int64_t)((o_er - o_st) / 8);
-    k_init<<<grid_for(std::max<int64_t>(cap, n_small), 256, ctx->num_sms), 256, 0, s>>>(c->table.keys, claim, cap,
-                                                                                       small, n_small, err);
+    k_init<<<grid_for(std::max<int64_t>((int64_t)nb * 4, n_small), 256, ctx->num_sms), 256, 0, s>>>(
+        c->table.buckets, claim, nb, small, n_small, err);
     g_launches++;
   }
   if (n > 0) {
-    k_insert<Src><<<grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s>>>(src, n, claim, cap - 1, slot_of, err);
+    k_insert<Src><<<grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s>>>(src, n, claim, nb - 1, slot_of, err);
     g_launches++;
-    k_rank<Src><<<(int)ntiles, kBlock, 0, s>>>(src, n, claim, slot_of, c->table.keys, c->table.vals, c->keys,
+    k_rank<Src><<<(int)ntiles, kBlock, 0, s>>>(src, n, claim, slot_of, c->table.buckets, c->keys,
                                                  d_first, status, ticket, count);
     g_launches++;
     if (d_p2r) {
-      k_p2r<<<grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s>>>(n, slot_of, c->table.vals, d_p2r);
+      k_p2r<<<grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s>>>(n, slot_of, c->table.buckets, d_p2r);
       g_launches++;
     }
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "launch");
@@ -386,11 +394,13 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
   // err and count are adjacent device words: one 16-byte copy
   if ((e = cudaMemcpyAsync(hr, err, sizeof(Result), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail_cuda(e, "D2H");
   dev_free(c->alloc, sbase, s);
+  ht.mark("launched");
   if ((e = cudaStreamSynchronize(s)) != cudaSuccess) {
     mk_coords_destroy(c);
     set_error(MK_ERR_CUDA, std::string("coords: ") + cudaGetErrorString(e));
     return MK_ERR_CUDA;
   }
+  ht.mark("synced");
   const Result h = *hr;
   if (h.err != ~0ull) {
     const int64_t row = (int64_t)(h.err >> 8);
@@ -494,8 +504,8 @@ mk_status mk_coords_lookup(const mk_coords* c, const int32_t* d_queries, int64_t
   clear_error();
   if (!c || q < 0 || (q > 0 && (!d_queries || !d_rows))) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_lookup: bad argument");
   if (q == 0) return MK_OK;
-  k_lookup<<<grid_for(q, 256, 148), 256, 0, (cudaStream_t)stream>>>(d_queries, q, c->D, c->table.keys,
-                                                                      c->table.vals, c->table.mask, d_rows);
+  k_lookup<<<grid_for(q, 256, 148), 256, 0, (cudaStream_t)stream>>>(d_queries, q, c->D, c->table.buckets,
+                                                                      c->table.bmask, d_rows);
   MK_LAUNCH_CHECK();
   return MK_OK;
 }

@@ -27,6 +27,8 @@ namespace {
 
 constexpr int kTileRows = 128;
 constexpr int kThreads = 256;
+constexpr int kRM = 32;       // row-major staging width: entries per row (K <= 32)
+constexpr int kRMPitch = 33;  // smem pitch of a staged row (bank-conflict free)
 
 // u + sign * off * scale, per spatial axis, batch unchanged (R18).  False when the
 // shifted coordinate cannot exist (outside int32 or the packed-key domain).
@@ -44,44 +46,133 @@ __device__ __forceinline__ bool shift_key(int4 u, int D, const int32_t* off, int
   return pack_key(c, D, key_batch(u, D), q);
 }
 
-__global__ void __launch_bounds__(kThreads) k_probe(const int4* __restrict__ okeys, int64_t n_out, int64_t n_pad,
-                                                    const int4* __restrict__ tkeys, const int32_t* __restrict__ tvals,
-                                                    uint32_t mask, const int32_t* __restrict__ offs, int K, int D,
-                                                    int sign, int4 scale4, int32_t* __restrict__ nbr,
+// Probing.  One CTA per tile of 128 output rows, 256 threads; thread t owns row t % 128
+// and its offsets k = t / 128 + 2i.  A query u + sign*i_k*s reads the key's whole 64-byte
+// bucket (three keys and their rows: four independent 16-byte loads, one round trip) and
+// kPB queries are in flight per thread; a query continues to the next bucket only when all
+// three slots hold other keys (rare).  (A 4-lane cooperative variant — lane j loads word j
+// of the bucket, a ballot resolves — was measured at 172 us on configs[1]: every lane of a
+// group recomputes the query key and hash, so it is instruction bound.)
+// Results are staged in shared memory per chunk of <= 32 offsets, then:
+//   RM (K <= 32): written as a row-major block [row][32] (coalesced; k_permute_rm turns it
+//                 into the permuted k-major table), plus per-row neighbour bitmasks;
+//   otherwise:    written k-major [K][n_pad] (coalesced per offset).
+// Per (offset, tile) pair counts and the tile's active-offset mask come from warp ballots
+// over the staged block.
+constexpr int kPB = 4;  // queries in flight per thread
+
+template <bool RM>
+__global__ void __launch_bounds__(kThreads, 2) k_probe(const int4* __restrict__ okeys, int64_t n_out, int64_t n_pad,
+                                                    const int4* __restrict__ buckets, uint32_t bmask,
+                                                    const int32_t* __restrict__ offs, int K, int D, int sign,
+                                                    int4 scale4, int32_t* __restrict__ nbr,
                                                     int32_t* __restrict__ tile_cnt, int64_t ntiles,
                                                     uint32_t* __restrict__ tile_mask, int mw,
                                                     uint32_t* __restrict__ rowmask) {
   extern __shared__ int32_t sm[];
-  int32_t* s_off = sm;              // [K*D]
-  int32_t* s_cnt = sm + K * D;      // [K]
-  uint32_t* s_rm = (uint32_t*)(s_cnt + K);  // [128] row masks (K <= 32)
+  int4* s_doff = (int4*)sm;                  // [K] offset deltas of a packed key (fast path)
+  int32_t* s_off = sm + 4 * K;               // [K*D]
+  int32_t* s_cnt = s_off + K * D;            // [32] counts of the current chunk
+  int32_t* s_tab = s_cnt + kRM;              // [128][33]
+  __shared__ int s_slow;                     // some offset delta does not fit the fast path
+  if (threadIdx.x == 0) s_slow = 0;
   for (int i = threadIdx.x; i < K * D; i += kThreads) s_off[i] = offs[i];
-  for (int i = threadIdx.x; i < K; i += kThreads) s_cnt[i] = 0;
-  if (threadIdx.x < kTileRows) s_rm[threadIdx.x] = 0;
+  __syncthreads();
+  // Fast path: key(u + sign*i_k*s) = key(u) + delta_k as one int4 add, valid whenever the row's
+  // components are small enough that no component can leave its range (|u| < 2^30 and
+  // |delta| < 2^30; D = 4 packs t in 16 bits: |t| < 2^14 and |dt| < 2^14).
+  for (int k = threadIdx.x; k < K; k += kThreads) {
+    int64_t d[4] = {0, 0, 0, 0};
+    const int32_t sc[4] = {scale4.x, scale4.y, scale4.z, scale4.w};
+    bool fits = true;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+      if (a < D) {
+        d[a] = (int64_t)sign * s_off[k * D + a] * sc[a];
+        fits &= (d[a] > -(1ll << 30) && d[a] < (1ll << 30)) && (a < 3 || (d[a] > -(1 << 14) && d[a] < (1 << 14)));
+      }
+    if (!fits) atomicOr(&s_slow, 1);
+    s_doff[k] = make_int4((int32_t)d[0], (int32_t)d[1], (int32_t)d[2], D == 4 ? (int32_t)((uint32_t)d[3] << 16) : 0);
+  }
   __syncthreads();
   const int64_t tile = blockIdx.x;
-  const int64_t o = tile * kTileRows + (threadIdx.x & (kTileRows - 1));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int r = threadIdx.x & (kTileRows - 1), kl = threadIdx.x >> 7;
+  const int64_t o = tile * kTileRows + r;
   const bool valid = o < n_out;
-  int4 u = make_int4(0, 0, 0, 0);
-  if (valid) u = okeys[o];
-  uint32_t rm = 0;
-  for (int k = threadIdx.x / kTileRows; k < K; k += kThreads / kTileRows) {
-    int32_t a = -1;
-    int4 q;
-    if (valid && shift_key(u, D, s_off + k * D, sign, scale4, &q)) a = probe(tkeys, tvals, mask, q);
-    nbr[(int64_t)k * n_pad + o] = a;  // rows padded to whole tiles (-1)
-    if (a >= 0 && k < 32) rm |= 1u << k;
-    const unsigned b = __ballot_sync(0xffffffffu, a >= 0);
-    if ((threadIdx.x & 31) == 0 && b) atomicAdd(s_cnt + k, __popc(b));
-  }
-  if (rowmask) atomicOr(s_rm + (threadIdx.x & (kTileRows - 1)), rm);
-  __syncthreads();
-  if (rowmask && threadIdx.x < kTileRows && valid) rowmask[o] = s_rm[threadIdx.x];
-  for (int k = threadIdx.x; k < K; k += kThreads) tile_cnt[(int64_t)k * ntiles + tile] = s_cnt[k];
-  for (int w = threadIdx.x; w < mw; w += kThreads) {
-    uint32_t bits = 0;
-    for (int j = 0; j < 32 && w * 32 + j < K; ++j) bits |= (s_cnt[w * 32 + j] > 0 ? 1u : 0u) << j;
-    tile_mask[tile * mw + w] = bits;
+  const int4 u = valid ? __ldg(okeys + o) : make_int4(0, 0, 0, 0);
+  auto small = [](int32_t v, int32_t lim) { return v > -lim && v < lim; };
+  // block-uniform: one row outside the fast-path range sends the whole tile down the slow path
+  const bool fast = __syncthreads_and(!s_slow && small(u.x, 1 << 30) && small(u.y, 1 << 30) &&
+                                      small(u.z, 1 << 30) && (D < 4 || small(key_axis(u, D, 3), 1 << 14)));
+  for (int kc = 0; kc < K; kc += kRM) {
+    const int kn = min(kRM, K - kc);
+    for (int kb = kl; kb < kn; kb += 2 * kPB) {
+      int4 q[kPB];
+      Bucket w[kPB];
+      bool ok[kPB];
+#pragma unroll
+      for (int b = 0; b < kPB; ++b) {
+        const int k = kb + 2 * b;
+        if (fast) {
+          const int4 dq = s_doff[kc + (k < kn ? k : 0)];
+          q[b] = make_int4(u.x + dq.x, u.y + dq.y, u.z + dq.z, u.w + dq.w);
+          ok[b] = valid && k < kn;
+        } else {
+          ok[b] = valid && k < kn && shift_key(u, D, s_off + (kc + k) * D, sign, scale4, &q[b]);
+        }
+        // unconditional loads (bucket 0 for masked queries): no divergent regions, all
+        // 4 * kPB loads of the thread are issued back to back
+        w[b] = load_bucket(buckets + (size_t)(ok[b] ? hash_key(q[b]) & bmask : 0u) * 4u);
+      }
+#pragma unroll
+      for (int b = 0; b < kPB; ++b) {
+        const int k = kb + 2 * b;
+        if (k < kn) {
+          const bool m0 = ok[b] && key_eq(w[b].k0, q[b]), m1 = ok[b] && key_eq(w[b].k1, q[b]),
+                     m2 = ok[b] && key_eq(w[b].k2, q[b]);
+          int32_t a = m0 ? w[b].v.x : m1 ? w[b].v.y : m2 ? w[b].v.z : -1;
+          if (ok[b] && !(m0 | m1 | m2) && w[b].k0.w != kEmptyWord && w[b].k1.w != kEmptyWord &&
+              w[b].k2.w != kEmptyWord)
+            a = probe_next(buckets, bmask, q[b]);  // bucket full of other keys (rare)
+          s_tab[r * kRMPitch + k] = a;
+        }
+      }
+    }
+    __syncthreads();
+    // pair counts per offset of the chunk: ballots over the 128 staged rows
+    for (int k = warp; k < kn; k += kThreads / 32) {
+      int c = 0;
+#pragma unroll
+      for (int r0 = 0; r0 < kTileRows; r0 += 32) c += __popc(__ballot_sync(0xffffffffu, s_tab[(r0 + lane) * kRMPitch + k] >= 0));
+      if (lane == 0) s_cnt[k] = c;
+    }
+    if (RM) {
+      int32_t* dst = nbr + tile * (kTileRows * kRM);
+      for (int i = threadIdx.x; i < kTileRows * kRM; i += kThreads) {
+        const int rr = i >> 5, k = i & (kRM - 1);
+        dst[i] = k < kn ? s_tab[rr * kRMPitch + k] : -1;
+      }
+      if (rowmask && threadIdx.x < kTileRows) {
+        const int64_t o = tile * kTileRows + threadIdx.x;
+        uint32_t rm = 0;
+        for (int k = 0; k < kn; ++k) rm |= (s_tab[threadIdx.x * kRMPitch + k] >= 0 ? 1u : 0u) << k;
+        if (o < n_out) rowmask[o] = rm;
+      }
+    } else {
+      for (int i = threadIdx.x; i < kn * kTileRows; i += kThreads) {
+        const int k = i >> 7, rr = i & (kTileRows - 1);
+        nbr[(int64_t)(kc + k) * n_pad + tile * kTileRows + rr] = s_tab[rr * kRMPitch + k];  // padding rows: -1
+      }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < kn; k += kThreads) tile_cnt[(int64_t)(kc + k) * ntiles + tile] = s_cnt[k];
+    if (threadIdx.x == 0) {
+      uint32_t bits = 0;
+      for (int k = 0; k < kn; ++k) bits |= (s_cnt[k] > 0 ? 1u : 0u) << k;
+      tile_mask[tile * mw + kc / 32] = bits;
+    }
+    __syncthreads();
   }
 }
 
@@ -124,29 +215,75 @@ __global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ tile_
   if (threadIdx.x == 0) totals[k] = s_carry;
 }
 
+// Per-offset CSR offsets ptr[k] = sum of totals[0..k) computed on the device (block-local
+// copy in shared memory; block 0 also publishes ptr[0..K]).  Then ballot/popc compaction of
+// the tile's neighbour entries into the pair lists (output-ascending within an offset,
+// S:157); for maps that are not symmetric also the transposed table nbrT[k][a] = o (dgrad).
+template <bool RM>
 __global__ void __launch_bounds__(kThreads) k_emit(const int32_t* __restrict__ nbr, int64_t n_out, int64_t n_pad, int K,
-                                                   const int64_t* __restrict__ ptr, const int64_t* __restrict__ tile_off,
-                                                   int64_t ntiles, int32_t* __restrict__ in_idx,
-                                                   int32_t* __restrict__ out_idx, int32_t* __restrict__ nbrT,
-                                                   int64_t nT_pad, uint32_t* __restrict__ tile_maskT, int mw) {
-  extern __shared__ int32_t s_wc[];  // [K][4] pairs per (offset, warp of the tile)
+                                                   const int64_t* __restrict__ totals, int64_t* __restrict__ ptr_out,
+                                                   const int64_t* __restrict__ tile_off, int64_t ntiles,
+                                                   int32_t* __restrict__ in_idx, int32_t* __restrict__ out_idx,
+                                                   int32_t* __restrict__ nbrT, int64_t nT_pad,
+                                                   uint32_t* __restrict__ tile_maskT, int mw) {
+  extern __shared__ int64_t s_ptr[];                  // [K + 1]
+  int64_t* s_toff = s_ptr + K + 1;                    // [K] this tile's offset inside each offset's list
+  int32_t* s_wc = (int32_t*)(s_toff + K);             // [K][4] pairs per (offset, warp of the tile)
+  int32_t* s_tab = s_wc + 4 * K;                      // [128][33] (RM)
   const int64_t tile = blockIdx.x;
   const int r = threadIdx.x & (kTileRows - 1);
   const int64_t o = tile * kTileRows + r;
   const bool valid = o < n_out;
   const int lane = threadIdx.x & 31, wq = r >> 5;  // warp quarter of the 128-row tile
   const unsigned lt = (1u << lane) - 1u;
+  if (threadIdx.x < 32) {  // warp 0: exclusive scan of the offset totals
+    int64_t carry = 0;
+    for (int b = 0; b < K; b += 32) {
+      const int64_t v = b + lane < K ? totals[b + lane] : 0;
+      int64_t x = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int64_t y = __shfl_up_sync(0xffffffffu, x, d);
+        if (lane >= d) x += y;
+      }
+      if (b + lane < K) s_ptr[b + lane] = carry + x - v;
+      carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) s_ptr[K] = carry;
+  }
+  for (int k = threadIdx.x; k < K; k += kThreads) s_toff[k] = tile_off[(int64_t)k * ntiles + tile];
+  if (RM) {  // 16 KB block: four independent 16-byte loads per thread, then scalar stores
+    const int4* src = (const int4*)(nbr + tile * (kTileRows * kRM));
+    int4 v[kTileRows * kRM / 4 / kThreads];
+#pragma unroll
+    for (int j = 0; j < kTileRows * kRM / 4 / kThreads; ++j) v[j] = __ldg(src + threadIdx.x + j * kThreads);
+#pragma unroll
+    for (int j = 0; j < kTileRows * kRM / 4 / kThreads; ++j) {
+      const int i = 4 * (threadIdx.x + j * kThreads);
+      int32_t* d = s_tab + (i >> 5) * kRMPitch + (i & (kRM - 1));
+      d[0] = v[j].x;
+      d[1] = v[j].y;
+      d[2] = v[j].z;
+      d[3] = v[j].w;
+    }
+  }
+  __syncthreads();
+  if (blockIdx.x == 0)
+    for (int k = threadIdx.x; k <= K; k += kThreads) ptr_out[k] = s_ptr[k];
+  auto get = [&](int k) -> int32_t {
+    if (!valid) return -1;
+    return RM ? s_tab[r * kRMPitch + k] : nbr[(int64_t)k * n_pad + o];
+  };
   for (int k = threadIdx.x / kTileRows; k < K; k += kThreads / kTileRows) {
-    const int32_t a = valid ? nbr[(int64_t)k * n_pad + o] : -1;
-    const unsigned b = __ballot_sync(0xffffffffu, a >= 0);
+    const unsigned b = __ballot_sync(0xffffffffu, get(k) >= 0);
     if (lane == 0) s_wc[k * 4 + wq] = __popc(b);
   }
   __syncthreads();
   for (int k = threadIdx.x / kTileRows; k < K; k += kThreads / kTileRows) {
-    const int32_t a = valid ? nbr[(int64_t)k * n_pad + o] : -1;
+    const int32_t a = get(k);
     const unsigned b = __ballot_sync(0xffffffffu, a >= 0);
     if (a < 0) continue;
-    int64_t pos = ptr[k] + tile_off[(int64_t)k * ntiles + tile] + __popc(b & lt);
+    int64_t pos = s_ptr[k] + s_toff[k] + __popc(b & lt);
     for (int w = 0; w < wq; ++w) pos += s_wc[k * 4 + w];
     in_idx[pos] = a;
     out_idx[pos] = (int32_t)o;
@@ -154,6 +291,54 @@ __global__ void __launch_bounds__(kThreads) k_emit(const int32_t* __restrict__ n
       nbrT[(int64_t)k * nT_pad + a] = (int32_t)o;
       atomicOr(tile_maskT + (int64_t)(a / kTileRows) * mw + (k >> 5), 1u << (k & 31));
     }
+  }
+}
+
+// Permuted k-major table from the row-major block (K <= 32): position i holds row perm[i];
+// out[k][i] = nbr_rm[perm[i]][k] (one 128-byte row load per position, coalesced k-major
+// stores), plus the active-offset mask of every permuted 128-row tile.
+// With `mirror` set (symmetric submanifold map) it also writes the dgrad tile mask: bit k of
+// the dgrad view = bit mirror[k] of the forward mask.
+__global__ void __launch_bounds__(kTileRows) k_permute_rm(const int32_t* __restrict__ nbr_rm, int64_t stride, int64_t n,
+                                                          int K, const int32_t* __restrict__ perm,
+                                                          int32_t* __restrict__ out, uint32_t* __restrict__ tmask,
+                                                          const int32_t* __restrict__ mirror,
+                                                          uint32_t* __restrict__ tmaskT) {
+  __shared__ uint32_t s_bits;
+  if (threadIdx.x == 0) s_bits = 0;
+  __syncthreads();
+  const int64_t i = (int64_t)blockIdx.x * kTileRows + threadIdx.x;
+  const int32_t r = i < n ? (perm ? perm[i] : (int32_t)i) : -1;
+  int32_t v[kRM];
+  if (r >= 0) {
+    const int4* src = (const int4*)(nbr_rm + (int64_t)r * kRM);
+#pragma unroll
+    for (int j = 0; j < kRM / 4; ++j) {
+      const int4 x = __ldg(src + j);
+      v[4 * j] = x.x;
+      v[4 * j + 1] = x.y;
+      v[4 * j + 2] = x.z;
+      v[4 * j + 3] = x.w;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < kRM; ++j) v[j] = -1;
+  }
+  uint32_t bits = 0;
+#pragma unroll
+  for (int k = 0; k < kRM; ++k) {
+    if (k < K) {
+      out[(int64_t)k * stride + i] = v[k];
+      if (__any_sync(0xffffffffu, v[k] >= 0)) bits |= 1u << k;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) atomicOr(&s_bits, bits);
+  __syncthreads();
+  if (threadIdx.x == 0) tmask[blockIdx.x] = s_bits;
+  if (mirror && threadIdx.x < 32) {
+    const uint32_t bT = threadIdx.x < K ? ((s_bits >> __ldg(mirror + threadIdx.x)) & 1u) << threadIdx.x : 0u;
+    const uint32_t m = __reduce_or_sync(0xffffffffu, bT);
+    if (threadIdx.x == 0) tmaskT[blockIdx.x] = m;
   }
 }
 
@@ -169,7 +354,7 @@ __global__ void k_rowmask_T(const int32_t* __restrict__ nbrT, int64_t stride, in
 
 // Neighbour table in permuted row order: out[k][i] = tab[k][perm[i]] (padding rows -1), and
 // the active-offset mask of every permuted 128-row tile (K <= 32: one word).
-__global__ void __launch_bounds__(kTileRows) k_permute(const int32_t* __restrict__ tab, int64_t stride, int64_t n,
+__global__ void __launch_bounds__(kTileRows) k_permute_km(const int32_t* __restrict__ tab, int64_t stride, int64_t n,
                                                        int K, const int32_t* __restrict__ perm,
                                                        int32_t* __restrict__ out, uint32_t* __restrict__ tmask) {
   __shared__ uint32_t s_bits;
@@ -211,6 +396,7 @@ extern "C" {
 
 mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* out, const mk_region* region,
                         int32_t transposed, void* stream_, mk_kmap** out_map) {
+  HostTimer ht("kmap_build");
   clear_error();
   cudaStream_t s = (cudaStream_t)stream_;
   if (!ctx || !in || !out || !region || !out_map) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_kmap_build: null argument");
@@ -258,6 +444,11 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   const int64_t n_pad = ntiles * kTileRows, nT_pad = ntilesT * kTileRows;  // table rows padded to whole tiles
   m->nbr_stride = n_pad;
   m->nbrT_stride = symmetric ? n_pad : nT_pad;
+  // K <= 32: row-major staging + bitmask row ordering, and pair lists allocated at their
+  // upper bound K * n_out so the build needs its one host sync only at the very end.
+  // K > 32: k-major table, identity order, exact pair lists (sync after the count).
+  const bool rm = K <= kRM;
+  const bool upper_bound = rm;
 
   auto fail = [&](mk_status code, const std::string& msg) {
     mk_kmap_destroy(m);
@@ -269,32 +460,37 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     if (p) m->owned.push_back(p);
     return p;
   };
+  // scratch (freed stream-ordered at the end of the build)
+  std::vector<void*> scratch;
+  auto salloc = [&](size_t bytes) -> void* {
+    void* p = dev_alloc(m->alloc, bytes, s);
+    if (p) scratch.push_back(p);
+    return p;
+  };
+  auto free_scratch = [&]() {
+    for (void* p : scratch) dev_free(m->alloc, p, s);
+    scratch.clear();
+  };
+  auto oom = [&]() {
+    free_scratch();
+    return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: device allocation failed");
+  };
 
-  // persistent: offsets/mirror, ptr, nbr, tile masks (+ nbrT / maskT when not symmetric)
   int32_t* d_offs = (int32_t*)alloc(sizeof(int32_t) * (K * D + K));  // offsets, then mirror
   m->d_mirror = d_offs ? d_offs + K * D : nullptr;
   m->nbr = (int32_t*)alloc(sizeof(int32_t) * (int64_t)K * n_pad);
   m->tile_mask = (uint32_t*)alloc(sizeof(uint32_t) * ntiles * mw);
   m->tile_maskT = (uint32_t*)alloc(sizeof(uint32_t) * ntilesT * mw);
+  m->ptr = (int64_t*)alloc(sizeof(int64_t) * (K + 1));
   if (!symmetric) m->nbrT = (int32_t*)alloc(sizeof(int32_t) * (int64_t)K * nT_pad);
-  // scratch: tile counts, tile offsets, totals
-  void* scratch = dev_alloc(m->alloc, sizeof(int32_t) * K * ntiles + sizeof(int64_t) * K * ntiles + 256 +
-                                          sizeof(int64_t) * K, s);
-  if (!m->d_mirror || !d_offs || !m->nbr || !m->tile_mask || !m->tile_maskT || (!symmetric && !m->nbrT) ||
-      !scratch) {
-    if (scratch) dev_free(m->alloc, scratch, s);
-    return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: device allocation failed");
-  }
-  // Row masks for the bitmask ordering of the conv tiles (K <= 32 offsets only).
-  const bool sort_rows = K <= 32;
-  uint32_t* rowmask = sort_rows ? (uint32_t*)dev_alloc(m->alloc, sizeof(uint32_t) * std::max<int64_t>(1, std::max(n_out, n_in)), s) : nullptr;
-  if (sort_rows && !rowmask) {
-    dev_free(m->alloc, scratch, s);
-    return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: device allocation failed");
-  }
-  int64_t* tile_off = (int64_t*)scratch;
-  int64_t* totals = tile_off + K * ntiles;
-  int32_t* tile_cnt = (int32_t*)(totals + K);
+  int32_t* nbr_rm = rm ? (int32_t*)salloc(sizeof(int32_t) * n_pad * kRM) : nullptr;
+  int64_t* tile_off = (int64_t*)salloc(sizeof(int64_t) * K * ntiles);
+  int64_t* totals = (int64_t*)salloc(sizeof(int64_t) * K);
+  int32_t* tile_cnt = (int32_t*)salloc(sizeof(int32_t) * K * ntiles);
+  uint32_t* rowmask = rm ? (uint32_t*)salloc(sizeof(uint32_t) * std::max<int64_t>(1, std::max(n_out, n_in))) : nullptr;
+  if (!d_offs || !m->nbr || !m->tile_mask || !m->tile_maskT || !m->ptr || (!symmetric && !m->nbrT) ||
+      (rm && (!nbr_rm || !rowmask)) || !tile_off || !totals || !tile_cnt)
+    return oom();
 
   cudaError_t e = cudaSuccess;
   auto ck = [&](cudaError_t r) {
@@ -302,10 +498,7 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   };
   {  // one pinned H2D copy of the offsets and their mirror indices
     int32_t* h = (int32_t*)pinned_stage(sizeof(int32_t) * (K * D + K));
-    if (!h) {
-      dev_free(m->alloc, scratch, s);
-      return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: pinned staging failed");
-    }
+    if (!h) return oom();
     std::copy(offs.begin(), offs.end(), h);
     std::copy(m->mirror.begin(), m->mirror.end(), h + K * D);
     ck(cudaMemcpyAsync(d_offs, h, sizeof(int32_t) * (K * D + K), cudaMemcpyHostToDevice, s));
@@ -315,45 +508,124 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     ck(cudaMemsetAsync(m->nbrT, 0xFF, sizeof(int32_t) * K * nT_pad, s));
     ck(cudaMemsetAsync(m->tile_maskT, 0, sizeof(uint32_t) * ntilesT * mw, s));
   }
+  ht.mark("setup");
   if (n_out > 0) {
-    k_probe<<<(unsigned)ntiles, kThreads, sizeof(int32_t) * (K * D + K + kTileRows), s>>>(
-        out->keys, n_out, n_pad, in->table.keys, in->table.vals, in->table.mask, d_offs, K, D, sign, scale4, m->nbr,
-        tile_cnt, ntiles, m->tile_mask, mw, rowmask);
+    const size_t smem = sizeof(int32_t) * (4 * K + K * D + kRM + kTileRows * kRMPitch);
+    if (smem > 48 * 1024) {
+      cudaFuncSetAttribute(k_probe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_probe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    if (rm)
+      k_probe<true><<<(unsigned)ntiles, kThreads, smem, s>>>(out->keys, n_out, n_pad, in->table.buckets,
+                                                             in->table.bmask, d_offs, K, D, sign, scale4, nbr_rm,
+                                                             tile_cnt, ntiles, m->tile_mask, mw, rowmask);
+    else
+      k_probe<false><<<(unsigned)ntiles, kThreads, smem, s>>>(out->keys, n_out, n_pad, in->table.buckets,
+                                                              in->table.bmask, d_offs, K, D, sign, scale4, m->nbr,
+                                                              tile_cnt, ntiles, m->tile_mask, mw, nullptr);
     g_launches++;
     k_scan<<<K, 1024, 0, s>>>(tile_cnt, ntiles, tile_off, totals);
     g_launches++;
+    ht.mark("probe+scan");
   } else {
     ck(cudaMemsetAsync(m->tile_mask, 0, sizeof(uint32_t) * ntiles * mw, s));
     ck(cudaMemsetAsync(m->nbr, 0xFF, sizeof(int32_t) * K * n_pad, s));
     ck(cudaMemsetAsync(totals, 0, sizeof(int64_t) * K, s));
+    ck(cudaMemsetAsync(m->ptr, 0, sizeof(int64_t) * (K + 1), s));
   }
   ck(cudaGetLastError());
-  int64_t* h_tot = (int64_t*)pinned_stage(sizeof(int64_t) * K);
-  if (!h_tot) {
-    dev_free(m->alloc, scratch, s);
-    return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: pinned staging failed");
+  // Host copy of the per-offset pair counts (pinned D2H, then the build's single stream sync;
+  // the copy is enqueued before the scratch holding `totals` is released).
+  int64_t* h_tot = nullptr;
+  auto copy_totals = [&]() -> bool {
+    h_tot = (int64_t*)pinned_stage(sizeof(int64_t) * K);
+    if (!h_tot) return false;
+    ck(cudaMemcpyAsync(h_tot, totals, sizeof(int64_t) * K, cudaMemcpyDeviceToHost, s));
+    return true;
+  };
+  auto finish_totals = [&]() {
+    ck(cudaStreamSynchronize(s));
+    m->h_ptr.assign(K + 1, 0);
+    for (int k = 0; k < K; ++k) m->h_ptr[k + 1] = m->h_ptr[k] + (e == cudaSuccess ? h_tot[k] : 0);
+    m->n_pairs = m->h_ptr[K];
+  };
+  int64_t pair_cap = (int64_t)K * n_out;
+  if (!upper_bound) {
+    if (!copy_totals()) return oom();
+    finish_totals();
+    if (e != cudaSuccess) {
+      free_scratch();
+      return fail(MK_ERR_CUDA, std::string("mk_kmap_build: ") + cudaGetErrorString(e));
+    }
+    pair_cap = m->n_pairs;
   }
-  ck(cudaMemcpyAsync(h_tot, totals, sizeof(int64_t) * K, cudaMemcpyDeviceToHost, s));
-  ck(cudaStreamSynchronize(s));
-  if (e != cudaSuccess) {
-    dev_free(m->alloc, scratch, s);
-    return fail(MK_ERR_CUDA, std::string("mk_kmap_build: ") + cudaGetErrorString(e));
-  }
-  m->h_ptr.assign(K + 1, 0);
-  for (int k = 0; k < K; ++k) m->h_ptr[k + 1] = m->h_ptr[k] + h_tot[k];
-  m->n_pairs = m->h_ptr[K];
-  if (m->n_pairs > INT32_MAX) {
-    dev_free(m->alloc, scratch, s);
+  if (!upper_bound && pair_cap > INT32_MAX) {
+    free_scratch();
     return fail(MK_ERR_UNSUPPORTED, "mk_kmap_build: more than 2^31 pairs");
   }
-  // +4 entries of padding: the wgrad kernel bulk-copies 16-byte aligned supersets of ranges
-  m->in_idx = (int32_t*)alloc(sizeof(int32_t) * (m->n_pairs + 4));
-  m->out_idx = (int32_t*)alloc(sizeof(int32_t) * (m->n_pairs + 4));
-  if (!m->in_idx || !m->out_idx) {
-    dev_free(m->alloc, scratch, s);
-    return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: device allocation failed");
+  // +4 entries of padding: the wgrad kernel reads 16-byte aligned supersets of ranges
+  m->in_idx = (int32_t*)alloc(sizeof(int32_t) * (pair_cap + 4));
+  m->out_idx = (int32_t*)alloc(sizeof(int32_t) * (pair_cap + 4));
+  if (!m->in_idx || !m->out_idx) return oom();
+  if (n_out > 0) {
+    const size_t smem = sizeof(int64_t) * (2 * K + 1) + sizeof(int32_t) * (4 * K + (rm ? kTileRows * kRMPitch : 0));
+    if (rm)
+      k_emit<true><<<(unsigned)ntiles, kThreads, smem, s>>>(nbr_rm, n_out, n_pad, K, totals, m->ptr, tile_off, ntiles,
+                                                            m->in_idx, m->out_idx, m->nbrT, nT_pad, m->tile_maskT, mw);
+    else
+      k_emit<false><<<(unsigned)ntiles, kThreads, smem, s>>>(m->nbr, n_out, n_pad, K, totals, m->ptr, tile_off,
+                                                             ntiles, m->in_idx, m->out_idx, m->nbrT, nT_pad,
+                                                             m->tile_maskT, mw);
+    g_launches++;
   }
-  {  // CSR offsets + weight-gradient split-K plan: one device block, one pinned H2D copy
+  // Order the conv tiles' rows by neighbour bitmask (stable radix sort of the row masks):
+  // rows sharing offsets share tiles, so the tensor-core kernels skip empty (tile, k) units.
+  // The permutation is internal; the CSR above and all exported row orders are unchanged.
+  if (rm && n_out > 0) {
+    m->perm = (int32_t*)alloc(sizeof(int32_t) * n_pad);
+    if (!m->perm) return oom();
+    ht.mark("emit");
+    st = radix_sort_perm(m->alloc, rowmask, n_out, K, m->perm, s);
+    ht.mark("sort");
+    if (st == MK_OK) {
+      k_permute_rm<<<(unsigned)ntiles, kTileRows, 0, s>>>(nbr_rm, n_pad, n_out, K, m->perm, m->nbr, m->tile_mask,
+                                                          symmetric ? m->d_mirror : nullptr, m->tile_maskT);
+      g_launches++;
+    }
+    if (st == MK_OK && !symmetric && n_in > 0) {
+      k_rowmask_T<<<(unsigned)std::min<int64_t>(ceil_div(n_in, 256), 4096), 256, 0, s>>>(m->nbrT, nT_pad, n_in, K,
+                                                                                        rowmask);
+      g_launches++;
+      m->permT = (int32_t*)alloc(sizeof(int32_t) * nT_pad);
+      int32_t* tabP = (int32_t*)alloc(sizeof(int32_t) * (int64_t)K * nT_pad);
+      if (!m->permT || !tabP) return oom();
+      st = radix_sort_perm(m->alloc, rowmask, n_in, K, m->permT, s);
+      if (st == MK_OK) {
+        k_permute_km<<<(unsigned)ntilesT, kTileRows, 0, s>>>(m->nbrT, nT_pad, n_in, K, m->permT, tabP, m->tile_maskT);
+        g_launches++;
+        m->nbrT = tabP;  // the unpermuted table stays owned (freed with the map) but is no longer read
+      }
+    }
+    if (st != MK_OK) {
+      free_scratch();
+      return fail(st, "mk_kmap_build: row ordering failed");
+    }
+  }
+  if (symmetric && !(rm && n_out > 0)) {  // (k_permute_rm already wrote the mirrored masks)
+    k_mirror_mask<<<(unsigned)std::min<int64_t>(ceil_div(ntiles, 256), 1024), 256, 0, s>>>(m->tile_mask, ntiles, mw,
+                                                                                          m->d_mirror, K, m->tile_maskT);
+    g_launches++;
+  }
+  if (symmetric) m->permT = m->perm;  // same row set, mirrored masks: same ordering
+  ck(cudaGetLastError());
+  if (upper_bound && !copy_totals()) return oom();
+  free_scratch();  // stream-ordered: after every kernel and copy above
+  ht.mark("launched");
+  if (upper_bound) finish_totals();
+  ht.mark("synced");
+  if (e != cudaSuccess) return fail(MK_ERR_CUDA, std::string("mk_kmap_build: ") + cudaGetErrorString(e));
+  if (m->n_pairs > INT32_MAX) return fail(MK_ERR_UNSUPPORTED, "mk_kmap_build: more than 2^31 pairs");
+  {  // weight-gradient split-K plan: one device block, one pinned H2D copy
     std::vector<int4> segs;
     std::vector<int32_t> seg_begin, slot_begin(K + 1, 0);
     const int64_t P = m->n_pairs;
@@ -374,70 +646,22 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     }
     m->n_wcta = (int32_t)ncta;
     m->n_wslots = (int64_t)segs.size();
-    const size_t b_ptr = (sizeof(int64_t) * (K + 1) + 15) & ~size_t(15), b_seg = sizeof(int4) * std::max<size_t>(1, segs.size());
+    const size_t b_seg = sizeof(int4) * std::max<size_t>(1, segs.size());
     const size_t b_sb = sizeof(int32_t) * seg_begin.size(), b_kb = sizeof(int32_t) * (K + 1);
-    const size_t total = b_ptr + b_seg + b_sb + b_kb;
+    const size_t total = b_seg + b_sb + b_kb;
     char* d = (char*)alloc(total);
     char* h = (char*)pinned_stage(total);
-    if (!d || !h) {
-      dev_free(m->alloc, scratch, s);
-      return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: allocation failed");
-    }
-    std::memcpy(h, m->h_ptr.data(), sizeof(int64_t) * (K + 1));
-    if (!segs.empty()) std::memcpy(h + b_ptr, segs.data(), sizeof(int4) * segs.size());
-    std::memcpy(h + b_ptr + b_seg, seg_begin.data(), b_sb);
-    std::memcpy(h + b_ptr + b_seg + b_sb, slot_begin.data(), b_kb);
-    ck(cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, s));
+    if (!d || !h) return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: allocation failed");
+    if (!segs.empty()) std::memcpy(h, segs.data(), sizeof(int4) * segs.size());
+    std::memcpy(h + b_seg, seg_begin.data(), b_sb);
+    std::memcpy(h + b_seg + b_sb, slot_begin.data(), b_kb);
+    e = cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, s);
     pinned_in_flight(s);
-    m->ptr = (int64_t*)d;  // b_ptr is padded to 16 bytes so the int4 plan stays aligned
-    m->wseg = (int4*)(d + b_ptr);
-    m->wseg_begin = (int32_t*)(d + b_ptr + b_seg);
-    m->wslot_begin = (int32_t*)(d + b_ptr + b_seg + b_sb);
+    if (e != cudaSuccess) return fail(MK_ERR_CUDA, std::string("mk_kmap_build: ") + cudaGetErrorString(e));
+    m->wseg = (int4*)d;
+    m->wseg_begin = (int32_t*)(d + b_seg);
+    m->wslot_begin = (int32_t*)(d + b_seg + b_sb);
   }
-  if (n_out > 0) {
-    k_emit<<<(unsigned)ntiles, kThreads, sizeof(int32_t) * K * 4, s>>>(m->nbr, n_out, n_pad, K, m->ptr, tile_off,
-                                                                        ntiles, m->in_idx, m->out_idx, m->nbrT, nT_pad,
-                                                                        m->tile_maskT, mw);
-    g_launches++;
-  }
-  // Order the conv tiles' rows by neighbour bitmask (stable radix sort of the row masks):
-  // rows sharing offsets share tiles, so the tensor-core kernels skip empty (tile, k) units.
-  // The permutation is internal; the CSR above and all exported row orders are unchanged.
-  if (sort_rows && n_out > 0) {
-    auto permute = [&](int32_t*& tab, int64_t stride, int64_t n, int64_t nt, uint32_t* tmask, int32_t*& perm_out) {
-      int32_t* perm = (int32_t*)alloc(sizeof(int32_t) * stride);
-      int32_t* tabP = (int32_t*)alloc(sizeof(int32_t) * (int64_t)K * stride);
-      if (!perm || !tabP) return MK_ERR_OUT_OF_MEMORY;
-      mk_status st2 = radix_sort_perm(m->alloc, rowmask, n, K, perm, s);
-      if (st2 != MK_OK) return st2;
-      k_permute<<<(unsigned)nt, kTileRows, 0, s>>>(tab, stride, n, K, perm, tabP, tmask);
-      g_launches++;
-      tab = tabP;  // the unpermuted table stays owned (freed with the map) but is no longer read
-      perm_out = perm;
-      return MK_OK;
-    };
-    mk_status st2 = permute(m->nbr, n_pad, n_out, ntiles, m->tile_mask, m->perm);
-    if (st2 == MK_OK && !symmetric && n_in > 0) {
-      k_rowmask_T<<<(unsigned)std::min<int64_t>(ceil_div(n_in, 256), 4096), 256, 0, s>>>(m->nbrT, nT_pad, n_in, K, rowmask);
-      g_launches++;
-      st2 = permute(m->nbrT, nT_pad, n_in, ntilesT, m->tile_maskT, m->permT);
-    }
-    if (st2 != MK_OK) {
-      dev_free(m->alloc, rowmask, s);
-      dev_free(m->alloc, scratch, s);
-      return fail(st2, "mk_kmap_build: row ordering failed");
-    }
-  }
-  if (rowmask) dev_free(m->alloc, rowmask, s);
-  if (symmetric) {
-    k_mirror_mask<<<(unsigned)std::min<int64_t>(ceil_div(ntiles, 256), 1024), 256, 0, s>>>(m->tile_mask, ntiles, mw,
-                                                                                          m->d_mirror, K, m->tile_maskT);
-    g_launches++;
-    m->permT = m->perm;  // same row set, mirrored masks: same ordering
-  }
-  ck(cudaGetLastError());
-  dev_free(m->alloc, scratch, s);
-  if (e != cudaSuccess) return fail(MK_ERR_CUDA, std::string("mk_kmap_build: ") + cudaGetErrorString(e));
   *out_map = m;
   return MK_OK;
 }

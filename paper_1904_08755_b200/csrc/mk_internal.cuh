@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <atomic>
 #include <string>
 #include <vector>
@@ -55,6 +56,8 @@ extern std::atomic<int64_t> g_launches;
 // for D == 4).
 constexpr int32_t kEmptyWord = -1;
 
+// Multiply-xor combine of the four key words and a murmur3 32-bit finaliser (cheap: the
+// kernel-map builder hashes every (row, offset) query).
 __host__ __device__ __forceinline__ uint32_t hash_key(int4 k) {
   uint32_t h = (uint32_t)k.x * 0x9E3779B1u;
   h ^= (uint32_t)k.y * 0x85EBCA77u;
@@ -102,34 +105,81 @@ __host__ __device__ __forceinline__ bool pack_key(const int64_t* c, int D, int64
   return true;
 }
 
-// Linear probing from slot h onward; row or -1.
-__device__ __forceinline__ int32_t probe_from(const int4* __restrict__ tkeys, const int32_t* __restrict__ tvals,
-                                              uint32_t mask, int4 q, uint32_t h) {
+// ------------------------------------------------------------------ hash table
+// Open addressing over 64-byte buckets (half a 128-byte line): three 16-byte key slots
+// followed by one 16-byte word holding the three slots' row values:
+//   bucket b = { key[0], key[1], key[2], (row[0], row[1], row[2], unused) }
+// A key hashes to bucket hash & bmask and is stored in the first free slot of the
+// linear-probing sequence of slots 3b, 3b+1, ... (wrapping).  A lookup reads a whole
+// bucket — keys and rows — in one round trip (four lanes of a warp cooperatively, one
+// 16-byte load each, or one thread with four loads) and continues to the next bucket only
+// when all three slots are occupied by other keys.
+constexpr int kSlotsPerBucket = 3;
+
+__host__ __device__ __forceinline__ int4* slot_key(int4* buckets, uint32_t slot) {
+  return buckets + (size_t)(slot / 3u) * 4u + slot % 3u;
+}
+__host__ __device__ __forceinline__ int32_t* slot_val(int4* buckets, uint32_t slot) {
+  return (int32_t*)(buckets + (size_t)(slot / 3u) * 4u + 3u) + slot % 3u;
+}
+
+// One bucket in two 256-bit loads (sm_100 LDG.E.ENL2.256): keys 0-1, then key 2 + rows.
+struct Bucket {
+  int4 k0, k1, k2, v;
+};
+__device__ __forceinline__ Bucket load_bucket(const int4* B) {
+  Bucket b;
+  asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(b.k0.x), "=r"(b.k0.y), "=r"(b.k0.z), "=r"(b.k0.w), "=r"(b.k1.x), "=r"(b.k1.y), "=r"(b.k1.z),
+                 "=r"(b.k1.w)
+               : "l"(B));
+  asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(b.k2.x), "=r"(b.k2.y), "=r"(b.k2.z), "=r"(b.k2.w), "=r"(b.v.x), "=r"(b.v.y), "=r"(b.v.z),
+                 "=r"(b.v.w)
+               : "l"(B + 2));
+  return b;
+}
+
+// Continues the lookup of q after its home bucket (which was full of other keys).
+static __device__ __noinline__ int32_t probe_next(const int4* __restrict__ buckets, uint32_t bmask, int4 q) {
+  uint32_t b = ((hash_key(q) & bmask) + 1) & bmask;
   while (true) {
-    const int4 k = __ldg(tkeys + h);
-    if (key_eq(k, q)) return __ldg(tvals + h);
-    if (k.w == kEmptyWord) return -1;
-    h = (h + 1) & mask;
+    const int4* B = buckets + (size_t)b * 4u;
+    Bucket w;
+    w.k0 = __ldg(B);
+    w.k1 = __ldg(B + 1);
+    w.k2 = __ldg(B + 2);
+    w.v = __ldg(B + 3);
+    if (key_eq(w.k0, q)) return w.v.x;
+    if (key_eq(w.k1, q)) return w.v.y;
+    if (key_eq(w.k2, q)) return w.v.z;
+    if (w.k0.w == kEmptyWord || w.k1.w == kEmptyWord || w.k2.w == kEmptyWord) return -1;
+    b = (b + 1) & bmask;
   }
 }
 
-// Linear-probing lookup of key q; row or -1.  One 16-byte load per probed slot.
-__device__ __forceinline__ int32_t probe(const int4* __restrict__ tkeys, const int32_t* __restrict__ tvals,
-                                         uint32_t mask, int4 q) {
-  uint32_t h = hash_key(q) & mask;
+// Thread-level lookup of key q; row or -1.
+__device__ __forceinline__ int32_t probe(const int4* __restrict__ buckets, uint32_t bmask, int4 q) {
+  uint32_t b = hash_key(q) & bmask;
   while (true) {
-    const int4 k = __ldg(tkeys + h);
-    if (key_eq(k, q)) return __ldg(tvals + h);
-    if (k.w == kEmptyWord) return -1;
-    h = (h + 1) & mask;
+    const int4* B = buckets + (size_t)b * 4u;
+    Bucket w;
+    w.k0 = __ldg(B);
+    w.k1 = __ldg(B + 1);
+    w.k2 = __ldg(B + 2);
+    w.v = __ldg(B + 3);
+    if (key_eq(w.k0, q)) return w.v.x;
+    if (key_eq(w.k1, q)) return w.v.y;
+    if (key_eq(w.k2, q)) return w.v.z;
+    if (w.k0.w == kEmptyWord || w.k1.w == kEmptyWord || w.k2.w == kEmptyWord) return -1;
+    b = (b + 1) & bmask;
   }
 }
 
 // ------------------------------------------------------------------ handles
 struct Table {
-  int4* keys = nullptr;     // [cap]
-  int32_t* vals = nullptr;  // [cap] row of the key
-  uint32_t mask = 0;        // cap - 1 (cap is a power of two >= 2n)
+  int4* buckets = nullptr;  // [nb][4] (see "hash table" above)
+  uint32_t bmask = 0;       // nb - 1 (nb is a power of two; 3 nb >= 2n slots)
 };
 
 struct Alloc {
@@ -200,6 +250,23 @@ struct mk_kmap {
 };
 
 namespace mk {
+// Development aid: MK_HOST_TIMING=1 prints host-side timestamps of a call's stages (us).
+struct HostTimer {
+  const char* name;
+  bool on;
+  int n = 0;
+  const char* lab[16];
+  double t[16];
+  static double now();
+  explicit HostTimer(const char* nm);
+  void mark(const char* l) {
+    if (on && n < 16) {
+      lab[n] = l;
+      t[n++] = now();
+    }
+  }
+  ~HostTimer();
+};
 void* dev_alloc(const Alloc& a, size_t bytes, cudaStream_t s);
 void dev_free(const Alloc& a, void* p, cudaStream_t s);
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
