@@ -19,8 +19,11 @@
  *    device memory and release it (stream-ordered, on the stream they were created on)
  *    in *_destroy.  Feature/weight/gradient buffers are caller-owned; outputs are
  *    overwritten, never accumulated into.
- *  - Calls that must report a size (coords_*, kmap_build) synchronize their stream once.
- *    Every other call is asynchronous.
+ *  - Calls that must report a size (coords_quantize / create / stride) synchronize their
+ *    stream once.  mk_kmap_build is asynchronous: the pair count is read back lazily, the
+ *    first time mk_kmap_info is asked for n_pairs (or a call needs it: export, weight
+ *    gradient), by waiting for the build's completion event only.  Every other call is
+ *    asynchronous.
  *  - Every call returns mk_status.  On failure mk_last_error_message() (thread-local)
  *    describes it and mk_last_error_row() gives the first offending input row, or -1.
  *    No C++ exception crosses this boundary.  On failure no handle is returned and
@@ -157,6 +160,8 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
                         const mk_region* region, int32_t transposed, void* stream,
                         mk_kmap** out_map);
 
+/* K, |M|, N_in, N_out.  Any pointer may be NULL.  Requesting n_pairs waits (once per map)
+ * for the build to complete on the device (event wait, not a stream sync). */
 mk_status mk_kmap_info(const mk_kmap* m, int32_t* K, int64_t* n_pairs, int64_t* n_in,
                        int64_t* n_out);
 

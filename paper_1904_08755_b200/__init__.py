@@ -224,10 +224,19 @@ class KernelMap:
         self.device = device
         self.transposed = transposed
         self._keep = (cin, cout)  # a map never outlives the coordinate sets it indexes
-        K, npairs, nin, nout = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
-        _check(_L.mk_kmap_info(handle, ctypes.byref(K), ctypes.byref(npairs), ctypes.byref(nin), ctypes.byref(nout)),
-               "mk_kmap_info")
-        self.K, self.n_pairs, self.n_in, self.n_out = K.value, npairs.value, nin.value, nout.value
+        K, nin, nout = ctypes.c_int32(), ctypes.c_int64(), ctypes.c_int64()
+        _check(_L.mk_kmap_info(handle, ctypes.byref(K), None, ctypes.byref(nin), ctypes.byref(nout)), "mk_kmap_info")
+        self.K, self.n_in, self.n_out = K.value, nin.value, nout.value
+        self._n_pairs = None
+
+    @property
+    def n_pairs(self) -> int:
+        """|M|.  The build is asynchronous; the first access waits for it (event wait)."""
+        if self._n_pairs is None:
+            n = ctypes.c_int64()
+            _check(_L.mk_kmap_info(self._h, None, ctypes.byref(n), None, None), "mk_kmap_info")
+            self._n_pairs = n.value
+        return self._n_pairs
 
     def __del__(self):
         if getattr(self, "_h", None) and _L is not None:

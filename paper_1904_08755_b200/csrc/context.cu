@@ -134,11 +134,19 @@ mk_status mk_context_create(int device, mk_alloc_fn alloc, mk_free_fn free_fn, v
   c->alloc.alloc = alloc;
   c->alloc.free_fn = free_fn;
   c->alloc.user = user;
+  if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    MK_FAIL(MK_ERR_CUDA, "mk_context_create: stream creation failed");
+  }
   *out = c;
   return MK_OK;
 }
 
-void mk_context_destroy(mk_context* ctx) { delete ctx; }
+void mk_context_destroy(mk_context* ctx) {
+  if (!ctx) return;
+  if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  delete ctx;
+}
 
 const char* mk_last_error_message(void) { return mk::t_msg.c_str(); }
 int64_t mk_last_error_row(void) { return mk::t_row; }

@@ -51,7 +51,7 @@ mk_status forward_impl(mk_context* ctx, const mk_kmap* m, const void* d_fin, int
   if (st != MK_OK) return st;
   if (out_dt != MK_F32 && out_dt != MK_BF16) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv: unknown output dtype");
   if (m->n_out > 0 && !d_fout) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv: null output");
-  if (m->n_pairs > 0 && (!d_fin || !d_w)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv: null input or weights");
+  if (m->n_in > 0 && m->n_out > 0 && (!d_fin || !d_w)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv: null input or weights");
   if (m->n_out == 0) return MK_OK;
   const NbrView v = forward_view(m);
   if (in_dt == MK_F32)
@@ -64,9 +64,9 @@ mk_status backward_impl(mk_context* ctx, const mk_kmap* m, const void* d_gout, c
                         int32_t c_in, int32_t c_out, mk_dtype dt, void* d_gin, float* d_gw, cudaStream_t s) {
   mk_status st = check_common(ctx, m, c_in, c_out, dt);
   if (st != MK_OK) return st;
-  if (m->n_out > 0 && m->n_pairs > 0 && !d_gout) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv backward: null grad_out");
+  if (m->n_out > 0 && m->n_in > 0 && !d_gout) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv backward: null grad_out");
   if (d_gin && m->n_in > 0) {
-    if (m->n_pairs > 0 && !d_w) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv backward: null weights");
+    if (m->n_out > 0 && !d_w) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv backward: null weights");
     const NbrView v = dgrad_view(m);
     if (dt == MK_F32)
       st = launch_conv_f32(v, (const float*)d_gout, c_out, (const float*)d_w, c_in, c_out, d_gin, c_in, MK_F32,
@@ -76,8 +76,10 @@ mk_status backward_impl(mk_context* ctx, const mk_kmap* m, const void* d_gout, c
     if (st != MK_OK) return st;
   }
   if (d_gw) {
-    if (m->n_pairs > 0 && !d_fin) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv backward: null input features");
+    if (m->n_out > 0 && m->n_in > 0 && !d_fin) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv backward: null input features");
     if (dt == MK_F32) {
+      st = kmap_host(m);  // per-offset pair counts on the host (waits for the build only)
+      if (st != MK_OK) return st;
       // split-K plan: chunks of <= 4096 pairs per offset
       const int64_t P = 4096;
       std::vector<int4> chunks;

@@ -587,7 +587,7 @@ struct WgradParams {
 };
 
 constexpr int kPairsPerStage = 64;
-constexpr int kMaxSegs = 64;  // segments per CTA (<= 1 + K)
+constexpr int kMaxSegs = kWgradMaxSegs + 1;  // per-CTA plan capacity (kmap_wplan cuts ranges to fit)
 
 // Weight gradient: split-K over the pairs.  Step g = 64 pairs of one segment (k, range) of
 // this CTA, done by producer warp g % sa in its own stage slot (warp-per-stage, as in the
@@ -959,6 +959,8 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
 
 mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, int c_out, const void* x, int c_in,
                             float* dW, cudaStream_t s) {
+  const mk_status pst = kmap_wplan(m, s);  // split-K plan (built once per map, on first use)
+  if (pst != MK_OK) return pst;
   const int64_t te = (int64_t)c_out * c_in;
   WgradParams p;
   p.g = (const __nv_bfloat16*)g;
@@ -973,7 +975,6 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   p.pwb = c_in % 64 == 0 ? 64 : c_in % 32 == 0 ? 32 : 16;
   p.halves = c_out > 128 ? 2 : 1;
   if (c_out > 256) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: C_out above 256");
-  if (m->K + 1 > kMaxSegs) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: more than 63 kernel offsets");
   p.a_bytes = (uint32_t)(p.halves * 128) * kPairsPerStage * 2;  // M padded to 128 per half
   p.b_bytes = (uint32_t)c_in * kPairsPerStage * 2;
   p.slot_bytes = (p.a_bytes + p.b_bytes + 1023) & ~1023u;

@@ -388,6 +388,103 @@ __global__ void k_mirror_mask(const uint32_t* __restrict__ mask, int64_t ntiles,
 }
 
 }  // namespace
+
+namespace {
+// h_ptr / n_pairs from the device totals; caller holds m->mu.
+mk_status kmap_host_locked(mk_kmap* m) {
+  if (m->host_ready) return MK_OK;
+  cudaError_t e = cudaEventSynchronize(m->done);  // the build only, not the stream's later work
+  int64_t* h = (int64_t*)pinned_stage(sizeof(int64_t) * m->K);
+  if (!h) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "kmap: pinned staging failed");
+  if (e == cudaSuccess) e = cudaMemcpyAsync(h, m->d_totals, sizeof(int64_t) * m->K, cudaMemcpyDeviceToHost, m->aux);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(m->aux);
+  if (e != cudaSuccess) MK_FAIL(MK_ERR_CUDA, std::string("kmap: pair count read-back: ") + cudaGetErrorString(e));
+  m->h_ptr.assign(m->K + 1, 0);
+  for (int k = 0; k < m->K; ++k) m->h_ptr[k + 1] = m->h_ptr[k] + h[k];
+  m->n_pairs = m->h_ptr[m->K];
+  if (m->n_pairs > INT32_MAX) MK_FAIL(MK_ERR_UNSUPPORTED, "kmap: more than 2^31 pairs");
+  m->host_ready = true;
+  return MK_OK;
+}
+}  // namespace
+
+mk_status kmap_host(const mk_kmap* cm) {
+  mk_kmap* m = const_cast<mk_kmap*>(cm);
+  std::lock_guard<std::mutex> lk(*m->mu);
+  return kmap_host_locked(m);
+}
+
+// Weight-gradient split-K plan (tensor-core path): the concatenated pair list is cut into
+// per-CTA ranges of <= L pairs (L = 64 * ceil(|M| / #SM / 64)) and <= kWgradMaxSegs
+// (range, offset) segments; every segment has its own partial slot; slots are in offset
+// order.
+mk_status kmap_wplan(const mk_kmap* cm, cudaStream_t s) {
+  mk_kmap* m = const_cast<mk_kmap*>(cm);
+  std::lock_guard<std::mutex> lk(*m->mu);
+  mk_status st = kmap_host_locked(m);
+  if (st != MK_OK) return st;
+  if (m->wplan_ready) {
+    if (s != m->wplan_stream && cudaStreamWaitEvent(s, m->wplan_ev, 0) != cudaSuccess)
+      MK_FAIL(MK_ERR_CUDA, "kmap: stream wait failed");
+    return MK_OK;
+  }
+  const int K = m->K;
+  std::vector<int4> segs;
+  std::vector<int32_t> seg_begin, slot_begin(K + 1, 0);
+  const int64_t P = m->n_pairs;
+  const int64_t L = std::max<int64_t>(64, ceil_div(ceil_div(std::max<int64_t>(P, 1), m->num_sms), 64) * 64);
+  // Greedy cut of the concatenated pair list: a CTA takes up to L pairs and at most
+  // kWgradMaxSegs segments (the kernel's per-CTA plan size), cutting at offset boundaries.
+  int64_t cta_pairs = L;  // forces a new CTA at the first segment
+  int cta_segs = 0;
+  for (int k = 0; k < K; ++k) {
+    for (int64_t b = m->h_ptr[k]; b < m->h_ptr[k + 1];) {
+      if (cta_pairs >= L || cta_segs >= kWgradMaxSegs) {
+        seg_begin.push_back((int32_t)segs.size());
+        cta_pairs = 0;
+        cta_segs = 0;
+      }
+      const int64_t e2 = std::min(m->h_ptr[k + 1], b + (L - cta_pairs));
+      segs.push_back(make_int4(k, (int)b, (int)e2, (int)segs.size()));
+      cta_pairs += e2 - b;
+      ++cta_segs;
+      b = e2;
+    }
+  }
+  const int64_t ncta = (int64_t)seg_begin.size();
+  seg_begin.push_back((int32_t)segs.size());
+  for (int k = 0, i = 0; k <= K; ++k) {
+    while (i < (int)segs.size() && segs[i].x < k) ++i;
+    slot_begin[k] = i;
+  }
+  const size_t b_seg = sizeof(int4) * std::max<size_t>(1, segs.size());
+  const size_t b_sb = sizeof(int32_t) * seg_begin.size(), b_kb = sizeof(int32_t) * (K + 1);
+  const size_t total = b_seg + b_sb + b_kb;
+  char* d = (char*)dev_alloc(m->alloc, total, m->stream);
+  char* h = (char*)pinned_stage(total);
+  if (!d || !h) {
+    if (d) dev_free(m->alloc, d, m->stream);
+    MK_FAIL(MK_ERR_OUT_OF_MEMORY, "kmap: weight-gradient plan allocation failed");
+  }
+  m->owned.push_back(d);
+  if (!segs.empty()) std::memcpy(h, segs.data(), sizeof(int4) * segs.size());
+  std::memcpy(h + b_seg, seg_begin.data(), b_sb);
+  std::memcpy(h + b_seg + b_sb, slot_begin.data(), b_kb);
+  cudaError_t e = cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, s);
+  pinned_in_flight(s);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&m->wplan_ev, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(m->wplan_ev, s);
+  if (e != cudaSuccess) MK_FAIL(MK_ERR_CUDA, std::string("kmap: plan upload: ") + cudaGetErrorString(e));
+  m->wseg = (int4*)d;
+  m->wseg_begin = (int32_t*)(d + b_seg);
+  m->wslot_begin = (int32_t*)(d + b_seg + b_sb);
+  m->n_wcta = (int32_t)ncta;
+  m->n_wslots = (int64_t)segs.size();
+  m->wplan_stream = s;
+  m->wplan_ready = true;
+  return MK_OK;
+}
+
 }  // namespace mk
 
 using namespace mk;
@@ -412,6 +509,9 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   mk_kmap* m = new mk_kmap();
   m->alloc = ctx->alloc;
   m->stream = s;
+  m->aux = ctx->aux;
+  m->num_sms = ctx->num_sms;
+  m->mu = new std::mutex();
   m->K = K;
   m->D = D;
   m->transposed = transposed ? 1 : 0;
@@ -485,7 +585,8 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   if (!symmetric) m->nbrT = (int32_t*)alloc(sizeof(int32_t) * (int64_t)K * nT_pad);
   int32_t* nbr_rm = rm ? (int32_t*)salloc(sizeof(int32_t) * n_pad * kRM) : nullptr;
   int64_t* tile_off = (int64_t*)salloc(sizeof(int64_t) * K * ntiles);
-  int64_t* totals = (int64_t*)salloc(sizeof(int64_t) * K);
+  int64_t* totals = (int64_t*)alloc(sizeof(int64_t) * K);  // persistent: lazy host read-back
+  m->d_totals = totals;
   int32_t* tile_cnt = (int32_t*)salloc(sizeof(int32_t) * K * ntiles);
   uint32_t* rowmask = rm ? (uint32_t*)salloc(sizeof(uint32_t) * std::max<int64_t>(1, std::max(n_out, n_in))) : nullptr;
   if (!d_offs || !m->nbr || !m->tile_mask || !m->tile_maskT || !m->ptr || (!symmetric && !m->nbrT) ||
@@ -534,25 +635,22 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     ck(cudaMemsetAsync(m->ptr, 0, sizeof(int64_t) * (K + 1), s));
   }
   ck(cudaGetLastError());
-  // Host copy of the per-offset pair counts (pinned D2H, then the build's single stream sync;
-  // the copy is enqueued before the scratch holding `totals` is released).
-  int64_t* h_tot = nullptr;
-  auto copy_totals = [&]() -> bool {
-    h_tot = (int64_t*)pinned_stage(sizeof(int64_t) * K);
+  // Host copy of the per-offset pair counts.  K > 32 maps size their pair lists exactly and
+  // read the counts back here (one stream sync); K <= 32 maps defer it (mk::kmap_host).
+  auto read_totals_now = [&]() -> bool {
+    int64_t* h_tot = (int64_t*)pinned_stage(sizeof(int64_t) * K);
     if (!h_tot) return false;
     ck(cudaMemcpyAsync(h_tot, totals, sizeof(int64_t) * K, cudaMemcpyDeviceToHost, s));
-    return true;
-  };
-  auto finish_totals = [&]() {
     ck(cudaStreamSynchronize(s));
     m->h_ptr.assign(K + 1, 0);
     for (int k = 0; k < K; ++k) m->h_ptr[k + 1] = m->h_ptr[k] + (e == cudaSuccess ? h_tot[k] : 0);
     m->n_pairs = m->h_ptr[K];
+    m->host_ready = true;
+    return true;
   };
   int64_t pair_cap = (int64_t)K * n_out;
   if (!upper_bound) {
-    if (!copy_totals()) return oom();
-    finish_totals();
+    if (!read_totals_now()) return oom();
     if (e != cudaSuccess) {
       free_scratch();
       return fail(MK_ERR_CUDA, std::string("mk_kmap_build: ") + cudaGetErrorString(e));
@@ -618,50 +716,10 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   }
   if (symmetric) m->permT = m->perm;  // same row set, mirrored masks: same ordering
   ck(cudaGetLastError());
-  if (upper_bound && !copy_totals()) return oom();
-  free_scratch();  // stream-ordered: after every kernel and copy above
-  ht.mark("launched");
-  if (upper_bound) finish_totals();
-  ht.mark("synced");
+  free_scratch();  // stream-ordered: after every kernel above
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&m->done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaEventRecord(m->done, s);
   if (e != cudaSuccess) return fail(MK_ERR_CUDA, std::string("mk_kmap_build: ") + cudaGetErrorString(e));
-  if (m->n_pairs > INT32_MAX) return fail(MK_ERR_UNSUPPORTED, "mk_kmap_build: more than 2^31 pairs");
-  {  // weight-gradient split-K plan: one device block, one pinned H2D copy
-    std::vector<int4> segs;
-    std::vector<int32_t> seg_begin, slot_begin(K + 1, 0);
-    const int64_t P = m->n_pairs;
-    int64_t L = std::max<int64_t>(64, ceil_div(ceil_div(std::max<int64_t>(P, 1), ctx->num_sms), 64) * 64);
-    const int64_t ncta = P > 0 ? ceil_div(P, L) : 0;
-    for (int64_t c = 0; c < ncta; ++c) {
-      seg_begin.push_back((int32_t)segs.size());
-      const int64_t cb = c * L, ce = std::min(P, cb + L);
-      for (int k = 0; k < K; ++k) {
-        const int64_t b = std::max(cb, m->h_ptr[k]), e2 = std::min(ce, m->h_ptr[k + 1]);
-        if (b < e2) segs.push_back(make_int4(k, (int)b, (int)e2, (int)segs.size()));
-      }
-    }
-    seg_begin.push_back((int32_t)segs.size());
-    for (int k = 0, i = 0; k <= K; ++k) {
-      while (i < (int)segs.size() && segs[i].x < k) ++i;
-      slot_begin[k] = i;
-    }
-    m->n_wcta = (int32_t)ncta;
-    m->n_wslots = (int64_t)segs.size();
-    const size_t b_seg = sizeof(int4) * std::max<size_t>(1, segs.size());
-    const size_t b_sb = sizeof(int32_t) * seg_begin.size(), b_kb = sizeof(int32_t) * (K + 1);
-    const size_t total = b_seg + b_sb + b_kb;
-    char* d = (char*)alloc(total);
-    char* h = (char*)pinned_stage(total);
-    if (!d || !h) return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: allocation failed");
-    if (!segs.empty()) std::memcpy(h, segs.data(), sizeof(int4) * segs.size());
-    std::memcpy(h + b_seg, seg_begin.data(), b_sb);
-    std::memcpy(h + b_seg + b_sb, slot_begin.data(), b_kb);
-    e = cudaMemcpyAsync(d, h, total, cudaMemcpyHostToDevice, s);
-    pinned_in_flight(s);
-    if (e != cudaSuccess) return fail(MK_ERR_CUDA, std::string("mk_kmap_build: ") + cudaGetErrorString(e));
-    m->wseg = (int4*)d;
-    m->wseg_begin = (int32_t*)(d + b_seg);
-    m->wslot_begin = (int32_t*)(d + b_seg + b_sb);
-  }
   *out_map = m;
   return MK_OK;
 }
@@ -670,7 +728,11 @@ mk_status mk_kmap_info(const mk_kmap* m, int32_t* K, int64_t* n_pairs, int64_t* 
   clear_error();
   if (!m) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_kmap_info: null handle");
   if (K) *K = m->K;
-  if (n_pairs) *n_pairs = m->n_pairs;
+  if (n_pairs) {
+    const mk_status st = kmap_host(m);
+    if (st != MK_OK) return st;
+    *n_pairs = m->n_pairs;
+  }
   if (n_in) *n_in = m->n_in;
   if (n_out) *n_out = m->n_out;
   return MK_OK;
@@ -680,6 +742,8 @@ mk_status mk_kmap_export(const mk_kmap* m, int64_t* d_ptr, int32_t* d_in, int32_
   clear_error();
   if (!m) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_kmap_export: null handle");
   cudaStream_t s = (cudaStream_t)stream;
+  const mk_status st = kmap_host(m);
+  if (st != MK_OK) return st;
   if (d_ptr) MK_CUDA_TRY(cudaMemcpyAsync(d_ptr, m->ptr, sizeof(int64_t) * (m->K + 1), cudaMemcpyDeviceToDevice, s));
   if (m->n_pairs > 0) {
     if (d_in) MK_CUDA_TRY(cudaMemcpyAsync(d_in, m->in_idx, sizeof(int32_t) * m->n_pairs, cudaMemcpyDeviceToDevice, s));
@@ -691,6 +755,9 @@ mk_status mk_kmap_export(const mk_kmap* m, int64_t* d_ptr, int32_t* d_in, int32_
 void mk_kmap_destroy(mk_kmap* m) {
   if (!m) return;
   for (void* p : m->owned) dev_free(m->alloc, p, m->stream);
+  if (m->done) cudaEventDestroy(m->done);
+  if (m->wplan_ev) cudaEventDestroy(m->wplan_ev);
+  delete m->mu;
   delete m;
 }
 

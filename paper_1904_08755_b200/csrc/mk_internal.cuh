@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -194,6 +195,7 @@ struct mk_context {
   int device = 0;
   int num_sms = 148;
   mk::Alloc alloc;
+  cudaStream_t aux = nullptr;  // private non-blocking stream for small lazy read-backs
 };
 
 struct mk_coords {
@@ -210,6 +212,17 @@ struct mk_coords {
 struct mk_kmap {
   mk::Alloc alloc;
   cudaStream_t stream = nullptr;
+  cudaStream_t aux = nullptr;       // the context's private stream (lazy read-backs)
+  int num_sms = 148;
+  // Host-side counts are materialised lazily (mk::kmap_host / mk::kmap_wplan), guarded by
+  // `mu`: the handle stays logically immutable (the values are fixed by the build).
+  std::mutex* mu = nullptr;
+  cudaEvent_t done = nullptr;       // recorded after the build's last kernel
+  int64_t* d_totals = nullptr;      // [K] pairs per offset (device)
+  bool host_ready = false;
+  bool wplan_ready = false;
+  cudaEvent_t wplan_ev = nullptr;   // recorded after the split-K plan upload
+  cudaStream_t wplan_stream = nullptr;
   int32_t K = 0;
   int32_t D = 0;
   int32_t transposed = 0;
@@ -280,6 +293,11 @@ void pinned_in_flight(cudaStream_t s);
 // Table-building pipeline shared by quantize / create / stride (coords.cu).
 // Region enumeration (region.cu):
 mk_status region_enumerate(const mk_region* r, std::vector<int32_t>* offsets, int32_t* K);
+// Lazy host state of a kernel map (kmap.cu): h_ptr / n_pairs, and the bf16 weight-gradient
+// split-K plan (uploaded on `s`; other streams wait for it).
+mk_status kmap_host(const mk_kmap* m);
+mk_status kmap_wplan(const mk_kmap* m, cudaStream_t s);
+constexpr int kWgradMaxSegs = 63;  // segments per CTA of the bf16 weight-gradient kernel
 // Stable radix sort of keys (low `bits` bits) -> permutation (sort.cu).  Clobbers keys.
 mk_status radix_sort_perm(const Alloc& a, uint32_t* keys, int64_t n, int bits, int32_t* perm, cudaStream_t s);
 }  // namespace mk

@@ -133,3 +133,20 @@ def test_room_full_size_sampled(mk, orc, dt, tol):
     y64 = orc.conv_forward_rows(km, X, W, rows)
     s64 = orc.conv_forward_rows(km, np.abs(X), np.abs(W), rows)
     assert_close(y[rows], y64, s64, tol, f"room {dt}")
+
+
+@pytest.mark.parametrize("dt,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
+def test_tesseract_4d_conv(mk, orc, dt, tol):
+    # K = 3^4 = 81 offsets (the 4D hypercube of P:253): exercises the K > 32 kernel-map path
+    # (k-major table, identity row order, exact pair lists) and the conv kernels' multi-word
+    # offset masks.
+    c, oc = _sparse(mk, orc, 81, 6000, 7, D=4)
+    m = mk.kmap_build(c, c, mk.Region(mk.HYPERCUBE, 4, 3))
+    assert m.K == 81
+    km = csr_np(m)
+    optr, oin, oout = orc.kmap(oc, oc, mk.region_offsets(mk.Region(mk.HYPERCUBE, 4, 3)))
+    assert np.array_equal(km[0], optr) and np.array_equal(km[1], oin) and np.array_equal(km[2], oout)
+    X = synthetic.features(12, c.n, 16)
+    W = synthetic.weights(13, 81, 32, 16)
+    G = synthetic.features(14, c.n, 32)
+    _check_all(mk, orc, m, km, X, W, G, dt, tol, what="tesseract")
