@@ -3,16 +3,16 @@
 //
 // One sort-free pipeline serves all three constructors (a "key source" supplies row p's
 // packed key and validation):
-//   k_insert  one thread per input row: build the key, claim a slot of an open-addressing
-//             table (linear probing, power-of-two capacity >= 2n) by 32-bit atomicCAS of
-//             the row index; equal keys resolve to the smallest row via atomicMin.  Keys are
-//             compared by recomputing the occupant's key from the immutable input, so no
-//             128-bit atomics are needed and no thread ever reads a half-written key.
-//   k_rank    winners (claim[slot] == p) are ranked by a single-pass decoupled look-back
+//   k_init    bucket table to the empty sentinel, first-point words to INT32_MAX.
+//   k_insert  one thread per input row: build the key and claim-or-find its slot in the
+//             bucketed open-addressing table (mk_internal.cuh) with one 128-bit atomicCAS of
+//             the key itself (linear probing over slots); atomicMin records the smallest
+//             input row of each key.
+//   k_rank    winners (first[slot] == p) are ranked by a single-pass decoupled look-back
 //             scan in input order => rows in first-occurrence order (R8), first point of a
-//             voxel is its representative (R9).  Writes the row keys and finalises the
-//             table slot (key, row).
-//   k_p2r     optional inverse map point_to_row[p] = table value of its slot.
+//             voxel is its representative (R9).  Writes the row keys and the slot's row;
+//             then (optional) point_to_row[p] = row of p's slot (waits for the key's first
+//             point, which is in the same or an earlier block).
 // The host then reads the error word and the row count (the one sync of the call).
 #include <cuda/atomic>
 
@@ -110,33 +110,29 @@ struct StrideSrc {  // u' = floor_div(u, s_out) * s_out per spatial axis (R7, R1
 
 // ---------------------------------------------------------------- kernels
 template <class Src>
-__global__ void __launch_bounds__(kBlock) k_insert(Src src, int64_t n, int32_t* __restrict__ claim,
-                                                   uint32_t bmask, int32_t* __restrict__ slot_of,
-                                                   unsigned long long* err) {
+__global__ void __launch_bounds__(kBlock) k_insert(Src src, int64_t n, int4* __restrict__ buckets,
+                                                   int32_t* __restrict__ first, uint32_t bmask,
+                                                   int32_t* __restrict__ slot_of, unsigned long long* err) {
+  // Claim-or-find in one 128-bit atomicCAS of the key itself (sm_90+): the slot is ours or
+  // already holds the key -> record the smallest point index of the key (atomicMin).
+  const unsigned __int128 kEmpty = ~(unsigned __int128)0;
+  const uint32_t nslots = (bmask + 1u) * kSlotsPerBucket;
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
     int4 k;
     const uint32_t code = src.key(p, &k);
     if (code != E_NONE) {
       report(err, p, code);
-      slot_of[p] = -1;  // no slot: k_rank / k_p2r skip the row (the call fails anyway)
+      slot_of[p] = -1;  // no slot: k_rank skips the row (the call fails anyway)
       continue;
     }
-    const uint32_t nslots = (bmask + 1u) * kSlotsPerBucket;
+    unsigned __int128 kv;
+    memcpy(&kv, &k, sizeof(kv));
     uint32_t h = (hash_key(k) & bmask) * kSlotsPerBucket;  // first slot of the key's bucket
     while (true) {
-      int32_t cur = __ldcg(claim + h);
-      if (cur == -1) {
-        cur = atomicCAS(claim + h, -1, (int32_t)p);
-        if (cur == -1) {
-          slot_of[p] = (int32_t)h;
-          break;
-        }
-      }
-      int4 occ;
-      src.key(cur, &occ);  // occupant keys are recomputed from the immutable input
-      if (key_eq(occ, k)) {
-        if (cur > p) atomicMin(claim + h, (int32_t)p);
+      const unsigned __int128 old = atomicCAS((unsigned __int128*)slot_key(buckets, h), kEmpty, kv);
+      if (old == kEmpty || old == kv) {
+        atomicMin(first + h, (int32_t)p);
         slot_of[p] = (int32_t)h;
         break;
       }
@@ -183,10 +179,11 @@ __device__ int64_t lookback(unsigned long long* status, int64_t tile, int64_t ag
 }
 
 template <class Src>
-__global__ void __launch_bounds__(kBlock) k_rank(Src src, int64_t n, const int32_t* __restrict__ claim,
+__global__ void __launch_bounds__(kBlock) k_rank(Src src, int64_t n, const int32_t* __restrict__ first,
                                                  const int32_t* __restrict__ slot_of, int4* __restrict__ buckets,
                                                  int4* __restrict__ out_keys,
                                                  int32_t* __restrict__ first_point,
+                                                 int32_t* __restrict__ p2r,
                                                  unsigned long long* status, unsigned int* ticket,
                                                  int64_t* count) {
   __shared__ int64_t s_tile;
@@ -205,7 +202,7 @@ __global__ void __launch_bounds__(kBlock) k_rank(Src src, int64_t n, const int32
     win[i] = false;
     if (p < n) {
       slot[i] = slot_of[p];
-      win[i] = slot[i] >= 0 && claim[slot[i]] == (int32_t)p;
+      win[i] = slot[i] >= 0 && first[slot[i]] == (int32_t)p;
     }
     cnt += win[i];
   }
@@ -241,37 +238,45 @@ __global__ void __launch_bounds__(kBlock) k_rank(Src src, int64_t n, const int32
     int4 k;
     src.key(p, &k);
     out_keys[row] = k;
-    *slot_key(buckets, (uint32_t)slot[i]) = k;
     *slot_val(buckets, (uint32_t)slot[i]) = (int32_t)row;
     if (first_point) first_point[row] = (int32_t)p;
     ++row;
   }
+  if (!p2r) return;
+  // Inverse map point -> row: the row of p's slot is written by the key's first point,
+  // which is in this block or an earlier one (block order by ticket: it is running or
+  // done), so the wait below terminates.
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kItems; ++i) {
+    const int64_t p = base + i;
+    if (p >= n) continue;
+    int32_t r = -1;
+    if (slot[i] >= 0) {
+      const volatile int32_t* v = slot_val(buckets, (uint32_t)slot[i]);
+      while ((r = *v) < 0) {
+      }
+    }
+    p2r[p] = r;
+  }
 }
 
-// Table init in one launch: bucket words and claims to the empty sentinel (all ones),
-// look-back status words / ticket / count to 0, the error word to all ones.
-__global__ void k_init(int4* __restrict__ buckets, int32_t* __restrict__ claim, uint32_t nb,
+// Table init in one launch: bucket words to the empty sentinel (all ones: empty keys, rows
+// -1), first-point words to INT32_MAX, look-back status words / ticket / count to 0, the
+// error word to all ones.
+__global__ void k_init(int4* __restrict__ buckets, int32_t* __restrict__ first, uint32_t nb,
                        unsigned long long* __restrict__ small, int64_t n_small, unsigned long long* err) {
   const int4 e = make_int4(-1, -1, -1, -1);
   const int64_t words = (int64_t)nb * 4, slots = (int64_t)nb * kSlotsPerBucket;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x) {
     buckets[i] = e;
-    if (i < slots) claim[i] = -1;
+    if (i < slots) first[i] = INT32_MAX;
   }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_small; i += (int64_t)gridDim.x * blockDim.x)
     small[i] = 0ull;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     err[0] = ~0ull;  // no error
     err[1] = 0ull;   // row count
-  }
-}
-
-__global__ void k_p2r(int64_t n, const int32_t* __restrict__ slot_of, int4* __restrict__ buckets,
-                      int32_t* __restrict__ p2r) {
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x)
-  {
-    const int32_t sl = slot_of[p];
-    p2r[p] = sl >= 0 ? *slot_val(buckets, (uint32_t)sl) : -1;
   }
 }
 
@@ -341,7 +346,7 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
   c->table.bmask = nb - 1;
   c->keys = (int4*)(pbase + o_rk);
 
-  // scratch: claims, slot per row, look-back status, ticket, error word, count
+  // scratch: first point per slot, slot per row, look-back status, ticket, error word, count
   Carver sc;
   const size_t o_cl = sc.take<int32_t>(nslots), o_sl = sc.take<int32_t>(std::max<int64_t>(n, 1)),
                o_st = sc.take<unsigned long long>(ntiles), o_ti = sc.take<unsigned int>(1),
@@ -357,7 +362,7 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
     set_error(MK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
     return MK_ERR_CUDA;
   };
-  int32_t* claim = (int32_t*)(sbase + o_cl);
+  int32_t* first = (int32_t*)(sbase + o_cl);
   int32_t* slot_of = (int32_t*)(sbase + o_sl);
   unsigned long long* status = (unsigned long long*)(sbase + o_st);
   unsigned int* ticket = (unsigned int*)(sbase + o_ti);
@@ -370,19 +375,16 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
     unsigned long long* small = (unsigned long long*)(sbase + o_st);
     const int64_t n_small = (int64_t)((o_er - o_st) / 8);
     k_init<<<grid_for(std::max<int64_t>((int64_t)nb * 4, n_small), 256, ctx->num_sms), 256, 0, s>>>(
-        c->table.buckets, claim, nb, small, n_small, err);
+        c->table.buckets, first, nb, small, n_small, err);
     g_launches++;
   }
   if (n > 0) {
-    k_insert<Src><<<grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s>>>(src, n, claim, nb - 1, slot_of, err);
+    k_insert<Src><<<grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s>>>(src, n, c->table.buckets, first, nb - 1,
+                                                                       slot_of, err);
     g_launches++;
-    k_rank<Src><<<(int)ntiles, kBlock, 0, s>>>(src, n, claim, slot_of, c->table.buckets, c->keys,
-                                                 d_first, status, ticket, count);
+    k_rank<Src><<<(int)ntiles, kBlock, 0, s>>>(src, n, first, slot_of, c->table.buckets, c->keys,
+                                                 d_first, d_p2r, status, ticket, count);
     g_launches++;
-    if (d_p2r) {
-      k_p2r<<<grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s>>>(n, slot_of, c->table.buckets, d_p2r);
-      g_launches++;
-    }
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "launch");
   }
   struct Result {
