@@ -581,6 +581,7 @@ struct WgradParams {
   const int32_t* seg_begin;  // [n_cta + 1]
   float* part;               // [n_slots][c_out][c_in]
   int c_out, c_in, halves;
+  int mrows;                 // UMMA M: 64 when C_out <= 64 (no zero panel), else 128 per half
   int sa, ga;                // stage slots (== producer warps), slots per commit group
   int pwa, pwb;              // panel widths (channels) of A (G) and B (X)
   uint32_t a_bytes, b_bytes, slot_bytes, tmem_cols;
@@ -756,7 +757,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
   } else if (warp == kMmaWarp) {
     {  // whole warp, warp-uniform values, lane 0 issues (see the forward kernel)
       const bool leader = lane == 0;
-      const uint32_t idesc = idesc_bf16(kTileM, p.c_in, 1, 1);
+      const uint32_t idesc = idesc_bf16((uint32_t)p.mrows, p.c_in, 1, 1);
       const uint64_t ahi = smem_desc(0, panel_a, 8 * rba, layout_code(rba));
       const uint64_t bhi = smem_desc(0, panel_b, 8 * rbb, layout_code(rbb));
       const uint32_t s0 = __shfl_sync(0xffffffffu, smem_u32(smem) >> 4, 0), sstep = p.slot_bytes >> 4,
@@ -802,7 +803,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
       ACCT_WAIT(0, tfull, i & 1);
       tc_fence_after();
       for (int h = 0; h < p.halves; ++h) {
-        const int co = h * 128 + q * 32 + lane;
+        // M = 128: row m in TMEM lane m.  M = 64: row m in lane (m % 16) + 32 * (m / 16)
+        // (half sub-partitions), so lanes 16..31 of each quarter hold no row.
+        const int co = p.mrows == 64 ? (lane < 16 ? q * 16 + lane : p.c_out) : h * 128 + q * 32 + lane;
         float* dst = p.part + ((int64_t)sg.w * p.c_out + co) * p.c_in;
         const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + h * (uint32_t)p.c_in;
         for (int col0 = 0; col0 < p.c_in; col0 += 16) {
@@ -974,8 +977,9 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   p.pwa = c_out % 64 == 0 ? 64 : c_out % 32 == 0 ? 32 : 16;
   p.pwb = c_in % 64 == 0 ? 64 : c_in % 32 == 0 ? 32 : 16;
   p.halves = c_out > 128 ? 2 : 1;
+  p.mrows = c_out <= 64 ? 64 : 128;
   if (c_out > 256) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: C_out above 256");
-  p.a_bytes = (uint32_t)(p.halves * 128) * kPairsPerStage * 2;  // M padded to 128 per half
+  p.a_bytes = (uint32_t)(p.halves * p.mrows) * kPairsPerStage * 2;  // M padded to 64 / 128 per half
   p.b_bytes = (uint32_t)c_in * kPairsPerStage * 2;
   p.slot_bytes = (p.a_bytes + p.b_bytes + 1023) & ~1023u;
   const int reserve = 1024 + 1024 + kProdWarps * 4 * kPairsPerStage * 4 + (kMaxSegs + 2) * 4;
