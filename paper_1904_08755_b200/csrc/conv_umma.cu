@@ -210,7 +210,8 @@ struct FwdParams {
   int64_t n_rows, ntiles;
   int c_x, c_y, nch, out_f32;
   int dbg;  // development switch (env MK_DEBUG_CONV): bit 0 = no MMAs, bit 1 = no gathers; 0 in production
-  int sa;  // A stages == producer warps (warp w owns stage slot w)
+  int sa;  // A stage slots
+  int np;  // producer warps (np divides sa)
   int ga;  // stage slots released together by one tcgen05.commit (sa % ga == 0)
   int sw;  // W chunk slots (a ring: W_k chunks are prefetched several offsets ahead)
   int tb;  // tiles per CTA (one TMEM accumulator each: tb * c_y <= 512 columns)
@@ -297,8 +298,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
   uint8_t* smem = align1024(smem_raw);
   uint8_t* a_base = smem;
   uint8_t* w_base = a_base + (size_t)p.sa * p.a_bytes;
-  int32_t* nbr_s = (int32_t*)(w_base + (size_t)p.sw * p.b_bytes);  // [kFwdProd][2][128] index buffers
-  Plan* pl = (Plan*)(nbr_s + kFwdProd * 2 * kTileM);
+  int32_t* nbr_s = (int32_t*)(w_base + (size_t)p.sw * p.b_bytes);  // [kFwdProd][3][128] index buffers
+  Plan* pl = (Plan*)(nbr_s + kFwdProd * 3 * kTileM);
   uint64_t* a_full = (uint64_t*)(((uintptr_t)(pl + 1) + 15) & ~(uintptr_t)15);
   uint64_t* cb = a_full + p.sa;  // [kNCB] commit ring (stage slots and W slots are released by it)
   uint64_t* w_full = cb + kNCB;
@@ -309,7 +310,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
 
   if (warp == 0) build_plan(p, pl);
   if (threadIdx.x == 32) {
-    for (int s = 0; s < p.sa; ++s) mbar_init(a_full + s, 1);
+    for (int s = 0; s < p.sa; ++s) mbar_init(a_full + s, 32);  // one cp.async arrival per lane
     for (int j = 0; j < kNCB; ++j) mbar_init(cb + j, 1);
     for (int s = 0; s < p.sw; ++s) mbar_init(w_full + s, 1);
     mbar_init(tfull, 1);
@@ -332,15 +333,18 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
   }
 #endif
 
-  if (warp < p.sa) {
+  if (warp < p.np) {
     // ------------------------------------------------------------ gather producers
-    // Step g belongs to warp g % sa and uses its stage slot: 128 rows x CH channels; lane
-    // group q4 = lane/8 owns rows [32 q4, 32 q4 + 32), 8 lanes per 128-byte row (4 full lines
-    // per instruction); absent neighbours are zero-filled in smem.  The next step's 128
-    // neighbour indices are prefetched into a private double buffer by one 16-byte cp.async
-    // per lane, in the same cp.async group.  Then: wait for the group, publish to the async
-    // proxy, one arrival on the slot's full barrier.
-    int32_t* ibuf = nbr_s + warp * 2 * kTileM;
+    // Step g (128 rows x CH channels of one (unit, tile, chunk)) belongs to warp g % np and
+    // uses stage slot g % sa (np divides sa; by default np = sa).  Lane group
+    // q4 = lane/8 owns rows [32 q4, 32 q4 + 32), 8 lanes per 128-byte row (4 full lines per
+    // instruction); absent neighbours are zero-filled by cp.async with a 0-byte source.
+    // Completion is announced by the copy engine itself: every lane's
+    // cp.async.mbarrier.arrive.noinc fires when its copies have landed (the slot's full
+    // barrier expects 32 arrivals), so the warp never waits for its own gathers.  The
+    // step's 128 neighbour indices are prefetched two steps ahead (ring of 3 buffers, in
+    // the cp.async group of the step two before); wait_group 1 keeps the ring safe.
+    int32_t* ibuf = nbr_s + warp * 3 * kTileM;
     int u = 0;
     auto locate = [&](int g, int* k, int64_t* tile, int* c) {
       while (pl->g0[u + 1] <= g) ++u;
@@ -352,34 +356,35 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
       *tile = tile0 + (__ffs(tw) - 1);
       *k = pl->k[u];
     };
-    int g = warp;
-    int k, c, kn = 0, cn = 0;
-    int64_t tile, tilen = 0;
-    if (g < n_steps) {
+    auto fetch_idx = [&](int g, int buf) {
+      int k, c;
+      int64_t tile;
       locate(g, &k, &tile, &c);
-      cp_async16(smem_u32(ibuf) + lane * 16, p.nb.tab + (int64_t)p.nb.kk(k) * p.nb.n + tile * kTileM + lane * 4, 16u);
-      cp_async_commit();
-      cp_async_wait_n(0);
-      __syncwarp();
-    }
-    uint32_t my = 0, ib = 0;
+      cp_async16(smem_u32(ibuf + buf * kTileM) + lane * 16,
+                 p.nb.tab + (int64_t)p.nb.kk(k) * p.nb.n + tile * kTileM + lane * 4, 16u);
+      return c;
+    };
+    const int np = p.np;
     const int q4 = lane >> 3, jj = lane & (J - 1);
-    for (; g < n_steps; g += p.sa) {
-      const bool have_n = g + p.sa < n_steps;
-      bool same = false;
-      if (have_n) {
-        locate(g + p.sa, &kn, &tilen, &cn);
-        same = kn == k && tilen == tile;  // further chunks of the same rows: indices reused
-        if (!same)
-          cp_async16(smem_u32(ibuf + (ib ^ 1) * kTileM) + lane * 16,
-                     p.nb.tab + (int64_t)p.nb.kk(kn) * p.nb.n + tilen * kTileM + lane * 4, 16u);
-      }
+    // indices of the warp's first two steps
+    int cq[3] = {0, 0, 0};  // channel chunk of the step whose indices sit in buffer i
+    if (warp < n_steps) cq[0] = fetch_idx(warp, 0);
+    if (warp + np < n_steps) cq[1] = fetch_idx(warp + np, 1);
+    cp_async_commit();
+    cp_async_wait_n(0);
+    __syncwarp();
+    int jl = 0;  // warp-local step index
+    for (int g = warp; g < n_steps; g += np, ++jl) {
+      const int b = jl % 3;
+      const int c = cq[b];
+      if (g + 2 * np < n_steps) cq[(jl + 2) % 3] = fetch_idx(g + 2 * np, (jl + 2) % 3);
+      const int slot = g % p.sa;
       if (g >= p.sa) {  // slot reuse: all MMAs of step g - sa done
         const int j = (g - p.sa) / p.ga;
         ACCT_WAIT(0, cb + j % kNCB, (uint32_t)(j / kNCB) & 1u);
       }
-      const uint32_t a_s = smem_u32(a_base + (size_t)warp * p.a_bytes);
-      const int32_t* ix = ibuf + ib * kTileM;
+      const uint32_t a_s = smem_u32(a_base + (size_t)slot * p.a_bytes);
+      const int32_t* ix = ibuf + b * kTileM;
       const __nv_bfloat16* xc = p.x + c * CH;
       if (p.dbg & 2) {
       } else if (J == 8) {
@@ -390,30 +395,23 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
             const int r = q4 * 32 + i + e;
-            if (av[e] >= 0) cp_async16(a_s + swz(r, jj, RB), xc + (int64_t)av[e] * p.c_x + jj * 8, 16u);
-            else st_shared_zero16(a_s + swz(r, jj, RB));
+            cp_async16(a_s + swz(r, jj, RB), xc + (int64_t)max(av[e], 0) * p.c_x + jj * 8, av[e] >= 0 ? 16u : 0u);
           }
         }
       } else {
 #pragma unroll 4
-        for (int slot = lane; slot < 128 * J; slot += 32) {
-          const int r = slot / J, j2 = slot % J;
+        for (int sl = lane; sl < 128 * J; sl += 32) {
+          const int r = sl / J, j2 = sl % J;
           const int32_t av = ix[r];
-          if (av >= 0) cp_async16(a_s + swz(r, j2, RB), xc + (int64_t)av * p.c_x + j2 * 8, 16u);
-          else st_shared_zero16(a_s + swz(r, j2, RB));
+          cp_async16(a_s + swz(r, j2, RB), xc + (int64_t)max(av, 0) * p.c_x + j2 * 8, av >= 0 ? 16u : 0u);
         }
       }
+      cp_async_arrive_noinc(a_full + slot);
       cp_async_commit();
-      cp_async_wait_n(0);
-      fence_proxy_async_smem();
+      cp_async_wait_n(1);  // group of step g - np done: the index buffer of step g + np is complete
       __syncwarp();
-      if (lane == 0) mbar_arrive(a_full + warp);
-      ++my;
-      if (have_n && !same) ib ^= 1;
-      k = kn;
-      tile = tilen;
-      c = cn;
     }
+    cp_async_wait_n(0);
   } else if (warp == kFwdStage) {
     // ------------------------------------------------------------ W stager (one thread)
     // Bulk copies (TMA engine) of the W_k chunks of every unit into a ring of sw slots.  A
@@ -475,6 +473,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
           uint32_t x = ws;
           for (int c = 0; c < p.nch; ++c) {
             ACCT_WAIT(2, a_full + s, sph);
+            fence_proxy_async_smem();  // the cp.async (generic proxy) rows -> tcgen05 (async proxy)
             tc_fence_after();
             const uint32_t alo = a0 + s * astep, blo = w0 + x * wstep;
             if (leader && !(p.dbg & 1)) {
@@ -922,12 +921,20 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   // index buffers and the plan (B200 gathers ~9 TB/s at 8 warps/SM, ubench_gather.cu).
   p.tb = std::max(1, std::min(2, 256 / c_y));
   p.tmem_cols = pow2_cols((uint32_t)(p.tb * c_y));
-  const int base = 1024 + 512 + kFwdProd * 2 * kTileM * 4 + (int)sizeof(Plan);
+  const int base = 1024 + 512 + kFwdProd * 3 * kTileM * 4 + (int)sizeof(Plan);
   p.sw = nch * 2;
   if (base + p.sw * (int)p.b_bytes + kFwdProd * (int)p.a_bytes <= kMaxSmem / 2 - 1024 - 2 * nch * (int)p.b_bytes)
     p.sw = nch * 4;
   const int fixed = base + p.sw * (int)p.b_bytes;
   p.sa = std::min(kFwdProd, (kMaxSmem - fixed) / (int)p.a_bytes);
+  p.sa -= p.sa % 2;
+  static const int env_np = [] {
+    const char* e = std::getenv("MK_FWD_NP");
+    return e ? std::atoi(e) : 0;
+  }();
+  // one producer warp per slot measured best (fwd 68.6 us vs 73.8 with two slots per warp,
+  // configs[1]): more warps issue the gathers faster than fewer warps with deeper queues
+  p.np = env_np > 0 ? std::min(env_np, p.sa) : p.sa;
   p.ga = p.sa % 2 == 0 ? 2 : 1;  // the W ring must hold >= ga units: sw / nch >= 2 >= ga
   if (p.sa < 2 || p.tmem_cols > 512)
     MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: channel counts too large for the smem pipeline");
