@@ -208,27 +208,60 @@ def run_mk(args, ws, rank, local):
     h2d = pts_p.numel() * 4 + (X_p.numel() + W_p.numel() + G_p.numel()) * 2
     d2h = (y_p.numel() + gi_p.numel()) * 2 + gw_p.numel() * 4
 
-    def e2e_step():
-        p = pts_p.to(dev, non_blocking=True)
-        x, w, g = (t.to(dev, non_blocking=True) for t in (X_p, W_p, G_p))
+    # Copies run on their own streams so they overlap the compute, as a user of the API
+    # would do: H2D of the points first (quantize needs them), then features and weights
+    # (fwd), then the output gradient (dgrad) while the coordinates and the map are built;
+    # each result goes back D2H as soon as its kernel finished (y during dgrad, grad_in
+    # during wgrad).  The step is PCIe bound: 84 MB cross the link per step.
+    h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def e2e_step(start):
+        h2d_s.wait_event(start)
+        with torch.cuda.stream(h2d_s):
+            p = pts_p.to(dev, non_blocking=True)
+            ev_p = torch.cuda.Event()
+            ev_p.record(h2d_s)
+            x, w = (t.to(dev, non_blocking=True) for t in (X_p, W_p))
+            ev_x = torch.cuda.Event()
+            ev_x.record(h2d_s)
+            g = G_p.to(dev, non_blocking=True)  # needed from dgrad on
+            ev_g = torch.cuda.Event()
+            ev_g.record(h2d_s)
+        for t in (p, x, w, g):
+            t.record_stream(stream)
+        stream.wait_event(ev_p)
         c, _, _ = mk.coords_quantize(p, synthetic.ROOM_VOXEL)
         m = mk.kmap_build(c, c, region)
+        stream.wait_event(ev_x)
+        def to_host(dev_t, host_t):  # D2H on its own stream as soon as dev_t is ready
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            d2h_s.wait_event(ev)
+            with torch.cuda.stream(d2h_s):
+                host_t.copy_(dev_t, non_blocking=True)
+            dev_t.record_stream(d2h_s)
+
         y = mk.conv_forward(m, x, w)
-        gin, gw = mk.conv_backward(m, g, x, w)
+        to_host(y, y_p)  # overlaps dgrad
+        stream.wait_event(ev_g)
+        gin, _ = mk.conv_backward(m, g, x, w, need_gin=True, need_gw=False)
+        to_host(gin, gi_p)  # overlaps wgrad
+        _, gw = mk.conv_backward(m, g, x, w, need_gin=False, need_gw=True)
         if ws > 1:
             allreduce_grad(gw)
-        y_p.copy_(y, non_blocking=True)
-        gi_p.copy_(gin, non_blocking=True)
-        gw_p.copy_(gw, non_blocking=True)
+        to_host(gw, gw_p)
+        stream.wait_stream(d2h_s)
 
     for _ in range(2):
-        e2e_step()
+        st0 = torch.cuda.Event()
+        st0.record(stream)
+        e2e_step(st0)
     torch.cuda.synchronize()
     e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     for i in range(args.steps):
         flush.zero_()
         e_ev[i][0].record(stream)
-        e2e_step()
+        e2e_step(e_ev[i][0])
         e_ev[i][1].record(stream)
     torch.cuda.synchronize()
     e2e_ms = float(sum(a.elapsed_time(b) for a, b in e_ev))

@@ -131,6 +131,16 @@ mk_status mk_coords_info(const mk_coords* c, int64_t* n, int32_t* D, int32_t* h_
 /* Copies the rows to d_out (device int32 [n][D+1]). */
 mk_status mk_coords_export(const mk_coords* c, int32_t* d_out, void* stream);
 
+/* Label reduction of Alg. 1: d_row_labels[r] = the label shared by
+ * every point of voxel r, or ignore_label when its points carry two or more distinct
+ * labels (the reduction f of P:181; R10: ignore_label is the caller's IGNORE_LABEL).
+ * d_point_to_row [n_points] and d_first_point [n_rows] are the outputs of
+ * mk_coords_quantize; d_labels device int32 [n_points]; d_row_labels device int32 [n_rows]
+ * (written).  Deterministic (no order-dependent step).  Asynchronous. */
+mk_status mk_coords_labels(const int32_t* d_point_to_row, const int32_t* d_first_point,
+                           const int32_t* d_labels, int64_t n_points, int64_t n_rows,
+                           int32_t ignore_label, int32_t* d_row_labels, void* stream);
+
 /* Exact membership: d_rows[i] = row of d_queries[i] ([q][D+1]) or -1. */
 mk_status mk_coords_lookup(const mk_coords* c, const int32_t* d_queries, int64_t q,
                            int32_t* d_rows, void* stream);

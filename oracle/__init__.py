@@ -58,6 +58,7 @@ def lib():
         L.orc_stride.argtypes = [P, i64, i32, P, P, P, P, P]
         L.orc_region.argtypes = [i32, i32, P, P, i32, P, i32, P, P]
         L.orc_lookup.argtypes = [P, i64, i32, P, i64, P]
+        L.orc_labels.argtypes = [P, P, i64, i64, i32, P]
         L.orc_kmap.argtypes = [P, i64, P, i64, i32, P, i32, P, i32, P, P, P]
         L.orc_conv_forward.argtypes = [P, P, P, i32, P, i32, P, P, i64, i32]
         L.orc_conv_forward_rows.argtypes = [P, P, P, i32, P, i32, P, i32, P, i64, P]
@@ -137,6 +138,17 @@ def region(kind: int, D: int, size=None, dilation=None, temporal_axis: int = -1,
     offs = np.zeros((K.value, D), np.int32)
     lib().orc_region(kind, D, _p(sz), _p(dl), temporal_axis, _p(cu), ncu, _p(offs), ctypes.byref(K))
     return offs
+
+
+def labels(point_to_row, point_labels, n_rows: int, ignore_label: int = -1):
+    """O1': per-voxel label, the points' common label or IGNORE_LABEL."""
+    p2r = _c(point_to_row, np.int32)
+    lab = _c(point_labels, np.int32)
+    out = np.zeros(max(n_rows, 1), np.int32)
+    st = lib().orc_labels(_p(p2r), _p(lab), p2r.shape[0], n_rows, ignore_label, _p(out))
+    if st:
+        raise OracleError(st)
+    return out[:n_rows].copy()
 
 
 def lookup(coords, queries):

@@ -269,6 +269,26 @@ int orc_region(int32_t type, int32_t D, const int32_t* size, const int32_t* dila
   return ORC_OK;
 }
 
+int orc_labels(const int32_t* point_to_row, const int32_t* labels, int64_t n_points, int64_t n_rows,
+               int32_t ignore_label, int32_t* row_labels) {
+  // Alg. 1 lines 5-6 reduce the (label, index) pairs of equal keys with f of
+  // P:181; folded here in input order, one point at a time.
+  std::vector<char> seen(static_cast<size_t>(n_rows), 0);
+  for (int64_t p = 0; p < n_points; ++p) {
+    const int32_t r = point_to_row[p];
+    if (r < 0 || r >= n_rows) return ORC_INVALID_ARGUMENT;
+    if (!seen[r]) {
+      seen[r] = 1;
+      row_labels[r] = labels[p];                      // (l_x, i_x): the first point
+    } else if (row_labels[r] != labels[p]) {
+      row_labels[r] = ignore_label;                   // f: l_x != l_y -> IGNORE_LABEL
+    }
+  }
+  for (int64_t r = 0; r < n_rows; ++r)
+    if (!seen[r]) return ORC_INVALID_ARGUMENT;        // every voxel has at least one point
+  return ORC_OK;
+}
+
 int orc_lookup(const int32_t* coords, int64_t n, int32_t D, const int32_t* queries, int64_t q,
                int32_t* rows) {
   if (D < 1 || D > 7) return ORC_INVALID_ARGUMENT;

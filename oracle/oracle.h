@@ -57,6 +57,12 @@ int orc_region(int32_t type, int32_t D, const int32_t* size, const int32_t* dila
                int32_t temporal_axis, const int32_t* custom, int32_t n_custom,
                int32_t* offsets, int32_t* K);
 
+/* O1' — label reduction of Alg. 1: the labels of the points of a voxel are
+ * folded in input order with f((l_x,i_x),(l_y,i_y)) = (l_x,i_x) if l_x == l_y else
+ * (IGNORE, i_x).  point_to_row is O1's inverse map (rows 0..n_rows-1). */
+int orc_labels(const int32_t* point_to_row, const int32_t* labels, int64_t n_points, int64_t n_rows,
+               int32_t ignore_label, int32_t* row_labels);
+
 /* Exact membership query: row of each query coordinate, -1 when absent. */
 int orc_lookup(const int32_t* coords, int64_t n, int32_t D, const int32_t* queries, int64_t q,
                int32_t* rows);

@@ -142,6 +142,22 @@ def coords_quantize(points: torch.Tensor, voxel: float, batch: Optional[torch.Te
     return c, p2r, first[:c.n]
 
 
+def coords_labels(point_to_row: torch.Tensor, first_point: torch.Tensor, labels: torch.Tensor,
+                  ignore_label: int = -1) -> torch.Tensor:
+    """Per-voxel labels of Alg. 1: the points' common label, else ignore_label.
+    point_to_row / first_point are the maps returned by coords_quantize."""
+    p2r = _cuda(point_to_row, torch.int32, "point_to_row")
+    first = _cuda(first_point, torch.int32, "first_point")
+    lab = _cuda(labels, torch.int32, "labels")
+    if lab.shape[0] != p2r.shape[0]:
+        raise ValueError("labels and point_to_row must have one entry per point")
+    out = torch.empty(first.shape[0], dtype=torch.int32, device=p2r.device)
+    with _on_device(p2r.device):
+        _check(_L.mk_coords_labels(_ptr(p2r), _ptr(first), _ptr(lab), p2r.shape[0], first.shape[0], int(ignore_label),
+                                   _ptr(out), _stream(p2r)), "mk_coords_labels")
+    return out
+
+
 def coords_create(coords: torch.Tensor, tensor_stride: Optional[Sequence[int]] = None, return_inverse: bool = False):
     """Coordinate set from integer rows [n][D+1] (batch last); first occurrence wins."""
     c = _cuda(coords, torch.int32, "coords")

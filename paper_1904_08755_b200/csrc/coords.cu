@@ -280,6 +280,23 @@ __global__ void k_init(int4* __restrict__ buckets, int32_t* __restrict__ first, 
   }
 }
 
+// Label reduction: candidate = label of the voxel's first point; any point whose
+// label differs marks the voxel IGNORE (every writer of the second kernel writes the same
+// value, so the result does not depend on the schedule).
+__global__ void k_labels_first(const int32_t* __restrict__ first_point, const int32_t* __restrict__ labels,
+                               int64_t n_rows, int32_t* __restrict__ row_labels) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n_rows; r += (int64_t)gridDim.x * blockDim.x)
+    row_labels[r] = __ldg(labels + __ldg(first_point + r));
+}
+__global__ void k_labels_mark(const int32_t* __restrict__ p2r, const int32_t* __restrict__ first_point,
+                              const int32_t* __restrict__ labels, int64_t n, int32_t ignore,
+                              int32_t* __restrict__ row_labels) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = __ldg(p2r + p);
+    if (__ldg(labels + p) != __ldg(labels + __ldg(first_point + r))) row_labels[r] = ignore;
+  }
+}
+
 __global__ void k_lookup(const int32_t* __restrict__ q, int64_t nq, int D, const int4* __restrict__ buckets,
                          uint32_t bmask, int32_t* __restrict__ rows) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
@@ -498,6 +515,23 @@ mk_status mk_coords_export(const mk_coords* c, int32_t* d_out, void* stream) {
   if (!c || (c->n > 0 && !d_out)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_export: null argument");
   if (c->n == 0) return MK_OK;
   k_export<<<grid_for(c->n, 256, 148), 256, 0, (cudaStream_t)stream>>>(c->keys, c->n, c->D, d_out);
+  MK_LAUNCH_CHECK();
+  return MK_OK;
+}
+
+mk_status mk_coords_labels(const int32_t* d_point_to_row, const int32_t* d_first_point, const int32_t* d_labels,
+                           int64_t n_points, int64_t n_rows, int32_t ignore_label, int32_t* d_row_labels, void* stream) {
+  clear_error();
+  if (n_points < 0 || n_rows < 0 || n_rows > n_points)
+    MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_labels: bad sizes (0 <= n_rows <= n_points)");
+  if (n_rows == 0) return MK_OK;
+  if (!d_point_to_row || !d_first_point || !d_labels || !d_row_labels)
+    MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_labels: null argument");
+  cudaStream_t s = (cudaStream_t)stream;
+  k_labels_first<<<grid_for(n_rows, 256, 148), 256, 0, s>>>(d_first_point, d_labels, n_rows, d_row_labels);
+  MK_LAUNCH_CHECK();
+  k_labels_mark<<<grid_for(n_points, 256, 148), 256, 0, s>>>(d_point_to_row, d_first_point, d_labels, n_points,
+                                                             ignore_label, d_row_labels);
   MK_LAUNCH_CHECK();
   return MK_OK;
 }

@@ -196,3 +196,27 @@ def test_kmap_video_hybrid_full_size(mk, orc):
     assert np.array_equal(c4.export().cpu().numpy(), o4)
     m = _check_map(mk, orc, o4, o4, mk.Region(mk.HYBRID, 4, 3), [1] * 4, False, c4, c4)
     assert m.K == 29
+
+
+@pytest.mark.parametrize("ignore", [-1, 255])
+def test_labels_room_full_size(mk, orc, ignore):
+    # BASELINE configs[1] scan with per-point labels that disagree inside some voxels
+    # (label = coarse 6 cm cell parity of x + y, so voxels straddling a boundary mix labels;
+    # plus 2% random label noise); bit-exact against the oracle's reduction.
+    pts = synthetic.room_points(2004)
+    g = np.random.default_rng(4)
+    labs = (np.floor(pts[:, 0] / 0.06).astype(np.int64) + np.floor(pts[:, 1] / 0.06).astype(np.int64)) % 2
+    labs = np.where(g.random(labs.shape[0]) < 0.02, 7, labs).astype(np.int32)
+    c, p2r, first = mk.coords_quantize(dev(pts), synthetic.ROOM_VOXEL)
+    got = mk.coords_labels(p2r, first, dev(labs), ignore_label=ignore).cpu().numpy()
+    oc, op2r, ofirst = orc.quantize(pts, synthetic.ROOM_VOXEL)
+    assert np.array_equal(p2r.cpu().numpy(), op2r)
+    want = orc.labels(op2r, labs, oc.shape[0], ignore)
+    assert np.array_equal(got, want)
+    assert 0 < (want == ignore).sum() < want.shape[0]  # both outcomes occur
+
+
+def test_labels_empty(mk):
+    c, p2r, first = mk.coords_quantize(torch.zeros((0, 3), device="cuda"), 0.1)
+    out = mk.coords_labels(p2r, first, torch.zeros(0, dtype=torch.int32, device="cuda"))
+    assert out.numel() == 0

@@ -116,3 +116,50 @@ def test_stride_brute_force(orc, sigma, ts):
             want.append(k)
     assert out.tolist() == [list(k) for k in want]
     assert out.shape[0] <= rows.shape[0]
+
+
+def test_labels_worked_examples(orc):
+    # golden: S:78 (two points {2,2} -> 2, {2,5} -> IGNORE), P:181 reduction
+    for line in golden_lines("labels_example.txt"):
+        ign, rest = line.split("|")
+        labs, want = rest.split("->")
+        labs = np.array([int(v) for v in labs.split()], np.int32)
+        pts = np.full((labs.shape[0], 3), 0.55, np.float32)  # all in one voxel
+        coords, p2r, first = orc.quantize(pts, 0.1)
+        assert coords.shape[0] == 1
+        assert orc.labels(p2r, labs, 1, int(ign)).tolist() == [int(want)]
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_labels_brute_force(orc, seed):
+    # brute force from the definition: a voxel keeps a label iff every point carries it
+    g = np.random.default_rng(seed)
+    pts = g.uniform(-1, 1, (4000, 3)).astype(np.float32)
+    labs = g.integers(0, 3, 4000).astype(np.int32)
+    # make some voxels label-pure on purpose
+    coords, p2r, first = orc.quantize(pts, 0.25)
+    pure = g.random(coords.shape[0]) < 0.5
+    labs = np.where(pure[p2r], 9, labs).astype(np.int32)
+    got = orc.labels(p2r, labs, coords.shape[0], -1)
+    sets = {}
+    for p, r in enumerate(p2r):
+        sets.setdefault(int(r), set()).add(int(labs[p]))
+    want = [next(iter(sets[r])) if len(sets[r]) == 1 else -1 for r in range(coords.shape[0])]
+    assert got.tolist() == want
+    assert (got == 9).sum() >= pure.sum() // 2  # the planted pure voxels survive
+
+
+def test_labels_point_order_invariant(orc):
+    # the reduction is a set function of the voxel's labels: permuting the points changes
+    # the row numbering (first occurrence, R8) but not the label of any voxel
+    g = np.random.default_rng(5)
+    pts = g.uniform(0, 1, (3000, 3)).astype(np.float32)
+    labs = g.integers(0, 2, 3000).astype(np.int32)
+    c1, p1, _ = orc.quantize(pts, 0.2)
+    l1 = orc.labels(p1, labs, c1.shape[0])
+    perm = g.permutation(3000)
+    c2, p2, _ = orc.quantize(pts[perm], 0.2)
+    l2 = orc.labels(p2, labs[perm], c2.shape[0])
+    d1 = {tuple(c): l for c, l in zip(c1.tolist(), l1.tolist())}
+    d2 = {tuple(c): l for c, l in zip(c2.tolist(), l2.tolist())}
+    assert d1 == d2
