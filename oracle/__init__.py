@@ -59,6 +59,9 @@ def lib():
         L.orc_region.argtypes = [i32, i32, P, P, i32, P, i32, P, P]
         L.orc_lookup.argtypes = [P, i64, i32, P, i64, P]
         L.orc_labels.argtypes = [P, P, i64, i64, i32, P]
+        L.orc_pool_forward.argtypes = [P, P, P, i32, P, i32, i64, i32, P, P]
+        L.orc_pool_backward.argtypes = [P, P, P, i32, P, i32, i64, i32, P, P, i64]
+        L.orc_global_pool.argtypes = [P, i64, P, i32, i32, i32, P]
         L.orc_kmap.argtypes = [P, i64, P, i64, i32, P, i32, P, i32, P, P, P]
         L.orc_conv_forward.argtypes = [P, P, P, i32, P, i32, P, P, i64, i32]
         L.orc_conv_forward_rows.argtypes = [P, P, P, i32, P, i32, P, i32, P, i64, P]
@@ -225,3 +228,38 @@ def conv_wgrad(kmap_csr, g_out, f_in, K: int):
     dW = np.zeros((K, c_out, c_in), np.float64)
     lib().orc_conv_wgrad(_p(ptr), _p(ins), _p(outs), K, _p(g), c_out, _p(x), c_in, _p(dW))
     return dW
+
+
+POOL_MAX, POOL_AVG, POOL_SUM = 0, 1, 2
+
+
+def pool_forward(kmap_csr, f_in, n_out: int, mode: int):
+    """f2: max (Alg. 3) / average / sum (Alg. 4) pooling over a kernel map, fp64.
+    Returns (f_out [n_out][C], argmax [n_out][C] int32 for max, else None)."""
+    ptr, ins, outs = kmap_csr
+    x = _c(f_in, np.float64)
+    C = x.shape[1]
+    y = np.zeros((max(n_out, 1), C), np.float64)
+    am = np.zeros((max(n_out, 1), C), np.int32) if mode == POOL_MAX else None
+    lib().orc_pool_forward(_p(ptr), _p(ins), _p(outs), len(ptr) - 1, _p(x), C, n_out, mode, _p(y), _p(am))
+    return y[:n_out].copy(), (am[:n_out].copy() if am is not None else None)
+
+
+def pool_backward(kmap_csr, g_out, n_in: int, mode: int, argmax=None):
+    ptr, ins, outs = kmap_csr
+    g = _c(g_out, np.float64)
+    C = g.shape[1]
+    am = _c(argmax, np.int32) if argmax is not None else None
+    gi = np.zeros((max(n_in, 1), C), np.float64)
+    lib().orc_pool_backward(_p(ptr), _p(ins), _p(outs), len(ptr) - 1, _p(g), C, g.shape[0], mode, _p(am), _p(gi),
+                            n_in)
+    return gi[:n_in].copy()
+
+
+def global_pool(batch, f_in, n_batch: int, mode: int):
+    """Global pooling: one row per batch index, sum or average of its rows."""
+    b = _c(batch, np.int32)
+    x = _c(f_in, np.float64)
+    y = np.zeros((max(n_batch, 1), x.shape[1]), np.float64)
+    lib().orc_global_pool(_p(b), b.shape[0], _p(x), x.shape[1], n_batch, mode, _p(y))
+    return y[:n_batch].copy()

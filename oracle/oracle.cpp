@@ -418,3 +418,75 @@ void orc_conv_wgrad(const int64_t* ptr, const int32_t* in_idx, const int32_t* ou
 }
 
 }  // extern "C"
+
+// f2 — pooling.  The inputs of output o are visited in concatenated order:
+// offset k ascending (each offset contributes at most one pair per output).
+void orc_pool_forward(const int64_t* ptr, const int32_t* in_idx, const int32_t* out_idx, int32_t K,
+                      const double* f_in, int32_t C, int64_t n_out, int32_t mode, double* f_out,
+                      int32_t* argmax) {
+  std::vector<int64_t> cnt(static_cast<size_t>(n_out), 0);
+  std::fill(f_out, f_out + n_out * C, 0.0);
+  if (mode == ORC_POOL_MAX && argmax) std::fill(argmax, argmax + n_out * C, -1);
+  for (int32_t k = 0; k < K; ++k) {
+    for (int64_t p = ptr[k]; p < ptr[k + 1]; ++p) {
+      const int32_t a = in_idx[p], o = out_idx[p];
+      const double* x = f_in + (int64_t)a * C;
+      double* y = f_out + (int64_t)o * C;
+      for (int32_t c = 0; c < C; ++c) {
+        if (mode == ORC_POOL_MAX) {
+          // MaxPoolKernel (Alg. 3): the first input sets the value, a later one replaces it
+          // only when strictly larger (ties: lowest concatenated index)
+          if (cnt[o] == 0 || x[c] > y[c]) {
+            y[c] = x[c];
+            if (argmax) argmax[(int64_t)o * C + c] = a;
+          }
+        } else {
+          y[c] += x[c];  // cusparse_csrmm(S_M, F) of Alg. 4
+        }
+      }
+      ++cnt[o];
+    }
+  }
+  if (mode == ORC_POOL_AVG)
+    for (int64_t o = 0; o < n_out; ++o)
+      if (cnt[o] > 0)
+        for (int32_t c = 0; c < C; ++c) f_out[o * C + c] /= static_cast<double>(cnt[o]);  // F' / N
+}
+
+void orc_pool_backward(const int64_t* ptr, const int32_t* in_idx, const int32_t* out_idx, int32_t K,
+                       const double* g_out, int32_t C, int64_t n_out, int32_t mode, const int32_t* argmax,
+                       double* g_in, int64_t n_in) {
+  std::fill(g_in, g_in + n_in * C, 0.0);
+  if (mode == ORC_POOL_MAX) {
+    for (int64_t o = 0; o < n_out; ++o)
+      for (int32_t c = 0; c < C; ++c) {
+        const int32_t a = argmax[o * C + c];
+        if (a >= 0) g_in[(int64_t)a * C + c] += g_out[o * C + c];
+      }
+    return;
+  }
+  std::vector<int64_t> cnt(static_cast<size_t>(n_out), 0);
+  for (int32_t k = 0; k < K; ++k)
+    for (int64_t p = ptr[k]; p < ptr[k + 1]; ++p) ++cnt[out_idx[p]];
+  for (int32_t k = 0; k < K; ++k)
+    for (int64_t p = ptr[k]; p < ptr[k + 1]; ++p) {
+      const int32_t a = in_idx[p], o = out_idx[p];
+      const double s = mode == ORC_POOL_AVG ? 1.0 / static_cast<double>(cnt[o]) : 1.0;
+      for (int32_t c = 0; c < C; ++c) g_in[(int64_t)a * C + c] += s * g_out[(int64_t)o * C + c];
+    }
+}
+
+void orc_global_pool(const int32_t* batch, int64_t n, const double* f_in, int32_t C, int32_t n_batch,
+                     int32_t mode, double* f_out) {
+  std::vector<int64_t> cnt(static_cast<size_t>(n_batch), 0);
+  std::fill(f_out, f_out + (int64_t)n_batch * C, 0.0);
+  for (int64_t r = 0; r < n; ++r) {
+    const int32_t b = batch[r];
+    for (int32_t c = 0; c < C; ++c) f_out[(int64_t)b * C + c] += f_in[r * C + c];
+    ++cnt[b];
+  }
+  if (mode == ORC_POOL_AVG)
+    for (int32_t b = 0; b < n_batch; ++b)
+      if (cnt[b] > 0)
+        for (int32_t c = 0; c < C; ++c) f_out[(int64_t)b * C + c] /= static_cast<double>(cnt[b]);
+}

@@ -91,6 +91,26 @@ void orc_conv_wgrad(const int64_t* ptr, const int32_t* in_idx, const int32_t* ou
                     const double* g_out, int32_t c_out, const double* f_in, int32_t c_in,
                     double* dW);
 
+/* f2 — pooling over a kernel map.  mode: 0 = max (Alg. 3), 1 = average
+ * (Alg. 4: F' / N), 2 = sum (Alg. 4 without the division, "sum pooling").  For every output
+ * o the inputs are the pairs (a, o) of all offsets, in concatenated order (offset k
+ * ascending, "I and O ... concatenated"); max keeps the FIRST maximal input in that
+ * order (ties) and reports it in argmax[o][c].  Outputs with no input are 0 (argmax
+ * -1).  fp64. */
+enum { ORC_POOL_MAX = 0, ORC_POOL_AVG = 1, ORC_POOL_SUM = 2 };
+void orc_pool_forward(const int64_t* ptr, const int32_t* in_idx, const int32_t* out_idx, int32_t K,
+                      const double* f_in, int32_t C, int64_t n_out, int32_t mode, double* f_out,
+                      int32_t* argmax);
+/* Reverse mode: max routes G_out[o][c] to argmax[o][c]; avg spreads G_out[o] / N_o over the
+ * inputs of o; sum copies G_out[o] to them. */
+void orc_pool_backward(const int64_t* ptr, const int32_t* in_idx, const int32_t* out_idx, int32_t K,
+                       const double* g_out, int32_t C, int64_t n_out, int32_t mode, const int32_t* argmax,
+                       double* g_in, int64_t n_in);
+/* Global pooling ("maps all inputs to the origin"): one output per batch index b,
+ * sum (mode 2) or average (mode 1) of the rows whose batch is b.  batch[r] in [0, n_batch). */
+void orc_global_pool(const int32_t* batch, int64_t n, const double* f_in, int32_t C, int32_t n_batch,
+                     int32_t mode, double* f_out);
+
 #ifdef __cplusplus
 }
 #endif
