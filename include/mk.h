@@ -181,6 +181,30 @@ mk_status mk_kmap_export(const mk_kmap* m, int64_t* d_ptr, int32_t* d_in, int32_
 
 void mk_kmap_destroy(mk_kmap* m);
 
+/* ---------------------------------------------------------------- pooling ---------- */
+/* Pooling over a kernel map.  The inputs of output row o are
+ * the pairs (a, o) of every offset, in concatenated order (offset k ascending).
+ *   MK_POOL_MAX  Alg. 3: F_out[o][c] = max_a F_in[a][c]; d_argmax [n_out][C] (device int32,
+ *                written when non-NULL) = the first maximal input row (ties: lowest
+ *                concatenated index), needed by the reverse mode.
+ *   MK_POOL_AVG  Alg. 4: the mean over the inputs (F' / N).
+ *   MK_POOL_SUM  Alg. 4 without the division ("sum pooling").
+ * Features [n][C] row-major, fp32 or bf16 (computed in fp32; bf16 outputs rounded RNE).
+ * Output rows with no input are 0 (argmax -1) — reading R23.  Strided pooling uses a map from
+ * a set to its strided set (mk_coords_stride); unpooling uses a transposed map.
+ * Asynchronous; deterministic (fixed reduction order, no atomics). */
+typedef enum { MK_POOL_MAX = 0, MK_POOL_AVG = 1, MK_POOL_SUM = 2 } mk_pool_mode;
+
+mk_status mk_pool_forward(mk_context* ctx, const mk_kmap* m, int32_t mode, const void* d_fin,
+                          int32_t C, mk_dtype dt, void* d_fout, int32_t* d_argmax, void* stream);
+
+/* Reverse mode: G_in[a] = sum over the outputs o of a (offset order) of G_out[o] (SUM),
+ * G_out[o] / N_o (AVG), or G_out[o][c] where argmax[o][c] == a (MAX; d_argmax from the
+ * forward call).  d_gin [n_in][C] is overwritten. */
+mk_status mk_pool_backward(mk_context* ctx, const mk_kmap* m, int32_t mode, const void* d_gout,
+                           int32_t C, mk_dtype dt, const int32_t* d_argmax, void* d_gin,
+                           void* stream);
+
 /* ---------------------------------------------------------------- convolution ------ */
 /* Generalized sparse convolution, Alg. 2:
  *   F_out[o] = sum over pairs (a, o) of offset k of W_k F_in[a];  rows without any pair

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import BF16, CUSTOM, F32, HYBRID, HYPERCROSS, HYPERCUBE
+from ._lib import BF16, CUSTOM, F32, HYBRID, HYPERCROSS, HYPERCUBE, POOL_AVG, POOL_MAX, POOL_SUM
 
 __all__ = [
     "MkError", "Coords", "KernelMap", "Region", "context",
@@ -341,3 +341,36 @@ def conv_backward(m: KernelMap, g_out, f_in, W, need_gin=True, need_gw=True, gin
 def conv_transpose_backward(m: KernelMap, g_out, f_in, W, need_gin=True, need_gw=True, gin=None, gw=None):
     return _backward(_L.mk_conv_transpose_backward, "mk_conv_transpose_backward", m, g_out, f_in, W, need_gin,
                      need_gw, gin, gw)
+
+
+# ------------------------------------------------------------------------------ pooling
+def pool_forward(m: KernelMap, f_in: torch.Tensor, mode: int = POOL_MAX, out=None, argmax=None):
+    """Pooling over a kernel map: POOL_MAX (Alg. 3), POOL_AVG / POOL_SUM (Alg. 4).
+    Returns (f_out [n_out][C], argmax [n_out][C] int32 for max pooling, else None)."""
+    if not f_in.is_cuda:
+        raise ValueError("pool inputs must be CUDA tensors (no CPU path)")
+    if f_in.shape[0] != m.n_in:
+        raise ValueError(f"pool_forward: f_in has {f_in.shape[0]} rows, the map has n_in={m.n_in}")
+    x = f_in.contiguous()
+    C = x.shape[1]
+    y = out if out is not None else torch.empty((m.n_out, C), dtype=x.dtype, device=x.device)
+    am = None
+    if mode == POOL_MAX:
+        am = argmax if argmax is not None else torch.empty((m.n_out, C), dtype=torch.int32, device=x.device)
+    with _on_device(x.device):
+        _check(_L.mk_pool_forward(context(x.device.index), m._h, int(mode), _ptr(x), C, _dt(x), _ptr(y), _ptr(am),
+                                  _stream(x)), "mk_pool_forward")
+    return y, am
+
+
+def pool_backward(m: KernelMap, g_out: torch.Tensor, mode: int = POOL_MAX, argmax=None, out=None):
+    """Reverse mode of pool_forward: G_in [n_in][C] (argmax required for POOL_MAX)."""
+    if g_out.shape[0] != m.n_out:
+        raise ValueError(f"pool_backward: g_out has {g_out.shape[0]} rows, the map has n_out={m.n_out}")
+    g = g_out.contiguous()
+    C = g.shape[1]
+    gi = out if out is not None else torch.empty((m.n_in, C), dtype=g.dtype, device=g.device)
+    with _on_device(g.device):
+        _check(_L.mk_pool_backward(context(g.device.index), m._h, int(mode), _ptr(g), C, _dt(g), _ptr(argmax),
+                                   _ptr(gi), _stream(g)), "mk_pool_backward")
+    return gi

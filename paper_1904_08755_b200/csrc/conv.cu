@@ -18,33 +18,6 @@ mk_status check_common(mk_context* ctx, const mk_kmap* m, int32_t c_in, int32_t 
   return MK_OK;
 }
 
-NbrView forward_view(const mk_kmap* m) {
-  NbrView v;
-  v.tab = m->nbr;
-  v.mask = m->tile_mask;
-  v.perm = m->perm;
-  v.n = m->nbr_stride;
-  v.K = m->K;
-  v.mw = m->mask_words;
-  return v;
-}
-
-NbrView dgrad_view(const mk_kmap* m) {
-  NbrView v;
-  v.K = m->K;
-  v.mw = m->mask_words;
-  v.n = m->nbrT_stride;
-  v.mask = m->tile_maskT;
-  v.perm = m->permT;
-  if (m->nbrT) {
-    v.tab = m->nbrT;
-  } else {  // symmetric submanifold map: nbrT[k] = nbr[mirror[k]]
-    v.tab = m->nbr;
-    v.mirror = m->d_mirror;
-  }
-  return v;
-}
-
 mk_status forward_impl(mk_context* ctx, const mk_kmap* m, const void* d_fin, int32_t c_in, const void* d_w,
                        void* d_fout, int32_t c_out, mk_dtype in_dt, mk_dtype out_dt, cudaStream_t s) {
   mk_status st = check_common(ctx, m, c_in, c_out, in_dt);

@@ -25,6 +25,36 @@ struct NbrView {
   }
 };
 
+// The forward view of a map (rows = outputs, entries = input rows) and its reverse view
+// (rows = inputs, entries = output rows; nbrT, or nbr read at the mirrored offset when the
+// map is a symmetric submanifold map).
+inline NbrView forward_view(const mk_kmap* m) {
+  NbrView v;
+  v.tab = m->nbr;
+  v.mask = m->tile_mask;
+  v.perm = m->perm;
+  v.n = m->nbr_stride;
+  v.K = m->K;
+  v.mw = m->mask_words;
+  return v;
+}
+
+inline NbrView dgrad_view(const mk_kmap* m) {
+  NbrView v;
+  v.K = m->K;
+  v.mw = m->mask_words;
+  v.n = m->nbrT_stride;
+  v.mask = m->tile_maskT;
+  v.perm = m->permT;
+  if (m->nbrT) {
+    v.tab = m->nbrT;
+  } else {  // symmetric submanifold map: nbrT[k] = nbr[mirror[k]]
+    v.tab = m->nbr;
+    v.mirror = m->d_mirror;
+  }
+  return v;
+}
+
 // Split-K plan for the weight gradient: the pairs of offset k are cut into chunks of at
 // most `chunk` pairs; chunks[c] = (k, begin, end, c); chunk_begin[k] = first chunk of k.
 struct WgradPlan {

@@ -1,0 +1,159 @@
+// pool.cu — pooling over a kernel map:
+//   max pooling (Alg. 3)   F_out[o][c] = max over the inputs a of o of F_in[a][c], with the
+//                          argmax (first maximal input in concatenated order: offset k
+//                          ascending — ties as S:262) for the reverse mode;
+//   average pooling (Alg. 4)  F' / N with N = number of inputs of o;
+//   sum pooling (Alg. 4 without the division).
+// The paper sorts (I, O) by output and reduces with a custom kernel / cuSPARSE csrmm.  Here
+// the map's dense neighbour table already groups the inputs of every output row, so one
+// warp reduces one output row over its K table entries (32 channels per lane pass) — a
+// gather-reduce bound by L2 traffic.  The reverse mode walks the map's reverse view (the
+// outputs of every input row) and sums in offset order: no atomics, deterministic.
+// Outputs with no input are written as 0 (argmax -1).
+#include <cuda_bf16.h>
+
+#include "conv.cuh"
+
+namespace mk {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kRowsPerBlock = kThreads / 32;
+
+__device__ __forceinline__ float ld_feat(const void* p, int64_t i, int bf16) {
+  return bf16 ? __bfloat162float(((const __nv_bfloat16*)p)[i]) : ((const float*)p)[i];
+}
+__device__ __forceinline__ void st_feat(void* p, int64_t i, float v, int bf16) {
+  if (bf16) ((__nv_bfloat16*)p)[i] = __float2bfloat16_rn(v);
+  else ((float*)p)[i] = v;
+}
+
+// One warp per table position i (output row perm[i]); lanes over channels.
+__global__ void __launch_bounds__(kThreads) k_pool_fwd(NbrView nb, int64_t n_rows, const void* __restrict__ x,
+                                                       int C, int bf16, int mode, void* __restrict__ y,
+                                                       int32_t* __restrict__ argmax) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+  if (i >= n_rows) return;
+  const int64_t o = nb.row_of(i);
+  for (int c = lane; c < C; c += 32) {
+    float acc = 0.f;
+    int32_t best = -1, cnt = 0;
+    for (int k = 0; k < nb.K; ++k) {
+      const int32_t a = nb.at(k, i);
+      if (a < 0) continue;
+      const float v = ld_feat(x, (int64_t)a * C + c, bf16);
+      if (mode == MK_POOL_MAX) {
+        if (best < 0 || v > acc) {  // strictly greater: the first maximal input wins
+          acc = v;
+          best = a;
+        }
+      } else {
+        acc += v;
+      }
+      ++cnt;
+    }
+    if (mode == MK_POOL_AVG && cnt > 0) acc /= (float)cnt;
+    st_feat(y, o * C + c, acc, bf16);
+    if (mode == MK_POOL_MAX && argmax) argmax[o * C + c] = best;
+  }
+}
+
+// Number of inputs of every output row (average pooling's N), from the forward table.
+__global__ void k_pool_counts(NbrView nb, int64_t n_rows, int32_t* __restrict__ cnt) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n_rows; i += (int64_t)gridDim.x * blockDim.x) {
+    int32_t c = 0;
+    for (int k = 0; k < nb.K; ++k) c += nb.at(k, i) >= 0;
+    cnt[nb.row_of(i)] = c;
+  }
+}
+
+// One warp per position i of the reverse view (input row a = permT[i]); the outputs o of a
+// are visited in offset order.
+__global__ void __launch_bounds__(kThreads) k_pool_bwd(NbrView nt, int64_t n_rows, const void* __restrict__ g,
+                                                       int C, int bf16, int mode, const int32_t* __restrict__ argmax,
+                                                       const int32_t* __restrict__ cnt, void* __restrict__ gx) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+  if (i >= n_rows) return;
+  const int64_t a = nt.row_of(i);
+  for (int c = lane; c < C; c += 32) {
+    float acc = 0.f;
+    for (int k = 0; k < nt.K; ++k) {
+      const int32_t o = nt.at(k, i);
+      if (o < 0) continue;
+      const int64_t e = (int64_t)o * C + c;
+      if (mode == MK_POOL_MAX) {
+        if (__ldg(argmax + e) == (int32_t)a) acc += ld_feat(g, e, bf16);
+      } else if (mode == MK_POOL_AVG) {
+        acc += ld_feat(g, e, bf16) / (float)__ldg(cnt + o);
+      } else {
+        acc += ld_feat(g, e, bf16);
+      }
+    }
+    st_feat(gx, a * C + c, acc, bf16);
+  }
+}
+
+mk_status check_pool(const mk_kmap* m, int32_t mode, int32_t C, mk_dtype dt) {
+  if (!m) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "pool: null map");
+  if (mode != MK_POOL_MAX && mode != MK_POOL_AVG && mode != MK_POOL_SUM)
+    MK_FAIL(MK_ERR_INVALID_ARGUMENT, "pool: unknown mode");
+  if (C < 1) MK_FAIL(MK_ERR_SHAPE_MISMATCH, "pool: channel count must be >= 1");
+  if (dt != MK_F32 && dt != MK_BF16) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "pool: unknown dtype");
+  return MK_OK;
+}
+
+}  // namespace
+}  // namespace mk
+
+using namespace mk;
+
+extern "C" {
+
+mk_status mk_pool_forward(mk_context* ctx, const mk_kmap* m, int32_t mode, const void* d_fin, int32_t C, mk_dtype dt,
+                          void* d_fout, int32_t* d_argmax, void* stream) {
+  clear_error();
+  mk_status st = check_pool(m, mode, C, dt);
+  if (st != MK_OK) return st;
+  if (!ctx) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_pool_forward: null context");
+  if (m->n_out == 0) return MK_OK;
+  if (!d_fout || (m->n_in > 0 && !d_fin)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_pool_forward: null features");
+  const NbrView v = forward_view(m);
+  const unsigned grid = (unsigned)ceil_div(m->n_out, kRowsPerBlock);
+  k_pool_fwd<<<grid, kThreads, 0, (cudaStream_t)stream>>>(v, m->n_out, d_fin, C, dt == MK_BF16, mode, d_fout,
+                                                           mode == MK_POOL_MAX ? d_argmax : nullptr);
+  MK_LAUNCH_CHECK();
+  return MK_OK;
+}
+
+mk_status mk_pool_backward(mk_context* ctx, const mk_kmap* m, int32_t mode, const void* d_gout, int32_t C,
+                           mk_dtype dt, const int32_t* d_argmax, void* d_gin, void* stream) {
+  clear_error();
+  mk_status st = check_pool(m, mode, C, dt);
+  if (st != MK_OK) return st;
+  if (!ctx) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_pool_backward: null context");
+  if (m->n_in == 0) return MK_OK;
+  if (!d_gin || (m->n_out > 0 && !d_gout)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_pool_backward: null gradients");
+  if (mode == MK_POOL_MAX && m->n_out > 0 && !d_argmax)
+    MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_pool_backward: max pooling needs the forward argmax");
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t* cnt = nullptr;
+  if (mode == MK_POOL_AVG && m->n_out > 0) {
+    cnt = (int32_t*)dev_alloc(ctx->alloc, sizeof(int32_t) * m->n_out, s);
+    if (!cnt) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "mk_pool_backward: workspace allocation failed");
+    k_pool_counts<<<(unsigned)std::min<int64_t>(ceil_div(m->n_out, 256), 4 * ctx->num_sms), 256, 0, s>>>(
+        forward_view(m), m->n_out, cnt);
+    g_launches++;
+  }
+  const NbrView v = dgrad_view(m);
+  const unsigned grid = (unsigned)ceil_div(m->n_in, kRowsPerBlock);
+  k_pool_bwd<<<grid, kThreads, 0, s>>>(v, m->n_in, d_gout, C, dt == MK_BF16, mode, d_argmax, cnt, d_gin);
+  g_launches++;
+  const cudaError_t e = cudaGetLastError();
+  if (cnt) dev_free(ctx->alloc, cnt, s);
+  if (e != cudaSuccess) MK_FAIL(MK_ERR_CUDA, std::string("mk_pool_backward: ") + cudaGetErrorString(e));
+  return MK_OK;
+}
+
+}  // extern "C"
