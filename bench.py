@@ -271,6 +271,39 @@ def run_mk(args, ws, rank, local):
         e2e_ms = float(t.item())
     e2e_value = ws * flops_step / (e2e_ms / args.steps * 1e-3) / 1e12
 
+    # ---- SURVEY §8(f) rows built so far, timed on the same scan (not part of the step):
+    #      f1 label reduction and f2 stride-2 2^3 max / average pooling (Alg. 3/4)
+    def timed(fn, reps=20):
+        fn()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        tot = 0.0
+        for _ in range(reps):
+            flush.zero_()
+            ev[0].record(stream)
+            fn()
+            ev[1].record(stream)
+            torch.cuda.synchronize()
+            tot += ev[0].elapsed_time(ev[1])
+        return tot / reps * 1e3  # us
+
+    cq, p2r, first = mk.coords_quantize(pts, synthetic.ROOM_VOXEL)
+    labs = (torch.arange(pts.shape[0], device=dev, dtype=torch.int32) // 7) % 5
+    t_lab = timed(lambda: mk.coords_labels(p2r, first, labs))
+    coarse = mk.coords_stride(cq, [2, 2, 2])
+    mp = mk.kmap_build(cq, coarse, mk.Region(mk.HYPERCUBE, 3, 2))
+    yp, am = mk.pool_forward(mp, X, mk.POOL_MAX)
+    Gp = torch.ones_like(yp)
+    t_pf = timed(lambda: mk.pool_forward(mp, X, mk.POOL_MAX, out=yp, argmax=am))
+    t_pb = timed(lambda: mk.pool_backward(mp, Gp, mk.POOL_MAX, am))
+    t_af = timed(lambda: mk.pool_forward(mp, X, mk.POOL_AVG, out=yp))
+    pool_bytes = mp.n_in * C_IN * 2 + mp.n_out * C_IN * (2 + 4)  # x read, y + argmax written
+    extras = {
+        "labels_us": round(t_lab, 2), "labels_mpts": round(pts.shape[0] / t_lab, 1),
+        "maxpool2_fwd_us": round(t_pf, 2), "maxpool2_bwd_us": round(t_pb, 2), "avgpool2_fwd_us": round(t_af, 2),
+        "maxpool2_fwd_gbs": round(pool_bytes / (t_pf * 1e-6) / 1e9, 1),
+        "pool_rows": [int(mp.n_in), int(mp.n_out)],
+    }
+
     # ---- roofline of the dominant kernel (largest phase among the conv kernels / map build)
     pk = peaks()
     conv_ph = {"conv_fwd": mean_ph[2], "conv_dgrad": mean_ph[3], "conv_wgrad": mean_ph[4]}
@@ -312,6 +345,7 @@ def run_mk(args, ws, rank, local):
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_ms / args.steps, 4)},
         "gpu_launches": int(launches),
+        "extras_f1_f2": extras,
         "roofline": roof,
         "clocks": clocks,
     }

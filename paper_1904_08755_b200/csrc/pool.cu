@@ -28,7 +28,9 @@ __device__ __forceinline__ void st_feat(void* p, int64_t i, float v, int bf16) {
   else ((float*)p)[i] = v;
 }
 
-// One warp per table position i (output row perm[i]); lanes over channels.
+// One warp per table position i (output row perm[i]).  The K <= 32 neighbour indices of
+// the row are loaded once (lane k holds entry k) and broadcast with shuffles, so the value
+// loads of all offsets are independent; lanes cover 32 channels per pass.
 __global__ void __launch_bounds__(kThreads) k_pool_fwd(NbrView nb, int64_t n_rows, const void* __restrict__ x,
                                                        int C, int bf16, int mode, void* __restrict__ y,
                                                        int32_t* __restrict__ argmax) {
@@ -36,22 +38,27 @@ __global__ void __launch_bounds__(kThreads) k_pool_fwd(NbrView nb, int64_t n_row
   const int64_t i = (int64_t)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
   if (i >= n_rows) return;
   const int64_t o = nb.row_of(i);
+  const int kw = min(nb.K, 32);
   for (int c = lane; c < C; c += 32) {
     float acc = 0.f;
     int32_t best = -1, cnt = 0;
-    for (int k = 0; k < nb.K; ++k) {
-      const int32_t a = nb.at(k, i);
-      if (a < 0) continue;
-      const float v = ld_feat(x, (int64_t)a * C + c, bf16);
-      if (mode == MK_POOL_MAX) {
-        if (best < 0 || v > acc) {  // strictly greater: the first maximal input wins
-          acc = v;
-          best = a;
+    for (int k0 = 0; k0 < nb.K; k0 += kw) {
+      const int32_t mine = k0 + lane < nb.K ? nb.at(k0 + lane, i) : -1;
+#pragma unroll 8
+      for (int kk = 0; kk < kw && k0 + kk < nb.K; ++kk) {
+        const int32_t a = __shfl_sync(0xffffffffu, mine, kk);
+        if (a < 0) continue;
+        const float v = ld_feat(x, (int64_t)a * C + c, bf16);
+        if (mode == MK_POOL_MAX) {
+          if (best < 0 || v > acc) {  // strictly greater: the first maximal input wins
+            acc = v;
+            best = a;
+          }
+        } else {
+          acc += v;
         }
-      } else {
-        acc += v;
+        ++cnt;
       }
-      ++cnt;
     }
     if (mode == MK_POOL_AVG && cnt > 0) acc /= (float)cnt;
     st_feat(y, o * C + c, acc, bf16);
@@ -69,7 +76,7 @@ __global__ void k_pool_counts(NbrView nb, int64_t n_rows, int32_t* __restrict__ 
 }
 
 // One warp per position i of the reverse view (input row a = permT[i]); the outputs o of a
-// are visited in offset order.
+// are visited in offset order (indices loaded once per lane, broadcast with shuffles).
 __global__ void __launch_bounds__(kThreads) k_pool_bwd(NbrView nt, int64_t n_rows, const void* __restrict__ g,
                                                        int C, int bf16, int mode, const int32_t* __restrict__ argmax,
                                                        const int32_t* __restrict__ cnt, void* __restrict__ gx) {
@@ -77,18 +84,23 @@ __global__ void __launch_bounds__(kThreads) k_pool_bwd(NbrView nt, int64_t n_row
   const int64_t i = (int64_t)blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
   if (i >= n_rows) return;
   const int64_t a = nt.row_of(i);
+  const int kw = min(nt.K, 32);
   for (int c = lane; c < C; c += 32) {
     float acc = 0.f;
-    for (int k = 0; k < nt.K; ++k) {
-      const int32_t o = nt.at(k, i);
-      if (o < 0) continue;
-      const int64_t e = (int64_t)o * C + c;
-      if (mode == MK_POOL_MAX) {
-        if (__ldg(argmax + e) == (int32_t)a) acc += ld_feat(g, e, bf16);
-      } else if (mode == MK_POOL_AVG) {
-        acc += ld_feat(g, e, bf16) / (float)__ldg(cnt + o);
-      } else {
-        acc += ld_feat(g, e, bf16);
+    for (int k0 = 0; k0 < nt.K; k0 += kw) {
+      const int32_t mine = k0 + lane < nt.K ? nt.at(k0 + lane, i) : -1;
+#pragma unroll 8
+      for (int kk = 0; kk < kw && k0 + kk < nt.K; ++kk) {
+        const int32_t o = __shfl_sync(0xffffffffu, mine, kk);
+        if (o < 0) continue;
+        const int64_t e = (int64_t)o * C + c;
+        if (mode == MK_POOL_MAX) {
+          if (__ldg(argmax + e) == (int32_t)a) acc += ld_feat(g, e, bf16);
+        } else if (mode == MK_POOL_AVG) {
+          acc += ld_feat(g, e, bf16) / (float)__ldg(cnt + o);
+        } else {
+          acc += ld_feat(g, e, bf16);
+        }
       }
     }
     st_feat(gx, a * C + c, acc, bf16);
