@@ -39,7 +39,9 @@ __global__ void __launch_bounds__(kThreads) k_pool_fwd(NbrView nb, int64_t n_row
   if (i >= n_rows) return;
   const int64_t o = nb.row_of(i);
   const int kw = min(nb.K, 32);
-  for (int c = lane; c < C; c += 32) {
+  for (int c0 = 0; c0 < C; c0 += 32) {  // warp-uniform trip count: the shuffles see every lane
+    const int c = c0 + lane;
+    const bool valid = c < C;
     float acc = 0.f;
     int32_t best = -1, cnt = 0;
     for (int k0 = 0; k0 < nb.K; k0 += kw) {
@@ -47,7 +49,7 @@ __global__ void __launch_bounds__(kThreads) k_pool_fwd(NbrView nb, int64_t n_row
 #pragma unroll 8
       for (int kk = 0; kk < kw && k0 + kk < nb.K; ++kk) {
         const int32_t a = __shfl_sync(0xffffffffu, mine, kk);
-        if (a < 0) continue;
+        if (a < 0 || !valid) continue;
         const float v = ld_feat(x, (int64_t)a * C + c, bf16);
         if (mode == MK_POOL_MAX) {
           if (best < 0 || v > acc) {  // strictly greater: the first maximal input wins
@@ -60,6 +62,7 @@ __global__ void __launch_bounds__(kThreads) k_pool_fwd(NbrView nb, int64_t n_row
         ++cnt;
       }
     }
+    if (!valid) continue;
     if (mode == MK_POOL_AVG && cnt > 0) acc /= (float)cnt;
     st_feat(y, o * C + c, acc, bf16);
     if (mode == MK_POOL_MAX && argmax) argmax[o * C + c] = best;
@@ -85,14 +88,16 @@ __global__ void __launch_bounds__(kThreads) k_pool_bwd(NbrView nt, int64_t n_row
   if (i >= n_rows) return;
   const int64_t a = nt.row_of(i);
   const int kw = min(nt.K, 32);
-  for (int c = lane; c < C; c += 32) {
+  for (int c0 = 0; c0 < C; c0 += 32) {  // warp-uniform trip count: the shuffles see every lane
+    const int c = c0 + lane;
+    const bool valid = c < C;
     float acc = 0.f;
     for (int k0 = 0; k0 < nt.K; k0 += kw) {
       const int32_t mine = k0 + lane < nt.K ? nt.at(k0 + lane, i) : -1;
 #pragma unroll 8
       for (int kk = 0; kk < kw && k0 + kk < nt.K; ++kk) {
         const int32_t o = __shfl_sync(0xffffffffu, mine, kk);
-        if (o < 0) continue;
+        if (o < 0 || !valid) continue;
         const int64_t e = (int64_t)o * C + c;
         if (mode == MK_POOL_MAX) {
           if (__ldg(argmax + e) == (int32_t)a) acc += ld_feat(g, e, bf16);
@@ -103,7 +108,7 @@ __global__ void __launch_bounds__(kThreads) k_pool_bwd(NbrView nt, int64_t n_row
         }
       }
     }
-    st_feat(gx, a * C + c, acc, bf16);
+    if (valid) st_feat(gx, a * C + c, acc, bf16);
   }
 }
 
