@@ -59,6 +59,7 @@ def lib():
         L.orc_region.argtypes = [i32, i32, P, P, i32, P, i32, P, P]
         L.orc_lookup.argtypes = [P, i64, i32, P, i64, P]
         L.orc_labels.argtypes = [P, P, i64, i64, i32, P]
+        L.orc_expand.argtypes = [P, i64, i32, P, i32, P, P, P, P]
         L.orc_pool_forward.argtypes = [P, P, P, i32, P, i32, i64, i32, P, P]
         L.orc_pool_backward.argtypes = [P, P, P, i32, P, i32, i64, i32, P, P, i64]
         L.orc_global_pool.argtypes = [P, i64, P, i32, i32, i32, P]
@@ -141,6 +142,22 @@ def region(kind: int, D: int, size=None, dilation=None, temporal_axis: int = -1,
     offs = np.zeros((K.value, D), np.int32)
     lib().orc_region(kind, D, _p(sz), _p(dl), temporal_axis, _p(cu), ncu, _p(offs), ctypes.byref(K))
     return offs
+
+
+def expand(coords, offsets, scale=None):
+    """f4: output coordinates of a generative transposed conv, {u + i * scale}."""
+    c = _c(coords, np.int32)
+    offs = _c(offsets, np.int32)
+    n, Dp1 = c.shape
+    D = Dp1 - 1
+    K = offs.shape[0]
+    sc = None if scale is None else _c(scale, np.int32)
+    out = np.zeros((max(n * K, 1), Dp1), np.int32)
+    n_out, err = ctypes.c_int64(), ctypes.c_int64()
+    st = lib().orc_expand(_p(c), n, D, _p(offs), K, _p(sc), _p(out), ctypes.byref(n_out), ctypes.byref(err))
+    if st:
+        raise OracleError(st, err.value)
+    return out[:n_out.value].copy()
 
 
 def labels(point_to_row, point_labels, n_rows: int, ignore_label: int = -1):

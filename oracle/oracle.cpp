@@ -189,6 +189,38 @@ int orc_stride(const int32_t* coords, int64_t n, int32_t D, const int32_t* tenso
   return ORC_OK;
 }
 
+int orc_expand(const int32_t* coords, int64_t n, int32_t D, const int32_t* offsets, int32_t K,
+               const int32_t* scale, int32_t* coords_out, int64_t* n_out, int64_t* err_row) {
+  *err_row = -1;
+  *n_out = 0;
+  if (D < 1 || D > 7 || n < 0 || K < 1) return ORC_INVALID_ARGUMENT;
+  // every u + i * scale (the output coordinates of a transposed conv may be any set;
+  // the generative one is the union of the input rows' receptive fields), batch unchanged,
+  // first occurrence in (row, offset) order
+  CoordMap map;
+  map.reserve(static_cast<size_t>(n) * K * 2 + 1);
+  int32_t next = 0;
+  for (int64_t p = 0; p < n; ++p) {
+    const int32_t* r = coords + p * (D + 1);
+    for (int32_t k = 0; k < K; ++k) {
+      Key key{};
+      for (int d = 0; d < D; ++d) {
+        const int64_t v = (int64_t)r[d] + (int64_t)offsets[k * D + d] * (scale ? scale[d] : 1);
+        if (!fits_i32(v)) { *err_row = p; return ORC_COORD_RANGE; }
+        key[d] = static_cast<int32_t>(v);
+      }
+      key[D] = r[D];
+      if (map.find(key) == map.end()) {
+        const int32_t row = next++;
+        map.emplace(key, row);
+        for (int d = 0; d <= D; ++d) coords_out[(int64_t)row * (D + 1) + d] = key[d];
+      }
+    }
+  }
+  *n_out = next;
+  return ORC_OK;
+}
+
 int orc_region(int32_t type, int32_t D, const int32_t* size, const int32_t* dilation,
                int32_t temporal_axis, const int32_t* custom, int32_t n_custom,
                int32_t* offsets, int32_t* K) {

@@ -52,6 +52,13 @@ int orc_create(const int32_t* coords, int64_t n, int32_t D, const int32_t* tenso
 int orc_stride(const int32_t* coords, int64_t n, int32_t D, const int32_t* tensor_stride,
                const int32_t* conv_stride, int32_t* coords_out, int64_t* n_out, int64_t* err_row);
 
+/* f4 — output coordinates of a generative transposed convolution ("arbitrary output
+ * coordinates"): C_out = union over rows u of C_in and offsets i of
+ * {u + i * scale}, batch unchanged, first occurrence in (row, offset) order; coords_out
+ * holds up to n * K rows. */
+int orc_expand(const int32_t* coords, int64_t n, int32_t D, const int32_t* offsets, int32_t K,
+               const int32_t* scale, int32_t* coords_out, int64_t* n_out, int64_t* err_row);
+
 /* O4 — kernel offset set N^D.  offsets may be NULL (count only). */
 int orc_region(int32_t type, int32_t D, const int32_t* size, const int32_t* dilation,
                int32_t temporal_axis, const int32_t* custom, int32_t n_custom,

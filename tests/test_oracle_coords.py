@@ -3,7 +3,7 @@ examples, brute force and invariants.  No GPU."""
 import numpy as np
 import pytest
 
-from conftest import golden_lines
+from conftest import full_grid, golden_lines
 
 
 def test_quantize_worked_examples(orc):
@@ -163,3 +163,31 @@ def test_labels_point_order_invariant(orc):
     d1 = {tuple(c): l for c, l in zip(c1.tolist(), l1.tolist())}
     d2 = {tuple(c): l for c, l in zip(c2.tolist(), l2.tolist())}
     assert d1 == d2
+
+
+def test_expand_pins(orc):
+    # f4 generative output coordinates: {u + i * s}.
+    # (1) the region {0} is the identity (same rows, same order)
+    g = np.random.default_rng(8)
+    rows = np.concatenate([g.integers(-20, 20, (500, 3)) * 2, g.integers(0, 2, (500, 1))], axis=1).astype(np.int32)
+    c, _ = orc.create(rows, [2, 2, 2])
+    assert np.array_equal(orc.expand(c, np.zeros((1, 3), np.int32)), c)
+    # (2) brute force: the set and the first-occurrence order of (row, offset)
+    offs = orc.region(0, 3, [3, 3, 3])
+    got = orc.expand(c, offs, [1, 1, 1])
+    want, seen = [], set()
+    for r in c.tolist():
+        for o in offs.tolist():
+            key = (r[0] + o[0], r[1] + o[1], r[2] + o[2], r[3])
+            if key not in seen:
+                seen.add(key)
+                want.append(key)
+    assert [tuple(x) for x in got.tolist()] == want
+    # (3) upsampling: expanding the stride-2 set of a full grid by {0,1}^3 at the fine stride
+    #     recovers exactly the full grid (as a set) — the generative transposed conv's output
+    fine = full_grid(6, 3)
+    coarse = orc.stride(fine, [2, 2, 2])
+    up = orc.expand(coarse, orc.region(0, 3, [2, 2, 2]), [1, 1, 1])
+    assert sorted(map(tuple, up.tolist())) == sorted(map(tuple, fine.tolist()))
+    # (4) batch indices never move (R18)
+    assert set(got[:, 3].tolist()) == set(c[:, 3].tolist())
