@@ -151,6 +151,16 @@ mk_status mk_coords_lookup(const mk_coords* c, const int32_t* d_queries, int64_t
 mk_status mk_coords_stride(mk_context* ctx, const mk_coords* in, const int32_t* h_conv_stride,
                            void* stream, mk_coords** out);
 
+/* Output coordinates of a generative transposed convolution (a transposed conv may
+ * produce "arbitrary output coordinates"): the union over rows u of `in`
+ * and offsets i of `region` of u + i * s_out, batch unchanged (R18), rows in first
+ * occurrence of (row, offset) order.  h_out_stride host [D] (NULL = in's tensor stride)
+ * must divide in's tensor stride (MK_ERR_STRIDE); it is the new set's tensor stride.
+ * Typical use: upsampling a stride-2s set to stride s with the region {0,1}^D, then
+ * mk_kmap_build(in, out, region, transposed = 1).  Synchronizes once (row count). */
+mk_status mk_coords_expand(mk_context* ctx, const mk_coords* in, const mk_region* region,
+                           const int32_t* h_out_stride, void* stream, mk_coords** out);
+
 void mk_coords_destroy(mk_coords* c);
 
 /* ---------------------------------------------------------------- kernel region ---- */

@@ -183,6 +183,17 @@ def coords_stride(cin: Coords, conv_stride: Sequence[int]) -> Coords:
     return Coords(h, cin.device)
 
 
+def coords_expand(cin: Coords, region: "Region", tensor_stride: Optional[Sequence[int]] = None) -> Coords:
+    """Generative transposed-conv output coordinates (f4): {u + i * s_out}."""
+    r = region._struct()
+    ts = None if tensor_stride is None else (ctypes.c_int32 * cin.D)(*tensor_stride)
+    h = ctypes.c_void_p()
+    with _on_device(cin.device):
+        _check(_L.mk_coords_expand(context(cin.device.index), cin._h, ctypes.byref(r), ts, _stream(),
+                                   ctypes.byref(h)), "mk_coords_expand")
+    return Coords(h, cin.device)
+
+
 def coords_export(c: Coords) -> torch.Tensor:
     out = torch.empty((c.n, c.D + 1), dtype=torch.int32, device=c.device)
     with _on_device(c.device):

@@ -40,7 +40,7 @@ class MkRegion(ctypes.Structure):
 EXPORTS = [
     "mk_context_create", "mk_context_destroy",
     "mk_coords_quantize", "mk_coords_create", "mk_coords_info", "mk_coords_export", "mk_coords_lookup",
-    "mk_coords_labels",
+    "mk_coords_labels", "mk_coords_expand",
     "mk_coords_stride", "mk_coords_destroy",
     "mk_region_offsets",
     "mk_kmap_build", "mk_kmap_info", "mk_kmap_export", "mk_kmap_destroy",
@@ -64,6 +64,7 @@ def load() -> ctypes.CDLL:
         "mk_coords_export": [P, P, P],
         "mk_coords_lookup": [P, P, i64, P, P],
         "mk_coords_labels": [P, P, P, i64, i64, i32, P, P],
+        "mk_coords_expand": [P, P, ctypes.POINTER(MkRegion), P, P, PP],
         "mk_coords_stride": [P, P, P, P, PP],
         "mk_region_offsets": [ctypes.POINTER(MkRegion), P, P],
         "mk_kmap_build": [P, P, P, ctypes.POINTER(MkRegion), i32, P, PP],

@@ -18,6 +18,7 @@
 
 #include <climits>
 #include <cstring>
+#include <vector>
 
 #include "mk_internal.cuh"
 
@@ -100,6 +101,28 @@ struct StrideSrc {  // u' = floor_div(u, s_out) * s_out per spatial axis (R7, R1
         int64_t q = u / s[d];
         if (q * s[d] != u && u < 0) q -= 1;
         const int64_t v = q * s[d];
+        if (v < INT32_MIN || v > INT32_MAX) return E_RANGE;
+        c[d] = v;
+      }
+    }
+    return pack_key(c, D, key_batch(in, D), k) ? E_NONE : E_RANGE;
+  }
+};
+
+struct ExpandSrc {  // f4: expanded row p = (input row p / K, offset p % K) -> u + i_k * s (R18)
+  const int4* keys;
+  const int32_t* offs;  // [K][D] device
+  int K, D;
+  int64_t s[4];
+  __device__ __forceinline__ uint32_t key(int64_t p, int4* k) const {
+    const int64_t r = p / K;
+    const int j = (int)(p - r * K);
+    const int4 in = keys[r];
+    int64_t c[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      if (d < D) {
+        const int64_t v = (int64_t)key_axis(in, D, d) + (int64_t)__ldg(offs + j * D + d) * s[d];
         if (v < INT32_MIN || v > INT32_MAX) return E_RANGE;
         c[d] = v;
       }
@@ -498,6 +521,50 @@ mk_status mk_coords_stride(mk_context* ctx, const mk_coords* in, const int32_t* 
   }
   for (int d = in->D; d < 4; ++d) src.s[d] = 1;
   return build_coords(ctx, src, in->n, in->D, ts, (cudaStream_t)stream, out, nullptr, nullptr);
+}
+
+mk_status mk_coords_expand(mk_context* ctx, const mk_coords* in, const mk_region* region,
+                           const int32_t* h_out_stride, void* stream, mk_coords** out) {
+  clear_error();
+  if (!ctx || !in || !region || !out) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_expand: null argument");
+  if (region->D != in->D) MK_FAIL(MK_ERR_DIMENSION_MISMATCH, "mk_coords_expand: region and coordinates differ in D");
+  std::vector<int32_t> offs;
+  int32_t K = 0;
+  mk_status st = region_enumerate(region, &offs, &K);
+  if (st != MK_OK) return st;
+  const int D = in->D;
+  ExpandSrc src;
+  src.keys = in->keys;
+  src.K = K;
+  src.D = D;
+  int32_t ts[4] = {1, 1, 1, 1};
+  for (int d = 0; d < 4; ++d) src.s[d] = 1;
+  for (int d = 0; d < D; ++d) {
+    ts[d] = h_out_stride ? h_out_stride[d] : in->tensor_stride[d];
+    if (ts[d] < 1) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_expand: output stride must be >= 1");
+    if (in->tensor_stride[d] % ts[d] != 0)
+      MK_FAIL(MK_ERR_STRIDE, "mk_coords_expand: the output stride must divide the input tensor stride");
+    src.s[d] = ts[d];
+  }
+  const int64_t n = in->n * (int64_t)K;
+  if (n > INT32_MAX) MK_FAIL(MK_ERR_UNSUPPORTED, "mk_coords_expand: more than 2^31 candidate rows");
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t* d_offs = (int32_t*)dev_alloc(ctx->alloc, sizeof(int32_t) * K * D, s);
+  int32_t* h = (int32_t*)pinned_stage(sizeof(int32_t) * K * D);
+  if (!d_offs || !h) {
+    if (d_offs) dev_free(ctx->alloc, d_offs, s);
+    MK_FAIL(MK_ERR_OUT_OF_MEMORY, "mk_coords_expand: allocation failed");
+  }
+  std::copy(offs.begin(), offs.end(), h);
+  if (cudaMemcpyAsync(d_offs, h, sizeof(int32_t) * K * D, cudaMemcpyHostToDevice, s) != cudaSuccess) {
+    dev_free(ctx->alloc, d_offs, s);
+    MK_FAIL(MK_ERR_CUDA, "mk_coords_expand: offset upload failed");
+  }
+  pinned_in_flight(s);
+  src.offs = d_offs;
+  st = build_coords(ctx, src, n, D, ts, s, out, nullptr, nullptr);
+  dev_free(ctx->alloc, d_offs, s);
+  return st;
 }
 
 mk_status mk_coords_info(const mk_coords* c, int64_t* n, int32_t* D, int32_t* h_tensor_stride) {

@@ -220,3 +220,35 @@ def test_labels_empty(mk):
     c, p2r, first = mk.coords_quantize(torch.zeros((0, 3), device="cuda"), 0.1)
     out = mk.coords_labels(p2r, first, torch.zeros(0, dtype=torch.int32, device="cuda"))
     assert out.numel() == 0
+
+
+@pytest.mark.parametrize("K", [2, 3])
+def test_expand_and_generative_transposed_conv(mk, orc, K):
+    # f4: generative output coordinates {u + i * s_f} of a stride-2 set, byte-identical
+    # to the oracle, then the transposed conv onto them against the fp64 oracle.
+    from gpu_util import FP32_TOL, assert_close
+    g = np.random.default_rng(40 + K)
+    rows = np.concatenate([g.integers(-40, 40, (20000, 3)), g.integers(0, 2, (20000, 1))], axis=1).astype(np.int32)
+    oc, _ = orc.create(rows)
+    fine = mk.coords_create(dev(oc))
+    coarse = mk.coords_stride(fine, [2, 2, 2])
+    region = mk.Region(mk.HYPERCUBE, 3, K)
+    up = mk.coords_expand(coarse, region, [1, 1, 1])
+    ocoarse = orc.stride(oc, [2, 2, 2])
+    offs = mk.region_offsets(region)
+    oup = orc.expand(ocoarse, offs, [1, 1, 1])
+    assert np.array_equal(up.export().cpu().numpy(), oup)
+    assert up.tensor_stride == [1, 1, 1]
+    m = mk.kmap_build(coarse, up, region, transposed=True)
+    km = csr_np(m)
+    okm = orc.kmap(ocoarse, oup, offs, [1, 1, 1], transposed=True)
+    for a, b in zip(km, okm):
+        assert np.array_equal(a, b)
+    Y = g.standard_normal((coarse.n, 32)).astype(np.float32)
+    W = (g.standard_normal((m.K, 16, 32)) * 0.1).astype(np.float32)
+    z = mk.conv_transpose_forward(m, dev(Y), dev(W)).cpu().numpy()
+    z64 = orc.conv_forward(okm, Y, W, up.n)
+    assert_close(z, z64, orc.conv_forward(okm, np.abs(Y), np.abs(W), up.n), FP32_TOL, "generative convT")
+    with pytest.raises(mk.MkError) as e:  # the output stride must divide the input stride
+        mk.coords_expand(coarse, region, [3, 3, 3])
+    assert e.value.name == "MK_ERR_STRIDE"
