@@ -578,6 +578,8 @@ struct WgradParams {
   const int32_t* out_idx;
   const int4* segs;          // (k, begin, end, slot), grouped by CTA
   const int32_t* seg_begin;  // [n_cta + 1]
+  const int64_t* ptr;        // [K + 1] device CSR offsets (device-side plan when segs == NULL)
+  int K;
   float* part;               // [n_slots][c_out][c_in]
   int c_out, c_in, halves;
   int mrows;                 // UMMA M: 64 when C_out <= 64 (no zero panel), else 128 per half
@@ -587,6 +589,30 @@ struct WgradParams {
 };
 
 constexpr int kPairsPerStage = 64;
+
+// Pairs per CTA of the weight-gradient split (the same rule as kmap_wplan's host plan):
+// L = 64 * ceil(ceil(P / n_cta) / 64), at least 64.
+__host__ __device__ __forceinline__ int64_t wgrad_range(int64_t P, int64_t n_cta) {
+  const int64_t per = (P > 0 ? P : 1) / n_cta + (((P > 0 ? P : 1) % n_cta) != 0);
+  const int64_t L = ((per + 63) / 64) * 64;
+  return L < 64 ? 64 : L;
+}
+
+// dW_k = sum of the partials of offset k's segments, in CTA order (deterministic).  With the
+// device plan, segment (c, k) sits in slot c + k and offset k spans CTAs ptr[k] / L ..
+// (ptr[k+1] - 1) / L.
+__global__ void k_reduce_partials_dev(const int64_t* __restrict__ ptr, int n_cta, const float* __restrict__ part,
+                                      int64_t tile_elems, float* __restrict__ dW) {
+  const int k = blockIdx.y;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= tile_elems) return;
+  const int64_t L = wgrad_range(__ldg(ptr + gridDim.y), n_cta);
+  const int64_t b = __ldg(ptr + k), en = __ldg(ptr + k + 1);
+  float s = 0.f;
+  if (b < en)
+    for (int64_t c = b / L; c <= (en - 1) / L; ++c) s += part[(c + k) * tile_elems + e];
+  dW[(int64_t)k * tile_elems + e] = s;
+}
 constexpr int kMaxSegs = kWgradMaxSegs + 1;  // per-CTA plan capacity (kmap_wplan cuts ranges to fit)
 
 // Weight gradient: split-K over the pairs.  Step g = 64 pairs of one segment (k, range) of
@@ -604,7 +630,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
   uint8_t* smem = align1024(smem_raw);
   int32_t* ibuf_all = (int32_t*)(smem + (size_t)p.sa * p.slot_bytes);  // [sa][2][2][64]
   int32_t* seg_g0 = ibuf_all + p.sa * 4 * PS;                          // [kMaxSegs + 1]
-  uint64_t* a_full = (uint64_t*)(seg_g0 + kMaxSegs + 2);
+  uint64_t* a_full =
+      (uint64_t*)(((uintptr_t)(seg_g0 + kMaxSegs + 2) + 15 + sizeof(int4) * kMaxSegs + 16 + 15) & ~(uintptr_t)15);
   uint64_t* a_empty = a_full + p.sa;
   uint64_t* tfull = a_empty + p.sa;
   uint64_t* tempty = tfull + 1;
@@ -613,14 +640,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
   const int rba = p.pwa * 2, rbb = p.pwb * 2;             // panel row bytes
   const int npa = p.c_out / p.pwa, npb = p.c_in / p.pwb;  // real panels
   const uint32_t panel_a = PS * rba, panel_b = PS * rbb;  // panel strides (LBO)
-  const int sb = p.seg_begin[blockIdx.x], se = min(p.seg_begin[blockIdx.x + 1], sb + kMaxSegs);
-  const int nseg = se - sb;
+  int4* s_segs = (int4*)(((uintptr_t)(seg_g0 + kMaxSegs + 2) + 15) & ~(uintptr_t)15);  // [kMaxSegs]
+  int* s_nseg = (int*)(s_segs + kMaxSegs);
 
-  if (warp == 0) {  // plan: first step of every segment
+  if (warp == 0) {  // plan: this CTA's segments and the first step of every segment
+    int nseg = 0;
+    if (p.segs) {  // host plan (kmap_wplan)
+      const int sb = p.seg_begin[blockIdx.x], se = min(p.seg_begin[blockIdx.x + 1], sb + kMaxSegs);
+      nseg = se - sb;
+      for (int i = lane; i < nseg; i += 32) s_segs[i] = p.segs[sb + i];
+    } else {  // device plan: CTA c takes pairs [c L, (c+1) L); segment (c, k) uses slot c + k
+      const int64_t P = __ldg(p.ptr + p.K), L = wgrad_range(P, gridDim.x);
+      const int64_t cb = (int64_t)blockIdx.x * L, ce = min(P, cb + L);
+      for (int k0 = 0; k0 < p.K; k0 += 32) {
+        const int k = k0 + lane;
+        int64_t b = 0, e = 0;
+        if (k < p.K) {
+          b = max(cb, __ldg(p.ptr + k));
+          e = min(ce, __ldg(p.ptr + k + 1));
+        }
+        const bool has = k < p.K && b < e;
+        const unsigned bal = __ballot_sync(0xffffffffu, has);
+        if (has) s_segs[nseg + __popc(bal & ((1u << lane) - 1u))] = make_int4(k, (int)b, (int)e, (int)blockIdx.x + k);
+        nseg += __popc(bal);
+      }
+    }
+    __syncwarp();
     int base = 0;
     for (int i0 = 0; i0 < nseg; i0 += 32) {
       const int i = i0 + lane;
-      const int4 sg = i < nseg ? p.segs[sb + i] : make_int4(0, 0, 0, 0);
+      const int4 sg = i < nseg ? s_segs[i] : make_int4(0, 0, 0, 0);
       const int st = i < nseg ? (sg.z - sg.y + PS - 1) / PS : 0;
       int incl = st;
 #pragma unroll
@@ -631,7 +680,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
       if (i < nseg) seg_g0[i] = base + incl - st;
       base += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (lane == 0) seg_g0[nseg] = base;
+    if (lane == 0) {
+      seg_g0[nseg] = base;
+      *s_nseg = nseg;
+    }
   }
   if (threadIdx.x == 32) {
     for (int s = 0; s < p.sa; ++s) {
@@ -657,6 +709,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
+  const int nseg = *s_nseg;
   const int n_steps = seg_g0[nseg];
   ACCT_DECL
 
@@ -666,7 +719,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
     int si = 0;
     auto locate = [&](int g, int* b0, int* e) {
       while (seg_g0[si + 1] <= g) ++si;
-      const int4 sg = p.segs[sb + si];
+      const int4 sg = s_segs[si];
       *b0 = sg.y + (g - seg_g0[si]) * PS;
       *e = sg.z;
     };
@@ -798,7 +851,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
     const int q = warp & 3;
     for (int i = 0; i < nseg; ++i) {
-      const int4 sg = p.segs[sb + i];
+      const int4 sg = s_segs[i];
       ACCT_WAIT(0, tfull, i & 1);
       tc_fence_after();
       for (int h = 0; h < p.halves; ++h) {
@@ -969,16 +1022,23 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
 
 mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, int c_out, const void* x, int c_in,
                             float* dW, cudaStream_t s) {
-  const mk_status pst = kmap_wplan(m, s);  // split-K plan (built once per map, on first use)
-  if (pst != MK_OK) return pst;
+  // K <= 63: the split-K plan is computed by the kernel from the device CSR offsets (no host
+  // read-back, fully asynchronous); larger K: the host plan caps the segments per CTA.
+  const bool dev_plan = m->K <= kWgradMaxSegs;
+  if (!dev_plan) {
+    const mk_status pst = kmap_wplan(m, s);  // built once per map, on first use
+    if (pst != MK_OK) return pst;
+  }
   const int64_t te = (int64_t)c_out * c_in;
   WgradParams p;
   p.g = (const __nv_bfloat16*)g;
   p.x = (const __nv_bfloat16*)x;
   p.in_idx = m->in_idx;
   p.out_idx = m->out_idx;
-  p.segs = m->wseg;
-  p.seg_begin = m->wseg_begin;
+  p.segs = dev_plan ? nullptr : m->wseg;
+  p.seg_begin = dev_plan ? nullptr : m->wseg_begin;
+  p.ptr = m->ptr;
+  p.K = m->K;
   p.c_out = c_out;
   p.c_in = c_in;
   p.pwa = c_out % 64 == 0 ? 64 : c_out % 32 == 0 ? 32 : 16;
@@ -989,25 +1049,43 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   p.a_bytes = (uint32_t)(p.halves * p.mrows) * kPairsPerStage * 2;  // M padded to 64 / 128 per half
   p.b_bytes = (uint32_t)c_in * kPairsPerStage * 2;
   p.slot_bytes = (p.a_bytes + p.b_bytes + 1023) & ~1023u;
-  const int reserve = 1024 + 1024 + kProdWarps * 4 * kPairsPerStage * 4 + (kMaxSegs + 2) * 4;
+  const int reserve = 1024 + 1024 + kProdWarps * 4 * kPairsPerStage * 4 + (kMaxSegs + 2) * 4 +
+                      (int)sizeof(int4) * kMaxSegs + 64;
   p.sa = std::min(kProdWarps, (kMaxSmem - reserve) / (int)p.slot_bytes);
   if (p.sa >= 8) p.sa -= p.sa % 4;
   p.ga = p.sa % 4 == 0 ? 4 : p.sa % 2 == 0 ? 2 : 1;
   p.tmem_cols = pow2_cols((uint32_t)(p.halves * c_in));
   if (p.sa < 2 || p.tmem_cols > 512) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: channel counts too large");
+  const int smem = p.sa * (int)p.slot_bytes + reserve;
   float* part = nullptr;
-  if (m->n_wslots > 0) {
-    part = (float*)dev_alloc(ctx->alloc, sizeof(float) * m->n_wslots * te, s);
-    if (!part) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 wgrad: workspace allocation failed");
-    p.part = part;
-    const int smem = p.sa * (int)p.slot_bytes + reserve;
-    set_smem_once(k_wgrad_umma, smem);
-    k_wgrad_umma<<<m->n_wcta, kThreads, smem, s>>>(p);
+  if (dev_plan) {
+    if (m->n_out > 0 && m->n_in > 0) {
+      const int n_cta = ctx->num_sms;
+      part = (float*)dev_alloc(ctx->alloc, sizeof(float) * (n_cta + m->K) * te, s);
+      if (!part) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 wgrad: workspace allocation failed");
+      p.part = part;
+      set_smem_once(k_wgrad_umma, smem);
+      k_wgrad_umma<<<n_cta, kThreads, smem, s>>>(p);
+      dim3 rg((unsigned)ceil_div(te, 256), (unsigned)m->K);
+      k_reduce_partials_dev<<<rg, 256, 0, s>>>(m->ptr, n_cta, part, te, dW);
+      g_launches += 2;
+    } else {
+      const cudaError_t z = cudaMemsetAsync(dW, 0, sizeof(float) * m->K * te, s);
+      if (z != cudaSuccess) MK_FAIL(MK_ERR_CUDA, "bf16 wgrad: memset failed");
+    }
+  } else {
+    if (m->n_wslots > 0) {
+      part = (float*)dev_alloc(ctx->alloc, sizeof(float) * m->n_wslots * te, s);
+      if (!part) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 wgrad: workspace allocation failed");
+      p.part = part;
+      set_smem_once(k_wgrad_umma, smem);
+      k_wgrad_umma<<<m->n_wcta, kThreads, smem, s>>>(p);
+      g_launches++;
+    }
+    dim3 rg((unsigned)ceil_div(te, 256), (unsigned)m->K);
+    k_reduce_partials<<<rg, 256, 0, s>>>(m->wslot_begin, part, te, dW);
     g_launches++;
   }
-  dim3 rg((unsigned)ceil_div(te, 256), (unsigned)m->K);
-  k_reduce_partials<<<rg, 256, 0, s>>>(m->wslot_begin, part, te, dW);
-  g_launches++;
   cudaError_t e = cudaGetLastError();
   if (part) dev_free(ctx->alloc, part, s);
   if (e != cudaSuccess) MK_FAIL(MK_ERR_CUDA, std::string("bf16 wgrad launch: ") + cudaGetErrorString(e));
