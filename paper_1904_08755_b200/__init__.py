@@ -221,6 +221,12 @@ class Region:
         self.offsets = None if offsets is None else np.ascontiguousarray(offsets, np.int32).reshape(-1, D)
 
     def _struct(self) -> _lib.MkRegion:
+        s = getattr(self, "_s", None)  # built once: a Region is not modified after construction
+        if s is None:
+            s = self._s = self._build_struct()
+        return s
+
+    def _build_struct(self) -> _lib.MkRegion:
         r = _lib.MkRegion()
         r.type, r.D, r.temporal_axis = self.kind, self.D, self.temporal_axis
         for d in range(self.D):

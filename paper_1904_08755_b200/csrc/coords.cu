@@ -410,6 +410,7 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
   int64_t* count = (int64_t*)(err + 1);
 
   cudaError_t e;
+  ht.mark("alloc");
   {
     // status[ntiles], ticket, count are contiguous 8-byte words from o_st; err follows.
     unsigned long long* small = (unsigned long long*)(sbase + o_st);
@@ -419,8 +420,10 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
     g_launches++;
   }
   if (n > 0) {
+    ht.mark("init");
     k_insert<Src><<<grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s>>>(src, n, c->table.buckets, first, nb - 1,
                                                                        slot_of, err);
+    ht.mark("insert");
     g_launches++;
     k_rank<Src><<<(int)ntiles, kBlock, 0, s>>>(src, n, first, slot_of, c->table.buckets, c->keys,
                                                  d_first, d_p2r, status, ticket, count);

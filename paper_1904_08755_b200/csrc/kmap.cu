@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstring>
+#include <deque>
 #include <map>
 
 #include "mk_internal.cuh"
@@ -387,6 +388,49 @@ __global__ void k_mirror_mask(const uint32_t* __restrict__ mask, int64_t ntiles,
     }
 }
 
+// Region enumeration + mirror indices, cached per thread by region description (the
+// offsets of a region never change; a layer stack rebuilds maps for the same regions).
+struct RegionInfo {
+  std::vector<int32_t> offs;    // [K][D]
+  int32_t K = 0;
+  std::vector<int32_t> mirror;  // [K] index of -offset_k or -1
+  bool closed = true;           // every offset's negation is in the set
+};
+
+mk_status region_info(const mk_region* r, const RegionInfo** out) {
+  std::vector<int32_t> key = {r->type, r->D, r->temporal_axis, r->n_offsets};
+  for (int d = 0; d < r->D && d < MK_MAX_REGION; ++d) {
+    key.push_back(r->size[d]);
+    key.push_back(r->dilation[d]);
+  }
+  if (r->type == MK_CUSTOM && r->offsets && r->n_offsets > 0)
+    key.insert(key.end(), r->offsets, r->offsets + (int64_t)r->n_offsets * r->D);
+  thread_local std::deque<std::pair<std::vector<int32_t>, RegionInfo>> cache;  // stable element addresses
+  for (auto& e : cache)
+    if (e.first == key) {
+      *out = &e.second;
+      return MK_OK;
+    }
+  RegionInfo ri;
+  mk_status st = region_enumerate(r, &ri.offs, &ri.K);
+  if (st != MK_OK) return st;
+  const int D = r->D, K = ri.K;
+  std::map<std::vector<int32_t>, int32_t> index;
+  for (int k = 0; k < K; ++k) index[std::vector<int32_t>(ri.offs.begin() + k * D, ri.offs.begin() + (k + 1) * D)] = k;
+  ri.mirror.assign(K, -1);
+  for (int k = 0; k < K; ++k) {
+    std::vector<int32_t> neg(D);
+    for (int d = 0; d < D; ++d) neg[d] = -ri.offs[k * D + d];
+    auto it = index.find(neg);
+    if (it == index.end()) ri.closed = false;
+    else ri.mirror[k] = it->second;
+  }
+  if (cache.size() >= 16) cache.pop_front();
+  cache.emplace_back(std::move(key), std::move(ri));
+  *out = &cache.back().second;
+  return MK_OK;
+}
+
 }  // namespace
 
 namespace {
@@ -500,11 +544,13 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   if (in->D != out->D || region->D != in->D)
     MK_FAIL(MK_ERR_DIMENSION_MISMATCH, "mk_kmap_build: input, output and region must have the same D");
   const int D = in->D;
-  std::vector<int32_t> offs;
-  int32_t K = 0;
-  mk_status st = region_enumerate(region, &offs, &K);
+  const RegionInfo* ri = nullptr;
+  mk_status st = region_info(region, &ri);
   if (st != MK_OK) return st;
+  const std::vector<int32_t>& offs = ri->offs;
+  const int32_t K = ri->K;
   if (K > 4096) MK_FAIL(MK_ERR_UNSUPPORTED, "mk_kmap_build: more than 4096 kernel offsets");
+  ht.mark("region");
 
   mk_kmap* m = new mk_kmap();
   m->alloc = ctx->alloc;
@@ -526,17 +572,8 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   const int sign = transposed ? -1 : 1;
 
   // mirror[k]: index of -offset_k (used to reuse nbr for dgrad on submanifold maps)
-  std::map<std::vector<int32_t>, int32_t> index;
-  for (int k = 0; k < K; ++k) index[std::vector<int32_t>(offs.begin() + k * D, offs.begin() + (k + 1) * D)] = k;
-  m->mirror.assign(K, -1);
-  bool symmetric = (in == out);
-  for (int k = 0; k < K; ++k) {
-    std::vector<int32_t> neg(D);
-    for (int d = 0; d < D; ++d) neg[d] = -offs[k * D + d];
-    auto it = index.find(neg);
-    if (it == index.end()) symmetric = false;
-    else m->mirror[k] = it->second;
-  }
+  m->mirror = ri->mirror;
+  const bool symmetric = (in == out) && ri->closed;
 
   const int64_t n_out = out->n, n_in = in->n;
   const int64_t ntiles = std::max<int64_t>(1, ceil_div(n_out, kTileRows));
@@ -576,27 +613,62 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     return fail(MK_ERR_OUT_OF_MEMORY, "mk_kmap_build: device allocation failed");
   };
 
-  int32_t* d_offs = (int32_t*)alloc(sizeof(int32_t) * (K * D + K));  // offsets, then mirror
-  m->d_mirror = d_offs ? d_offs + K * D : nullptr;
-  m->nbr = (int32_t*)alloc(sizeof(int32_t) * (int64_t)K * n_pad);
-  m->tile_mask = (uint32_t*)alloc(sizeof(uint32_t) * ntiles * mw);
-  m->tile_maskT = (uint32_t*)alloc(sizeof(uint32_t) * ntilesT * mw);
-  m->ptr = (int64_t*)alloc(sizeof(int64_t) * (K + 1));
-  if (!symmetric) m->nbrT = (int32_t*)alloc(sizeof(int32_t) * (int64_t)K * nT_pad);
-  int32_t* nbr_rm = rm ? (int32_t*)salloc(sizeof(int32_t) * n_pad * kRM) : nullptr;
-  int64_t* tile_off = (int64_t*)salloc(sizeof(int64_t) * K * ntiles);
-  int64_t* totals = (int64_t*)alloc(sizeof(int64_t) * K);  // persistent: lazy host read-back
+  ht.mark("mirror");
+  // Two device allocations per build: one persistent block (owned by the map) and one
+  // scratch block, carved into 256-byte aligned arrays.
+  struct Bump {
+    size_t off = 0;
+    size_t take(size_t b) {
+      const size_t o = off;
+      off += (b + 255) & ~size_t(255);
+      return o;
+    }
+  };
+  const bool sort_fwd = rm && n_out > 0, sort_bwd = rm && !symmetric && n_in > 0;
+  const int64_t ub_pairs = upper_bound ? (int64_t)K * n_out : 0;
+  Bump pb;
+  const size_t o_offs = pb.take(sizeof(int32_t) * (K * D + K)), o_nbr = pb.take(sizeof(int32_t) * K * n_pad),
+               o_tm = pb.take(sizeof(uint32_t) * ntiles * mw), o_tmT = pb.take(sizeof(uint32_t) * ntilesT * mw),
+               o_ptr = pb.take(sizeof(int64_t) * (K + 1)), o_tot = pb.take(sizeof(int64_t) * K),
+               o_nbrT = symmetric ? 0 : pb.take(sizeof(int32_t) * K * nT_pad),
+               o_in = upper_bound ? pb.take(sizeof(int32_t) * (ub_pairs + 4)) : 0,
+               o_out = upper_bound ? pb.take(sizeof(int32_t) * (ub_pairs + 4)) : 0,
+               o_perm = sort_fwd ? pb.take(sizeof(int32_t) * n_pad) : 0,
+               o_permT = sort_bwd ? pb.take(sizeof(int32_t) * nT_pad) : 0,
+               o_tabP = sort_bwd ? pb.take(sizeof(int32_t) * K * nT_pad) : 0;
+  Bump sbm;
+  const size_t o_rm = rm ? sbm.take(sizeof(int32_t) * n_pad * kRM) : 0,
+               o_toff = sbm.take(sizeof(int64_t) * K * ntiles), o_tcnt = sbm.take(sizeof(int32_t) * K * ntiles),
+               o_rowm = rm ? sbm.take(sizeof(uint32_t) * std::max<int64_t>(1, std::max(n_out, n_in))) : 0;
+  char* pbase = (char*)alloc(pb.off);
+  char* sbase = (char*)salloc(sbm.off);
+  if (!pbase || !sbase) return oom();
+  int32_t* d_offs = (int32_t*)(pbase + o_offs);  // offsets, then mirror
+  m->d_mirror = d_offs + K * D;
+  m->nbr = (int32_t*)(pbase + o_nbr);
+  m->tile_mask = (uint32_t*)(pbase + o_tm);
+  m->tile_maskT = (uint32_t*)(pbase + o_tmT);
+  m->ptr = (int64_t*)(pbase + o_ptr);
+  if (!symmetric) m->nbrT = (int32_t*)(pbase + o_nbrT);
+  int64_t* totals = (int64_t*)(pbase + o_tot);  // persistent: lazy host read-back
   m->d_totals = totals;
-  int32_t* tile_cnt = (int32_t*)salloc(sizeof(int32_t) * K * ntiles);
-  uint32_t* rowmask = rm ? (uint32_t*)salloc(sizeof(uint32_t) * std::max<int64_t>(1, std::max(n_out, n_in))) : nullptr;
-  if (!d_offs || !m->nbr || !m->tile_mask || !m->tile_maskT || !m->ptr || (!symmetric && !m->nbrT) ||
-      (rm && (!nbr_rm || !rowmask)) || !tile_off || !totals || !tile_cnt)
-    return oom();
+  if (upper_bound) {
+    m->in_idx = (int32_t*)(pbase + o_in);
+    m->out_idx = (int32_t*)(pbase + o_out);
+  }
+  if (sort_fwd) m->perm = (int32_t*)(pbase + o_perm);
+  int32_t* tabP = sort_bwd ? (int32_t*)(pbase + o_tabP) : nullptr;
+  if (sort_bwd) m->permT = (int32_t*)(pbase + o_permT);
+  int32_t* nbr_rm = rm ? (int32_t*)(sbase + o_rm) : nullptr;
+  int64_t* tile_off = (int64_t*)(sbase + o_toff);
+  int32_t* tile_cnt = (int32_t*)(sbase + o_tcnt);
+  uint32_t* rowmask = rm ? (uint32_t*)(sbase + o_rowm) : nullptr;
 
   cudaError_t e = cudaSuccess;
   auto ck = [&](cudaError_t r) {
     if (e == cudaSuccess) e = r;
   };
+  ht.mark("allocs");
   {  // one pinned H2D copy of the offsets and their mirror indices
     int32_t* h = (int32_t*)pinned_stage(sizeof(int32_t) * (K * D + K));
     if (!h) return oom();
@@ -662,9 +734,11 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     return fail(MK_ERR_UNSUPPORTED, "mk_kmap_build: more than 2^31 pairs");
   }
   // +4 entries of padding: the wgrad kernel reads 16-byte aligned supersets of ranges
-  m->in_idx = (int32_t*)alloc(sizeof(int32_t) * (pair_cap + 4));
-  m->out_idx = (int32_t*)alloc(sizeof(int32_t) * (pair_cap + 4));
-  if (!m->in_idx || !m->out_idx) return oom();
+  if (!upper_bound) {
+    m->in_idx = (int32_t*)alloc(sizeof(int32_t) * (pair_cap + 4));
+    m->out_idx = (int32_t*)alloc(sizeof(int32_t) * (pair_cap + 4));
+    if (!m->in_idx || !m->out_idx) return oom();
+  }
   if (n_out > 0) {
     const size_t smem = sizeof(int64_t) * (2 * K + 1) + sizeof(int32_t) * (4 * K + (rm ? kTileRows * kRMPitch : 0));
     if (rm)
@@ -694,9 +768,6 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
       k_rowmask_T<<<(unsigned)std::min<int64_t>(ceil_div(n_in, 256), 4096), 256, 0, s>>>(m->nbrT, nT_pad, n_in, K,
                                                                                         rowmask);
       g_launches++;
-      m->permT = (int32_t*)alloc(sizeof(int32_t) * nT_pad);
-      int32_t* tabP = (int32_t*)alloc(sizeof(int32_t) * (int64_t)K * nT_pad);
-      if (!m->permT || !tabP) return oom();
       st = radix_sort_perm(m->alloc, rowmask, n_in, K, m->permT, s);
       if (st == MK_OK) {
         k_permute_km<<<(unsigned)ntilesT, kTileRows, 0, s>>>(m->nbrT, nT_pad, n_in, K, m->permT, tabP, m->tile_maskT);
