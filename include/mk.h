@@ -215,6 +215,13 @@ mk_status mk_pool_backward(mk_context* ctx, const mk_kmap* m, int32_t mode, cons
                            int32_t C, mk_dtype dt, const int32_t* d_argmax, void* d_gin,
                            void* stream);
 
+/* Global pooling (every input maps to the origin of its batch): d_fout [n_batch][C]
+ * = sum (MK_POOL_SUM) or mean (MK_POOL_AVG) of the rows of `c` whose batch index is b; rows
+ * with b >= n_batch are ignored; a batch without rows gives 0.  Deterministic (fixed-order
+ * two-level reduction).  n_batch * C <= 51200.  Asynchronous. */
+mk_status mk_global_pool(mk_context* ctx, const mk_coords* c, int32_t mode, const void* d_fin,
+                         int32_t C, mk_dtype dt, int32_t n_batch, void* d_fout, void* stream);
+
 /* ---------------------------------------------------------------- convolution ------ */
 /* Generalized sparse convolution, Alg. 2:
  *   F_out[o] = sum over pairs (a, o) of offset k of W_k F_in[a];  rows without any pair

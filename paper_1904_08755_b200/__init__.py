@@ -391,3 +391,15 @@ def pool_backward(m: KernelMap, g_out: torch.Tensor, mode: int = POOL_MAX, argma
         _check(_L.mk_pool_backward(context(g.device.index), m._h, int(mode), _ptr(g), C, _dt(g), _ptr(argmax),
                                    _ptr(gi), _stream(g)), "mk_pool_backward")
     return gi
+
+
+def global_pool(c: Coords, f_in: torch.Tensor, n_batch: int, mode: int = POOL_AVG) -> torch.Tensor:
+    """Global pooling: [n_batch][C] sum / mean of the rows of each batch index."""
+    if f_in.shape[0] != c.n:
+        raise ValueError("global_pool: f_in must have one row per coordinate")
+    x = f_in.contiguous()
+    y = torch.empty((n_batch, x.shape[1]), dtype=x.dtype, device=x.device)
+    with _on_device(x.device):
+        _check(_L.mk_global_pool(context(x.device.index), c._h, int(mode), _ptr(x), x.shape[1], _dt(x), int(n_batch),
+                                 _ptr(y), _stream(x)), "mk_global_pool")
+    return y

@@ -174,3 +174,82 @@ mk_status mk_pool_backward(mk_context* ctx, const mk_kmap* m, int32_t mode, cons
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ global pooling
+// Global pooling ("the kernel map that maps all inputs to the origin"): one output
+// row per batch index b, the sum (or mean) of the rows whose batch is b.  Deterministic
+// two-level reduction: CTA j owns a contiguous range of rows and sums them in row order into
+// a shared [n_batch][C] accumulator (thread = channel, so every element has one writer),
+// then writes its partial; the partials are summed in CTA order.
+namespace mk {
+namespace {
+
+constexpr int kGpCtas = 296;
+
+__global__ void __launch_bounds__(256) k_global_partial(const int4* __restrict__ keys, int64_t n, int D,
+                                                        const void* __restrict__ x, int C, int bf16, int n_batch,
+                                                        float* __restrict__ part, int32_t* __restrict__ pcnt) {
+  extern __shared__ float s_acc[];  // [n_batch][C], then counts [n_batch]
+  int32_t* s_cnt = (int32_t*)(s_acc + (int64_t)n_batch * C);
+  for (int i = threadIdx.x; i < n_batch * C; i += blockDim.x) s_acc[i] = 0.f;
+  for (int i = threadIdx.x; i < n_batch; i += blockDim.x) s_cnt[i] = 0;
+  __syncthreads();
+  const int64_t per = (n + gridDim.x - 1) / gridDim.x;
+  const int64_t r0 = blockIdx.x * per, r1 = min(n, r0 + per);
+  for (int64_t r = r0; r < r1; ++r) {
+    const int b = key_batch(__ldg(keys + r), D);
+    if (b < 0 || b >= n_batch) continue;  // (uniform across the block)
+    for (int c = threadIdx.x; c < C; c += blockDim.x) s_acc[b * C + c] += ld_feat(x, r * C + c, bf16);
+    if (threadIdx.x == 0) ++s_cnt[b];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_batch * C; i += blockDim.x) part[(int64_t)blockIdx.x * n_batch * C + i] = s_acc[i];
+  for (int i = threadIdx.x; i < n_batch; i += blockDim.x) pcnt[(int64_t)blockIdx.x * n_batch + i] = s_cnt[i];
+}
+
+__global__ void k_global_reduce(const float* __restrict__ part, const int32_t* __restrict__ pcnt, int n_cta,
+                                int n_batch, int C, int avg, int bf16, void* __restrict__ y) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)n_batch * C) return;
+  const int b = (int)(i / C);
+  float s = 0.f;
+  int64_t cnt = 0;
+  for (int j = 0; j < n_cta; ++j) {
+    s += part[(int64_t)j * n_batch * C + i];
+    cnt += pcnt[(int64_t)j * n_batch + b];
+  }
+  if (avg && cnt > 0) s /= (float)cnt;
+  st_feat(y, i, s, bf16);
+}
+
+}  // namespace
+}  // namespace mk
+
+extern "C" mk_status mk_global_pool(mk_context* ctx, const mk_coords* c, int32_t mode, const void* d_fin, int32_t C,
+                                    mk_dtype dt, int32_t n_batch, void* d_fout, void* stream) {
+  using namespace mk;
+  clear_error();
+  if (!ctx || !c) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_global_pool: null argument");
+  if (mode != MK_POOL_AVG && mode != MK_POOL_SUM) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_global_pool: mode must be AVG or SUM");
+  if (C < 1 || n_batch < 0) MK_FAIL(MK_ERR_SHAPE_MISMATCH, "mk_global_pool: bad sizes");
+  if (dt != MK_F32 && dt != MK_BF16) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_global_pool: unknown dtype");
+  if (n_batch == 0) return MK_OK;
+  if (!d_fout || (c->n > 0 && !d_fin)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_global_pool: null features");
+  const size_t smem = sizeof(float) * (size_t)n_batch * C + sizeof(int32_t) * n_batch;
+  if (smem > 200 * 1024) MK_FAIL(MK_ERR_UNSUPPORTED, "mk_global_pool: n_batch * C above 51200");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int n_cta = kGpCtas;
+  char* ws = (char*)dev_alloc(ctx->alloc, sizeof(float) * (size_t)n_cta * n_batch * C + sizeof(int32_t) * n_cta * n_batch, s);
+  if (!ws) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "mk_global_pool: workspace allocation failed");
+  float* part = (float*)ws;
+  int32_t* pcnt = (int32_t*)(part + (size_t)n_cta * n_batch * C);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_global_partial, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_global_partial<<<n_cta, 256, smem, s>>>(c->keys, c->n, c->D, d_fin, C, dt == MK_BF16, n_batch, part, pcnt);
+  k_global_reduce<<<(unsigned)ceil_div((int64_t)n_batch * C, 256), 256, 0, s>>>(part, pcnt, n_cta, n_batch, C,
+                                                                               mode == MK_POOL_AVG, dt == MK_BF16, d_fout);
+  g_launches += 2;
+  const cudaError_t e = cudaGetLastError();
+  dev_free(ctx->alloc, ws, s);
+  if (e != cudaSuccess) MK_FAIL(MK_ERR_CUDA, std::string("mk_global_pool: ") + cudaGetErrorString(e));
+  return MK_OK;
+}

@@ -72,3 +72,25 @@ def test_pool_matches_oracle(mk, orc, dt, K, kind):
     y1, a1 = mk.pool_forward(m, X, mk.POOL_MAX)
     y2, a2 = mk.pool_forward(m, X, mk.POOL_MAX)
     assert torch.equal(y1, y2) and torch.equal(a1, a2)
+
+
+@pytest.mark.parametrize("dt", ["f32", "bf16"])
+def test_global_pool_matches_oracle(mk, orc, dt):
+    # P:222 global pooling: one row per batch index (sum / mean), vs the oracle's group-by
+    g = np.random.default_rng(21)
+    n = 30000
+    rows = np.concatenate([g.integers(-50, 50, (n, 3)), g.integers(0, 5, (n, 1))], axis=1).astype(np.int32)
+    oc, _ = orc.create(rows)
+    c = mk.coords_create(dev(oc))
+    tdt = torch.float32 if dt == "f32" else torch.bfloat16
+    X = dev(g.standard_normal((c.n, 48)).astype(np.float32)).to(tdt)
+    Xn = X.float().cpu().numpy()
+    tol = FP32_TOL if dt == "f32" else 1e-2
+    for mode in (1, 2):
+        y = mk.global_pool(c, X, 6, mode).float().cpu().numpy()  # batch 5 has no rows -> 0
+        y64 = orc.global_pool(oc[:, 3], Xn, 6, mode)
+        s64 = orc.global_pool(oc[:, 3], np.abs(Xn), 6, mode)
+        assert_close(y, y64, s64, tol, f"global mode {mode}")
+        assert np.all(y[5] == 0)
+        y2 = mk.global_pool(c, X, 6, mode).float().cpu().numpy()
+        assert np.array_equal(y, y2)  # deterministic
