@@ -11,7 +11,12 @@
  *    a cudaStream_t passed as void* (NULL = legacy default stream).  All device work is
  *    enqueued on that stream; the caller owns ordering with other streams.
  *  - Coordinates are int32 rows [n][D+1]: D spatial components, then the batch index
- *    (Eq. 1).  D is 1..4 on this implementation.  Batch indices are >= 0.
+ *    (Eq. 1).  D is 1..7 on this implementation.  Batch indices are >= 0.
+ *    A row is packed into one 128-bit key (reading R19): D <= 3 any int32 components;
+ *    D = 4: t in [-2^15, 2^15), batch <= 65534; D = 5..7 (e.g. the 7D space-time-chroma
+ *    lattice of the TS-CRF): axes 0-2 in [-2^19, 2^19), axes 3-5 in
+ *    [-2^11, 2^11), axis 6 in [-2^15, 2^15), batch <= 65534 for D = 7.  Rows outside
+ *    these ranges are COORD_RANGE errors.
  *  - Features are row-major [n][C] (row i = f_i^T, Eq. 1).  Weights are [K][C_out][C_in]
  *    row-major: the K matrices W_i of size N_out x N_in (R17).
  *  - Handles (mk_coords, mk_kmap) are immutable once created ("build then freeze",
@@ -39,7 +44,8 @@
 extern "C" {
 #endif
 
-#define MK_MAX_DIM 4        /* spatial dimensions supported on the GPU path (D <= 4) */
+#define MK_MAX_DIM 7        /* dimensions supported on the GPU path (D <= 7; see R19 for the
+                               component ranges of D = 4 and D = 5..7 packed keys) */
 #define MK_MAX_REGION 8     /* entries of mk_region.size / .dilation */
 
 typedef enum {
@@ -107,9 +113,8 @@ void mk_context_destroy(mk_context* ctx);
  *   d_point_to_row  device int32 [n] or NULL: row of each point's voxel
  *   d_first_point   device int32 [n] (capacity n) or NULL: first point of each row
  * Errors: NONFINITE_INPUT / COORD_RANGE / INVALID_ARGUMENT (negative batch) with the first
- * offending point row; for D = 4 COORD_RANGE also flags t outside [-2^15, 2^15) or a batch
- * index above 65534 (packed-key limit of this implementation).  n = 0 is
- * valid and yields an empty set. */
+ * offending point row; for D >= 4 COORD_RANGE also flags components or a batch index
+ * outside the packed-key ranges above (R19).  n = 0 is valid and yields an empty set. */
 mk_status mk_coords_quantize(mk_context* ctx, const float* d_points, const int32_t* d_batch,
                              int64_t n, int32_t D, float voxel, void* stream, mk_coords** out,
                              int32_t* d_point_to_row, int32_t* d_first_point);
@@ -119,8 +124,8 @@ mk_status mk_coords_quantize(mk_context* ctx, const float* d_points, const int32
  *   h_tensor_stride host int32 [D] or NULL (all 1): every spatial component must be a
  *                   multiple of it ("minimum distance between coordinates")
  *   d_inverse       device int32 [n] or NULL: row of each input row
- * Errors: STRIDE, INVALID_ARGUMENT (negative batch), COORD_RANGE (D = 4 packing) with the
- * first offending row. */
+ * Errors: STRIDE, INVALID_ARGUMENT (negative batch), COORD_RANGE (D >= 4 packing) with
+ * the first offending row. */
 mk_status mk_coords_create(mk_context* ctx, const int32_t* d_coords, int64_t n, int32_t D,
                            const int32_t* h_tensor_stride, void* stream, mk_coords** out,
                            int32_t* d_inverse);

@@ -63,6 +63,7 @@ def lib():
         L.orc_pool_forward.argtypes = [P, P, P, i32, P, i32, i64, i32, P, P]
         L.orc_pool_backward.argtypes = [P, P, P, i32, P, i32, i64, i32, P, P, i64]
         L.orc_global_pool.argtypes = [P, i64, P, i32, i32, i32, P]
+        L.orc_crf_infer.argtypes = [P, P, P, i32, P, i64, i32, P, i32, P]
         L.orc_kmap.argtypes = [P, i64, P, i64, i32, P, i32, P, i32, P, P, P]
         L.orc_conv_forward.argtypes = [P, P, P, i32, P, i32, P, P, i64, i32]
         L.orc_conv_forward_rows.argtypes = [P, P, P, i32, P, i32, P, i32, P, i64, P]
@@ -280,3 +281,14 @@ def global_pool(batch, f_in, n_batch: int, mode: int):
     y = np.zeros((max(n_batch, 1), x.shape[1]), np.float64)
     lib().orc_global_pool(_p(b), b.shape[0], _p(x), x.shape[1], n_batch, mode, _p(y))
     return y[:n_batch].copy()
+
+
+def crf_infer(kmap_csr, phi_u, W, n_iters: int):
+    """f3 (Alg. 5): mean-field TS-CRF inference over a (7D) kernel map, fp64."""
+    ptr, ins, outs = kmap_csr
+    phi = _c(phi_u, np.float64)
+    w = _c(W, np.float64)
+    n, C = phi.shape
+    q = np.zeros((max(n, 1), C), np.float64)
+    lib().orc_crf_infer(_p(ptr), _p(ins), _p(outs), len(ptr) - 1, _p(phi), n, C, _p(w), n_iters, _p(q))
+    return q[:n].copy()

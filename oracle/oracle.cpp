@@ -522,3 +522,31 @@ void orc_global_pool(const int32_t* batch, int64_t n, const double* f_in, int32_
       if (cnt[b] > 0)
         for (int32_t c = 0; c < C; ++c) f_out[(int64_t)b * C + c] /= static_cast<double>(cnt[b]);
 }
+
+// f3 — Alg. 5 written out: softmax of the unary logits, then N rounds of
+// "sparse conv of Q with phi_p, add phi_u, softmax".
+namespace {
+void softmax_rows(const double* a, const double* b, int64_t n, int32_t C, double* out) {
+  for (int64_t i = 0; i < n; ++i) {
+    double m = -1e300;
+    for (int32_t c = 0; c < C; ++c) m = std::max(m, a[i * C + c] + (b ? b[i * C + c] : 0.0));
+    double z = 0.0;
+    for (int32_t c = 0; c < C; ++c) {
+      out[i * C + c] = std::exp(a[i * C + c] + (b ? b[i * C + c] : 0.0) - m);
+      z += out[i * C + c];
+    }
+    for (int32_t c = 0; c < C; ++c) out[i * C + c] /= z;
+  }
+}
+}  // namespace
+
+void orc_crf_infer(const int64_t* ptr, const int32_t* in_idx, const int32_t* out_idx, int32_t K,
+                   const double* phi_u, int64_t n, int32_t C, const double* W, int32_t n_iters, double* q) {
+  std::vector<double> qt(static_cast<size_t>(n) * C), prev(static_cast<size_t>(n) * C);
+  softmax_rows(phi_u, nullptr, n, C, q);                                  // Q^0
+  for (int32_t it = 0; it < n_iters; ++it) {
+    std::copy(q, q + n * C, prev.begin());
+    orc_conv_forward(ptr, in_idx, out_idx, K, prev.data(), C, W, qt.data(), n, C);  // Q~^n
+    softmax_rows(phi_u, qt.data(), n, C, q);                              // Q^n
+  }
+}

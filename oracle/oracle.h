@@ -118,6 +118,14 @@ void orc_pool_backward(const int64_t* ptr, const int32_t* in_idx, const int32_t*
 void orc_global_pool(const int32_t* batch, int64_t n, const double* f_in, int32_t C, int32_t n_batch,
                      int32_t mode, double* f_out);
 
+/* f3 — mean-field inference of the TS-CRF (Alg. 5, Eq. 4): Q^0 = softmax(phi_u)
+ * (reading R25: the normalised form of Alg. 5's exp(phi_u)); for n = 1..N:
+ * Q~^n = generalized sparse conv of Q^(n-1) with the pairwise kernel phi_p = W [K][C][C]
+ * over the 7D kernel map (Eq. 4's sum over j in N^7(x_i) of phi_p(x_i, x_j) Q_j), then
+ * Q^n = softmax(phi_u + Q~^n) per node.  fp64. */
+void orc_crf_infer(const int64_t* ptr, const int32_t* in_idx, const int32_t* out_idx, int32_t K,
+                   const double* phi_u, int64_t n, int32_t C, const double* W, int32_t n_iters, double* q);
+
 #ifdef __cplusplus
 }
 #endif

@@ -104,7 +104,7 @@ class Coords:
         self._h = handle
         self.device = device
         n, D = ctypes.c_int64(), ctypes.c_int32()
-        ts = (ctypes.c_int32 * 4)()
+        ts = (ctypes.c_int32 * 8)()  # >= MK_MAX_DIM
         _check(_L.mk_coords_info(handle, ctypes.byref(n), ctypes.byref(D), ts), "mk_coords_info")
         self.n, self.D = int(n.value), int(D.value)
         self.tensor_stride = [int(ts[d]) for d in range(self.D)]

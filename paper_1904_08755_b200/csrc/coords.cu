@@ -43,10 +43,10 @@ struct QuantSrc {  // Alg. 1 line 1: C_p' <- floor(C_p / v_l)   (R6: fp32 divisi
   int D;
   float voxel;
   __device__ __forceinline__ uint32_t key(int64_t p, int4* k) const {
-    int64_t c[4] = {0, 0, 0, 0};
+    int64_t c[kMaxD] = {0, 0, 0, 0, 0, 0, 0};
     bool nonfinite = false, range = false;
 #pragma unroll
-    for (int d = 0; d < 4; ++d) {  // fully unrolled: c[] stays in registers
+    for (int d = 0; d < kMaxD; ++d) {  // fully unrolled: c[] stays in registers
       if (d < D) {
         const float x = pts[p * D + d];
         if (!isfinite(x)) {
@@ -69,12 +69,12 @@ struct QuantSrc {  // Alg. 1 line 1: C_p' <- floor(C_p / v_l)   (R6: fp32 divisi
 struct IntSrc {  // integer rows [n][D+1], batch last (Eq. 1); multiples of the tensor stride
   const int32_t* rows;
   int D;
-  int32_t ts[4];
+  int32_t ts[kMaxD];
   __device__ __forceinline__ uint32_t key(int64_t p, int4* k) const {
-    int64_t c[4] = {0, 0, 0, 0};
+    int64_t c[kMaxD] = {0, 0, 0, 0, 0, 0, 0};
     const int32_t* r = rows + p * (D + 1);
 #pragma unroll
-    for (int d = 0; d < 4; ++d) {
+    for (int d = 0; d < kMaxD; ++d) {
       if (d < D) {
         const int32_t v = r[d];
         if (v % ts[d] != 0) return E_STRIDE;
@@ -90,12 +90,12 @@ struct IntSrc {  // integer rows [n][D+1], batch last (Eq. 1); multiples of the 
 struct StrideSrc {  // u' = floor_div(u, s_out) * s_out per spatial axis (R7, R11)
   const int4* keys;
   int D;
-  int64_t s[4];
+  int64_t s[kMaxD];
   __device__ __forceinline__ uint32_t key(int64_t p, int4* k) const {
     const int4 in = keys[p];
-    int64_t c[4] = {0, 0, 0, 0};
+    int64_t c[kMaxD] = {0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-    for (int d = 0; d < 4; ++d) {
+    for (int d = 0; d < kMaxD; ++d) {
       if (d < D) {
         const int64_t u = key_axis(in, D, d);
         int64_t q = u / s[d];
@@ -113,14 +113,14 @@ struct ExpandSrc {  // f4: expanded row p = (input row p / K, offset p % K) -> u
   const int4* keys;
   const int32_t* offs;  // [K][D] device
   int K, D;
-  int64_t s[4];
+  int64_t s[kMaxD];
   __device__ __forceinline__ uint32_t key(int64_t p, int4* k) const {
     const int64_t r = p / K;
     const int j = (int)(p - r * K);
     const int4 in = keys[r];
-    int64_t c[4] = {0, 0, 0, 0};
+    int64_t c[kMaxD] = {0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-    for (int d = 0; d < 4; ++d) {
+    for (int d = 0; d < kMaxD; ++d) {
       if (d < D) {
         const int64_t v = (int64_t)key_axis(in, D, d) + (int64_t)__ldg(offs + j * D + d) * s[d];
         if (v < INT32_MIN || v > INT32_MAX) return E_RANGE;
@@ -323,9 +323,9 @@ __global__ void k_labels_mark(const int32_t* __restrict__ p2r, const int32_t* __
 __global__ void k_lookup(const int32_t* __restrict__ q, int64_t nq, int D, const int4* __restrict__ buckets,
                          uint32_t bmask, int32_t* __restrict__ rows) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t c[4] = {0, 0, 0, 0};
+    int64_t c[kMaxD] = {0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-    for (int d = 0; d < 4; ++d)
+    for (int d = 0; d < kMaxD; ++d)
       if (d < D) c[d] = q[i * (D + 1) + d];
     int4 k;
     rows[i] = pack_key(c, D, q[i * (D + 1) + D], &k) ? probe(buckets, bmask, k) : -1;
@@ -482,10 +482,10 @@ mk_status mk_coords_quantize(mk_context* ctx, const float* d_points, const int32
   clear_error();
   if (!ctx || !out || (n > 0 && !d_points)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_quantize: null argument");
   if (!valid_stream_dim(D)) MK_FAIL(D > MK_MAX_DIM ? MK_ERR_UNSUPPORTED : MK_ERR_INVALID_ARGUMENT,
-                                    "mk_coords_quantize: D must be in 1..4");
+                                    "mk_coords_quantize: D must be in 1..7");
   if (!(voxel > 0.0f) || !isfinite(voxel)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_quantize: voxel must be > 0");
   QuantSrc src{d_points, d_batch, D, voxel};
-  const int32_t ts[4] = {1, 1, 1, 1};
+  const int32_t ts[kMaxD] = {1, 1, 1, 1, 1, 1, 1};
   return build_coords(ctx, src, n, D, ts, (cudaStream_t)stream, out, d_point_to_row, d_first_point);
 }
 
@@ -494,16 +494,16 @@ mk_status mk_coords_create(mk_context* ctx, const int32_t* d_coords, int64_t n, 
   clear_error();
   if (!ctx || !out || (n > 0 && !d_coords)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_create: null argument");
   if (!valid_stream_dim(D)) MK_FAIL(D > MK_MAX_DIM ? MK_ERR_UNSUPPORTED : MK_ERR_INVALID_ARGUMENT,
-                                    "mk_coords_create: D must be in 1..4");
+                                    "mk_coords_create: D must be in 1..7");
   IntSrc src;
   src.rows = d_coords;
   src.D = D;
-  int32_t ts[4] = {1, 1, 1, 1};
+  int32_t ts[kMaxD] = {1, 1, 1, 1, 1, 1, 1};
   for (int d = 0; d < D; ++d) {
     ts[d] = h_tensor_stride ? h_tensor_stride[d] : 1;
     if (ts[d] < 1) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_create: tensor stride must be >= 1");
   }
-  for (int d = 0; d < 4; ++d) src.ts[d] = ts[d];
+  for (int d = 0; d < kMaxD; ++d) src.ts[d] = ts[d];
   return build_coords(ctx, src, n, D, ts, (cudaStream_t)stream, out, d_inverse, nullptr);
 }
 
@@ -514,7 +514,7 @@ mk_status mk_coords_stride(mk_context* ctx, const mk_coords* in, const int32_t* 
   StrideSrc src;
   src.keys = in->keys;
   src.D = in->D;
-  int32_t ts[4] = {1, 1, 1, 1};
+  int32_t ts[kMaxD] = {1, 1, 1, 1, 1, 1, 1};
   for (int d = 0; d < in->D; ++d) {
     if (h_conv_stride[d] < 1) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_stride: stride must be >= 1");
     const int64_t s = (int64_t)in->tensor_stride[d] * h_conv_stride[d];
@@ -522,7 +522,7 @@ mk_status mk_coords_stride(mk_context* ctx, const mk_coords* in, const int32_t* 
     ts[d] = (int32_t)s;
     src.s[d] = s;
   }
-  for (int d = in->D; d < 4; ++d) src.s[d] = 1;
+  for (int d = in->D; d < kMaxD; ++d) src.s[d] = 1;
   return build_coords(ctx, src, in->n, in->D, ts, (cudaStream_t)stream, out, nullptr, nullptr);
 }
 
@@ -540,8 +540,8 @@ mk_status mk_coords_expand(mk_context* ctx, const mk_coords* in, const mk_region
   src.keys = in->keys;
   src.K = K;
   src.D = D;
-  int32_t ts[4] = {1, 1, 1, 1};
-  for (int d = 0; d < 4; ++d) src.s[d] = 1;
+  int32_t ts[kMaxD] = {1, 1, 1, 1, 1, 1, 1};
+  for (int d = 0; d < kMaxD; ++d) src.s[d] = 1;
   for (int d = 0; d < D; ++d) {
     ts[d] = h_out_stride ? h_out_stride[d] : in->tensor_stride[d];
     if (ts[d] < 1) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_expand: output stride must be >= 1");

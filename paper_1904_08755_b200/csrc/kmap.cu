@@ -33,13 +33,16 @@ constexpr int kRMPitch = 33;  // smem pitch of a staged row (bank-conflict free)
 
 // u + sign * off * scale, per spatial axis, batch unchanged (R18).  False when the
 // shifted coordinate cannot exist (outside int32 or the packed-key domain).
-__device__ __forceinline__ bool shift_key(int4 u, int D, const int32_t* off, int sign, int4 scale, int4* q) {
-  int64_t c[4] = {0, 0, 0, 0};
-  const int32_t sc[4] = {scale.x, scale.y, scale.z, scale.w};
+struct Scale {  // offset scale per axis (the fine tensor stride, R14)
+  int32_t s[kMaxD];
+};
+
+__device__ __forceinline__ bool shift_key(int4 u, int D, const int32_t* off, int sign, const Scale& scale, int4* q) {
+  int64_t c[kMaxD] = {0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
-  for (int d = 0; d < 4; ++d) {  // fully unrolled: c[] and sc[] stay in registers
+  for (int d = 0; d < kMaxD; ++d) {  // fully unrolled: c[] stays in registers
     if (d < D) {
-      const int64_t v = (int64_t)key_axis(u, D, d) + (int64_t)sign * off[d] * sc[d];
+      const int64_t v = (int64_t)key_axis(u, D, d) + (int64_t)sign * off[d] * scale.s[d];
       if (v < INT32_MIN || v > INT32_MAX) return false;
       c[d] = v;
     }
@@ -66,7 +69,7 @@ template <bool RM>
 __global__ void __launch_bounds__(kThreads, 2) k_probe(const int4* __restrict__ okeys, int64_t n_out, int64_t n_pad,
                                                     const int4* __restrict__ buckets, uint32_t bmask,
                                                     const int32_t* __restrict__ offs, int K, int D, int sign,
-                                                    int4 scale4, int32_t* __restrict__ nbr,
+                                                    Scale scale4, int32_t* __restrict__ nbr,
                                                     int32_t* __restrict__ tile_cnt, int64_t ntiles,
                                                     uint32_t* __restrict__ tile_mask, int mw,
                                                     uint32_t* __restrict__ rowmask) {
@@ -84,12 +87,11 @@ __global__ void __launch_bounds__(kThreads, 2) k_probe(const int4* __restrict__ 
   // |delta| < 2^30; D = 4 packs t in 16 bits: |t| < 2^14 and |dt| < 2^14).
   for (int k = threadIdx.x; k < K; k += kThreads) {
     int64_t d[4] = {0, 0, 0, 0};
-    const int32_t sc[4] = {scale4.x, scale4.y, scale4.z, scale4.w};
-    bool fits = true;
+    bool fits = D <= 4;  // packed D = 5..7 keys always take the exact slow path
 #pragma unroll
     for (int a = 0; a < 4; ++a)
       if (a < D) {
-        d[a] = (int64_t)sign * s_off[k * D + a] * sc[a];
+        d[a] = (int64_t)sign * s_off[k * D + a] * scale4.s[a];
         fits &= (d[a] > -(1ll << 30) && d[a] < (1ll << 30)) && (a < 3 || (d[a] > -(1 << 14) && d[a] < (1 << 14)));
       }
     if (!fits) atomicOr(&s_slow, 1);
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_probe(const int4* __restrict__ 
   const int4 u = valid ? __ldg(okeys + o) : make_int4(0, 0, 0, 0);
   auto small = [](int32_t v, int32_t lim) { return v > -lim && v < lim; };
   // block-uniform: one row outside the fast-path range sends the whole tile down the slow path
-  const bool fast = __syncthreads_and(!s_slow && small(u.x, 1 << 30) && small(u.y, 1 << 30) &&
+  const bool fast = __syncthreads_and(!s_slow && D <= 4 && small(u.x, 1 << 30) && small(u.y, 1 << 30) &&
                                       small(u.z, 1 << 30) && (D < 4 || small(key_axis(u, D, 3), 1 << 14)));
   for (int kc = 0; kc < K; kc += kRM) {
     const int kn = min(kRM, K - kc);
@@ -568,7 +570,8 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   // Offsets scale with the fine tensor stride: the input's for a conv, the output's for a
   // transposed conv (R14).
   const int32_t* sc = transposed ? out->tensor_stride : in->tensor_stride;
-  const int4 scale4 = make_int4(sc[0], D > 1 ? sc[1] : 1, D > 2 ? sc[2] : 1, D > 3 ? sc[3] : 1);
+  Scale scale4;
+  for (int d = 0; d < kMaxD; ++d) scale4.s[d] = d < D ? sc[d] : 1;
   const int sign = transposed ? -1 : 1;
 
   // mirror[k]: index of -offset_k (used to reuse nbr for dgrad on submanifold maps)

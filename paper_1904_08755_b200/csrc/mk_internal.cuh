@@ -77,30 +77,61 @@ __host__ __device__ __forceinline__ bool key_eq(int4 a, int4 b) {
   return a.x == b.x && a.y == b.y && a.z == b.z && a.w == b.w;
 }
 
-// Spatial component d of a packed key.
+// Largest D of the GPU path and the packed-key layouts (one 128-bit key per row):
+//   D <= 3 : (u_0, u_1, u_2, b)                               missing axes 0
+//   D == 4 : (u_0, u_1, u_2, u_3 << 16 | b)                   u_3 in [-2^15, 2^15), b <= 65534
+//   D 5..7 : (u_0 << 12 | u_3, u_1 << 12 | u_4, u_2 << 12 | u_5, u_6 << 16 | b)
+//            u_0..u_2 in [-2^19, 2^19) (20 bits), u_3..u_5 in [-2^11, 2^11) (12 bits),
+//            u_6 in [-2^15, 2^15), b <= 65534 when D == 7 (else word 3 = b) — the 7D
+//            space-time-chroma lattice of the TS-CRF (3D space, 3D colour, time).
+constexpr int kMaxD = 7;
+
+// Component d of a packed key.
 __host__ __device__ __forceinline__ int32_t key_axis(int4 k, int D, int d) {
-  if (d == 0) return k.x;
-  if (d == 1) return k.y;
-  if (d == 2) return k.z;
-  return (int32_t)(int16_t)((uint32_t)k.w >> 16);  // d == 3, D == 4
+  const int32_t w = d == 0 ? k.x : d == 1 ? k.y : d == 2 ? k.z : k.w;
+  if (D <= 3) return w;
+  if (D == 4) return d < 3 ? w : (int32_t)(int16_t)((uint32_t)k.w >> 16);
+  if (d < 3) return w >> 12;                                       // arithmetic: 20-bit signed
+  if (d < 6) {
+    const int32_t v = d == 3 ? k.x : d == 4 ? k.y : k.z;
+    return (int32_t)((uint32_t)v << 20) >> 20;                      // 12-bit signed
+  }
+  return (int32_t)(int16_t)((uint32_t)k.w >> 16);                  // d == 6
 }
 __host__ __device__ __forceinline__ int32_t key_batch(int4 k, int D) {
-  return D == 4 ? (int32_t)((uint32_t)k.w & 0xFFFFu) : k.w;
+  return (D == 4 || D == 7) ? (int32_t)((uint32_t)k.w & 0xFFFFu) : k.w;
 }
-// Packs spatial components c[0..D) (int64, already range-checked by the caller for
-// int32) and batch b.  Returns false when D == 4 and the packed-key limits are violated.
+// Packs components c[0..D) (int64, already range-checked by the caller for int32) and
+// batch b.  Returns false when a component or b does not fit the layout above.
 __host__ __device__ __forceinline__ bool pack_key(const int64_t* c, int D, int64_t b, int4* out) {
   // c[] is indexed with compile-time constants only (keeps it in registers)
   int4 k;
-  k.x = D > 0 ? (int32_t)c[0] : 0;
-  k.y = D > 1 ? (int32_t)c[1] : 0;
-  k.z = D > 2 ? (int32_t)c[2] : 0;
-  if (D == 4) {
-    if (c[3] < -32768 || c[3] > 32767 || b < 0 || b > 65534) return false;
-    k.w = (int32_t)(((uint32_t)(uint16_t)(int16_t)c[3] << 16) | (uint32_t)b);
+  if (D <= 4) {
+    k.x = D > 0 ? (int32_t)c[0] : 0;
+    k.y = D > 1 ? (int32_t)c[1] : 0;
+    k.z = D > 2 ? (int32_t)c[2] : 0;
+    if (D == 4) {
+      if (c[3] < -32768 || c[3] > 32767 || b < 0 || b > 65534) return false;
+      k.w = (int32_t)(((uint32_t)(uint16_t)(int16_t)c[3] << 16) | (uint32_t)b);
+    } else {
+      if (b < 0 || b > INT32_MAX) return false;
+      k.w = (int32_t)b;
+    }
   } else {
-    if (b < 0 || b > INT32_MAX) return false;
-    k.w = (int32_t)b;
+    const int64_t hi = 1 << 19, lo = 1 << 11;
+    if (c[0] < -hi || c[0] >= hi || c[1] < -hi || c[1] >= hi || c[2] < -hi || c[2] >= hi) return false;
+    const int64_t c3 = c[3], c4 = c[4], c5 = D > 5 ? c[5] : 0, c6 = D > 6 ? c[6] : 0;
+    if (c3 < -lo || c3 >= lo || c4 < -lo || c4 >= lo || c5 < -lo || c5 >= lo) return false;
+    k.x = (int32_t)(((uint32_t)c[0] << 12) | ((uint32_t)c3 & 0xFFFu));
+    k.y = (int32_t)(((uint32_t)c[1] << 12) | ((uint32_t)c4 & 0xFFFu));
+    k.z = (int32_t)(((uint32_t)c[2] << 12) | ((uint32_t)c5 & 0xFFFu));
+    if (D == 7) {
+      if (c6 < -32768 || c6 > 32767 || b < 0 || b > 65534) return false;
+      k.w = (int32_t)(((uint32_t)(uint16_t)(int16_t)c6 << 16) | (uint32_t)b);
+    } else {
+      if (b < 0 || b > INT32_MAX) return false;
+      k.w = (int32_t)b;
+    }
   }
   *out = k;
   return true;
@@ -203,7 +234,7 @@ struct mk_coords {
   cudaStream_t stream = nullptr;  // stream the handle was created on (frees are ordered there)
   int64_t n = 0;
   int32_t D = 0;
-  int32_t tensor_stride[MK_MAX_DIM] = {1, 1, 1, 1};
+  int32_t tensor_stride[MK_MAX_DIM] = {1, 1, 1, 1, 1, 1, 1};
   int4* keys = nullptr;  // [n] packed rows, row order = first occurrence
   mk::Table table;
   std::vector<void*> owned;
