@@ -227,6 +227,17 @@ mk_status mk_pool_backward(mk_context* ctx, const mk_kmap* m, int32_t mode, cons
 mk_status mk_global_pool(mk_context* ctx, const mk_coords* c, int32_t mode, const void* d_fin,
                          int32_t C, mk_dtype dt, int32_t n_batch, void* d_fout, void* stream);
 
+/* ---------------------------------------------------------------- TS-CRF ----------- */
+/* Mean-field inference of the trilateral stationary CRF (Alg. 5, Eq. 4) over a
+ * map that connects a (typically 7D space-time-chroma, D = 7) coordinate set to itself
+ * (e.g. mk_kmap_build(c, c, hypercross 3^7 = 15 offsets)):
+ *   Q^0 = softmax(phi_u)  (R25);  for n = 1..n_iters:  Q^n = softmax(phi_u + conv(Q^(n-1); W))
+ * d_phi_u device fp32 [n][C] unary logits; d_W device fp32 [K][C][C] the pairwise kernel
+ * phi_p per offset (same layout as conv weights); d_q device fp32 [n][C] receives Q^N.
+ * fp32 throughout (exact-FFMA convolution).  Asynchronous. */
+mk_status mk_crf_infer(mk_context* ctx, const mk_kmap* m, const float* d_phi_u, const float* d_W,
+                       int32_t C, int32_t n_iters, float* d_q, void* stream);
+
 /* ---------------------------------------------------------------- convolution ------ */
 /* Generalized sparse convolution, Alg. 2:
  *   F_out[o] = sum over pairs (a, o) of offset k of W_k F_in[a];  rows without any pair

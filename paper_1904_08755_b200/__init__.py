@@ -403,3 +403,18 @@ def global_pool(c: Coords, f_in: torch.Tensor, n_batch: int, mode: int = POOL_AV
         _check(_L.mk_global_pool(context(x.device.index), c._h, int(mode), _ptr(x), x.shape[1], _dt(x), int(n_batch),
                                  _ptr(y), _stream(x)), "mk_global_pool")
     return y
+
+
+# ------------------------------------------------------------------------------ TS-CRF
+def crf_infer(m: KernelMap, phi_u: torch.Tensor, W: torch.Tensor, n_iters: int = 3) -> torch.Tensor:
+    """Mean-field TS-CRF inference (Alg. 5): Q^N over the map's node set; fp32."""
+    phi = _cuda(phi_u, torch.float32, "phi_u")
+    w = _cuda(W, torch.float32, "W")
+    n, C = phi.shape
+    if n != m.n_out or m.n_in != m.n_out or tuple(w.shape) != (m.K, C, C):
+        raise ValueError("crf_infer: phi_u [n][C] over the map's nodes and W [K][C][C] expected")
+    q = torch.empty_like(phi)
+    with _on_device(phi.device):
+        _check(_L.mk_crf_infer(context(phi.device.index), m._h, _ptr(phi), _ptr(w), C, int(n_iters), _ptr(q),
+                               _stream(phi)), "mk_crf_infer")
+    return q
