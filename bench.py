@@ -272,7 +272,8 @@ def run_mk(args, ws, rank, local):
     e2e_value = ws * flops_step / (e2e_ms / args.steps * 1e-3) / 1e12
 
     # ---- SURVEY §8(f) rows built so far, timed on the same scan (not part of the step):
-    #      f1 label reduction and f2 stride-2 2^3 max / average pooling (Alg. 3/4)
+    #      f1 label reduction, f2 stride-2 2^3 max / average pooling (Alg. 3/4),
+    #      f4 generative output coordinates + transposed conv, f3 TS-CRF (Alg. 5)
     def timed(fn, reps=20):
         fn()
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -297,11 +298,31 @@ def run_mk(args, ws, rank, local):
     t_pb = timed(lambda: mk.pool_backward(mp, Gp, mk.POOL_MAX, am))
     t_af = timed(lambda: mk.pool_forward(mp, X, mk.POOL_AVG, out=yp))
     pool_bytes = mp.n_in * C_IN * 2 + mp.n_out * C_IN * (2 + 4)  # x read, y + argmax written
+    # f4: generative upsampling of the stride-2 set back to stride 1 ({0,1}^3) + its convT
+    r2 = mk.Region(mk.HYPERCUBE, 3, 2)
+    t_exp = timed(lambda: mk.coords_expand(coarse, r2, [1, 1, 1]), reps=10)
+    up = mk.coords_expand(coarse, r2, [1, 1, 1])
+    mup = mk.kmap_build(coarse, up, r2, transposed=True)
+    Yc = torch.ones((coarse.n, C_IN), dtype=torch.bfloat16, device=dev)
+    Wt = torch.full((8, C_OUT, C_IN), 0.01, dtype=torch.bfloat16, device=dev)
+    t_gen = timed(lambda: mk.conv_transpose_forward(mup, Yc, Wt))
+    # f3: TS-CRF mean-field inference (3 iterations, 16 classes) on the scan lifted to 7D
+    #     (x, y, z, r, g, b, t) with a synthetic colour per 10 cm cell, 7D hypercross (15)
+    ck = cq.export()
+    col = (torch.div(ck[:, :3], 5, rounding_mode="floor") % 7).to(torch.int32)
+    c7rows = torch.cat([ck[:, :3], col, torch.zeros_like(ck[:, :1]), ck[:, 3:]], dim=1)
+    c7 = mk.coords_create(c7rows)
+    m7 = mk.kmap_build(c7, c7, mk.Region(mk.HYPERCROSS, 7, 3))
+    phi = torch.randn((c7.n, 16), device=dev)
+    W7 = torch.randn((15, 16, 16), device=dev) * 0.1
+    t_crf = timed(lambda: mk.crf_infer(m7, phi, W7, 3), reps=10)
     extras = {
         "labels_us": round(t_lab, 2), "labels_mpts": round(pts.shape[0] / t_lab, 1),
         "maxpool2_fwd_us": round(t_pf, 2), "maxpool2_bwd_us": round(t_pb, 2), "avgpool2_fwd_us": round(t_af, 2),
         "maxpool2_fwd_gbs": round(pool_bytes / (t_pf * 1e-6) / 1e9, 1),
         "pool_rows": [int(mp.n_in), int(mp.n_out)],
+        "expand_us": round(t_exp, 2), "generative_convT_us": round(t_gen, 2), "expand_rows": int(up.n),
+        "crf7d_3iter_us": round(t_crf, 2), "crf_nodes": int(c7.n), "crf_pairs": int(m7.n_pairs),
     }
 
     # ---- roofline of the dominant kernel (largest phase among the conv kernels / map build)
@@ -345,7 +366,7 @@ def run_mk(args, ws, rank, local):
         "e2e": {"value": round(e2e_value, 3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h), "ms_per_step": round(e2e_ms / args.steps, 4)},
         "gpu_launches": int(launches),
-        "extras_f1_f2": extras,
+        "extras_f1_f4": extras,
         "roofline": roof,
         "clocks": clocks,
     }
