@@ -215,6 +215,7 @@ struct FwdParams {
   int ga;  // stage slots released together by one tcgen05.commit (sa % ga == 0)
   int sw;  // W chunk slots (a ring: W_k chunks are prefetched several offsets ahead)
   int tb;  // tiles per CTA (one TMEM accumulator each: tb * c_y <= 512 columns)
+  int fold;  // tile order (see cta_tile)
   uint32_t a_bytes, b_bytes, tmem_cols;
 };
 
@@ -246,11 +247,24 @@ __device__ __forceinline__ int64_t cta_tile0(const FwdParams& p) {
   const int64_t nb = (p.ntiles + p.tb - 1) / p.tb;
   return (nb - 1 - (int64_t)blockIdx.x) * p.tb;
 }
+// i-th tile of this CTA, or -1.  fold = 0: tb adjacent tiles, heaviest batches first.
+// fold = 1: positions j = tb*blockIdx + i of the order 0, N-1, 1, N-2, ... (tiles taken from
+// both ends of the bitmask-sorted order, so every CTA gets a similar amount of work and the
+// grid is a single wave).
+__device__ __forceinline__ int64_t cta_tile(const FwdParams& p, int i) {
+  if (!p.fold) {
+    const int64_t t = cta_tile0(p) + i;
+    return t < p.ntiles ? t : -1;
+  }
+  const int64_t j = (int64_t)blockIdx.x * p.tb + i;
+  if (j >= p.ntiles) return -1;
+  return (j & 1) ? p.ntiles - 1 - (j >> 1) : (j >> 1);
+}
 
 __device__ void build_plan(const FwdParams& p, Plan* pl) {
   const int lane = threadIdx.x & 31;
-  const int64_t t0 = cta_tile0(p);
-  const int nt = (int)min((int64_t)p.tb, p.ntiles - t0);
+  int nt = 0;
+  while (nt < p.tb && cta_tile(p, nt) >= 0) ++nt;
   const int K = p.nb.K;
   const int rot = (int)(blockIdx.x % (unsigned)K);
   uint32_t act = 0;
@@ -261,7 +275,7 @@ __device__ void build_plan(const FwdParams& p, Plan* pl) {
     const int k = v < K ? (rot + v) % K : 0;
     uint32_t tw = 0;
     if (v < K)
-      for (int i = 0; i < nt; ++i) tw |= ((__ldg(p.nb.mask + (t0 + i) * p.nb.mw + (k >> 5)) >> (k & 31)) & 1u) << i;
+      for (int i = 0; i < nt; ++i) tw |= ((__ldg(p.nb.mask + cta_tile(p, i) * p.nb.mw + (k >> 5)) >> (k & 31)) & 1u) << i;
     act |= __reduce_or_sync(0xffffffffu, tw);
     const bool has = tw != 0;
     const unsigned bal = __ballot_sync(0xffffffffu, has);
@@ -353,7 +367,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
       *c = q - j * p.nch;
       uint32_t tw = pl->tw[u];
       for (int t = 0; t < j; ++t) tw &= tw - 1;
-      *tile = tile0 + (__ffs(tw) - 1);
+      *tile = cta_tile(p, __ffs(tw) - 1);
       *k = pl->k[u];
     };
     auto fetch_idx = [&](int g, int buf) {
@@ -515,8 +529,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
     }
     const uint32_t act = pl->active_tiles;
     for (int i = 0; i < p.tb; ++i) {
-      const int64_t tile = tile0 + i;
-      if (tile >= p.ntiles) break;
+      const int64_t tile = cta_tile(p, i);
+      if (tile < 0) break;
       const int64_t pos = tile * kTileM + q * 32 + lane;  // position in the map's row order
       const bool valid = pos < p.n_rows;
       const int64_t row = valid ? p.nb.row_of(pos) : 0;
@@ -972,7 +986,12 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   // Two tiles per CTA (one TMEM accumulator each, <= 256 columns so two CTAs share an SM);
   // smem ~100 KB per CTA: 4 A stages (16 KB each at CH=64), a ring of 4 W chunks, per-warp
   // index buffers and the plan (B200 gathers ~9 TB/s at 8 warps/SM, ubench_gather.cu).
-  p.tb = std::max(1, std::min(2, 256 / c_y));
+  static const int env_fold = [] {  // default: 2 tiles per CTA, folded order (measured best)
+    const char* e = std::getenv("MK_FWD_FOLD");
+    return e ? std::atoi(e) : 2;
+  }();
+  p.fold = env_fold > 0 ? 1 : 0;
+  p.tb = p.fold ? std::max(1, std::min(env_fold, 256 / c_y)) : std::max(1, std::min(2, 256 / c_y));
   p.tmem_cols = pow2_cols((uint32_t)(p.tb * c_y));
   const int base = 1024 + 512 + kFwdProd * 3 * kTileM * 4 + (int)sizeof(Plan);
   p.sw = nch * 2;
