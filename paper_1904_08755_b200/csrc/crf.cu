@@ -4,8 +4,9 @@
 //   for n = 1..N:  Q~^n = generalized sparse conv(Q^(n-1); phi_p)   (the pairwise sum of
 //                  Eq. 4 is a 7D sparse convolution because phi_p is stationary)
 //                  Q^n  = softmax(phi_u + Q~^n)
-// The convolution is the exact-FFMA fp32 kernel of conv_simt.cu (channels = classes: tiny
-// dense products, memory bound); the softmax is one warp per node.
+// C <= 32 classes: one fused kernel per step (gather of the neighbours' Q rows, the C x C
+// products from shared-memory W, softmax across the node's lane group); larger C: the
+// exact-FFMA fp32 conv of conv_simt.cu followed by a warp-per-node softmax.
 #include "conv.cuh"
 
 namespace mk {
@@ -40,6 +41,65 @@ __global__ void __launch_bounds__(256) k_crf_softmax(const float* __restrict__ p
   }
 }
 
+// One fused mean-field step for C <= 32 classes: Q_out[o] = softmax(phi[o] + sum_k W_k Q_in[a_k])
+// over the pairs (a_k, o) of the map (Eq. 4).  A group of Cp = pow2(C) lanes owns one node
+// (32 / Cp nodes per warp); lane j computes class j: the neighbour indices are broadcast
+// within the group, the neighbour's Q row is spread over the group and broadcast one class
+// at a time.  W lives in shared memory.  Fixed summation order (k, then c): deterministic.
+__global__ void __launch_bounds__(256) k_crf_step(NbrView nb, int64_t n_rows, const float* __restrict__ phi,
+                                                  const float* __restrict__ q_in, const float* __restrict__ W, int C,
+                                                  int Cp, float* __restrict__ q_out) {
+  extern __shared__ float s_w[];  // [K][c][j] = W[k][j][c] (lanes j read consecutive words)
+  for (int i = threadIdx.x; i < nb.K * C * C; i += blockDim.x) {
+    const int k = i / (C * C), r = i - k * C * C, jj = r / C, c = r - jj * C;
+    s_w[(k * C + c) * C + jj] = W[i];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, j = lane & (Cp - 1);
+  const int per_warp = 32 / Cp;
+  float* s_q = s_w + nb.K * C * C + (threadIdx.x & ~(Cp - 1)) * Cp;  // [Cp offsets][Cp classes]
+  const int gsh = lane & ~(Cp - 1);
+  const unsigned lowmask = Cp == 32 ? 0xffffffffu : ((1u << Cp) - 1u);
+  // grid-stride over node groups (W is staged once per block)
+  const int64_t n_groups = (n_rows + per_warp - 1) / per_warp;
+  for (int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); gw < n_groups;
+       gw += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+    const int64_t pos = gw * per_warp + (lane / Cp);
+    const bool valid = pos < n_rows;
+    float acc = 0.f;
+    // The neighbours' Q rows of the node are staged in shared memory first (independent
+    // loads), then lane j forms sum_k sum_c W_k[j][c] Q_k[c] from broadcast reads.
+    for (int k0 = 0; k0 < nb.K; k0 += Cp) {
+      const int32_t mine = valid && k0 + j < nb.K ? nb.at(k0 + j, pos) : -1;
+      const unsigned present = (__ballot_sync(0xffffffffu, mine >= 0) >> gsh) & lowmask;
+#pragma unroll 8
+      for (int kk = 0; kk < Cp; ++kk) {
+        const int32_t a = __shfl_sync(0xffffffffu, mine, kk, Cp);
+        s_q[kk * Cp + j] = (a >= 0 && j < C) ? __ldg(q_in + (int64_t)a * C + j) : 0.f;
+      }
+      __syncwarp();
+      for (unsigned pr = present; pr; pr &= pr - 1) {
+        const int kk = __ffs(pr) - 1;
+        const float* wk = s_w + (k0 + kk) * C * C + min(j, C - 1);
+        const float* qk = s_q + kk * Cp;
+        float t = 0.f;
+        for (int c = 0; c < C; ++c) t = fmaf(wk[c * C], qk[c], t);
+        acc += t;
+      }
+      __syncwarp();
+    }
+    // softmax over the group's C classes
+    const int64_t o = valid ? nb.row_of(pos) : 0;
+    const float v = (valid && j < C) ? __ldg(phi + o * C + j) + acc : -INFINITY;
+    float m = v;
+    for (int w = Cp / 2; w > 0; w >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, w, Cp));
+    const float e = (valid && j < C) ? expf(v - m) : 0.f;
+    float z = e;
+    for (int w = Cp / 2; w > 0; w >>= 1) z += __shfl_xor_sync(0xffffffffu, z, w, Cp);
+    if (valid && j < C) q_out[o * C + j] = e / z;
+  }
+}
+
 }  // namespace
 }  // namespace mk
 
@@ -64,6 +124,26 @@ extern "C" mk_status mk_crf_infer(mk_context* ctx, const mk_kmap* m, const float
   if (!qt) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "mk_crf_infer: workspace allocation failed");
   const NbrView v = forward_view(m);
   mk_status st = MK_OK;
+  if (C <= 32 && (v.K * C * C + 256 * 32) * (int)sizeof(float) <= 48 * 1024) {
+    // fused steps (conv + softmax in one kernel); ping-pong between d_q and the workspace
+    int Cp = 1;
+    while (Cp < C) Cp <<= 1;
+    const int64_t groups = ceil_div(n, 32 / Cp);
+    const unsigned g2 = (unsigned)std::min<int64_t>(ceil_div(groups, 8), 6 * ctx->num_sms);
+    float* bufs[2] = {d_q, qt};
+    for (int it = 0; it < n_iters; ++it) {
+      const float* src = bufs[it & 1];
+      float* dst = bufs[(it + 1) & 1];
+      k_crf_step<<<g2, 256, sizeof(float) * (v.K * C * C + 256 * Cp), s>>>(v, n, d_phi_u, src, d_W, C, Cp, dst);
+      g_launches++;
+    }
+    cudaError_t e2 = cudaSuccess;
+    if (n_iters & 1) e2 = cudaMemcpyAsync(d_q, qt, sizeof(float) * n * C, cudaMemcpyDeviceToDevice, s);
+    const cudaError_t e = e2 == cudaSuccess ? cudaGetLastError() : e2;
+    dev_free(ctx->alloc, qt, s);
+    if (e != cudaSuccess) MK_FAIL(MK_ERR_CUDA, std::string("mk_crf_infer: ") + cudaGetErrorString(e));
+    return MK_OK;
+  }
   for (int it = 0; it < n_iters && st == MK_OK; ++it) {
     st = launch_conv_f32(v, d_q, C, d_W, C, C, qt, C, MK_F32, n, false, s);  // Q~^n
     if (st == MK_OK) {
