@@ -104,6 +104,15 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
+def step_config(N, M, n_points, seed, ws):
+    """The `config` of the bench line (shared by the GPU arm and the --impl reference arm)."""
+    return {"workload": "configs[1]: ScanNet-shaped room, 2 cm voxels, 3x3x3 hypercube, C 64->64, "
+                        "quantize + hash + kernel map + fwd + dgrad + wgrad",
+            "voxels_per_gpu": int(N), "pairs_per_gpu": int(M), "points_per_gpu": int(n_points),
+            "seed": seed, "parallelism": f"batch-index dp{ws}",
+            "l2": "flushed before every timed step (256 MiB write, outside the step events)"}
+
+
 def workload(seed):
     import synthetic
     pts = synthetic.room_points(seed)
@@ -354,11 +363,7 @@ def run_mk(args, ws, rank, local):
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": "configs[1]: ScanNet-shaped room, 2 cm voxels, 3x3x3 hypercube, C 64->64, "
-                               "quantize + hash + kernel map + fwd + dgrad + wgrad",
-                   "voxels_per_gpu": N, "pairs_per_gpu": M, "points_per_gpu": int(pts_h.shape[0]),
-                   "seed": args.seed, "parallelism": f"batch-index dp{ws}",
-                   "l2": "flushed before every timed step (256 MiB write, outside the step events)"},
+        "config": step_config(N, M, int(pts_h.shape[0]), args.seed, ws),
         "phases_us": phases,
         "conv_tflops": round(flops_step / ((mean_ph[2] + mean_ph[3] + mean_ph[4]) * 1e-3) / 1e12, 3),
         "kmap_mpts": round(N / (mean_ph[1] * 1e-3) / 1e6, 2),
@@ -429,10 +434,14 @@ def run_reference(args, ws, rank):
         flops += f
         secs += s
     v = flops / secs / 1e12
+    import oracle
+    import synthetic
+    coords, _, _ = oracle.quantize(pts_h, synthetic.ROOM_VOXEL)
+    ptr, _, _ = oracle.kmap(coords, coords, oracle.region(0, 3, [3, 3, 3]))
     out = {"impl": "reference", "metric": METRIC, "value": round(v, 6), "unit": UNIT, "n_gpus": ws,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(secs / args.steps * 1e3, 3),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": "configs[1] (bounded sample per step, see cpu_baseline.sample)"},
+           "config": step_config(coords.shape[0], int(ptr[-1]), pts_h.shape[0], args.seed, ws),
            "cpu_baseline": {"value": round(v, 6), "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
            "e2e": {"value": round(v, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
