@@ -85,6 +85,14 @@ void pinned_in_flight(cudaStream_t s) {
 double HostTimer::now() {
   return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("MK_NO_PDL");
+    return !(v && v[0] && v[0] != '0');
+  }();
+  return on;
+}
+
 HostTimer::HostTimer(const char* nm) : name(nm) {
   static const bool enabled = std::getenv("MK_HOST_TIMING") != nullptr;
   on = enabled;

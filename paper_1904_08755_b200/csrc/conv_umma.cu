@@ -64,6 +64,7 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 //   dgrad  : B(n, kx) = W[k][kx][n]   (n = c_in,  kx = c_out)  i.e. W_k^T
 __global__ void k_pack_w(const __nv_bfloat16* __restrict__ W, int K, int c_out, int c_in, int trans, int CH,
                          uint8_t* __restrict__ out) {
+  pdl_enter();
   const int c_y = trans ? c_in : c_out, c_x = trans ? c_out : c_in;
   const int nch = c_x / CH, J = CH / 8, RB = CH * 2;
   const int64_t total = (int64_t)K * nch * c_y * J;
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tile0 = cta_tile0(p);
 
-  if (warp == 0) build_plan(p, pl);
+  // prologue that touches no global memory overlaps the predecessor kernel (PDL)
   if (threadIdx.x == 32) {
     for (int s = 0; s < p.sa; ++s) mbar_init(a_full + s, 32);  // one cp.async arrival per lane
     for (int j = 0; j < kNCB; ++j) mbar_init(cb + j, 1);
@@ -331,6 +332,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
     fence_mbar_init();
   }
   if (warp == kFwdMma) tmem_alloc_dyn(tmem_slot, p.tmem_cols);
+  pdl_enter();
+  if (warp == 0) build_plan(p, pl);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -617,6 +620,7 @@ __host__ __device__ __forceinline__ int64_t wgrad_range(int64_t P, int64_t n_cta
 // (ptr[k+1] - 1) / L.
 __global__ void k_reduce_partials_dev(const int64_t* __restrict__ ptr, int n_cta, const float* __restrict__ part,
                                       int64_t tile_elems, float* __restrict__ dW) {
+  pdl_enter();
   const int k = blockIdx.y;
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= tile_elems) return;
@@ -657,6 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constan
   int4* s_segs = (int4*)(((uintptr_t)(seg_g0 + kMaxSegs + 2) + 15) & ~(uintptr_t)15);  // [kMaxSegs]
   int* s_nseg = (int*)(s_segs + kMaxSegs);
 
+  pdl_enter();
   if (warp == 0) {  // plan: this CTA's segments and the first step of every segment
     int nseg = 0;
     if (p.segs) {  // host plan (kmap_wplan)
@@ -1016,24 +1021,23 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   {
     const int64_t chunks = (int64_t)nb.K * nch * c_y * (CH / 8);
     const int grid = (int)std::min<int64_t>(ceil_div(chunks, 256), 4 * ctx->num_sms);
-    k_pack_w<<<grid, 256, 0, s>>>((const __nv_bfloat16*)W, nb.K, c_out_w, c_in_w, trans ? 1 : 0, CH, wpack);
-    g_launches++;
+    pdl_launch(k_pack_w, grid, 256, 0, s, (const __nv_bfloat16*)W, nb.K, c_out_w, c_in_w, trans ? 1 : 0, CH, wpack);
   }
   p.wpack = wpack;
   const int smem = fixed + p.sa * (int)p.a_bytes;
   const int64_t grid = ceil_div(p.ntiles, p.tb);  // one CTA per tb adjacent tiles
+  cudaError_t e;
   if (CH == 64) {
     set_smem_once(k_conv_umma<64>, smem);
-    k_conv_umma<64><<<(unsigned)grid, kFwdThreads, smem, s>>>(p);
+    e = pdl_launch(k_conv_umma<64>, (unsigned)grid, kFwdThreads, smem, s, p);
   } else if (CH == 32) {
     set_smem_once(k_conv_umma<32>, smem);
-    k_conv_umma<32><<<(unsigned)grid, kFwdThreads, smem, s>>>(p);
+    e = pdl_launch(k_conv_umma<32>, (unsigned)grid, kFwdThreads, smem, s, p);
   } else {
     set_smem_once(k_conv_umma<16>, smem);
-    k_conv_umma<16><<<(unsigned)grid, kFwdThreads, smem, s>>>(p);
+    e = pdl_launch(k_conv_umma<16>, (unsigned)grid, kFwdThreads, smem, s, p);
   }
-  g_launches++;
-  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaGetLastError();
   dev_free(ctx->alloc, wpack, s);
   if (e != cudaSuccess) MK_FAIL(MK_ERR_CUDA, std::string("bf16 conv launch: ") + cudaGetErrorString(e));
   return MK_OK;
@@ -1084,10 +1088,9 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
       if (!part) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 wgrad: workspace allocation failed");
       p.part = part;
       set_smem_once(k_wgrad_umma, smem);
-      k_wgrad_umma<<<n_cta, kThreads, smem, s>>>(p);
+      pdl_launch(k_wgrad_umma, n_cta, kThreads, smem, s, p);
       dim3 rg((unsigned)ceil_div(te, 256), (unsigned)m->K);
-      k_reduce_partials_dev<<<rg, 256, 0, s>>>(m->ptr, n_cta, part, te, dW);
-      g_launches += 2;
+      pdl_launch(k_reduce_partials_dev, rg, 256, 0, s, (const int64_t*)m->ptr, n_cta, (const float*)part, te, dW);
     } else {
       const cudaError_t z = cudaMemsetAsync(dW, 0, sizeof(float) * m->K * te, s);
       if (z != cudaSuccess) MK_FAIL(MK_ERR_CUDA, "bf16 wgrad: memset failed");
@@ -1098,8 +1101,7 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
       if (!part) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 wgrad: workspace allocation failed");
       p.part = part;
       set_smem_once(k_wgrad_umma, smem);
-      k_wgrad_umma<<<m->n_wcta, kThreads, smem, s>>>(p);
-      g_launches++;
+      pdl_launch(k_wgrad_umma, m->n_wcta, kThreads, smem, s, p);
     }
     dim3 rg((unsigned)ceil_div(te, 256), (unsigned)m->K);
     k_reduce_partials<<<rg, 256, 0, s>>>(m->wslot_begin, part, te, dW);

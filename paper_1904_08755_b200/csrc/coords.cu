@@ -136,6 +136,7 @@ template <class Src>
 __global__ void __launch_bounds__(kBlock) k_insert(Src src, int64_t n, int4* __restrict__ buckets,
                                                    int32_t* __restrict__ first, uint32_t bmask,
                                                    int32_t* __restrict__ slot_of, unsigned long long* err) {
+  pdl_enter();
   // Claim-or-find in one 128-bit atomicCAS of the key itself (sm_90+): the slot is ours or
   // already holds the key -> record the smallest point index of the key (atomicMin).
   const unsigned __int128 kEmpty = ~(unsigned __int128)0;
@@ -209,6 +210,7 @@ __global__ void __launch_bounds__(kBlock) k_rank(Src src, int64_t n, const int32
                                                  int32_t* __restrict__ p2r,
                                                  unsigned long long* status, unsigned int* ticket,
                                                  int64_t* count) {
+  pdl_enter();
   __shared__ int64_t s_tile;
   __shared__ int32_t s_warp[kBlock / 32];
   __shared__ int64_t s_prefix;
@@ -289,6 +291,7 @@ __global__ void __launch_bounds__(kBlock) k_rank(Src src, int64_t n, const int32
 // error word to all ones.
 __global__ void k_init(int4* __restrict__ buckets, int32_t* __restrict__ first, uint32_t nb,
                        unsigned long long* __restrict__ small, int64_t n_small, unsigned long long* err) {
+  pdl_enter();
   const int4 e = make_int4(-1, -1, -1, -1);
   const int64_t words = (int64_t)nb * 4, slots = (int64_t)nb * kSlotsPerBucket;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x) {
@@ -415,19 +418,16 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
     // status[ntiles], ticket, count are contiguous 8-byte words from o_st; err follows.
     unsigned long long* small = (unsigned long long*)(sbase + o_st);
     const int64_t n_small = (int64_t)((o_er - o_st) / 8);
-    k_init<<<grid_for(std::max<int64_t>((int64_t)nb * 4, n_small), 256, ctx->num_sms), 256, 0, s>>>(
-        c->table.buckets, first, nb, small, n_small, err);
-    g_launches++;
+    pdl_launch(k_init, grid_for(std::max<int64_t>((int64_t)nb * 4, n_small), 256, ctx->num_sms), 256, 0, s,
+               c->table.buckets, first, nb, small, n_small, err);
   }
   if (n > 0) {
     ht.mark("init");
-    k_insert<Src><<<grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s>>>(src, n, c->table.buckets, first, nb - 1,
-                                                                       slot_of, err);
+    pdl_launch(k_insert<Src>, grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s, src, n, c->table.buckets, first,
+               nb - 1, slot_of, err);
     ht.mark("insert");
-    g_launches++;
-    k_rank<Src><<<(int)ntiles, kBlock, 0, s>>>(src, n, first, slot_of, c->table.buckets, c->keys,
-                                                 d_first, d_p2r, status, ticket, count);
-    g_launches++;
+    pdl_launch(k_rank<Src>, (int)ntiles, kBlock, 0, s, src, n, (const int32_t*)first, (const int32_t*)slot_of,
+               c->table.buckets, c->keys, d_first, d_p2r, status, ticket, count);
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "launch");
   }
   struct Result {

@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_probe(const int4* __restrict__ 
                                                     int32_t* __restrict__ tile_cnt, int64_t ntiles,
                                                     uint32_t* __restrict__ tile_mask, int mw,
                                                     uint32_t* __restrict__ rowmask) {
+  pdl_enter();
   extern __shared__ int32_t sm[];
   int4* s_doff = (int4*)sm;                  // [K] offset deltas of a packed key (fast path)
   int32_t* s_off = sm + 4 * K;               // [K*D]
@@ -181,6 +182,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_probe(const int4* __restrict__ 
 
 __global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ tile_cnt, int64_t ntiles,
                                                int64_t* __restrict__ tile_off, int64_t* __restrict__ totals) {
+  pdl_enter();
   __shared__ int64_t s_w[32];
   __shared__ int64_t s_carry;
   const int k = blockIdx.x;
@@ -229,6 +231,7 @@ __global__ void __launch_bounds__(kThreads) k_emit(const int32_t* __restrict__ n
                                                    int32_t* __restrict__ in_idx, int32_t* __restrict__ out_idx,
                                                    int32_t* __restrict__ nbrT, int64_t nT_pad,
                                                    uint32_t* __restrict__ tile_maskT, int mw) {
+  pdl_enter();
   extern __shared__ int64_t s_ptr[];                  // [K + 1]
   int64_t* s_toff = s_ptr + K + 1;                    // [K] this tile's offset inside each offset's list
   int32_t* s_wc = (int32_t*)(s_toff + K);             // [K][4] pairs per (offset, warp of the tile)
@@ -307,6 +310,7 @@ __global__ void __launch_bounds__(kTileRows) k_permute_rm(const int32_t* __restr
                                                           int32_t* __restrict__ out, uint32_t* __restrict__ tmask,
                                                           const int32_t* __restrict__ mirror,
                                                           uint32_t* __restrict__ tmaskT) {
+  pdl_enter();
   __shared__ uint32_t s_bits;
   if (threadIdx.x == 0) s_bits = 0;
   __syncthreads();
@@ -348,6 +352,7 @@ __global__ void __launch_bounds__(kTileRows) k_permute_rm(const int32_t* __restr
 // Row masks of the dgrad table: bit k set when nbrT[k][a] >= 0 (K <= 32).
 __global__ void k_rowmask_T(const int32_t* __restrict__ nbrT, int64_t stride, int64_t n, int K,
                             uint32_t* __restrict__ rowmask) {
+  pdl_enter();
   for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; a < n; a += (int64_t)gridDim.x * blockDim.x) {
     uint32_t rm = 0;
     for (int k = 0; k < K; ++k) rm |= (nbrT[(int64_t)k * stride + a] >= 0 ? 1u : 0u) << k;
@@ -360,6 +365,7 @@ __global__ void k_rowmask_T(const int32_t* __restrict__ nbrT, int64_t stride, in
 __global__ void __launch_bounds__(kTileRows) k_permute_km(const int32_t* __restrict__ tab, int64_t stride, int64_t n,
                                                        int K, const int32_t* __restrict__ perm,
                                                        int32_t* __restrict__ out, uint32_t* __restrict__ tmask) {
+  pdl_enter();
   __shared__ uint32_t s_bits;
   if (threadIdx.x == 0) s_bits = 0;
   __syncthreads();
@@ -379,6 +385,7 @@ __global__ void __launch_bounds__(kTileRows) k_permute_km(const int32_t* __restr
 // Dgrad tile masks of a symmetric map: bit k of tile t = bit mirror[k] of the forward mask.
 __global__ void k_mirror_mask(const uint32_t* __restrict__ mask, int64_t ntiles, int mw, const int32_t* __restrict__ mirror,
                               int K, uint32_t* __restrict__ maskT) {
+  pdl_enter();
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < ntiles; t += (int64_t)gridDim.x * blockDim.x)
     for (int w = 0; w < mw; ++w) {
       uint32_t bits = 0;
@@ -692,16 +699,12 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
       cudaFuncSetAttribute(k_probe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     if (rm)
-      k_probe<true><<<(unsigned)ntiles, kThreads, smem, s>>>(out->keys, n_out, n_pad, in->table.buckets,
-                                                             in->table.bmask, d_offs, K, D, sign, scale4, nbr_rm,
-                                                             tile_cnt, ntiles, m->tile_mask, mw, rowmask);
+      ck(pdl_launch(k_probe<true>, (unsigned)ntiles, kThreads, smem, s, out->keys, n_out, n_pad, in->table.buckets,
+                    in->table.bmask, d_offs, K, D, sign, scale4, nbr_rm, tile_cnt, ntiles, m->tile_mask, mw, rowmask));
     else
-      k_probe<false><<<(unsigned)ntiles, kThreads, smem, s>>>(out->keys, n_out, n_pad, in->table.buckets,
-                                                              in->table.bmask, d_offs, K, D, sign, scale4, m->nbr,
-                                                              tile_cnt, ntiles, m->tile_mask, mw, nullptr);
-    g_launches++;
-    k_scan<<<K, 1024, 0, s>>>(tile_cnt, ntiles, tile_off, totals);
-    g_launches++;
+      ck(pdl_launch(k_probe<false>, (unsigned)ntiles, kThreads, smem, s, out->keys, n_out, n_pad, in->table.buckets,
+                    in->table.bmask, d_offs, K, D, sign, scale4, m->nbr, tile_cnt, ntiles, m->tile_mask, mw, nullptr));
+    ck(pdl_launch(k_scan, K, 1024, 0, s, tile_cnt, ntiles, tile_off, totals));
     ht.mark("probe+scan");
   } else {
     ck(cudaMemsetAsync(m->tile_mask, 0, sizeof(uint32_t) * ntiles * mw, s));
@@ -745,13 +748,11 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   if (n_out > 0) {
     const size_t smem = sizeof(int64_t) * (2 * K + 1) + sizeof(int32_t) * (4 * K + (rm ? kTileRows * kRMPitch : 0));
     if (rm)
-      k_emit<true><<<(unsigned)ntiles, kThreads, smem, s>>>(nbr_rm, n_out, n_pad, K, totals, m->ptr, tile_off, ntiles,
-                                                            m->in_idx, m->out_idx, m->nbrT, nT_pad, m->tile_maskT, mw);
+      ck(pdl_launch(k_emit<true>, (unsigned)ntiles, kThreads, smem, s, nbr_rm, n_out, n_pad, K, totals, m->ptr,
+                    tile_off, ntiles, m->in_idx, m->out_idx, m->nbrT, nT_pad, m->tile_maskT, mw));
     else
-      k_emit<false><<<(unsigned)ntiles, kThreads, smem, s>>>(m->nbr, n_out, n_pad, K, totals, m->ptr, tile_off,
-                                                             ntiles, m->in_idx, m->out_idx, m->nbrT, nT_pad,
-                                                             m->tile_maskT, mw);
-    g_launches++;
+      ck(pdl_launch(k_emit<false>, (unsigned)ntiles, kThreads, smem, s, m->nbr, n_out, n_pad, K, totals, m->ptr,
+                    tile_off, ntiles, m->in_idx, m->out_idx, m->nbrT, nT_pad, m->tile_maskT, mw));
   }
   // Order the conv tiles' rows by neighbour bitmask (stable radix sort of the row masks):
   // rows sharing offsets share tiles, so the tensor-core kernels skip empty (tile, k) units.
@@ -763,18 +764,16 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     st = radix_sort_perm(m->alloc, rowmask, n_out, K, m->perm, s);
     ht.mark("sort");
     if (st == MK_OK) {
-      k_permute_rm<<<(unsigned)ntiles, kTileRows, 0, s>>>(nbr_rm, n_pad, n_out, K, m->perm, m->nbr, m->tile_mask,
-                                                          symmetric ? m->d_mirror : nullptr, m->tile_maskT);
-      g_launches++;
+      ck(pdl_launch(k_permute_rm, (unsigned)ntiles, kTileRows, 0, s, nbr_rm, n_pad, n_out, K, m->perm, m->nbr,
+                    m->tile_mask, symmetric ? m->d_mirror : nullptr, m->tile_maskT));
     }
     if (st == MK_OK && !symmetric && n_in > 0) {
-      k_rowmask_T<<<(unsigned)std::min<int64_t>(ceil_div(n_in, 256), 4096), 256, 0, s>>>(m->nbrT, nT_pad, n_in, K,
-                                                                                        rowmask);
-      g_launches++;
+      ck(pdl_launch(k_rowmask_T, (unsigned)std::min<int64_t>(ceil_div(n_in, 256), 4096), 256, 0, s, m->nbrT, nT_pad,
+                    n_in, K, rowmask));
       st = radix_sort_perm(m->alloc, rowmask, n_in, K, m->permT, s);
       if (st == MK_OK) {
-        k_permute_km<<<(unsigned)ntilesT, kTileRows, 0, s>>>(m->nbrT, nT_pad, n_in, K, m->permT, tabP, m->tile_maskT);
-        g_launches++;
+        ck(pdl_launch(k_permute_km, (unsigned)ntilesT, kTileRows, 0, s, m->nbrT, nT_pad, n_in, K, m->permT, tabP,
+                      m->tile_maskT));
         m->nbrT = tabP;  // the unpermuted table stays owned (freed with the map) but is no longer read
       }
     }
@@ -784,9 +783,8 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     }
   }
   if (symmetric && !(rm && n_out > 0)) {  // (k_permute_rm already wrote the mirrored masks)
-    k_mirror_mask<<<(unsigned)std::min<int64_t>(ceil_div(ntiles, 256), 1024), 256, 0, s>>>(m->tile_mask, ntiles, mw,
-                                                                                          m->d_mirror, K, m->tile_maskT);
-    g_launches++;
+    ck(pdl_launch(k_mirror_mask, (unsigned)std::min<int64_t>(ceil_div(ntiles, 256), 1024), 256, 0, s, m->tile_mask,
+                  ntiles, mw, m->d_mirror, K, m->tile_maskT));
   }
   if (symmetric) m->permT = m->perm;  // same row set, mirrored masks: same ordering
   ck(cudaGetLastError());

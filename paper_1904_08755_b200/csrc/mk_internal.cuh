@@ -48,6 +48,42 @@ extern std::atomic<int64_t> g_launches;
     return (status);                         \
   } while (0)
 
+// ------------------------------------------------------------------ launches
+// Programmatic dependent launch (PDL).  A kernel started by pdl_launch() may be scheduled
+// while its predecessor on the stream is still running, so it calls pdl_wait() in every CTA
+// before it reads or writes global memory that earlier work touches (griddepcontrol.wait
+// returns once the predecessor grid has completed and its writes are visible; it is a no-op
+// for a normal launch).  pdl_trigger() lets the next PDL kernel be scheduled once every CTA
+// of this grid has called it or exited.  Since every PDL kernel waits in every CTA, a
+// kernel's completion implies the completion of everything before it on the stream.
+// MK_NO_PDL=1 launches normally (A/B measurement).
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+// The common prologue of a PDL kernel: wait for the predecessor, then let the successor in.
+__device__ __forceinline__ void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
+}
+
 // ------------------------------------------------------------------ keys
 // A coordinate row (u_1..u_D, b) is packed into one 128-bit key (int4) so that a table
 // slot is a single 16-byte load (coalesced 128-bit coordinate access):
