@@ -26,12 +26,14 @@ def _stale(obj: Path, src: Path) -> bool:
     return obj.stat().st_mtime < max(d.stat().st_mtime for d in deps)
 
 
-def build(verbose: bool = False, jobs: int = 8, trace: bool = False) -> Path:
+def build(verbose: bool = False, jobs: int = 8, trace: bool = False, variant: str = "", defines=()) -> Path:
     """trace=True builds the MK_TRACE instrumented variant as tools/libmk_trace.so
-    (development timelines; load it with MK_LIBRARY)."""
-    objdir = PKG / ("build_trace" if trace else "build")
-    so = ROOT / "tools" / "libmk_trace.so" if trace else SO
-    defs = ["-DMK_TRACE"] if trace else []
+    (development timelines; load it with MK_LIBRARY).  variant="name" with defines=[...]
+    builds an experimental variant as build_variants/libmk_<name>.so (A/B measurements)."""
+    objdir = PKG / ("build_trace" if trace else f"build_{variant}" if variant else "build")
+    so = ROOT / "tools" / "libmk_trace.so" if trace else ROOT / "build_variants" / f"libmk_{variant}.so" if variant else SO
+    so.parent.mkdir(exist_ok=True)
+    defs = (["-DMK_TRACE"] if trace else []) + [f"-D{d}" for d in defines]
     objdir.mkdir(exist_ok=True)
     procs, objs = [], []
     for s in SOURCES:

@@ -1,4 +1,5 @@
 // context.cu — device binding, allocator plumbing and the thread-local error channel.
+#include <cstring>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -82,6 +83,46 @@ void pinned_in_flight(cudaStream_t s) {
   if (t_pin.ev && cudaEventRecord(t_pin.ev, s) == cudaSuccess) t_pin.pending = true;
 }
 
+namespace {
+struct MailboxHolder {
+  Mailbox* mb = nullptr;
+  unsigned long long seq = 0;
+  ~MailboxHolder() {
+    if (mb) cudaFreeHost(mb);
+  }
+};
+thread_local MailboxHolder t_mb;
+}  // namespace
+
+Mailbox* mailbox(unsigned long long* next_seq) {
+  if (!t_mb.mb) {
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, sizeof(Mailbox), cudaHostAllocMapped | cudaHostAllocPortable) != cudaSuccess) return nullptr;
+    t_mb.mb = (Mailbox*)p;
+    std::memset(p, 0, sizeof(Mailbox));
+  }
+  *next_seq = ++t_mb.seq;
+  return t_mb.mb;
+}
+
+cudaError_t mailbox_wait(const Mailbox* mb, unsigned long long seq, cudaStream_t s) {
+  const volatile unsigned long long* v = &mb->seq;
+  for (uint32_t it = 1;; ++it) {
+    if (*v == seq) {
+      std::atomic_thread_fence(std::memory_order_acquire);
+      return cudaSuccess;
+    }
+    if ((it & 255u) == 0) {  // every ~few us: a failed or finished stream ends the wait
+      const cudaError_t e = cudaStreamQuery(s);
+      if (e == cudaSuccess) {
+        if (*v == seq) continue;
+        return cudaErrorUnknown;  // the stream drained without posting
+      }
+      if (e != cudaErrorNotReady) return e;
+    }
+  }
+}
+
 double HostTimer::now() {
   return std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count();
 }
@@ -152,6 +193,7 @@ mk_status mk_context_create(int device, mk_alloc_fn alloc, mk_free_fn free_fn, v
 
 void mk_context_destroy(mk_context* ctx) {
   if (!ctx) return;
+  for (auto& r : ctx->region_dev) cudaFree(r.second);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   delete ctx;
 }

@@ -209,7 +209,8 @@ __global__ void __launch_bounds__(kBlock) k_rank(Src src, int64_t n, const int32
                                                  int32_t* __restrict__ first_point,
                                                  int32_t* __restrict__ p2r,
                                                  unsigned long long* status, unsigned int* ticket,
-                                                 int64_t* count) {
+                                                 int64_t* count, const unsigned long long* err, Mailbox* mb,
+                                                 unsigned long long seq) {
   pdl_enter();
   __shared__ int64_t s_tile;
   __shared__ int32_t s_warp[kBlock / 32];
@@ -251,7 +252,10 @@ __global__ void __launch_bounds__(kBlock) k_rank(Src src, int64_t n, const int32
     const int64_t pre = lookback(status, tile, agg);
     if (lane == 0) {
       s_prefix = pre;
-      if ((tile + 1) * kTile >= n) *count = pre + agg;
+      if ((tile + 1) * kTile >= n) {  // last tile: the row count is final (k_insert's errors too)
+        *count = pre + agg;
+        if (mb) mailbox_post(mb, seq, *(const volatile unsigned long long*)err, (unsigned long long)(pre + agg));
+      }
     }
   }
   __syncthreads();
@@ -421,32 +425,59 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
     pdl_launch(k_init, grid_for(std::max<int64_t>((int64_t)nb * 4, n_small), 256, ctx->num_sms), 256, 0, s,
                c->table.buckets, first, nb, small, n_small, err);
   }
+  unsigned long long seq = 0;
+  Mailbox* mb = n > 0 ? mailbox(&seq) : nullptr;
   if (n > 0) {
     ht.mark("init");
     pdl_launch(k_insert<Src>, grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s, src, n, c->table.buckets, first,
                nb - 1, slot_of, err);
     ht.mark("insert");
     pdl_launch(k_rank<Src>, (int)ntiles, kBlock, 0, s, src, n, (const int32_t*)first, (const int32_t*)slot_of,
-               c->table.buckets, c->keys, d_first, d_p2r, status, ticket, count);
+               c->table.buckets, c->keys, d_first, d_p2r, status, ticket, count, (const unsigned long long*)err, mb,
+               seq);
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "launch");
   }
   struct Result {
     unsigned long long err;
     int64_t count;
   };
-  Result* hr = (Result*)pinned_stage(sizeof(Result));
-  if (!hr) return fail_cuda(cudaErrorMemoryAllocation, "pinned staging");
-  // err and count are adjacent device words: one 16-byte copy
-  if ((e = cudaMemcpyAsync(hr, err, sizeof(Result), cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail_cuda(e, "D2H");
-  dev_free(c->alloc, sbase, s);
-  ht.mark("launched");
-  if ((e = cudaStreamSynchronize(s)) != cudaSuccess) {
-    mk_coords_destroy(c);
-    set_error(MK_ERR_CUDA, std::string("coords: ") + cudaGetErrorString(e));
-    return MK_ERR_CUDA;
+  Result h{~0ull, 0};
+  if (mb) {
+    // The last k_rank tile posts (error word, row count) into the host-mapped mailbox: the
+    // call returns as soon as the count is known, while the tail of k_rank still runs
+    // (everything after it is ordered on the stream).
+    dev_free(c->alloc, sbase, s);
+    ht.mark("launched");
+    if ((e = mailbox_wait(mb, seq, s)) != cudaSuccess) {
+      mk_coords_destroy(c);
+      set_error(MK_ERR_CUDA, std::string("coords: ") + cudaGetErrorString(e));
+      return MK_ERR_CUDA;
+    }
+    h.err = mb->w0;
+    h.count = (int64_t)mb->w1;
+  } else if (n > 0) {
+    Result* hr = (Result*)pinned_stage(sizeof(Result));
+    if (!hr) return fail_cuda(cudaErrorMemoryAllocation, "pinned staging");
+    // err and count are adjacent device words: one 16-byte copy
+    if ((e = cudaMemcpyAsync(hr, err, sizeof(Result), cudaMemcpyDeviceToHost, s)) != cudaSuccess)
+      return fail_cuda(e, "D2H");
+    dev_free(c->alloc, sbase, s);
+    ht.mark("launched");
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) {
+      mk_coords_destroy(c);
+      set_error(MK_ERR_CUDA, std::string("coords: ") + cudaGetErrorString(e));
+      return MK_ERR_CUDA;
+    }
+    h = *hr;
+  } else {
+    dev_free(c->alloc, sbase, s);
+    if ((e = cudaGetLastError()) != cudaSuccess) {
+      mk_coords_destroy(c);
+      set_error(MK_ERR_CUDA, std::string("coords: ") + cudaGetErrorString(e));
+      return MK_ERR_CUDA;
+    }
   }
   ht.mark("synced");
-  const Result h = *hr;
   if (h.err != ~0ull) {
     const int64_t row = (int64_t)(h.err >> 8);
     const uint32_t code = (uint32_t)(h.err & 0xFF);

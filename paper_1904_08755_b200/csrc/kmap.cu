@@ -63,10 +63,19 @@ __device__ __forceinline__ bool shift_key(int4 u, int D, const int32_t* off, int
 //   otherwise:    written k-major [K][n_pad] (coalesced per offset).
 // Per (offset, tile) pair counts and the tile's active-offset mask come from warp ballots
 // over the staged block.
-constexpr int kPB = 4;  // queries in flight per thread
+// Queries in flight per thread and CTAs per SM: the probe is latency bound, so occupancy
+// pays more than per-thread ILP (configs[1] kmap phase: PB 4 / 2 CTAs 153 us, PB 4 / 3 CTAs
+// 145 us, PB 2 / 4 CTAs 134 us, PB 2 / 5 CTAs 136 us).
+#ifndef MK_PROBE_PB
+#define MK_PROBE_PB 2
+#endif
+#ifndef MK_PROBE_MINB
+#define MK_PROBE_MINB 4
+#endif
+constexpr int kPB = MK_PROBE_PB;
 
 template <bool RM>
-__global__ void __launch_bounds__(kThreads, 2) k_probe(const int4* __restrict__ okeys, int64_t n_out, int64_t n_pad,
+__global__ void __launch_bounds__(kThreads, MK_PROBE_MINB) k_probe(const int4* __restrict__ okeys, int64_t n_out, int64_t n_pad,
                                                     const int4* __restrict__ buckets, uint32_t bmask,
                                                     const int32_t* __restrict__ offs, int K, int D, int sign,
                                                     Scale scale4, int32_t* __restrict__ nbr,
@@ -112,8 +121,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_probe(const int4* __restrict__ 
   for (int kc = 0; kc < K; kc += kRM) {
     const int kn = min(kRM, K - kc);
     for (int kb = kl; kb < kn; kb += 2 * kPB) {
-      int4 q[kPB];
-      Bucket w[kPB];
+      int4 q[kPB], k0[kPB], v[kPB];
+      uint32_t hb[kPB];
       bool ok[kPB];
 #pragma unroll
       for (int b = 0; b < kPB; ++b) {
@@ -125,20 +134,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_probe(const int4* __restrict__ 
         } else {
           ok[b] = valid && k < kn && shift_key(u, D, s_off + (kc + k) * D, sign, scale4, &q[b]);
         }
-        // unconditional loads (bucket 0 for masked queries): no divergent regions, all
-        // 4 * kPB loads of the thread are issued back to back
-        w[b] = load_bucket(buckets + (size_t)(ok[b] ? hash_key(q[b]) & bmask : 0u) * 4u);
+        // unconditional loads of the first sector (bucket 0 for masked queries): no
+        // divergent regions, all kPB loads of the thread are issued back to back
+        hb[b] = ok[b] ? hash_key(q[b]) & bmask : 0u;
+        load_sector(buckets + (size_t)hb[b] * 4u, &k0[b], &v[b]);
       }
 #pragma unroll
       for (int b = 0; b < kPB; ++b) {
         const int k = kb + 2 * b;
         if (k < kn) {
-          const bool m0 = ok[b] && key_eq(w[b].k0, q[b]), m1 = ok[b] && key_eq(w[b].k1, q[b]),
-                     m2 = ok[b] && key_eq(w[b].k2, q[b]);
-          int32_t a = m0 ? w[b].v.x : m1 ? w[b].v.y : m2 ? w[b].v.z : -1;
-          if (ok[b] && !(m0 | m1 | m2) && w[b].k0.w != kEmptyWord && w[b].k1.w != kEmptyWord &&
-              w[b].k2.w != kEmptyWord)
-            a = probe_next(buckets, bmask, q[b]);  // bucket full of other keys (rare)
+          int32_t a = -1;
+          if (ok[b]) {
+            if (key_eq(k0[b], q[b])) {
+              a = v[b].x;
+            } else if (k0[b].w != kEmptyWord && v[b].y >= 0) {  // slot 1 occupied (rare)
+              a = bucket_rest(buckets + (size_t)hb[b] * 4u, q[b], k0[b], v[b]);
+              if (a == -2) a = probe_next(buckets, bmask, q[b], hb[b]);  // bucket full of other keys
+            }
+          }
           s_tab[r * kRMPitch + k] = a;
         }
       }
@@ -406,6 +419,26 @@ struct RegionInfo {
   bool closed = true;           // every offset's negation is in the set
 };
 
+// Device copy of (offsets, mirror) for this context, uploaded on first use; nullptr when the
+// cache is full (the caller then uploads per build).
+const int32_t* region_device(mk_context* ctx, const std::vector<int32_t>& offs, const std::vector<int32_t>& mirror) {
+  constexpr size_t kMaxCached = 64;
+  std::vector<int32_t> key(offs);
+  key.insert(key.end(), mirror.begin(), mirror.end());
+  std::lock_guard<std::mutex> lock(ctx->region_mu);
+  for (auto& r : ctx->region_dev)
+    if (r.first == key) return r.second;
+  if (ctx->region_dev.size() >= kMaxCached) return nullptr;
+  int32_t* d = nullptr;
+  if (cudaMalloc(&d, sizeof(int32_t) * std::max<size_t>(key.size(), 1)) != cudaSuccess) return nullptr;
+  if (!key.empty() && cudaMemcpy(d, key.data(), sizeof(int32_t) * key.size(), cudaMemcpyHostToDevice) != cudaSuccess) {
+    cudaFree(d);
+    return nullptr;
+  }
+  ctx->region_dev.emplace_back(std::move(key), d);
+  return d;
+}
+
 mk_status region_info(const mk_region* r, const RegionInfo** out) {
   std::vector<int32_t> key = {r->type, r->D, r->temporal_axis, r->n_offsets};
   for (int d = 0; d < r->D && d < MK_MAX_REGION; ++d) {
@@ -653,8 +686,9 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   char* pbase = (char*)alloc(pb.off);
   char* sbase = (char*)salloc(sbm.off);
   if (!pbase || !sbase) return oom();
-  int32_t* d_offs = (int32_t*)(pbase + o_offs);  // offsets, then mirror
-  m->d_mirror = d_offs + K * D;
+  int32_t* d_offs_own = (int32_t*)(pbase + o_offs);  // offsets, then mirror (if not cached)
+  const int32_t* d_offs = d_offs_own;
+  m->d_mirror = d_offs_own + K * D;
   m->nbr = (int32_t*)(pbase + o_nbr);
   m->tile_mask = (uint32_t*)(pbase + o_tm);
   m->tile_maskT = (uint32_t*)(pbase + o_tmT);
@@ -679,12 +713,15 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     if (e == cudaSuccess) e = r;
   };
   ht.mark("allocs");
-  {  // one pinned H2D copy of the offsets and their mirror indices
+  if (const int32_t* cached = region_device(ctx, offs, m->mirror)) {  // uploaded once per region
+    d_offs = cached;
+    m->d_mirror = cached + K * D;
+  } else {  // cache full: one pinned H2D copy of the offsets and their mirror indices
     int32_t* h = (int32_t*)pinned_stage(sizeof(int32_t) * (K * D + K));
     if (!h) return oom();
     std::copy(offs.begin(), offs.end(), h);
     std::copy(m->mirror.begin(), m->mirror.end(), h + K * D);
-    ck(cudaMemcpyAsync(d_offs, h, sizeof(int32_t) * (K * D + K), cudaMemcpyHostToDevice, s));
+    ck(cudaMemcpyAsync(d_offs_own, h, sizeof(int32_t) * (K * D + K), cudaMemcpyHostToDevice, s));
     pinned_in_flight(s);
   }
   if (!symmetric) {

@@ -174,74 +174,67 @@ __host__ __device__ __forceinline__ bool pack_key(const int64_t* c, int D, int64
 }
 
 // ------------------------------------------------------------------ hash table
-// Open addressing over 64-byte buckets (half a 128-byte line): three 16-byte key slots
-// followed by one 16-byte word holding the three slots' row values:
-//   bucket b = { key[0], key[1], key[2], (row[0], row[1], row[2], unused) }
+// Open addressing over 64-byte buckets (half a 128-byte line) of three 16-byte key slots
+// and one 16-byte word holding the three slots' row values, laid out so that the first
+// 32-byte sector holds key slot 0 and the rows:
+//   bucket b = { key[0], (row[0], row[1], row[2], unused), key[1], key[2] }
 // A key hashes to bucket hash & bmask and is stored in the first free slot of the
-// linear-probing sequence of slots 3b, 3b+1, ... (wrapping).  A lookup reads a whole
-// bucket — keys and rows — in one round trip (four lanes of a warp cooperatively, one
-// 16-byte load each, or one thread with four loads) and continues to the next bucket only
-// when all three slots are occupied by other keys.
+// linear-probing sequence of slots 3b, 3b+1, ... (wrapping), so the occupied slots of a
+// bucket are a prefix and, once the table is built, row[j] >= 0 exactly when slot j is
+// occupied.  A lookup reads the first sector (key 0 + rows) and stops there unless key 0
+// is another key and slot 1 is occupied (rare at the table's load factor <= 1/2); only then
+// it reads keys 1-2, and continues to the next bucket only when all three slots hold other
+// keys.
 constexpr int kSlotsPerBucket = 3;
 
 __host__ __device__ __forceinline__ int4* slot_key(int4* buckets, uint32_t slot) {
-  return buckets + (size_t)(slot / 3u) * 4u + slot % 3u;
+  const uint32_t j = slot % 3u;
+  return buckets + (size_t)(slot / 3u) * 4u + (j ? j + 1u : 0u);
 }
 __host__ __device__ __forceinline__ int32_t* slot_val(int4* buckets, uint32_t slot) {
-  return (int32_t*)(buckets + (size_t)(slot / 3u) * 4u + 3u) + slot % 3u;
+  return (int32_t*)(buckets + (size_t)(slot / 3u) * 4u + 1u) + slot % 3u;
 }
 
-// One bucket in two 256-bit loads (sm_100 LDG.E.ENL2.256): keys 0-1, then key 2 + rows.
-struct Bucket {
-  int4 k0, k1, k2, v;
-};
-__device__ __forceinline__ Bucket load_bucket(const int4* B) {
-  Bucket b;
+// One 32-byte sector in one 256-bit load (sm_100 LDG.E.ENL2.256).
+__device__ __forceinline__ void load_sector(const int4* p, int4* a, int4* b) {
   asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(b.k0.x), "=r"(b.k0.y), "=r"(b.k0.z), "=r"(b.k0.w), "=r"(b.k1.x), "=r"(b.k1.y), "=r"(b.k1.z),
-                 "=r"(b.k1.w)
-               : "l"(B));
-  asm("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=r"(b.k2.x), "=r"(b.k2.y), "=r"(b.k2.z), "=r"(b.k2.w), "=r"(b.v.x), "=r"(b.v.y), "=r"(b.v.z),
-                 "=r"(b.v.w)
-               : "l"(B + 2));
-  return b;
+      : "=r"(a->x), "=r"(a->y), "=r"(a->z), "=r"(a->w), "=r"(b->x), "=r"(b->y), "=r"(b->z), "=r"(b->w)
+      : "l"(p));
 }
 
-// Continues the lookup of q after its home bucket (which was full of other keys).
-static __device__ __noinline__ int32_t probe_next(const int4* __restrict__ buckets, uint32_t bmask, int4 q) {
-  uint32_t b = ((hash_key(q) & bmask) + 1) & bmask;
+// Lookup of q in bucket B given its first sector (k0, v): row, -1 (absent), or -2 (all three
+// slots hold other keys: continue with the next bucket).
+__device__ __forceinline__ int32_t bucket_rest(const int4* B, int4 q, int4 k0, int4 v) {
+  if (key_eq(k0, q)) return v.x;
+  if (k0.w == kEmptyWord || v.y < 0) return -1;  // slot 1 empty (occupied slots are a prefix)
+  const int4 k1 = __ldg(B + 2);
+  if (key_eq(k1, q)) return v.y;
+  if (v.z < 0) return -1;
+  const int4 k2 = __ldg(B + 3);
+  if (key_eq(k2, q)) return v.z;
+  return -2;
+}
+
+// Continues the lookup of q after bucket b0 (which was full of other keys).
+static __device__ __noinline__ int32_t probe_next(const int4* __restrict__ buckets, uint32_t bmask, int4 q,
+                                                  uint32_t b0) {
+  uint32_t b = (b0 + 1) & bmask;
   while (true) {
     const int4* B = buckets + (size_t)b * 4u;
-    Bucket w;
-    w.k0 = __ldg(B);
-    w.k1 = __ldg(B + 1);
-    w.k2 = __ldg(B + 2);
-    w.v = __ldg(B + 3);
-    if (key_eq(w.k0, q)) return w.v.x;
-    if (key_eq(w.k1, q)) return w.v.y;
-    if (key_eq(w.k2, q)) return w.v.z;
-    if (w.k0.w == kEmptyWord || w.k1.w == kEmptyWord || w.k2.w == kEmptyWord) return -1;
+    const int32_t r = bucket_rest(B, q, __ldg(B), __ldg(B + 1));
+    if (r != -2) return r;
     b = (b + 1) & bmask;
   }
 }
 
 // Thread-level lookup of key q; row or -1.
 __device__ __forceinline__ int32_t probe(const int4* __restrict__ buckets, uint32_t bmask, int4 q) {
-  uint32_t b = hash_key(q) & bmask;
-  while (true) {
-    const int4* B = buckets + (size_t)b * 4u;
-    Bucket w;
-    w.k0 = __ldg(B);
-    w.k1 = __ldg(B + 1);
-    w.k2 = __ldg(B + 2);
-    w.v = __ldg(B + 3);
-    if (key_eq(w.k0, q)) return w.v.x;
-    if (key_eq(w.k1, q)) return w.v.y;
-    if (key_eq(w.k2, q)) return w.v.z;
-    if (w.k0.w == kEmptyWord || w.k1.w == kEmptyWord || w.k2.w == kEmptyWord) return -1;
-    b = (b + 1) & bmask;
-  }
+  const uint32_t b = hash_key(q) & bmask;
+  const int4* B = buckets + (size_t)b * 4u;
+  int4 k0, v;
+  load_sector(B, &k0, &v);
+  const int32_t r = bucket_rest(B, q, k0, v);
+  return r != -2 ? r : probe_next(buckets, bmask, q, b);
 }
 
 // ------------------------------------------------------------------ handles
@@ -263,6 +256,10 @@ struct mk_context {
   int num_sms = 148;
   mk::Alloc alloc;
   cudaStream_t aux = nullptr;  // private non-blocking stream for small lazy read-backs
+  // Device copies of kernel-region tables (offsets, then mirror indices), uploaded once per
+  // region and kept for the context's lifetime (mk::region_device).
+  std::mutex region_mu;
+  std::vector<std::pair<std::vector<int32_t>, int32_t*>> region_dev;
 };
 
 struct mk_coords {
@@ -312,7 +309,7 @@ struct mk_kmap {
   int32_t* permT = nullptr;
   int64_t nbrT_stride = 0;  // rows of the dgrad table (nbrT or, when symmetric, nbr)
   std::vector<int32_t> mirror;      // [K] index of -offset_k, or -1
-  int32_t* d_mirror = nullptr;      // [K]
+  const int32_t* d_mirror = nullptr;     // [K]
   // Per 128-row tile bitmasks of non-empty offsets (mask words = ceil(K/32)):
   uint32_t* tile_mask = nullptr;    // [ceil(n_out/128)][mw]  forward tiles
   uint32_t* tile_maskT = nullptr;   // [ceil(n_in/128)][mw]   dgrad tiles (mirrored when symmetric)
@@ -356,6 +353,26 @@ uint32_t next_pow2(uint64_t v);
 // reaches the current point.
 void* pinned_stage(size_t bytes);
 void pinned_in_flight(cudaStream_t s);
+
+// Host-mapped mailbox (context.cu): a kernel posts a few result words straight into pinned
+// host memory, so a call that needs them on the host spins on a sequence number instead of
+// a device->host copy plus a stream synchronize.  One mailbox per host thread (calls that
+// wait on it are synchronous); the device pointer equals the host pointer under UVA.
+struct Mailbox {
+  unsigned long long seq;  // written last (release), polled by the host
+  unsigned long long w0, w1, w2;
+};
+Mailbox* mailbox(unsigned long long* next_seq);  // nullptr if pinned memory is unavailable
+// Waits until mb->seq == seq, watching `s` for errors; returns cudaSuccess once posted.
+cudaError_t mailbox_wait(const Mailbox* mb, unsigned long long seq, cudaStream_t s);
+__device__ __forceinline__ void mailbox_post(Mailbox* mb, unsigned long long seq, unsigned long long w0,
+                                             unsigned long long w1) {
+  volatile Mailbox* v = mb;
+  v->w0 = w0;
+  v->w1 = w1;
+  __threadfence_system();
+  v->seq = seq;
+}
 
 // Table-building pipeline shared by quantize / create / stride (coords.cu).
 // Region enumeration (region.cu):
