@@ -187,6 +187,11 @@ mk_status mk_context_create(int device, mk_alloc_fn alloc, mk_free_fn free_fn, v
     delete c;
     MK_FAIL(MK_ERR_CUDA, "mk_context_create: stream creation failed");
   }
+  if (cudaMalloc(&c->d_bar, sizeof(unsigned) * 2 * mk_context::kBarSlots) != cudaSuccess ||
+      cudaMemset(c->d_bar, 0, sizeof(unsigned) * 2 * mk_context::kBarSlots) != cudaSuccess) {
+    c->d_bar = nullptr;  // the sort falls back to its three-kernel passes
+    cudaGetLastError();
+  }
   *out = c;
   return MK_OK;
 }
@@ -194,6 +199,7 @@ mk_status mk_context_create(int device, mk_alloc_fn alloc, mk_free_fn free_fn, v
 void mk_context_destroy(mk_context* ctx) {
   if (!ctx) return;
   for (auto& r : ctx->region_dev) cudaFree(r.second);
+  if (ctx->d_bar) cudaFree(ctx->d_bar);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   delete ctx;
 }

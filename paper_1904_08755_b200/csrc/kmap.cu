@@ -798,7 +798,7 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     m->perm = (int32_t*)alloc(sizeof(int32_t) * n_pad);
     if (!m->perm) return oom();
     ht.mark("emit");
-    st = radix_sort_perm(m->alloc, rowmask, n_out, K, m->perm, s);
+    st = radix_sort_perm(m->alloc, rowmask, n_out, K, m->perm, s, ctx->barrier_slot(), ctx->num_sms);
     ht.mark("sort");
     if (st == MK_OK) {
       ck(pdl_launch(k_permute_rm, (unsigned)ntiles, kTileRows, 0, s, nbr_rm, n_pad, n_out, K, m->perm, m->nbr,
@@ -807,7 +807,7 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     if (st == MK_OK && !symmetric && n_in > 0) {
       ck(pdl_launch(k_rowmask_T, (unsigned)std::min<int64_t>(ceil_div(n_in, 256), 4096), 256, 0, s, m->nbrT, nT_pad,
                     n_in, K, rowmask));
-      st = radix_sort_perm(m->alloc, rowmask, n_in, K, m->permT, s);
+      st = radix_sort_perm(m->alloc, rowmask, n_in, K, m->permT, s, ctx->barrier_slot(), ctx->num_sms);
       if (st == MK_OK) {
         ck(pdl_launch(k_permute_km, (unsigned)ntilesT, kTileRows, 0, s, m->nbrT, nT_pad, n_in, K, m->permT, tabP,
                       m->tile_maskT));

@@ -260,6 +260,13 @@ struct mk_context {
   // region and kept for the context's lifetime (mk::region_device).
   std::mutex region_mu;
   std::vector<std::pair<std::vector<int32_t>, int32_t*>> region_dev;
+  // Grid-barrier words of the cooperative sort: kBarSlots pairs, zero-initialised; a call
+  // takes the next pair round robin (concurrent calls on different streams get different
+  // pairs as long as fewer than kBarSlots sorts are in flight).
+  static constexpr unsigned kBarSlots = 256;
+  unsigned* d_bar = nullptr;
+  std::atomic<unsigned> bar_next{0};
+  unsigned* barrier_slot() { return d_bar ? d_bar + 2 * (bar_next.fetch_add(1) % kBarSlots) : nullptr; }
 };
 
 struct mk_coords {
@@ -383,5 +390,8 @@ mk_status kmap_host(const mk_kmap* m);
 mk_status kmap_wplan(const mk_kmap* m, cudaStream_t s);
 constexpr int kWgradMaxSegs = 63;  // segments per CTA of the bf16 weight-gradient kernel
 // Stable radix sort of keys (low `bits` bits) -> permutation (sort.cu).  Clobbers keys.
-mk_status radix_sort_perm(const Alloc& a, uint32_t* keys, int64_t n, int bits, int32_t* perm, cudaStream_t s);
+// bar: two zero-initialised device words private to this call's stream (grid barrier of
+// the one-kernel cooperative sort), or nullptr for the three-kernels-per-pass path.
+mk_status radix_sort_perm(const Alloc& a, uint32_t* keys, int64_t n, int bits, int32_t* perm, cudaStream_t s,
+                          unsigned* bar = nullptr, int num_sms = 148);
 }  // namespace mk
