@@ -24,8 +24,10 @@
  *    device memory and release it (stream-ordered, on the stream they were created on)
  *    in *_destroy.  Feature/weight/gradient buffers are caller-owned; outputs are
  *    overwritten, never accumulated into.
- *  - Calls that must report a size (coords_quantize / create / stride) synchronize their
- *    stream once.  mk_kmap_build is asynchronous: the pair count is read back lazily, the
+ *  - Calls that must report a size (coords_quantize / create / stride / expand) wait once
+ *    on the host until the size is known: the last block of the ranking kernel posts it into
+ *    a host-mapped mailbox, so the call returns while the tail of that kernel may still run
+ *    (all later work is ordered on the stream; the call does not drain it).  mk_kmap_build is asynchronous: the pair count is read back lazily, the
  *    first time mk_kmap_info is asked for n_pairs (or a call needs it: export, weight
  *    gradient), by waiting for the build's completion event only.  Every other call is
  *    asynchronous.
@@ -162,7 +164,7 @@ mk_status mk_coords_stride(mk_context* ctx, const mk_coords* in, const int32_t* 
  * occurrence of (row, offset) order.  h_out_stride host [D] (NULL = in's tensor stride)
  * must divide in's tensor stride (MK_ERR_STRIDE); it is the new set's tensor stride.
  * Typical use: upsampling a stride-2s set to stride s with the region {0,1}^D, then
- * mk_kmap_build(in, out, region, transposed = 1).  Synchronizes once (row count). */
+ * mk_kmap_build(in, out, region, transposed = 1).  Waits once for the row count. */
 mk_status mk_coords_expand(mk_context* ctx, const mk_coords* in, const mk_region* region,
                            const int32_t* h_out_stride, void* stream, mk_coords** out);
 

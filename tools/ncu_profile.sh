@@ -17,6 +17,7 @@ cap kmap_probe k_probe 2
 cap kmap_emit k_emit 2
 cap quant_insert k_insert 2
 cap quant_rank k_rank 2
+cap kmap_sort k_radix_sort_coop 2
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -c 400 --csv \
   --log-file $OUT/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
 ls $OUT
