@@ -21,12 +21,12 @@ for dt in (torch.bfloat16, torch.float32):
     y = mk.conv_forward(m, X, W)
     gi, gw = mk.conv_backward(m, G, X, W)
 cs = mk.coords_stride(c, [2, 2, 2])
-ms = mk.kmap_build(c, cs, mk.Region(mk.HYPERCUBE, 2, 3))
+ms = mk.kmap_build(c, cs, mk.Region(mk.HYPERCUBE, 3, 2))
 X = torch.randn(c.n, 32, device="cuda")
 yp, arg = mk.pool_forward(ms, X, mk.POOL_MAX)
 W = (torch.randn(8, 16, 32, device="cuda") * 0.1).bfloat16()
 yd = mk.conv_forward(ms, X.bfloat16(), W)
-mt = mk.kmap_build(cs, c, mk.Region(mk.HYPERCUBE, 2, 3), transposed=True)
+mt = mk.kmap_build(cs, c, mk.Region(mk.HYPERCUBE, 3, 2), transposed=True)
 yt = mk.conv_transpose_forward(mt, yd, (torch.randn(8, 32, 16, device="cuda") * 0.1).bfloat16())
 torch.cuda.synchronize()
 print("ok", c.n, m.n_pairs, cs.n, yt.shape)
