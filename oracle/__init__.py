@@ -292,3 +292,30 @@ def crf_infer(kmap_csr, phi_u, W, n_iters: int):
     q = np.zeros((max(n, 1), C), np.float64)
     lib().orc_crf_infer(_p(ptr), _p(ins), _p(outs), len(ptr) - 1, _p(phi), n, C, _p(w), n_iters, _p(q))
     return q[:n].copy()
+
+
+def epilogue(y, scale=None, shift=None, residual=None, relu: bool = False):
+    """f4 block epilogue (P:240: ReLU and 1D batch normalisation act on the rows of F;
+    P:303-306: residual blocks), reading R26: act(y * scale + shift + residual) per row,
+    BatchNorm in its folded inference form, act = max(0, .) or identity.  fp64."""
+    z = np.asarray(y, np.float64).copy()
+    if scale is not None:
+        z = z * np.asarray(scale, np.float64)[None, :]
+    if shift is not None:
+        z = z + np.asarray(shift, np.float64)[None, :]
+    if residual is not None:
+        z = z + np.asarray(residual, np.float64)
+    return np.maximum(z, 0.0) if relu else z
+
+
+def conv_forward_fused(kmap_csr, f_in, W, n_out: int, scale=None, shift=None, residual=None, relu: bool = False):
+    """Alg. 2 followed by the block epilogue (R26), fp64: epilogue(conv_forward(...))."""
+    return epilogue(conv_forward(kmap_csr, f_in, W, n_out), scale, shift, residual, relu)
+
+
+def bn_fold(gamma, beta, mean, var, eps: float = 1e-5):
+    """Inference BatchNorm as a per-channel affine map: y = gamma (x - mean) /
+    sqrt(var + eps) + beta = x * scale + shift."""
+    g, b, m, v = (np.asarray(a, np.float64) for a in (gamma, beta, mean, var))
+    scale = g / np.sqrt(v + eps)
+    return scale, b - m * scale
