@@ -252,6 +252,23 @@ mk_status mk_conv_forward(mk_context* ctx, const mk_kmap* m, const void* d_fin, 
                           const void* d_w, void* d_fout, int32_t c_out, mk_dtype in_dt,
                           mk_dtype out_dt, void* stream);
 
+/* mk_conv_forward with a fused row-wise epilogue ("functions that do not require
+ * spatial information (coordinates) such as ReLU ... apply directly to the features F";
+ * batch normalisation is 1D normalisation of the rows of F), for chaining MinkowskiNet /
+ * MinkUNet blocks without extra passes over F (R26):
+ *   F_out[o][j] = act(conv[o][j] * scale[j] + shift[j] + residual[o][j]),
+ *   act = max(0, .) when relu != 0, identity otherwise.
+ * d_scale, d_shift: device fp32 [c_out] — BatchNorm in its inference (folded) form,
+ *   scale = gamma / sqrt(var + eps), shift = beta - mean * scale; NULL means 1 / 0.
+ * d_residual: device [n_out][c_out] of out_dt (the block's skip input), NULL means 0.
+ * Applied in fp32 to the fp32 accumulator before the output conversion; rows without
+ * pairs get act(shift + residual).  Works on any map (also transposed maps, as the
+ * transposed forward).  Asynchronous. */
+mk_status mk_conv_forward_fused(mk_context* ctx, const mk_kmap* m, const void* d_fin, int32_t c_in,
+                                const void* d_w, void* d_fout, int32_t c_out, mk_dtype in_dt,
+                                mk_dtype out_dt, const float* d_scale, const float* d_shift,
+                                const void* d_residual, int32_t relu, void* stream);
+
 /* Reverse mode of mk_conv_forward (not in the paper, which covers forward only):
  *   d_gin[a]  = sum over pairs (a, o) of offset k of W_k^T G_out[o]       (NULL: skip)
  *   d_gw[k]   = sum over pairs (a, o) of offset k of G_out[o] F_in[a]^T   (NULL: skip),

@@ -323,9 +323,40 @@ def _conv(fn, name, m: KernelMap, f_in, W, out_dtype, out=None):
     return y
 
 
-def conv_forward(m: KernelMap, f_in: torch.Tensor, W: torch.Tensor, out_dtype=None, out=None) -> torch.Tensor:
-    """Alg. 2: F_out[o] = sum_k W_k F_in[I_k] scattered to O_k.  W [K][C_out][C_in]."""
-    return _conv(_L.mk_conv_forward, "mk_conv_forward", m, f_in, W, out_dtype, out)
+def conv_forward(m: KernelMap, f_in: torch.Tensor, W: torch.Tensor, out_dtype=None, out=None, scale=None,
+                 shift=None, residual=None, relu: bool = False) -> torch.Tensor:
+    """Alg. 2: F_out[o] = sum_k W_k F_in[I_k] scattered to O_k.  W [K][C_out][C_in].
+    With scale / shift (fp32 [C_out], folded BatchNorm), residual ([n_out][C_out], output
+    dtype) or relu, the row-wise epilogue act(conv * scale + shift + residual) runs fused in
+    the conv kernel (mk_conv_forward_fused)."""
+    if scale is None and shift is None and residual is None and not relu:
+        return _conv(_L.mk_conv_forward, "mk_conv_forward", m, f_in, W, out_dtype, out)
+    return _conv_fused(m, f_in, W, out_dtype, out, scale, shift, residual, relu)
+
+
+def _conv_fused(m: KernelMap, f_in, W, out_dtype, out, scale, shift, residual, relu):
+    if not (f_in.is_cuda and W.is_cuda):
+        raise ValueError("conv inputs must be CUDA tensors (no CPU path)")
+    K, c_out, c_in = W.shape
+    if K != m.K or f_in.shape[-1] != c_in or f_in.shape[0] != m.n_in or W.dtype != f_in.dtype:
+        raise ValueError(f"mk_conv_forward_fused: shape/dtype mismatch (K={m.K}, n_in={m.n_in})")
+    out_dtype = out_dtype or f_in.dtype
+    y = out if out is not None else torch.empty((m.n_out, c_out), dtype=out_dtype, device=f_in.device)
+    sc = None if scale is None else _cuda(scale, torch.float32, "scale")
+    sh = None if shift is None else _cuda(shift, torch.float32, "shift")
+    for t, nm in ((sc, "scale"), (sh, "shift")):
+        if t is not None and t.numel() != c_out:
+            raise ValueError(f"{nm} must have C_out = {c_out} entries")
+    res = None
+    if residual is not None:
+        res = _cuda(residual, out_dtype, "residual")
+        if tuple(res.shape) != (m.n_out, c_out):
+            raise ValueError("residual must be [n_out][C_out]")
+    with _on_device(f_in.device):
+        _check(_L.mk_conv_forward_fused(context(f_in.device.index), m._h, _ptr(f_in.contiguous()), c_in,
+                                        _ptr(W.contiguous()), _ptr(y), c_out, _dt(f_in), _DT[out_dtype], _ptr(sc),
+                                        _ptr(sh), _ptr(res), int(bool(relu)), _stream(f_in)), "mk_conv_forward_fused")
+    return y
 
 
 def conv_transpose_forward(m: KernelMap, f_in: torch.Tensor, W: torch.Tensor, out_dtype=None, out=None):

@@ -19,7 +19,8 @@ mk_status check_common(mk_context* ctx, const mk_kmap* m, int32_t c_in, int32_t 
 }
 
 mk_status forward_impl(mk_context* ctx, const mk_kmap* m, const void* d_fin, int32_t c_in, const void* d_w,
-                       void* d_fout, int32_t c_out, mk_dtype in_dt, mk_dtype out_dt, cudaStream_t s) {
+                       void* d_fout, int32_t c_out, mk_dtype in_dt, mk_dtype out_dt, cudaStream_t s,
+                       const Epilogue& ep = Epilogue()) {
   mk_status st = check_common(ctx, m, c_in, c_out, in_dt);
   if (st != MK_OK) return st;
   if (out_dt != MK_F32 && out_dt != MK_BF16) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv: unknown output dtype");
@@ -29,8 +30,9 @@ mk_status forward_impl(mk_context* ctx, const mk_kmap* m, const void* d_fin, int
   const NbrView v = forward_view(m);
   if (in_dt == MK_F32)
     return launch_conv_f32(v, (const float*)d_fin, c_in, (const float*)d_w, c_in, c_out, d_fout, c_out, out_dt,
-                           m->n_out, false, s);
-  return launch_conv_bf16(ctx, v, d_fin, m->n_in, c_in, d_w, c_in, c_out, d_fout, c_out, out_dt, m->n_out, false, s);
+                           m->n_out, false, s, ep);
+  return launch_conv_bf16(ctx, v, d_fin, m->n_in, c_in, d_w, c_in, c_out, d_fout, c_out, out_dt, m->n_out, false, s,
+                          ep);
 }
 
 mk_status backward_impl(mk_context* ctx, const mk_kmap* m, const void* d_gout, const void* d_fin, const void* d_w,
@@ -102,6 +104,18 @@ mk_status mk_conv_forward(mk_context* ctx, const mk_kmap* m, const void* d_fin, 
                           void* d_fout, int32_t c_out, mk_dtype in_dt, mk_dtype out_dt, void* stream) {
   clear_error();
   return forward_impl(ctx, m, d_fin, c_in, d_w, d_fout, c_out, in_dt, out_dt, (cudaStream_t)stream);
+}
+
+mk_status mk_conv_forward_fused(mk_context* ctx, const mk_kmap* m, const void* d_fin, int32_t c_in, const void* d_w,
+                                void* d_fout, int32_t c_out, mk_dtype in_dt, mk_dtype out_dt, const float* d_scale,
+                                const float* d_shift, const void* d_residual, int32_t relu, void* stream) {
+  clear_error();
+  Epilogue ep;
+  ep.scale = d_scale;
+  ep.shift = d_shift;
+  ep.residual = d_residual;
+  ep.relu = relu ? 1 : 0;
+  return forward_impl(ctx, m, d_fin, c_in, d_w, d_fout, c_out, in_dt, out_dt, (cudaStream_t)stream, ep);
 }
 
 mk_status mk_conv_backward(mk_context* ctx, const mk_kmap* m, const void* d_gout, const void* d_fin,

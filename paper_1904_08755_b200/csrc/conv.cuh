@@ -64,15 +64,34 @@ struct WgradPlan {
   int64_t n_chunks = 0;
 };
 
+// Fused forward epilogue (ReLU and batch normalisation act on the rows of F):
+//   y[r][j] = act(acc[r][j] * scale[j] + shift[j] + residual[r][j]),  act = ReLU or identity.
+// scale / shift fp32 [c_y] (null: 1 / 0); residual [n_rows][c_y] in the output dtype, indexed
+// by output row (null: 0).  Default-constructed = plain conv.
+struct Epilogue {
+  const float* scale = nullptr;
+  const float* shift = nullptr;
+  const void* residual = nullptr;
+  int relu = 0;
+  __host__ __device__ bool active() const { return scale || shift || residual || relu; }
+};
+__device__ __forceinline__ float epi_apply(const Epilogue& ep, float v, int j, float res) {
+  if (ep.scale) v *= __ldg(ep.scale + j);
+  if (ep.shift) v += __ldg(ep.shift + j);
+  v += res;
+  return ep.relu ? fmaxf(v, 0.f) : v;
+}
+
 mk_status launch_conv_f32(const NbrView& nb, const float* x, int c_x, const float* W, int c_in_w, int c_out_w,
-                          void* y, int c_y, mk_dtype out_dt, int64_t n_rows, bool trans, cudaStream_t s);
+                          void* y, int c_y, mk_dtype out_dt, int64_t n_rows, bool trans, cudaStream_t s,
+                          const Epilogue& ep = Epilogue());
 mk_status launch_wgrad_f32(const mk_kmap* m, const WgradPlan& plan, const float* g, int c_out, const float* x,
                            int c_in, float* dW, cudaStream_t s);
 
 // bf16 tensor-core path (conv_umma.cu)
 mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, int64_t n_src, int c_x, const void* W,
                            int c_in_w, int c_out_w, void* y, int c_y, mk_dtype out_dt, int64_t n_rows, bool trans,
-                           cudaStream_t s);
+                           cudaStream_t s, const Epilogue& ep = Epilogue());
 mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, int c_out, const void* x, int c_in,
                             float* dW, cudaStream_t s);
 __global__ void k_reduce_partials(const int32_t* __restrict__ chunk_begin, const float* __restrict__ part,

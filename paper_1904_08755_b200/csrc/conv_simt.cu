@@ -33,7 +33,8 @@ __device__ __forceinline__ void store_out<__nv_bfloat16>(__nv_bfloat16* p, float
 template <bool TRANS, typename TOut>
 __global__ void __launch_bounds__(kThreads) k_conv_f32(NbrView nb, const float* __restrict__ x, int c_x,
                                                        const float* __restrict__ W, int c_in_w, int c_out_w,
-                                                       TOut* __restrict__ y, int c_y, int64_t n_rows) {
+                                                       TOut* __restrict__ y, int c_y, int64_t n_rows,
+                                                       Epilogue ep) {
   __shared__ float s_x[kRows][kCk + 1];
   __shared__ float s_w[256][kCk + 1];  // [j][c chunk], c_y <= 256
   __shared__ int32_t s_nb[kRows];
@@ -85,10 +86,15 @@ __global__ void __launch_bounds__(kThreads) k_conv_f32(NbrView nb, const float* 
   const int64_t pos = row0 + r;
   if (pos < n_rows) {
     const int64_t row = nb.row_of(pos);  // tables are stored in the map's internal row order
+    const TOut* res = (const TOut*)ep.residual;
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       const int j = jg + 8 * i;
-      if (j < c_y) store_out<TOut>(y + row * c_y + j, acc[i]);
+      if (j < c_y) {
+        float v = acc[i];
+        if (ep.active()) v = epi_apply(ep, v, j, res ? (float)res[row * c_y + j] : 0.f);
+        store_out<TOut>(y + row * c_y + j, v);
+      }
     }
   }
 }
@@ -156,18 +162,19 @@ __global__ void k_reduce_partials(const int32_t* __restrict__ chunk_begin, const
 }
 
 mk_status launch_conv_f32(const NbrView& nb, const float* x, int c_x, const float* W, int c_in_w, int c_out_w,
-                          void* y, int c_y, mk_dtype out_dt, int64_t n_rows, bool trans, cudaStream_t s) {
+                          void* y, int c_y, mk_dtype out_dt, int64_t n_rows, bool trans, cudaStream_t s,
+                          const Epilogue& ep) {
   if (c_y > 256) MK_FAIL(MK_ERR_UNSUPPORTED, "fp32 conv: more than 256 output channels");
   if (n_rows == 0) return MK_OK;
   const unsigned grid = (unsigned)ceil_div(n_rows, kRows);
   if (out_dt == MK_F32) {
-    if (trans) k_conv_f32<true, float><<<grid, kThreads, 0, s>>>(nb, x, c_x, W, c_in_w, c_out_w, (float*)y, c_y, n_rows);
-    else k_conv_f32<false, float><<<grid, kThreads, 0, s>>>(nb, x, c_x, W, c_in_w, c_out_w, (float*)y, c_y, n_rows);
+    if (trans) k_conv_f32<true, float><<<grid, kThreads, 0, s>>>(nb, x, c_x, W, c_in_w, c_out_w, (float*)y, c_y, n_rows, ep);
+    else k_conv_f32<false, float><<<grid, kThreads, 0, s>>>(nb, x, c_x, W, c_in_w, c_out_w, (float*)y, c_y, n_rows, ep);
   } else {
     if (trans)
-      k_conv_f32<true, __nv_bfloat16><<<grid, kThreads, 0, s>>>(nb, x, c_x, W, c_in_w, c_out_w, (__nv_bfloat16*)y, c_y, n_rows);
+      k_conv_f32<true, __nv_bfloat16><<<grid, kThreads, 0, s>>>(nb, x, c_x, W, c_in_w, c_out_w, (__nv_bfloat16*)y, c_y, n_rows, ep);
     else
-      k_conv_f32<false, __nv_bfloat16><<<grid, kThreads, 0, s>>>(nb, x, c_x, W, c_in_w, c_out_w, (__nv_bfloat16*)y, c_y, n_rows);
+      k_conv_f32<false, __nv_bfloat16><<<grid, kThreads, 0, s>>>(nb, x, c_x, W, c_in_w, c_out_w, (__nv_bfloat16*)y, c_y, n_rows, ep);
   }
   MK_LAUNCH_CHECK();
   return MK_OK;

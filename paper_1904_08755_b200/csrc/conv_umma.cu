@@ -218,7 +218,59 @@ struct FwdParams {
   int tb;  // tiles per CTA (one TMEM accumulator each: tb * c_y <= 512 columns)
   int fold;  // tile order (see cta_tile)
   uint32_t a_bytes, b_bytes, tmem_cols;
+  Epilogue ep;  // fused scale / shift / residual / ReLU (forward only; identity otherwise)
 };
+
+// 16 consecutive outputs of one row through the fused epilogue (v: fp32 bit patterns).
+__device__ __forceinline__ void epi16(const FwdParams& p, int64_t row, int col0, uint32_t (&v)[16]) {
+  float res[16];
+#pragma unroll
+  for (int e = 0; e < 16; ++e) res[e] = 0.f;
+  if (p.ep.residual) {
+    if (p.out_f32) {
+      const float4* rr = (const float4*)((const float*)p.ep.residual + row * p.c_y + col0);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float4 f = __ldg(rr + e);
+        res[4 * e] = f.x, res[4 * e + 1] = f.y, res[4 * e + 2] = f.z, res[4 * e + 3] = f.w;
+      }
+    } else {
+      const uint4* rr = (const uint4*)((const __nv_bfloat16*)p.ep.residual + row * p.c_y + col0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint4 u = __ldg(rr + h);
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(*(const __nv_bfloat162*)&w[e]);
+          res[8 * h + 2 * e] = f.x, res[8 * h + 2 * e + 1] = f.y;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(epi_apply(p.ep, __uint_as_float(v[e]), col0 + e, res[e]));
+}
+
+__device__ __forceinline__ void store16(const FwdParams& p, int64_t row, int col0, const uint32_t (&v)[16]) {
+  if (p.out_f32) {
+    float4* yr = (float4*)((float*)p.y + row * p.c_y + col0);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      yr[e] = make_float4(__uint_as_float(v[4 * e]), __uint_as_float(v[4 * e + 1]), __uint_as_float(v[4 * e + 2]),
+                          __uint_as_float(v[4 * e + 3]));
+  } else {
+    uint32_t h[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      __nv_bfloat162 t2 = __floats2bfloat162_rn(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+      h[e] = *(uint32_t*)&t2;
+    }
+    uint4* yr = (uint4*)((__nv_bfloat16*)p.y + row * p.c_y + col0);
+    yr[0] = make_uint4(h[0], h[1], h[2], h[3]);
+    yr[1] = make_uint4(h[4], h[5], h[6], h[7]);
+  }
+}
 
 constexpr int kMaxK = 128;  // offsets supported by the tensor-core conv (4 mask words)
 // Ring of commit barriers: the MMA thread's j-th group commit (covering steps up to
@@ -537,16 +589,15 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
       const int64_t pos = tile * kTileM + q * 32 + lane;  // position in the map's row order
       const bool valid = pos < p.n_rows;
       const int64_t row = valid ? p.nb.row_of(pos) : 0;
-      if (!((act >> i) & 1u)) {
-        if (valid) {
-          if (p.out_f32) {
-            float4* yr = (float4*)((float*)p.y + row * p.c_y);
-            for (int c = 0; c < p.c_y / 4; ++c) yr[c] = make_float4(0.f, 0.f, 0.f, 0.f);
-          } else {
-            uint4* yr = (uint4*)((__nv_bfloat16*)p.y + row * p.c_y);
-            for (int c = 0; c < p.c_y / 8; ++c) yr[c] = make_uint4(0, 0, 0, 0);
+      if (!((act >> i) & 1u)) {  // no offset in this tile: the conv output is 0
+        if (valid)
+          for (int col0 = 0; col0 < p.c_y; col0 += 16) {
+            uint32_t v[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = 0u;
+            if (p.ep.active()) epi16(p, row, col0, v);
+            store16(p, row, col0, v);
           }
-        }
         continue;
       }
       const uint32_t tl_addr = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(i * p.c_y);
@@ -555,23 +606,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
         tmem_ld16(tl_addr + col0, v);
         tmem_ld_wait();
         if (valid) {
-          if (p.out_f32) {
-            float4* yr = (float4*)((float*)p.y + row * p.c_y + col0);
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              yr[e] = make_float4(__uint_as_float(v[4 * e]), __uint_as_float(v[4 * e + 1]),
-                                  __uint_as_float(v[4 * e + 2]), __uint_as_float(v[4 * e + 3]));
-          } else {
-            uint32_t h[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-              __nv_bfloat162 t2 = __floats2bfloat162_rn(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
-              h[e] = *(uint32_t*)&t2;
-            }
-            uint4* yr = (uint4*)((__nv_bfloat16*)p.y + row * p.c_y + col0);
-            yr[0] = make_uint4(h[0], h[1], h[2], h[3]);
-            yr[1] = make_uint4(h[4], h[5], h[6], h[7]);
-          }
+          if (p.ep.active()) epi16(p, row, col0, v);
+          store16(p, row, col0, v);
         }
       }
     }
@@ -965,7 +1001,7 @@ extern "C" int mk_debug_cta(unsigned long long* host_out) {
 
 mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, int64_t n_src, int c_x, const void* W,
                             int c_in_w, int c_out_w, void* y, int c_y, mk_dtype out_dt, int64_t n_rows, bool trans,
-                            cudaStream_t s) {
+                            cudaStream_t s, const Epilogue& ep) {
   if (n_rows == 0) return MK_OK;
   (void)n_src;
   if (nb.K > kMaxK) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: more than 128 kernel offsets");
@@ -981,6 +1017,7 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   p.c_y = c_y;
   p.nch = nch;
   p.out_f32 = out_dt == MK_F32;
+  p.ep = ep;
   static const int dbg = [] {
     const char* e = std::getenv("MK_DEBUG_CONV");
     return e ? std::atoi(e) : 0;
