@@ -325,7 +325,45 @@ def run_mk(args, ws, rank, local):
     phi = torch.randn((c7.n, 16), device=dev)
     W7 = torch.randn((15, 16, 16), device=dev) * 0.1
     t_crf = timed(lambda: mk.crf_infer(m7, phi, W7, 3), reps=10)
+    # f4: MinkUNet-shaped layer stack with cached coordinate sets and fused
+    #     BN/ReLU/residual epilogues, bf16: stem conv, residual block (stride 1, 64 ch),
+    #     stride-2 down conv 2^3 (64 -> 128), residual block (stride 2, 128 ch), transposed up
+    #     conv 2^3 (128 -> 64) back onto the cached stride-1 set with an additive skip from
+    #     the first block (R27).  Timed with the coordinate / map construction and without it.
+    def bn(c, seed):
+        g = torch.Generator(device="cpu").manual_seed(seed)
+        return (torch.rand(c, generator=g) * 0.5 + 0.75).to(dev), (torch.rand(c, generator=g) - 0.5).to(dev)
+    Ws = {k: (torch.randn(shape, device=dev) * (2.0 / (shape[0] * shape[2])) ** 0.5).to(torch.bfloat16)
+          for k, shape in {"stem": (27, 64, 64), "b0a": (27, 64, 64), "b0b": (27, 64, 64), "down": (8, 128, 64),
+                           "b1a": (27, 128, 128), "b1b": (27, 128, 128), "up": (8, 64, 128)}.items()}
+    Bs = {k: bn(W.shape[1], i) for i, (k, W) in enumerate(Ws.items())}
+    r3, r2 = mk.Region(mk.HYPERCUBE, 3, 3), mk.Region(mk.HYPERCUBE, 3, 2)
+
+    def unet_maps(c0):
+        c1 = mk.coords_stride(c0, [2, 2, 2])
+        return (mk.kmap_build(c0, c0, r3), mk.kmap_build(c0, c1, r2), mk.kmap_build(c1, c1, r3),
+                mk.kmap_build(c1, c0, r2, transposed=True))
+
+    def unet_layers(maps, x):
+        m0, md, m1, mu = maps
+        f = lambda m, h, k, **kw: mk.conv_forward(m, h, Ws[k], scale=Bs[k][0], shift=Bs[k][1], **kw)  # noqa: E731
+        h = f(m0, x, "stem", relu=True)
+        s0 = f(m0, f(m0, h, "b0a", relu=True), "b0b", residual=h, relu=True)
+        h = f(md, s0, "down", relu=True)
+        h = f(m1, f(m1, h, "b1a", relu=True), "b1b", residual=h, relu=True)
+        return mk.conv_transpose_forward(mu, h, Ws["up"], scale=Bs["up"][0], shift=Bs["up"][1], residual=s0,
+                                         relu=True)
+    maps = unet_maps(cq)
+    unet_flops = 2.0 * sum(m.n_pairs * W.shape[1] * W.shape[2] for m, W in (
+        (maps[0], Ws["stem"]), (maps[0], Ws["b0a"]), (maps[0], Ws["b0b"]), (maps[1], Ws["down"]),
+        (maps[2], Ws["b1a"]), (maps[2], Ws["b1b"]), (maps[3], Ws["up"])))
+    t_unet_layers = timed(lambda: unet_layers(maps, X))
+    t_unet_all = timed(lambda: unet_layers(unet_maps(mk.coords_quantize(pts, synthetic.ROOM_VOXEL, return_maps=False)),
+                                           X), reps=10)
     extras = {
+        "unet_stack_layers_us": round(t_unet_layers, 2), "unet_stack_with_maps_us": round(t_unet_all, 2),
+        "unet_stack_tflops": round(unet_flops / (t_unet_layers * 1e-6) / 1e12, 2),
+        "unet_stack_rows": [int(maps[0].n_out), int(maps[2].n_out)],
         "labels_us": round(t_lab, 2), "labels_mpts": round(pts.shape[0] / t_lab, 1),
         "maxpool2_fwd_us": round(t_pf, 2), "maxpool2_bwd_us": round(t_pb, 2), "avgpool2_fwd_us": round(t_af, 2),
         "maxpool2_fwd_gbs": round(pool_bytes / (t_pf * 1e-6) / 1e9, 1),

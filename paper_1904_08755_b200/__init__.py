@@ -359,9 +359,15 @@ def _conv_fused(m: KernelMap, f_in, W, out_dtype, out, scale, shift, residual, r
     return y
 
 
-def conv_transpose_forward(m: KernelMap, f_in: torch.Tensor, W: torch.Tensor, out_dtype=None, out=None):
-    """Transposed conv on a map built with transposed=True."""
-    return _conv(_L.mk_conv_transpose_forward, "mk_conv_transpose_forward", m, f_in, W, out_dtype, out)
+def conv_transpose_forward(m: KernelMap, f_in: torch.Tensor, W: torch.Tensor, out_dtype=None, out=None, scale=None,
+                           shift=None, residual=None, relu: bool = False):
+    """Transposed conv on a map built with transposed=True; the optional fused
+    epilogue is that of conv_forward."""
+    if scale is None and shift is None and residual is None and not relu:
+        return _conv(_L.mk_conv_transpose_forward, "mk_conv_transpose_forward", m, f_in, W, out_dtype, out)
+    if not m.transposed:
+        raise ValueError("conv_transpose_forward: the map is not transposed")
+    return _conv_fused(m, f_in, W, out_dtype, out, scale, shift, residual, relu)
 
 
 def _backward(fn, name, m: KernelMap, g_out, f_in, W, need_gin=True, need_gw=True, gin=None, gw=None):

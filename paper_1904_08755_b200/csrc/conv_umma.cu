@@ -236,15 +236,13 @@ __device__ __forceinline__ void epi16(const FwdParams& p, int64_t row, int col0,
       }
     } else {
       const uint4* rr = (const uint4*)((const __nv_bfloat16*)p.ep.residual + row * p.c_y + col0);
+      auto lo = [](uint32_t u) { return __uint_as_float(u << 16); };           // bf16 -> fp32 is exact:
+      auto hi = [](uint32_t u) { return __uint_as_float(u & 0xFFFF0000u); };  // the top 16 bits
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const uint4 u = __ldg(rr + h);
-        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float2 f = __bfloat1622float2(*(const __nv_bfloat162*)&w[e]);
-          res[8 * h + 2 * e] = f.x, res[8 * h + 2 * e + 1] = f.y;
-        }
+        res[8 * h + 0] = lo(u.x), res[8 * h + 1] = hi(u.x), res[8 * h + 2] = lo(u.y), res[8 * h + 3] = hi(u.y);
+        res[8 * h + 4] = lo(u.z), res[8 * h + 5] = hi(u.z), res[8 * h + 6] = lo(u.w), res[8 * h + 7] = hi(u.w);
       }
     }
   }
@@ -357,7 +355,7 @@ __device__ void build_plan(const FwdParams& p, Plan* pl) {
 }
 
 // Output-stationary gather-GEMM over the CTA's tb tiles, offset-outer (see file header).
-template <int CH>
+template <int CH, bool EPI>  // EPI: the fused epilogue is compiled in (plain convs keep the lean kernel)
 __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_constant__ FwdParams p) {
   constexpr int J = CH / 8;    // 16-byte chunks per gathered row
   constexpr int RB = CH * 2;   // bytes per gathered row (= swizzle span)
@@ -595,7 +593,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
             uint32_t v[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) v[e] = 0u;
-            if (p.ep.active()) epi16(p, row, col0, v);
+            if (EPI) epi16(p, row, col0, v);
             store16(p, row, col0, v);
           }
         continue;
@@ -606,7 +604,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
         tmem_ld16(tl_addr + col0, v);
         tmem_ld_wait();
         if (valid) {
-          if (p.ep.active()) epi16(p, row, col0, v);
+          if (EPI) epi16(p, row, col0, v);
           store16(p, row, col0, v);
         }
       }
@@ -980,9 +978,27 @@ uint32_t pow2_cols(uint32_t c) {
   return r;
 }
 
+// Raises a kernel's dynamic smem limit; the attribute call (~1 us of host time) is made only
+// when the requested size grows past what was set before for that kernel.
 template <class F>
 void set_smem_once(F* f, int bytes) {
-  cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  struct Set {
+    const void* f;
+    int dev, bytes;
+  };
+  static std::mutex mu;
+  static std::vector<Set> done;
+  int dev = 0;
+  cudaGetDevice(&dev);  // the attribute is per device
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& d : done)
+    if (d.f == (const void*)f && d.dev == dev) {
+      if (d.bytes >= bytes) return;
+      if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess) d.bytes = bytes;
+      return;
+    }
+  if (cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes) == cudaSuccess)
+    done.push_back({(const void*)f, dev, bytes});
 }
 
 }  // namespace
@@ -1064,16 +1080,17 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   const int smem = fixed + p.sa * (int)p.a_bytes;
   const int64_t grid = ceil_div(p.ntiles, p.tb);  // one CTA per tb adjacent tiles
   cudaError_t e;
-  if (CH == 64) {
-    set_smem_once(k_conv_umma<64>, smem);
-    e = pdl_launch(k_conv_umma<64>, (unsigned)grid, kFwdThreads, smem, s, p);
-  } else if (CH == 32) {
-    set_smem_once(k_conv_umma<32>, smem);
-    e = pdl_launch(k_conv_umma<32>, (unsigned)grid, kFwdThreads, smem, s, p);
-  } else {
-    set_smem_once(k_conv_umma<16>, smem);
-    e = pdl_launch(k_conv_umma<16>, (unsigned)grid, kFwdThreads, smem, s, p);
-  }
+  auto go = [&](auto kern) {
+    set_smem_once(kern, smem);
+    return pdl_launch(kern, (unsigned)grid, kFwdThreads, smem, s, p);
+  };
+  const bool epi = ep.active();
+  if (CH == 64)
+    e = epi ? go(k_conv_umma<64, true>) : go(k_conv_umma<64, false>);
+  else if (CH == 32)
+    e = epi ? go(k_conv_umma<32, true>) : go(k_conv_umma<32, false>);
+  else
+    e = epi ? go(k_conv_umma<16, true>) : go(k_conv_umma<16, false>);
   if (e == cudaSuccess) e = cudaGetLastError();
   dev_free(ctx->alloc, wpack, s);
   if (e != cudaSuccess) MK_FAIL(MK_ERR_CUDA, std::string("bf16 conv launch: ") + cudaGetErrorString(e));
