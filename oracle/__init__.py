@@ -319,3 +319,36 @@ def bn_fold(gamma, beta, mean, var, eps: float = 1e-5):
     g, b, m, v = (np.asarray(a, np.float64) for a in (gamma, beta, mean, var))
     scale = g / np.sqrt(v + eps)
     return scale, b - m * scale
+
+
+def crf_backward(kmap_csr, phi_u, W, n_iters: int, grad_q):
+    """f3 learning (Eq. 5), fp64: dL/dphi_u and dL/dphi_p of Q^N (Alg. 5 with
+    Q^0 = softmax(phi_u), reading R25) given dL/dQ^N, by backpropagation through the
+    n_iters mean-field steps: for n = N..1, dA^n = Q^n (g - <Q^n, g>) (softmax reverse),
+    dphi_u += dA^n, dphi_p += wgrad(dA^n, Q^(n-1)), g <- dgrad(dA^n, phi_p); finally
+    dphi_u += the softmax reverse of Q^0."""
+    phi = np.asarray(phi_u, np.float64)
+    w = np.asarray(W, np.float64)
+    n, C = phi.shape
+    K = w.shape[0]
+
+    def softmax(a):
+        e = np.exp(a - a.max(axis=1, keepdims=True))
+        return e / e.sum(axis=1, keepdims=True)
+
+    def softmax_rev(q, g):
+        return q * (g - (q * g).sum(axis=1, keepdims=True))
+
+    Q = [softmax(phi)]
+    for _ in range(n_iters):
+        Q.append(softmax(phi + conv_forward(kmap_csr, Q[-1], w, n)))
+    g = np.asarray(grad_q, np.float64)
+    gphi = np.zeros_like(phi)
+    gW = np.zeros_like(w)
+    for it in range(n_iters, 0, -1):
+        dA = softmax_rev(Q[it], g)
+        gphi += dA
+        gW += conv_wgrad(kmap_csr, dA, Q[it - 1], K)
+        g = conv_dgrad(kmap_csr, dA, w, n)
+    gphi += softmax_rev(Q[0], g)
+    return gphi, gW

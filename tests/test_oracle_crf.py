@@ -74,3 +74,49 @@ def test_crf_stationarity(orc):
     tau = np.array([5, -3, 2, 7, -1, 4, 9, 0], np.int32)
     c2 = c + tau
     np.testing.assert_allclose(orc.crf_infer(orc.kmap(c2, c2, offs), phi, W, 2), q, rtol=1e-13, atol=1e-15)
+
+
+def _tiny(orc, seed, n=40, C=3):
+    g = np.random.default_rng(seed)
+    c = _lattice(seed, n=n, span=1)
+    offs = orc.region(1, D, [3] * D)
+    km = orc.kmap(c, c, offs)
+    phi = g.standard_normal((c.shape[0], C))
+    W = g.standard_normal((offs.shape[0], C, C)) * 0.5
+    G = g.standard_normal((c.shape[0], C))
+    return km, phi, W, G
+
+
+def test_crf_backward_matches_finite_differences(orc):
+    # Eq. 5 pinned by central differences of L = sum(G * Q^N) (fp64; no shared formula)
+    km, phi, W, G = _tiny(orc, 11)
+    n_iters = 2
+    gphi, gW = orc.crf_backward(km, phi, W, n_iters, G)
+    L = lambda p, w: float((G * orc.crf_infer(km, p, w, n_iters)).sum())  # noqa: E731
+    h = 1e-6
+    g = np.random.default_rng(12)
+    for _ in range(12):
+        i, c = g.integers(0, phi.shape[0]), g.integers(0, phi.shape[1])
+        d = np.zeros_like(phi)
+        d[i, c] = h
+        fd = (L(phi + d, W) - L(phi - d, W)) / (2 * h)
+        assert abs(fd - gphi[i, c]) <= 1e-7 + 1e-6 * abs(fd)
+        k, a, b = g.integers(0, W.shape[0]), g.integers(0, W.shape[1]), g.integers(0, W.shape[2])
+        e = np.zeros_like(W)
+        e[k, a, b] = h
+        fd = (L(phi, W + e) - L(phi, W - e)) / (2 * h)
+        assert abs(fd - gW[k, a, b]) <= 1e-7 + 1e-6 * abs(fd)
+
+
+def test_crf_backward_shift_invariance_and_zero_iterations(orc):
+    # adding a constant to a node's logits leaves every Q^n unchanged, so each row of
+    # dL/dphi_u sums to 0; with N = 0 the gradient is the softmax Jacobian applied to G
+    km, phi, W, G = _tiny(orc, 13)
+    for n_iters in (0, 1, 3):
+        gphi, gW = orc.crf_backward(km, phi, W, n_iters, G)
+        np.testing.assert_allclose(gphi.sum(axis=1), 0.0, atol=1e-12)
+        if n_iters == 0:
+            q = _softmax(phi)
+            J = np.einsum("ic,cd->icd", q, np.eye(q.shape[1])) - np.einsum("ic,id->icd", q, q)
+            np.testing.assert_allclose(gphi, np.einsum("icd,ic->id", J, G), atol=1e-14)
+            assert not gW.any()
