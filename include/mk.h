@@ -240,6 +240,17 @@ mk_status mk_global_pool(mk_context* ctx, const mk_coords* c, int32_t mode, cons
 mk_status mk_crf_infer(mk_context* ctx, const mk_kmap* m, const float* d_phi_u, const float* d_W,
                        int32_t C, int32_t n_iters, float* d_q, void* stream);
 
+/* Learning through the mean-field iterations (Eq. 5): given dL/dQ^N (d_gq,
+ * device fp32 [n][C]) for the Q^N of mk_crf_infer(phi_u, W, n_iters), writes
+ *   d_gphi  [n][C]    dL/dphi_u = sum over n = 0..N of (dL/dQ^n) dQ^n/dphi_u,
+ *   d_gW    [K][C][C] dL/dphi_p = sum over n = 1..N of (dL/dQ^n) dQ^n/dphi_p
+ * (backpropagation through time; not touched when n_iters = 0).  The forward is recomputed
+ * with every Q^n kept: (n_iters + 4) n C + K C^2 floats of stream-ordered workspace.  fp32;
+ * deterministic (the weight gradient uses the fixed-order split-K reduction).  Asynchronous. */
+mk_status mk_crf_backward(mk_context* ctx, const mk_kmap* m, const float* d_phi_u, const float* d_W,
+                          int32_t C, int32_t n_iters, const float* d_gq, float* d_gphi, float* d_gW,
+                          void* stream);
+
 /* ---------------------------------------------------------------- convolution ------ */
 /* Generalized sparse convolution, Alg. 2:
  *   F_out[o] = sum over pairs (a, o) of offset k of W_k F_in[a];  rows without any pair

@@ -455,3 +455,20 @@ def crf_infer(m: KernelMap, phi_u: torch.Tensor, W: torch.Tensor, n_iters: int =
         _check(_L.mk_crf_infer(context(phi.device.index), m._h, _ptr(phi), _ptr(w), C, int(n_iters), _ptr(q),
                                _stream(phi)), "mk_crf_infer")
     return q
+
+
+def crf_backward(m: KernelMap, phi_u: torch.Tensor, W: torch.Tensor, n_iters: int, grad_q: torch.Tensor):
+    """Eq. 5: (dL/dphi_u [n][C], dL/dW [K][C][C]) of crf_infer's Q^N given
+    dL/dQ^N, by backpropagation through the n_iters mean-field steps; fp32."""
+    phi = _cuda(phi_u, torch.float32, "phi_u")
+    w = _cuda(W, torch.float32, "W")
+    g = _cuda(grad_q, torch.float32, "grad_q")
+    n, C = phi.shape
+    if n != m.n_out or m.n_in != m.n_out or tuple(w.shape) != (m.K, C, C) or tuple(g.shape) != (n, C):
+        raise ValueError("crf_backward: phi_u / grad_q [n][C] over the map's nodes and W [K][C][C] expected")
+    gphi = torch.empty_like(phi)
+    gw = torch.zeros_like(w)
+    with _on_device(phi.device):
+        _check(_L.mk_crf_backward(context(phi.device.index), m._h, _ptr(phi), _ptr(w), C, int(n_iters), _ptr(g),
+                                  _ptr(gphi), _ptr(gw), _stream(phi)), "mk_crf_backward")
+    return gphi, gw

@@ -157,3 +157,106 @@ extern "C" mk_status mk_crf_infer(mk_context* ctx, const mk_kmap* m, const float
   if (e != cudaSuccess) MK_FAIL(MK_ERR_CUDA, std::string("mk_crf_infer: ") + cudaGetErrorString(e));
   return MK_OK;
 }
+
+// ------------------------------------------------------------------ learning (Eq. 5)
+namespace mk {
+namespace {
+
+// Reverse of a row softmax: da[i][c] = q[i][c] * (g[i][c] - sum_j q[i][j] g[i][j]);
+// also accumulates da into acc (dL/dphi_u collects every iteration's da, Eq. 5).
+__global__ void __launch_bounds__(256) k_crf_softmax_bwd(const float* __restrict__ q, const float* __restrict__ g,
+                                                         int64_t n, int C, float* __restrict__ da,
+                                                         float* __restrict__ acc, int first) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (i >= n) return;
+  float dot = 0.f;
+  for (int c0 = 0; c0 < C; c0 += 32) {
+    const int c = c0 + lane;
+    if (c < C) dot += q[i * C + c] * g[i * C + c];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+  for (int c0 = 0; c0 < C; c0 += 32) {
+    const int c = c0 + lane;
+    if (c >= C) continue;
+    const float d = q[i * C + c] * (g[i * C + c] - dot);
+    if (da) da[i * C + c] = d;
+    acc[i * C + c] = first ? d : acc[i * C + c] + d;
+  }
+}
+
+__global__ void k_axpy(const float* __restrict__ x, int64_t n, float* __restrict__ y, int first) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = first ? x[i] : y[i] + x[i];
+}
+
+}  // namespace
+}  // namespace mk
+
+// Backpropagation through the N mean-field iterations (Eq. 5).  The forward is
+// recomputed with every Q^n kept (fp32, (N + 1) n C floats of workspace); then, from
+// n = N down to 1: dA^n = softmax'(Q^n) dQ^n, dphi_u += dA^n, dW += G-weighted wgrad of the
+// iteration's conv (dA^n against Q^(n-1)), dQ^(n-1) = dgrad of the conv; finally
+// dphi_u += softmax'(Q^0) dQ^0 (Q^0 = softmax(phi_u), reading R25).
+extern "C" mk_status mk_crf_backward(mk_context* ctx, const mk_kmap* m, const float* d_phi_u, const float* d_W,
+                                     int32_t C, int32_t n_iters, const float* d_gq, float* d_gphi, float* d_gW,
+                                     void* stream) {
+  using namespace mk;
+  clear_error();
+  if (!ctx || !m) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_crf_backward: null argument");
+  if (m->n_in != m->n_out || m->transposed)
+    MK_FAIL(MK_ERR_SHAPE_MISMATCH, "mk_crf_backward: the map must connect a coordinate set to itself");
+  if (C < 1 || n_iters < 0) MK_FAIL(MK_ERR_SHAPE_MISMATCH, "mk_crf_backward: bad sizes");
+  const int64_t n = m->n_out, wn = (int64_t)m->K * C * C;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n_iters > 0 && (!d_W || !d_gW)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_crf_backward: null weights");
+  if (n == 0) {
+    if (n_iters > 0) MK_CUDA_TRY(cudaMemsetAsync(d_gW, 0, sizeof(float) * wn, s));
+    return MK_OK;
+  }
+  if (!d_phi_u || !d_gq || !d_gphi) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_crf_backward: null buffers");
+  const int64_t nc = n * C;
+  // workspace: Q^0..Q^N, the conv output / dA, two dQ buffers, one dW partial
+  float* ws = (float*)dev_alloc(ctx->alloc, sizeof(float) * ((n_iters + 1) * nc + 3 * nc + wn), s);
+  if (!ws) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "mk_crf_backward: workspace allocation failed");
+  float* Q = ws;
+  float* tmp = Q + (n_iters + 1) * nc;
+  float* dq[2] = {tmp + nc, tmp + 2 * nc};
+  float* gw_tmp = tmp + 3 * nc;
+  const unsigned grid = (unsigned)ceil_div(n, 8);
+  const NbrView v = forward_view(m);
+  mk_status st = MK_OK;
+  k_crf_softmax<<<grid, 256, 0, s>>>(d_phi_u, nullptr, n, C, Q);  // Q^0
+  g_launches++;
+  for (int it = 0; it < n_iters && st == MK_OK; ++it) {
+    st = launch_conv_f32(v, Q + it * nc, C, d_W, C, C, tmp, C, MK_F32, n, false, s);
+    if (st == MK_OK) {
+      k_crf_softmax<<<grid, 256, 0, s>>>(d_phi_u, tmp, n, C, Q + (it + 1) * nc);
+      g_launches++;
+    }
+  }
+  cudaError_t e = cudaMemcpyAsync(dq[0], d_gq, sizeof(float) * nc, cudaMemcpyDeviceToDevice, s);
+  const unsigned wgrid = (unsigned)std::min<int64_t>(ceil_div(wn, 256), 4 * ctx->num_sms);
+  for (int it = n_iters; it >= 1 && st == MK_OK && e == cudaSuccess; --it) {
+    float* g_cur = dq[(n_iters - it) & 1];
+    float* g_prev = dq[(n_iters - it + 1) & 1];
+    k_crf_softmax_bwd<<<grid, 256, 0, s>>>(Q + it * nc, g_cur, n, C, tmp, d_gphi, it == n_iters);
+    g_launches++;
+    // dQ^(it-1) = conv dgrad of dA; dW_it = wgrad(dA, Q^(it-1))
+    st = mk_conv_backward(ctx, m, tmp, Q + (it - 1) * nc, d_W, C, C, MK_F32, g_prev, gw_tmp, stream);
+    if (st == MK_OK) {
+      k_axpy<<<wgrid, 256, 0, s>>>(gw_tmp, wn, d_gW, it == n_iters);
+      g_launches++;
+    }
+  }
+  if (st == MK_OK && e == cudaSuccess) {
+    k_crf_softmax_bwd<<<grid, 256, 0, s>>>(Q, dq[n_iters & 1], n, C, nullptr, d_gphi, n_iters == 0);
+    g_launches++;
+  }
+  if (e == cudaSuccess) e = cudaGetLastError();
+  dev_free(ctx->alloc, ws, s);
+  if (st != MK_OK) return st;
+  if (e != cudaSuccess) MK_FAIL(MK_ERR_CUDA, std::string("mk_crf_backward: ") + cudaGetErrorString(e));
+  return MK_OK;
+}

@@ -77,3 +77,35 @@ def test_crf_infer_matches_oracle(mk, orc, C, n_iters):
     q64 = orc.crf_infer(km, phi, W, n_iters)
     assert_close(q, q64, np.ones_like(q64), FP32_TOL, "crf")  # probabilities: absolute scale 1
     np.testing.assert_allclose(q.sum(axis=1), 1.0, rtol=1e-5)
+
+
+# Eq. 5 learning: the fp32 tolerance of north_star, normwise (measured: <= 3.4e-6 for dW,
+# <= 3.3e-7 for dphi_u at N = 3)
+CRF_BWD_TOL = FP32_TOL
+
+
+@pytest.mark.parametrize("C,n_iters", [(8, 3), (20, 1), (4, 0)])
+def test_crf_backward_matches_oracle(mk, orc, C, n_iters):
+    rows = _lattice7(5, n=12000)
+    oc, _ = orc.create(rows)
+    c = mk.coords_create(dev(oc))
+    m = mk.kmap_build(c, c, mk.Region(mk.HYPERCROSS, D, 3))
+    km = csr_np(m)
+    g = np.random.default_rng(100 + C)
+    phi = g.standard_normal((c.n, C)).astype(np.float32)
+    W = (g.standard_normal((15, C, C)) * 0.5).astype(np.float32)
+    G = g.standard_normal((c.n, C)).astype(np.float32)
+    gphi, gW = mk.crf_backward(m, dev(phi), dev(W), n_iters, dev(G))
+    gphi64, gW64 = orc.crf_backward(km, phi, W, n_iters, G)
+    e_phi = np.abs(gphi.cpu().numpy() - gphi64).max() / np.abs(gphi64).max()
+    print(f"crf backward C={C} N={n_iters}: dphi normwise {e_phi:.2e}", end="")
+    assert e_phi <= CRF_BWD_TOL
+    if n_iters > 0:
+        e_w = np.abs(gW.cpu().numpy() - gW64).max() / np.abs(gW64).max()
+        print(f", dW normwise {e_w:.2e}")
+        assert e_w <= CRF_BWD_TOL
+    else:
+        assert not gW.any()
+    np.testing.assert_allclose(gphi.cpu().numpy().sum(axis=1), 0.0, atol=1e-5)  # logit shift invariance
+    gphi2, gW2 = mk.crf_backward(m, dev(phi), dev(W), n_iters, dev(G))
+    assert torch.equal(gphi, gphi2) and torch.equal(gW, gW2)  # deterministic
