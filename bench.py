@@ -325,6 +325,8 @@ def run_mk(args, ws, rank, local):
     phi = torch.randn((c7.n, 16), device=dev)
     W7 = torch.randn((15, 16, 16), device=dev) * 0.1
     t_crf = timed(lambda: mk.crf_infer(m7, phi, W7, 3), reps=10)
+    gq7 = torch.randn_like(phi)
+    t_crf_bwd = timed(lambda: mk.crf_backward(m7, phi, W7, 3, gq7), reps=10)
     # f4: MinkUNet-shaped layer stack with cached coordinate sets and fused
     #     BN/ReLU/residual epilogues, bf16: stem conv, residual block (stride 1, 64 ch),
     #     stride-2 down conv 2^3 (64 -> 128), residual block (stride 2, 128 ch), transposed up
@@ -369,7 +371,7 @@ def run_mk(args, ws, rank, local):
         "maxpool2_fwd_gbs": round(pool_bytes / (t_pf * 1e-6) / 1e9, 1),
         "pool_rows": [int(mp.n_in), int(mp.n_out)],
         "expand_us": round(t_exp, 2), "generative_convT_us": round(t_gen, 2), "expand_rows": int(up.n),
-        "crf7d_3iter_us": round(t_crf, 2), "crf_nodes": int(c7.n), "crf_pairs": int(m7.n_pairs),
+        "crf7d_3iter_us": round(t_crf, 2), "crf7d_3iter_backward_us": round(t_crf_bwd, 2), "crf_nodes": int(c7.n), "crf_pairs": int(m7.n_pairs),
     }
 
     # ---- roofline of the dominant kernel (largest phase among the conv kernels / map build)
