@@ -112,6 +112,150 @@ __global__ void __launch_bounds__(kThreads) k_pool_bwd(NbrView nt, int64_t n_row
   }
 }
 
+// Vectorised variants (C a multiple of 8 for bf16 / 4 for fp32, 16-byte aligned rows): one
+// thread per (table position, 16-byte channel chunk), value loads of 4 offsets in flight,
+// 16-byte loads and stores, argmax as 8 / 4 int32 per chunk.  configs[1] stride-2 2^3
+// pooling, bf16 64 ch, cold L2: max fwd 38 us (warp-per-row scalar kernel: 33), max bwd 51
+// (72), avg fwd 29 (31); warm L2 max fwd 16.5 us.
+template <typename T>
+struct Vec16;
+template <>
+struct Vec16<__nv_bfloat16> {
+  static constexpr int N = 8;
+  __device__ static void load(const void* p, float (&v)[8]) {
+    const uint4 u = __ldg((const uint4*)p);
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      v[2 * e] = __uint_as_float(w[e] << 16);
+      v[2 * e + 1] = __uint_as_float(w[e] & 0xFFFF0000u);
+    }
+  }
+  __device__ static void store(void* p, const float (&v)[8]) {
+    uint32_t h[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const __nv_bfloat162 t = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+      h[e] = *(const uint32_t*)&t;
+    }
+    *(uint4*)p = make_uint4(h[0], h[1], h[2], h[3]);
+  }
+};
+template <>
+struct Vec16<float> {
+  static constexpr int N = 4;
+  __device__ static void load(const void* p, float (&v)[4]) {
+    const float4 f = __ldg((const float4*)p);
+    v[0] = f.x, v[1] = f.y, v[2] = f.z, v[3] = f.w;
+  }
+  __device__ static void store(void* p, const float (&v)[4]) { *(float4*)p = make_float4(v[0], v[1], v[2], v[3]); }
+};
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) k_pool_fwd_vec(NbrView nb, int64_t n_rows, const T* __restrict__ x, int C,
+                                                      T* __restrict__ y, int32_t* __restrict__ argmax) {
+  constexpr int mode = MODE;
+  constexpr int U = 4;  // value loads in flight per thread
+  constexpr int V = Vec16<T>::N;
+  const int L = C / V;  // chunks per row
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_rows * L; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / L;
+    const int ch = (int)(t - i * L);
+    const int64_t o = nb.row_of(i);
+    float acc[V];
+    int32_t best[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) acc[e] = 0.f, best[e] = -1;
+    int cnt = 0;
+    for (int k0 = 0; k0 < nb.K; k0 += U) {
+      int32_t a[U];
+#pragma unroll
+      for (int j = 0; j < U; ++j) a[j] = k0 + j < nb.K ? nb.at(k0 + j, i) : -1;
+      float v[U][V];
+#pragma unroll
+      for (int j = 0; j < U; ++j)
+        if (a[j] >= 0) Vec16<T>::load(x + (int64_t)a[j] * C + ch * V, v[j]);
+#pragma unroll
+      for (int j = 0; j < U; ++j) {
+        if (a[j] < 0) continue;
+        ++cnt;
+#pragma unroll
+        for (int e = 0; e < V; ++e) {
+          if (mode == MK_POOL_MAX) {
+            if (best[e] < 0 || v[j][e] > acc[e]) {  // strictly greater: the first maximal input wins
+              acc[e] = v[j][e];
+              best[e] = a[j];
+            }
+          } else {
+            acc[e] += v[j][e];
+          }
+        }
+      }
+    }
+    if (mode == MK_POOL_AVG && cnt > 0) {
+#pragma unroll
+      for (int e = 0; e < V; ++e) acc[e] /= (float)cnt;
+    }
+    Vec16<T>::store(y + o * C + ch * V, acc);
+    if (mode == MK_POOL_MAX && argmax) {
+      int4* am = (int4*)(argmax + o * C + ch * V);
+#pragma unroll
+      for (int e = 0; e < V; e += 4) am[e / 4] = make_int4(best[e], best[e + 1], best[e + 2], best[e + 3]);
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_pool_bwd_vec(NbrView nt, int64_t n_rows, const T* __restrict__ g, int C,
+                                                      int mode, const int32_t* __restrict__ argmax,
+                                                      const int32_t* __restrict__ cnt, T* __restrict__ gx) {
+  constexpr int V = Vec16<T>::N;
+  const int L = C / V;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n_rows * L; t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / L;
+    const int ch = (int)(t - i * L);
+    const int64_t a = nt.row_of(i);
+    float acc[V];
+#pragma unroll
+    for (int e = 0; e < V; ++e) acc[e] = 0.f;
+    for (int k0 = 0; k0 < nt.K; k0 += 8) {
+      int32_t o[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o[j] = k0 + j < nt.K ? nt.at(k0 + j, i) : -1;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {  // in offset order (fixed summation order)
+        if (o[j] < 0) continue;
+        const int64_t e0 = (int64_t)o[j] * C + ch * V;
+        float v[V];
+        Vec16<T>::load(g + e0, v);
+        if (mode == MK_POOL_MAX) {
+#pragma unroll
+          for (int e = 0; e < V; e += 4) {
+            const int4 am = __ldg((const int4*)(argmax + e0 + e));
+            acc[e] += am.x == (int32_t)a ? v[e] : 0.f;
+            acc[e + 1] += am.y == (int32_t)a ? v[e + 1] : 0.f;
+            acc[e + 2] += am.z == (int32_t)a ? v[e + 2] : 0.f;
+            acc[e + 3] += am.w == (int32_t)a ? v[e + 3] : 0.f;
+          }
+        } else if (mode == MK_POOL_AVG) {
+          const float c = (float)__ldg(cnt + o[j]);
+#pragma unroll
+          for (int e = 0; e < V; ++e) acc[e] += v[e] / c;
+        } else {
+#pragma unroll
+          for (int e = 0; e < V; ++e) acc[e] += v[e];
+        }
+      }
+    }
+    Vec16<T>::store(gx + a * C + ch * V, acc);
+  }
+}
+
+bool vec_ok(int C, bool bf16, const void* p0, const void* p1) {
+  const int V = bf16 ? 8 : 4;
+  return C % V == 0 && ((uintptr_t)p0 & 15) == 0 && ((uintptr_t)p1 & 15) == 0;
+}
+
 mk_status check_pool(const mk_kmap* m, int32_t mode, int32_t C, mk_dtype dt) {
   if (!m) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "pool: null map");
   if (mode != MK_POOL_MAX && mode != MK_POOL_AVG && mode != MK_POOL_SUM)
@@ -137,9 +281,30 @@ mk_status mk_pool_forward(mk_context* ctx, const mk_kmap* m, int32_t mode, const
   if (m->n_out == 0) return MK_OK;
   if (!d_fout || (m->n_in > 0 && !d_fin)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_pool_forward: null features");
   const NbrView v = forward_view(m);
-  const unsigned grid = (unsigned)ceil_div(m->n_out, kRowsPerBlock);
-  k_pool_fwd<<<grid, kThreads, 0, (cudaStream_t)stream>>>(v, m->n_out, d_fin, C, dt == MK_BF16, mode, d_fout,
-                                                           mode == MK_POOL_MAX ? d_argmax : nullptr);
+  cudaStream_t s = (cudaStream_t)stream;
+  int32_t* am = mode == MK_POOL_MAX ? d_argmax : nullptr;
+  if (vec_ok(C, dt == MK_BF16, d_fin, d_fout) && ((uintptr_t)am & 15) == 0) {
+    const int64_t work = m->n_out * (C / (dt == MK_BF16 ? 8 : 4));
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(work, 256), 16 * ctx->num_sms);
+    const bool b = dt == MK_BF16;
+    const auto* xb = (const __nv_bfloat16*)d_fin;
+    const auto* xf = (const float*)d_fin;
+    auto* yb = (__nv_bfloat16*)d_fout;
+    auto* yf = (float*)d_fout;
+    if (mode == MK_POOL_MAX) {
+      if (b) k_pool_fwd_vec<__nv_bfloat16, MK_POOL_MAX><<<grid, 256, 0, s>>>(v, m->n_out, xb, C, yb, am);
+      else k_pool_fwd_vec<float, MK_POOL_MAX><<<grid, 256, 0, s>>>(v, m->n_out, xf, C, yf, am);
+    } else if (mode == MK_POOL_AVG) {
+      if (b) k_pool_fwd_vec<__nv_bfloat16, MK_POOL_AVG><<<grid, 256, 0, s>>>(v, m->n_out, xb, C, yb, am);
+      else k_pool_fwd_vec<float, MK_POOL_AVG><<<grid, 256, 0, s>>>(v, m->n_out, xf, C, yf, am);
+    } else {
+      if (b) k_pool_fwd_vec<__nv_bfloat16, MK_POOL_SUM><<<grid, 256, 0, s>>>(v, m->n_out, xb, C, yb, am);
+      else k_pool_fwd_vec<float, MK_POOL_SUM><<<grid, 256, 0, s>>>(v, m->n_out, xf, C, yf, am);
+    }
+  } else {
+    const unsigned grid = (unsigned)ceil_div(m->n_out, kRowsPerBlock);
+    k_pool_fwd<<<grid, kThreads, 0, s>>>(v, m->n_out, d_fin, C, dt == MK_BF16, mode, d_fout, am);
+  }
   MK_LAUNCH_CHECK();
   return MK_OK;
 }
@@ -164,8 +329,19 @@ mk_status mk_pool_backward(mk_context* ctx, const mk_kmap* m, int32_t mode, cons
     g_launches++;
   }
   const NbrView v = dgrad_view(m);
-  const unsigned grid = (unsigned)ceil_div(m->n_in, kRowsPerBlock);
-  k_pool_bwd<<<grid, kThreads, 0, s>>>(v, m->n_in, d_gout, C, dt == MK_BF16, mode, d_argmax, cnt, d_gin);
+  if (vec_ok(C, dt == MK_BF16, d_gout, d_gin) && ((uintptr_t)d_argmax & 15) == 0) {
+    const int64_t work = m->n_in * (C / (dt == MK_BF16 ? 8 : 4));
+    const unsigned grid = (unsigned)std::min<int64_t>(ceil_div(work, 256), 16 * ctx->num_sms);
+    if (dt == MK_BF16)
+      k_pool_bwd_vec<__nv_bfloat16><<<grid, 256, 0, s>>>(v, m->n_in, (const __nv_bfloat16*)d_gout, C, mode, d_argmax,
+                                                          cnt, (__nv_bfloat16*)d_gin);
+    else
+      k_pool_bwd_vec<float><<<grid, 256, 0, s>>>(v, m->n_in, (const float*)d_gout, C, mode, d_argmax, cnt,
+                                                  (float*)d_gin);
+  } else {
+    const unsigned grid = (unsigned)ceil_div(m->n_in, kRowsPerBlock);
+    k_pool_bwd<<<grid, kThreads, 0, s>>>(v, m->n_in, d_gout, C, dt == MK_BF16, mode, d_argmax, cnt, d_gin);
+  }
   g_launches++;
   const cudaError_t e = cudaGetLastError();
   if (cnt) dev_free(ctx->alloc, cnt, s);
