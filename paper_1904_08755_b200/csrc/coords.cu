@@ -369,8 +369,12 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
                        cudaStream_t s, mk_coords** out, int32_t* d_p2r, int32_t* d_first) {
   HostTimer ht("build_coords");
   if (n < 0 || n > INT32_MAX) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "row count out of range [0, 2^31)");
-  // buckets of 3 slots, >= 2n slots in total (load factor <= 1/2)
-  const uint32_t nb = next_pow2(std::max<int64_t>(ceil_div(2 * n, kSlotsPerBucket), 32));
+  // buckets of 3 slots, >= MK_TABLE_SLOTS_X2 * n / 2 slots in total (default 4: load <= 1/2)
+#ifndef MK_TABLE_SLOTS_X2
+#define MK_TABLE_SLOTS_X2 4
+#endif
+  const uint32_t nb =
+      next_pow2(std::max<int64_t>(ceil_div(MK_TABLE_SLOTS_X2 * n, 2 * kSlotsPerBucket), 32));
   const uint32_t nslots = nb * kSlotsPerBucket;
   const int64_t ntiles = std::max<int64_t>(1, ceil_div(n, kTile));
 

@@ -298,12 +298,22 @@ __global__ void __launch_bounds__(kThreads) k_emit(const int32_t* __restrict__ n
     if (lane == 0) s_wc[k * 4 + wq] = __popc(b);
   }
   __syncthreads();
+  // first list position of every (offset, warp quarter): one thread per offset
+  for (int k = threadIdx.x; k < K; k += kThreads) {
+    int64_t base = s_ptr[k] + s_toff[k];
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const int32_t c = s_wc[k * 4 + w];
+      s_wc[k * 4 + w] = (int32_t)(base - s_ptr[k]);  // offset inside offset k's list (< 2^31)
+      base += c;
+    }
+  }
+  __syncthreads();
   for (int k = threadIdx.x / kTileRows; k < K; k += kThreads / kTileRows) {
     const int32_t a = get(k);
     const unsigned b = __ballot_sync(0xffffffffu, a >= 0);
     if (a < 0) continue;
-    int64_t pos = s_ptr[k] + s_toff[k] + __popc(b & lt);
-    for (int w = 0; w < wq; ++w) pos += s_wc[k * 4 + w];
+    const int64_t pos = s_ptr[k] + s_wc[k * 4 + wq] + __popc(b & lt);
     in_idx[pos] = a;
     out_idx[pos] = (int32_t)o;
     if (nbrT) {
