@@ -20,6 +20,8 @@
 #include <cstring>
 #include <vector>
 
+#include <cstdlib>
+
 #include "mk_internal.cuh"
 
 namespace mk {
@@ -27,7 +29,13 @@ namespace mk {
 namespace {
 
 constexpr int kBlock = 256;
-constexpr int kItems = 4;
+#ifndef MK_RANK_ITEMS
+#define MK_RANK_ITEMS 4
+#endif
+#ifndef MK_RANK_MINB
+#define MK_RANK_MINB 1
+#endif
+constexpr int kItems = MK_RANK_ITEMS;  // consecutive points per thread in k_rank
 constexpr int kTile = kBlock * kItems;
 
 enum : uint32_t { E_NONE = 0, E_NONFINITE = 1, E_RANGE = 2, E_BATCH = 3, E_STRIDE = 4 };
@@ -203,7 +211,7 @@ __device__ int64_t lookback(unsigned long long* status, int64_t tile, int64_t ag
 }
 
 template <class Src>
-__global__ void __launch_bounds__(kBlock) k_rank(Src src, int64_t n, const int32_t* __restrict__ first,
+__global__ void __launch_bounds__(kBlock, MK_RANK_MINB) k_rank(Src src, int64_t n, const int32_t* __restrict__ first,
                                                  const int32_t* __restrict__ slot_of, int4* __restrict__ buckets,
                                                  int4* __restrict__ out_keys,
                                                  int32_t* __restrict__ first_point,
@@ -429,8 +437,12 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
     pdl_launch(k_init, grid_for(std::max<int64_t>((int64_t)nb * 4, n_small), 256, ctx->num_sms), 256, 0, s,
                c->table.buckets, first, nb, small, n_small, err);
   }
+  static const bool no_mailbox = [] {  // MK_NO_MAILBOX=1: D2H copy + stream sync (A/B measurement)
+    const char* v = std::getenv("MK_NO_MAILBOX");
+    return v && v[0] && v[0] != '0';
+  }();
   unsigned long long seq = 0;
-  Mailbox* mb = n > 0 ? mailbox(&seq) : nullptr;
+  Mailbox* mb = n > 0 && !no_mailbox ? mailbox(&seq) : nullptr;
   if (n > 0) {
     ht.mark("init");
     pdl_launch(k_insert<Src>, grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s, src, n, c->table.buckets, first,
