@@ -155,7 +155,8 @@ def run_mk(args, ws, rank, local):
             if ev is not None:
                 ev[i].record(stream)
         mark(0)
-        c, _, _ = mk.coords_quantize(pts, synthetic.ROOM_VOXEL, return_maps=True)  # a1, a2
+        # a1, a2 (deferred row count: the map build collects it, the host runs ahead meanwhile)
+        c, _, _ = mk.coords_quantize(pts, synthetic.ROOM_VOXEL, return_maps=True, deferred=True)
         mark(1)
         m = mk.kmap_build(c, c, region)                                             # a4, a5
         mark(2)
@@ -239,7 +240,7 @@ def run_mk(args, ws, rank, local):
         for t in (p, x, w, g):
             t.record_stream(stream)
         stream.wait_event(ev_p)
-        c, _, _ = mk.coords_quantize(p, synthetic.ROOM_VOXEL)
+        c, _, _ = mk.coords_quantize(p, synthetic.ROOM_VOXEL, deferred=True)
         m = mk.kmap_build(c, c, region)
         stream.wait_event(ev_x)
         def to_host(dev_t, host_t):  # D2H on its own stream as soon as dev_t is ready

@@ -121,6 +121,16 @@ mk_status mk_coords_quantize(mk_context* ctx, const float* d_points, const int32
                              int64_t n, int32_t D, float voxel, void* stream, mk_coords** out,
                              int32_t* d_point_to_row, int32_t* d_first_point);
 
+/* mk_coords_quantize without the wait for the row count: returns the handle as soon as the
+ * kernels are enqueued.  The count (and any input error: NONFINITE_INPUT, COORD_RANGE, ...)
+ * is collected at its first use — mk_coords_info(n), export, stride / expand, or a
+ * kernel-map build on the handle — which then waits for it (the ranking kernel posts it to a
+ * host-mapped mailbox).  d_first_point needs room for n rows (only the first N are written).
+ * Lets the host prepare the next call (e.g. mk_kmap_build) while the GPU quantizes. */
+mk_status mk_coords_quantize_deferred(mk_context* ctx, const float* d_points, const int32_t* d_batch,
+                                      int64_t n, int32_t D, float voxel, void* stream, mk_coords** out,
+                                      int32_t* d_point_to_row, int32_t* d_first_point);
+
 /* A coordinate set from integer rows (Eq. 1), duplicates merged, first occurrence wins.
  *   d_coords        device int32 [n][D+1], batch last
  *   h_tensor_stride host int32 [D] or NULL (all 1): every spatial component must be a

@@ -100,14 +100,25 @@ def kernel_launch_count() -> int:
 class Coords:
     """Immutable coordinate set C (Eq. 1) with its GPU hash table (``mk_coords``)."""
 
-    def __init__(self, handle: ctypes.c_void_p, device: torch.device):
+    def __init__(self, handle: ctypes.c_void_p, device: torch.device, deferred: bool = False):
         self._h = handle
         self.device = device
         n, D = ctypes.c_int64(), ctypes.c_int32()
         ts = (ctypes.c_int32 * 8)()  # >= MK_MAX_DIM
-        _check(_L.mk_coords_info(handle, ctypes.byref(n), ctypes.byref(D), ts), "mk_coords_info")
-        self.n, self.D = int(n.value), int(D.value)
+        _check(_L.mk_coords_info(handle, None if deferred else ctypes.byref(n), ctypes.byref(D), ts), "mk_coords_info")
+        self.D = int(D.value)
         self.tensor_stride = [int(ts[d]) for d in range(self.D)]
+        self._n = None if deferred else int(n.value)
+
+    @property
+    def n(self) -> int:
+        """Row count N.  For a deferred quantize the first access waits for it (and raises
+        the input error, if any)."""
+        if self._n is None:
+            n = ctypes.c_int64()
+            _check(_L.mk_coords_info(self._h, ctypes.byref(n), None, None), "mk_coords_info")
+            self._n = int(n.value)
+        return self._n
 
     def __len__(self):
         return self.n
@@ -125,21 +136,25 @@ class Coords:
 
 
 def coords_quantize(points: torch.Tensor, voxel: float, batch: Optional[torch.Tensor] = None,
-                    return_maps: bool = True):
-    """Alg. 1 -> (Coords, point_to_row int32 [N_p], first_point int32 [N])."""
+                    return_maps: bool = True, deferred: bool = False):
+    """Alg. 1 -> (Coords, point_to_row int32 [N_p], first_point int32 [N]).
+    deferred=True returns before the row count is known (mk_coords_quantize_deferred): the
+    count is collected when first needed (Coords.n, a kernel-map build, ...), and first_point
+    is returned with its full capacity N_p (rows >= N undefined)."""
     pts = _cuda(points, torch.float32, "points")
     n, D = pts.shape
     b = None if batch is None else _cuda(batch, torch.int32, "batch")
     p2r = torch.empty(n, dtype=torch.int32, device=pts.device) if return_maps else None
     first = torch.empty(max(n, 1), dtype=torch.int32, device=pts.device) if return_maps else None
     h = ctypes.c_void_p()
+    fn = _L.mk_coords_quantize_deferred if deferred else _L.mk_coords_quantize
     with _on_device(pts.device):
-        _check(_L.mk_coords_quantize(context(pts.device.index), _ptr(pts), _ptr(b), n, D, ctypes.c_float(voxel),
-                                     _stream(pts), ctypes.byref(h), _ptr(p2r), _ptr(first)), "mk_coords_quantize")
-    c = Coords(h, pts.device)
+        _check(fn(context(pts.device.index), _ptr(pts), _ptr(b), n, D, ctypes.c_float(voxel), _stream(pts),
+                  ctypes.byref(h), _ptr(p2r), _ptr(first)), "mk_coords_quantize")
+    c = Coords(h, pts.device, deferred=deferred)
     if not return_maps:
         return c
-    return c, p2r, first[:c.n]
+    return c, p2r, (first if deferred else first[:c.n])
 
 
 def coords_labels(point_to_row: torch.Tensor, first_point: torch.Tensor, labels: torch.Tensor,

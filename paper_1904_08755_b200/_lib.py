@@ -39,7 +39,7 @@ class MkRegion(ctypes.Structure):
 
 EXPORTS = [
     "mk_context_create", "mk_context_destroy",
-    "mk_coords_quantize", "mk_coords_create", "mk_coords_info", "mk_coords_export", "mk_coords_lookup",
+    "mk_coords_quantize", "mk_coords_quantize_deferred", "mk_coords_create", "mk_coords_info", "mk_coords_export", "mk_coords_lookup",
     "mk_coords_labels", "mk_coords_expand",
     "mk_coords_stride", "mk_coords_destroy",
     "mk_region_offsets",
@@ -59,6 +59,7 @@ def load() -> ctypes.CDLL:
     sig = {
         "mk_context_create": [ctypes.c_int, P, P, P, PP],
         "mk_coords_quantize": [P, P, P, i64, i32, f32, P, PP, P, P],
+        "mk_coords_quantize_deferred": [P, P, P, i64, i32, f32, P, PP, P, P],
         "mk_coords_create": [P, P, i64, i32, P, P, PP, P],
         "mk_coords_info": [P, P, P, P],
         "mk_coords_export": [P, P, P],

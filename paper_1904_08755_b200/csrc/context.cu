@@ -105,6 +105,23 @@ Mailbox* mailbox(unsigned long long* next_seq) {
   return t_mb.mb;
 }
 
+Mailbox* mailbox_ring_slot(mk_context* ctx, unsigned long long* seq) {
+  static std::mutex mu;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (!ctx->mb_ring) {
+      void* p = nullptr;
+      if (cudaHostAlloc(&p, sizeof(Mailbox) * mk_context::kMbSlots, cudaHostAllocMapped | cudaHostAllocPortable) !=
+          cudaSuccess)
+        return nullptr;
+      std::memset(p, 0, sizeof(Mailbox) * mk_context::kMbSlots);
+      ctx->mb_ring = (Mailbox*)p;
+    }
+  }
+  *seq = ctx->mb_seq.fetch_add(1) + 1;  // never 0 (the slots start zeroed)
+  return ctx->mb_ring + (*seq % mk_context::kMbSlots);
+}
+
 cudaError_t mailbox_wait(const Mailbox* mb, unsigned long long seq, cudaStream_t s) {
   const volatile unsigned long long* v = &mb->seq;
   for (uint32_t it = 1;; ++it) {
@@ -200,6 +217,7 @@ void mk_context_destroy(mk_context* ctx) {
   if (!ctx) return;
   for (auto& r : ctx->region_dev) cudaFree(r.second);
   if (ctx->d_bar) cudaFree(ctx->d_bar);
+  if (ctx->mb_ring) cudaFreeHost(ctx->mb_ring);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   delete ctx;
 }

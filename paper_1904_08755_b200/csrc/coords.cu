@@ -372,9 +372,25 @@ struct Carver {
   }
 };
 
+// Status + message of a non-empty error word (first offending row << 8 | code).
+mk_status report_input_error(unsigned long long err) {
+  const int64_t row = (int64_t)(err >> 8);
+  const uint32_t code = (uint32_t)(err & 0xFF);
+  const mk_status st = code == E_NONFINITE ? MK_ERR_NONFINITE_INPUT
+                     : code == E_RANGE     ? MK_ERR_COORD_RANGE
+                     : code == E_STRIDE    ? MK_ERR_STRIDE
+                                           : MK_ERR_INVALID_ARGUMENT;
+  const char* what = code == E_NONFINITE ? "non-finite coordinate"
+                   : code == E_RANGE     ? "coordinate outside the representable range"
+                   : code == E_STRIDE    ? "coordinate not a multiple of the tensor stride"
+                                         : "negative batch index";
+  set_error(st, std::string("coords: ") + what + " at row " + std::to_string(row), row);
+  return st;
+}
+
 template <class Src>
 mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const int32_t* ts,
-                       cudaStream_t s, mk_coords** out, int32_t* d_p2r, int32_t* d_first) {
+                       cudaStream_t s, mk_coords** out, int32_t* d_p2r, int32_t* d_first, bool deferred = false) {
   HostTimer ht("build_coords");
   if (n < 0 || n > INT32_MAX) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "row count out of range [0, 2^31)");
   // buckets of 3 slots, >= MK_TABLE_SLOTS_X2 * n / 2 slots in total (default 4: load <= 1/2)
@@ -394,7 +410,8 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
 
   // persistent: table keys, table values, row keys
   Carver pc;
-  const size_t o_tk = pc.take<int4>((size_t)nb * 4), o_rk = pc.take<int4>(std::max<int64_t>(n, 1));
+  const size_t o_tk = pc.take<int4>((size_t)nb * 4), o_rk = pc.take<int4>(std::max<int64_t>(n, 1)),
+               o_res = pc.take<unsigned long long>(2);  // (error word, count) for a deferred count
   char* pbase = (char*)dev_alloc(c->alloc, pc.off, s);
   if (!pbase) {
     delete c;
@@ -426,6 +443,7 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
   unsigned long long* status = (unsigned long long*)(sbase + o_st);
   unsigned int* ticket = (unsigned int*)(sbase + o_ti);
   unsigned long long* err = (unsigned long long*)(sbase + o_er);
+  if (deferred && n > 0) err = (unsigned long long*)(pbase + o_res);  // outlives the call
   int64_t* count = (int64_t*)(err + 1);
 
   cudaError_t e;
@@ -442,7 +460,12 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
     return v && v[0] && v[0] != '0';
   }();
   unsigned long long seq = 0;
-  Mailbox* mb = n > 0 && !no_mailbox ? mailbox(&seq) : nullptr;
+  Mailbox* mb = nullptr;
+  if (deferred && n > 0) {
+    mb = mailbox_ring_slot(ctx, &seq);
+    if (!mb) deferred = false;  // no pinned ring: the eager path below
+  }
+  if (!deferred && n > 0 && !no_mailbox) mb = mailbox(&seq);
   if (n > 0) {
     ht.mark("init");
     pdl_launch(k_insert<Src>, grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s, src, n, c->table.buckets, first,
@@ -452,6 +475,19 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
                c->table.buckets, c->keys, d_first, d_p2r, status, ticket, count, (const unsigned long long*)err, mb,
                seq);
     if ((e = cudaGetLastError()) != cudaSuccess) return fail_cuda(e, "launch");
+  }
+  if (deferred && n > 0) {
+    c->mu = new std::mutex();
+    c->mb = mb;
+    c->seq = seq;
+    c->d_res = err;
+    c->n = -1;
+    if ((e = cudaEventCreateWithFlags(&c->ev, cudaEventDisableTiming)) != cudaSuccess ||
+        (e = cudaEventRecord(c->ev, s)) != cudaSuccess)
+      return fail_cuda(e, "event");
+    dev_free(c->alloc, sbase, s);
+    *out = c;
+    return MK_OK;
   }
   struct Result {
     unsigned long long err;
@@ -495,19 +531,8 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
   }
   ht.mark("synced");
   if (h.err != ~0ull) {
-    const int64_t row = (int64_t)(h.err >> 8);
-    const uint32_t code = (uint32_t)(h.err & 0xFF);
     mk_coords_destroy(c);
-    mk_status st = code == E_NONFINITE ? MK_ERR_NONFINITE_INPUT
-                 : code == E_RANGE     ? MK_ERR_COORD_RANGE
-                 : code == E_STRIDE    ? MK_ERR_STRIDE
-                                       : MK_ERR_INVALID_ARGUMENT;
-    const char* what = code == E_NONFINITE ? "non-finite coordinate"
-                     : code == E_RANGE     ? "coordinate outside the representable range"
-                     : code == E_STRIDE    ? "coordinate not a multiple of the tensor stride"
-                                           : "negative batch index";
-    set_error(st, std::string("coords: ") + what + " at row " + std::to_string(row), row);
-    return st;
+    return report_input_error(h.err);
   }
   c->n = n > 0 ? h.count : 0;
   *out = c;
@@ -515,6 +540,49 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
 }
 
 bool valid_stream_dim(int32_t D) { return D >= 1 && D <= MK_MAX_DIM; }
+
+}  // namespace
+
+mk_status coords_resolve(const mk_coords* cc) {
+  if (!cc || !cc->mu) return MK_OK;  // eager handle: count known
+  mk_coords* c = const_cast<mk_coords*>(cc);  // the count is fixed by the build: logically const
+  std::lock_guard<std::mutex> lock(*c->mu);
+  if (c->n >= 0) return c->err == ~0ull ? MK_OK : report_input_error(c->err);
+  unsigned long long err = ~0ull, count = 0;
+  const volatile unsigned long long* vseq = &c->mb->seq;
+  for (uint32_t it = 1;; ++it) {
+    if (*vseq == c->seq) {
+      std::atomic_thread_fence(std::memory_order_acquire);
+      err = c->mb->w0;
+      count = c->mb->w1;
+      if (*vseq == c->seq) break;  // not overwritten while reading
+    }
+    if ((it & 255u) == 0) {
+      const cudaError_t q = cudaEventQuery(c->ev);
+      if (q == cudaSuccess && *vseq != c->seq) {  // done, but the slot was reused: device words
+        unsigned long long r[2];
+        const cudaError_t e = cudaMemcpy(r, c->d_res, sizeof(r), cudaMemcpyDeviceToHost);
+        if (e != cudaSuccess) {
+          set_error(MK_ERR_CUDA, std::string("coords: ") + cudaGetErrorString(e));
+          return MK_ERR_CUDA;
+        }
+        err = r[0];
+        count = r[1];
+        break;
+      }
+      if (q != cudaSuccess && q != cudaErrorNotReady) {
+        set_error(MK_ERR_CUDA, std::string("coords: ") + cudaGetErrorString(q));
+        return MK_ERR_CUDA;
+      }
+    }
+  }
+  c->err = err;
+  c->n = err != ~0ull ? 0 : (int64_t)count;
+  if (err != ~0ull) return report_input_error(err);
+  return MK_OK;
+}
+
+namespace {
 
 }  // namespace
 }  // namespace mk
@@ -534,6 +602,20 @@ mk_status mk_coords_quantize(mk_context* ctx, const float* d_points, const int32
   QuantSrc src{d_points, d_batch, D, voxel};
   const int32_t ts[kMaxD] = {1, 1, 1, 1, 1, 1, 1};
   return build_coords(ctx, src, n, D, ts, (cudaStream_t)stream, out, d_point_to_row, d_first_point);
+}
+
+mk_status mk_coords_quantize_deferred(mk_context* ctx, const float* d_points, const int32_t* d_batch, int64_t n,
+                                      int32_t D, float voxel, void* stream, mk_coords** out, int32_t* d_point_to_row,
+                                      int32_t* d_first_point) {
+  clear_error();
+  if (!ctx || !out || (n > 0 && !d_points)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_quantize_deferred: null argument");
+  if (!valid_stream_dim(D)) MK_FAIL(D > MK_MAX_DIM ? MK_ERR_UNSUPPORTED : MK_ERR_INVALID_ARGUMENT,
+                                    "mk_coords_quantize_deferred: D must be in 1..7");
+  if (!(voxel > 0.0f) || !isfinite(voxel))
+    MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_quantize_deferred: voxel must be > 0");
+  QuantSrc src{d_points, d_batch, D, voxel};
+  const int32_t ts[kMaxD] = {1, 1, 1, 1, 1, 1, 1};
+  return build_coords(ctx, src, n, D, ts, (cudaStream_t)stream, out, d_point_to_row, d_first_point, true);
 }
 
 mk_status mk_coords_create(mk_context* ctx, const int32_t* d_coords, int64_t n, int32_t D,
@@ -570,6 +652,8 @@ mk_status mk_coords_stride(mk_context* ctx, const mk_coords* in, const int32_t* 
     src.s[d] = s;
   }
   for (int d = in->D; d < kMaxD; ++d) src.s[d] = 1;
+  const mk_status rs = coords_resolve(in);
+  if (rs != MK_OK) return rs;
   return build_coords(ctx, src, in->n, in->D, ts, (cudaStream_t)stream, out, nullptr, nullptr);
 }
 
@@ -596,6 +680,8 @@ mk_status mk_coords_expand(mk_context* ctx, const mk_coords* in, const mk_region
       MK_FAIL(MK_ERR_STRIDE, "mk_coords_expand: the output stride must divide the input tensor stride");
     src.s[d] = ts[d];
   }
+  st = coords_resolve(in);
+  if (st != MK_OK) return st;
   const int64_t n = in->n * (int64_t)K;
   if (n > INT32_MAX) MK_FAIL(MK_ERR_UNSUPPORTED, "mk_coords_expand: more than 2^31 candidate rows");
   cudaStream_t s = (cudaStream_t)stream;
@@ -620,7 +706,11 @@ mk_status mk_coords_expand(mk_context* ctx, const mk_coords* in, const mk_region
 mk_status mk_coords_info(const mk_coords* c, int64_t* n, int32_t* D, int32_t* h_tensor_stride) {
   clear_error();
   if (!c) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_info: null handle");
-  if (n) *n = c->n;
+  if (n) {
+    const mk_status rs = coords_resolve(c);
+    if (rs != MK_OK) return rs;
+    *n = c->n;
+  }
   if (D) *D = c->D;
   if (h_tensor_stride)
     for (int d = 0; d < c->D; ++d) h_tensor_stride[d] = c->tensor_stride[d];
@@ -629,7 +719,10 @@ mk_status mk_coords_info(const mk_coords* c, int64_t* n, int32_t* D, int32_t* h_
 
 mk_status mk_coords_export(const mk_coords* c, int32_t* d_out, void* stream) {
   clear_error();
-  if (!c || (c->n > 0 && !d_out)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_export: null argument");
+  if (!c) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_export: null argument");
+  const mk_status rs = coords_resolve(c);
+  if (rs != MK_OK) return rs;
+  if (c->n > 0 && !d_out) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_export: null argument");
   if (c->n == 0) return MK_OK;
   k_export<<<grid_for(c->n, 256, 148), 256, 0, (cudaStream_t)stream>>>(c->keys, c->n, c->D, d_out);
   MK_LAUNCH_CHECK();
@@ -666,6 +759,8 @@ mk_status mk_coords_lookup(const mk_coords* c, const int32_t* d_queries, int64_t
 void mk_coords_destroy(mk_coords* c) {
   if (!c) return;
   for (void* p : c->owned) dev_free(c->alloc, p, c->stream);
+  if (c->ev) cudaEventDestroy(c->ev);
+  delete c->mu;
   delete c;
 }
 

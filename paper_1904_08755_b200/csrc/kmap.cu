@@ -596,6 +596,9 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   if (in->D != out->D || region->D != in->D)
     MK_FAIL(MK_ERR_DIMENSION_MISMATCH, "mk_kmap_build: input, output and region must have the same D");
   const int D = in->D;
+  mk_status rs = coords_resolve(in);  // deferred row counts are needed from here on
+  if (rs == MK_OK && out != in) rs = coords_resolve(out);
+  if (rs != MK_OK) return rs;
   const RegionInfo* ri = nullptr;
   mk_status st = region_info(region, &ri);
   if (st != MK_OK) return st;

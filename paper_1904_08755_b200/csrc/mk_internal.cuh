@@ -251,6 +251,10 @@ struct Alloc {
 
 }  // namespace mk
 
+namespace mk {
+struct Mailbox;  // host-mapped result slot (below)
+}  // namespace mk
+
 struct mk_context {
   int device = 0;
   int num_sms = 148;
@@ -263,6 +267,10 @@ struct mk_context {
   // Grid-barrier words of the cooperative sort: kBarSlots pairs, zero-initialised; a call
   // takes the next pair round robin (concurrent calls on different streams get different
   // pairs as long as fewer than kBarSlots sorts are in flight).
+  // Host-mapped mailbox ring of the deferred quantize (lazily allocated, kMbSlots slots).
+  static constexpr unsigned kMbSlots = 1024;
+  mk::Mailbox* mb_ring = nullptr;
+  std::atomic<unsigned long long> mb_seq{0};
   static constexpr unsigned kBarSlots = 256;
   unsigned* d_bar = nullptr;
   std::atomic<unsigned> bar_next{0};
@@ -272,7 +280,16 @@ struct mk_context {
 struct mk_coords {
   mk::Alloc alloc;
   cudaStream_t stream = nullptr;  // stream the handle was created on (frees are ordered there)
+  // Row count; -1 while pending (mk_coords_quantize_deferred): mk::coords_resolve reads it
+  // from the mailbox slot (mb, seq) or, if the slot was reused, from the device words d_res
+  // (error word, count) once the build event has completed.  Guarded by mu.
   int64_t n = 0;
+  mk::Mailbox* mb = nullptr;
+  unsigned long long seq = 0;
+  unsigned long long err = ~0ull;  // input error found by a deferred build (reported at every use)
+  const unsigned long long* d_res = nullptr;
+  cudaEvent_t ev = nullptr;
+  std::mutex* mu = nullptr;
   int32_t D = 0;
   int32_t tensor_stride[MK_MAX_DIM] = {1, 1, 1, 1, 1, 1, 1};
   int4* keys = nullptr;  // [n] packed rows, row order = first occurrence
@@ -370,6 +387,9 @@ struct Mailbox {
   unsigned long long w0, w1, w2;
 };
 Mailbox* mailbox(unsigned long long* next_seq);  // nullptr if pinned memory is unavailable
+// A slot of the context's mailbox ring for a deferred count (its sequence number in *seq);
+// nullptr if the ring cannot be allocated.
+Mailbox* mailbox_ring_slot(mk_context* ctx, unsigned long long* seq);
 // Waits until mb->seq == seq, watching `s` for errors; returns cudaSuccess once posted.
 cudaError_t mailbox_wait(const Mailbox* mb, unsigned long long seq, cudaStream_t s);
 __device__ __forceinline__ void mailbox_post(Mailbox* mb, unsigned long long seq, unsigned long long w0,
@@ -392,6 +412,10 @@ constexpr int kWgradMaxSegs = 63;  // segments per CTA of the bf16 weight-gradie
 // Stable radix sort of keys (low `bits` bits) -> permutation (sort.cu).  Clobbers keys.
 // bar: two zero-initialised device words private to this call's stream (grid barrier of
 // the one-kernel cooperative sort), or nullptr for the three-kernels-per-pass path.
+// Resolves a deferred row count (no-op when known); on an input error reports it like the
+// eager quantize (status + message) and leaves the handle with 0 rows.
+mk_status coords_resolve(const mk_coords* c);
+
 mk_status radix_sort_perm(const Alloc& a, uint32_t* keys, int64_t n, int bits, int32_t* perm, cudaStream_t s,
                           unsigned* bar = nullptr, int num_sms = 148);
 }  // namespace mk

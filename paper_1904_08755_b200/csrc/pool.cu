@@ -410,6 +410,10 @@ extern "C" mk_status mk_global_pool(mk_context* ctx, const mk_coords* c, int32_t
   if (C < 1 || n_batch < 0) MK_FAIL(MK_ERR_SHAPE_MISMATCH, "mk_global_pool: bad sizes");
   if (dt != MK_F32 && dt != MK_BF16) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_global_pool: unknown dtype");
   if (n_batch == 0) return MK_OK;
+  {
+    const mk_status rs = coords_resolve(c);
+    if (rs != MK_OK) return rs;
+  }
   if (!d_fout || (c->n > 0 && !d_fin)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_global_pool: null features");
   const size_t smem = sizeof(float) * (size_t)n_batch * C + sizeof(int32_t) * n_batch;
   if (smem > 200 * 1024) MK_FAIL(MK_ERR_UNSUPPORTED, "mk_global_pool: n_batch * C above 51200");

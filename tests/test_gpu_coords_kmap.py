@@ -252,3 +252,41 @@ def test_expand_and_generative_transposed_conv(mk, orc, K):
     with pytest.raises(mk.MkError) as e:  # the output stride must divide the input stride
         mk.coords_expand(coarse, region, [3, 3, 3])
     assert e.value.name == "MK_ERR_STRIDE"
+
+
+def test_deferred_quantize_matches_eager(mk):
+    # mk_coords_quantize_deferred: same rows, maps and kernel map as the eager call; the count
+    # is collected by the kernel-map build (or Coords.n)
+    pts = torch.from_numpy(synthetic.room_points(2000)).cuda()
+    c0, p0, f0 = mk.coords_quantize(pts, synthetic.ROOM_VOXEL)
+    c1, p1, f1 = mk.coords_quantize(pts, synthetic.ROOM_VOXEL, deferred=True)
+    assert f1.shape[0] == pts.shape[0]  # full capacity
+    m1 = mk.kmap_build(c1, c1, mk.Region(mk.HYPERCUBE, 3, 3))  # resolves the count
+    assert c1.n == c0.n
+    assert torch.equal(c1.export(), c0.export())
+    assert torch.equal(p1, p0) and torch.equal(f1[: c1.n], f0)
+    m0 = mk.kmap_build(c0, c0, mk.Region(mk.HYPERCUBE, 3, 3))
+    for a, b in zip(mk.kmap_export(m1), mk.kmap_export(m0)):
+        assert torch.equal(a, b)
+
+
+def test_deferred_quantize_reports_errors_at_first_use(mk):
+    pts = torch.rand((500, 3), device="cuda")
+    pts[137, 1] = float("nan")
+    c = mk.coords_quantize(pts, 0.1, return_maps=False, deferred=True)  # enqueued, no wait
+    with pytest.raises(mk.MkError) as e:
+        _ = c.n
+    assert e.value.name == "MK_ERR_NONFINITE_INPUT" and e.value.row == 137
+    with pytest.raises(mk.MkError):
+        mk.kmap_build(c, c, mk.Region(mk.HYPERCUBE, 3, 3))
+
+
+def test_deferred_quantize_mailbox_slot_reuse(mk):
+    # more pending handles than mailbox slots (1024): the oldest ones find their slot reused
+    # and fall back to the device words once their build event has completed
+    g = np.random.default_rng(9)
+    pts = [torch.from_numpy(g.random((200 + i % 7, 3)).astype(np.float32)).cuda() for i in range(8)]
+    want = [mk.coords_quantize(p, 0.05, return_maps=False).n for p in pts]
+    hs = [mk.coords_quantize(pts[i % 8], 0.05, return_maps=False, deferred=True) for i in range(1100)]
+    torch.cuda.synchronize()
+    assert [h.n for h in hs] == [want[i % 8] for i in range(1100)]
