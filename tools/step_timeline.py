@@ -23,7 +23,7 @@ flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
 
 def step():
-    c, _, _ = mk.coords_quantize(pts, synthetic.ROOM_VOXEL, return_maps=True)
+    c, _, _ = mk.coords_quantize(pts, synthetic.ROOM_VOXEL, return_maps=True, deferred=True)
     m = mk.kmap_build(c, c, region)
     mk.conv_forward(m, X, W)
     mk.conv_backward(m, G, X, W, need_gin=True, need_gw=False)
