@@ -55,8 +55,10 @@ mk_status backward_impl(mk_context* ctx, const mk_kmap* m, const void* d_gout, c
     if (dt == MK_F32) {
       st = kmap_host(m);  // per-offset pair counts on the host (waits for the build only)
       if (st != MK_OK) return st;
-      // split-K plan: chunks of <= 4096 pairs per offset
-      const int64_t P = 4096;
+      // split-K plan: chunks of <= P pairs per offset, P = 4096 or smaller so that the grid has
+      // about 4 chunks per SM (small maps / few channels: a 7D CRF map has 600k pairs of 16 ch)
+      int64_t P = 4096;
+      while (P > 256 && m->h_ptr[m->K] / P < 4 * (int64_t)ctx->num_sms) P >>= 1;
       std::vector<int4> chunks;
       std::vector<int32_t> begin(m->K + 1, 0);
       for (int k = 0; k < m->K; ++k) {

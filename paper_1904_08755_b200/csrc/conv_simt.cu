@@ -180,10 +180,57 @@ mk_status launch_conv_f32(const NbrView& nb, const float* x, int c_x, const floa
   return MK_OK;
 }
 
+// Small channel counts (c_out, c_in <= 32, e.g. the TS-CRF's classes): the whole C_out x C_in
+// partial in one CTA, one output element per thread (up to 4), pairs staged 64 at a time.
+constexpr int kSmallPairs = 64;
+__global__ void __launch_bounds__(256) k_wgrad_f32_small(const int4* __restrict__ chunks,
+                                                         const int32_t* __restrict__ in_idx,
+                                                         const int32_t* __restrict__ out_idx,
+                                                         const float* __restrict__ g, int c_out,
+                                                         const float* __restrict__ x, int c_in,
+                                                         float* __restrict__ part) {
+  __shared__ float s_g[kSmallPairs][33];
+  __shared__ float s_x[kSmallPairs][33];
+  const int4 ch = chunks[blockIdx.x];  // (k, begin, end, chunk id)
+  const int te = c_out * c_in;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int p0 = ch.y; p0 < ch.z; p0 += kSmallPairs) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < kSmallPairs * 32; i += blockDim.x) {
+      const int pp = i >> 5, c = i & 31;
+      const int p = p0 + pp;
+      const bool in = p < ch.z;
+      s_g[pp][c] = in && c < c_out ? g[(int64_t)out_idx[p] * c_out + c] : 0.f;
+      s_x[pp][c] = in && c < c_in ? x[(int64_t)in_idx[p] * c_in + c] : 0.f;
+    }
+    __syncthreads();
+    const int np = min(kSmallPairs, ch.z - p0);
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int e = threadIdx.x + r * 256;
+      if (e >= te) break;
+      const int co = e / c_in, ci = e - co * c_in;
+      float a = acc[r];
+      for (int pp = 0; pp < np; ++pp) a = fmaf(s_g[pp][co], s_x[pp][ci], a);
+      acc[r] = a;
+    }
+  }
+  float* out = part + (int64_t)ch.w * te;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int e = threadIdx.x + r * 256;
+    if (e < te) out[e] = acc[r];
+  }
+}
+
 mk_status launch_wgrad_f32(const mk_kmap* m, const WgradPlan& plan, const float* g, int c_out, const float* x,
                            int c_in, float* dW, cudaStream_t s) {
-  dim3 grid((unsigned)plan.n_chunks, (unsigned)ceil_div(c_out, 64), (unsigned)ceil_div(c_in, 64));
-  if (plan.n_chunks > 0) {
+  if (plan.n_chunks > 0 && c_out <= 32 && c_in <= 32) {
+    k_wgrad_f32_small<<<(unsigned)plan.n_chunks, 256, 0, s>>>(plan.chunks, m->in_idx, m->out_idx, g, c_out, x, c_in,
+                                                              plan.part);
+    MK_LAUNCH_CHECK();
+  } else if (plan.n_chunks > 0) {
+    dim3 grid((unsigned)plan.n_chunks, (unsigned)ceil_div(c_out, 64), (unsigned)ceil_div(c_in, 64));
     k_wgrad_f32<<<grid, kThreads, 0, s>>>(plan.chunks, m->in_idx, m->out_idx, g, c_out, x, c_in, plan.part);
     MK_LAUNCH_CHECK();
   }

@@ -46,13 +46,17 @@ __global__ void __launch_bounds__(256) k_crf_softmax(const float* __restrict__ p
 // (32 / Cp nodes per warp); lane j computes class j: the neighbour indices are broadcast
 // within the group, the neighbour's Q row is spread over the group and broadcast one class
 // at a time.  W lives in shared memory.  Fixed summation order (k, then c): deterministic.
+// SOFTMAX = false: the convolution alone (out = sum_k W_k Q_in[a_k], or with trans = 1 the
+// transposed weights W_k^T: the input gradient of Eq. 5's backward pass on the reverse view).
+template <bool SOFTMAX>
 __global__ void __launch_bounds__(256) k_crf_step(NbrView nb, int64_t n_rows, const float* __restrict__ phi,
                                                   const float* __restrict__ q_in, const float* __restrict__ W, int C,
-                                                  int Cp, float* __restrict__ q_out) {
+                                                  int Cp, float* __restrict__ q_out, int trans) {
   extern __shared__ float s_w[];  // [K][c][j] = W[k][j][c] (lanes j read consecutive words)
   for (int i = threadIdx.x; i < nb.K * C * C; i += blockDim.x) {
     const int k = i / (C * C), r = i - k * C * C, jj = r / C, c = r - jj * C;
-    s_w[(k * C + c) * C + jj] = W[i];
+    if (trans) s_w[(k * C + jj) * C + c] = W[i];  // W^T[k][c][jj] = W[k][jj][c]
+    else s_w[(k * C + c) * C + jj] = W[i];
   }
   __syncthreads();
   const int lane = threadIdx.x & 31, j = lane & (Cp - 1);
@@ -88,8 +92,12 @@ __global__ void __launch_bounds__(256) k_crf_step(NbrView nb, int64_t n_rows, co
       }
       __syncwarp();
     }
-    // softmax over the group's C classes
     const int64_t o = valid ? nb.row_of(pos) : 0;
+    if (!SOFTMAX) {
+      if (valid && j < C) q_out[o * C + j] = acc;
+      continue;
+    }
+    // softmax over the group's C classes
     const float v = (valid && j < C) ? __ldg(phi + o * C + j) + acc : -INFINITY;
     float m = v;
     for (int w = Cp / 2; w > 0; w >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, w, Cp));
@@ -134,7 +142,8 @@ extern "C" mk_status mk_crf_infer(mk_context* ctx, const mk_kmap* m, const float
     for (int it = 0; it < n_iters; ++it) {
       const float* src = bufs[it & 1];
       float* dst = bufs[(it + 1) & 1];
-      k_crf_step<<<g2, 256, sizeof(float) * (v.K * C * C + 256 * Cp), s>>>(v, n, d_phi_u, src, d_W, C, Cp, dst);
+      k_crf_step<true><<<g2, 256, sizeof(float) * (v.K * C * C + 256 * Cp), s>>>(v, n, d_phi_u, src, d_W, C, Cp, dst,
+                                                                                 0);
       g_launches++;
     }
     cudaError_t e2 = cudaSuccess;
@@ -229,7 +238,19 @@ extern "C" mk_status mk_crf_backward(mk_context* ctx, const mk_kmap* m, const fl
   mk_status st = MK_OK;
   k_crf_softmax<<<grid, 256, 0, s>>>(d_phi_u, nullptr, n, C, Q);  // Q^0
   g_launches++;
+  // C <= 32: the fused group-per-node kernels of mk_crf_infer (conv + softmax forward,
+  // transposed-weight conv backward); larger C: the generic FFMA conv
+  const size_t fsmem = sizeof(float) * ((size_t)v.K * C * C + 256 * 32);
+  const bool fused = C <= 32 && fsmem <= 48 * 1024;
+  int Cp = 1;
+  while (Cp < C) Cp <<= 1;
+  const unsigned g2 = (unsigned)std::min<int64_t>(ceil_div(ceil_div(n, 32 / Cp), 8), 6 * ctx->num_sms);
   for (int it = 0; it < n_iters && st == MK_OK; ++it) {
+    if (fused) {
+      k_crf_step<true><<<g2, 256, fsmem, s>>>(v, n, d_phi_u, Q + it * nc, d_W, C, Cp, Q + (it + 1) * nc, 0);
+      g_launches++;
+      continue;
+    }
     st = launch_conv_f32(v, Q + it * nc, C, d_W, C, C, tmp, C, MK_F32, n, false, s);
     if (st == MK_OK) {
       k_crf_softmax<<<grid, 256, 0, s>>>(d_phi_u, tmp, n, C, Q + (it + 1) * nc);
@@ -244,7 +265,13 @@ extern "C" mk_status mk_crf_backward(mk_context* ctx, const mk_kmap* m, const fl
     k_crf_softmax_bwd<<<grid, 256, 0, s>>>(Q + it * nc, g_cur, n, C, tmp, d_gphi, it == n_iters);
     g_launches++;
     // dQ^(it-1) = conv dgrad of dA; dW_it = wgrad(dA, Q^(it-1))
-    st = mk_conv_backward(ctx, m, tmp, Q + (it - 1) * nc, d_W, C, C, MK_F32, g_prev, gw_tmp, stream);
+    if (fused) {
+      k_crf_step<false><<<g2, 256, fsmem, s>>>(dgrad_view(m), n, nullptr, tmp, d_W, C, Cp, g_prev, 1);
+      g_launches++;
+      st = mk_conv_backward(ctx, m, tmp, Q + (it - 1) * nc, d_W, C, C, MK_F32, nullptr, gw_tmp, stream);
+    } else {
+      st = mk_conv_backward(ctx, m, tmp, Q + (it - 1) * nc, d_W, C, C, MK_F32, g_prev, gw_tmp, stream);
+    }
     if (st == MK_OK) {
       k_axpy<<<wgrid, 256, 0, s>>>(gw_tmp, wn, d_gW, it == n_iters);
       g_launches++;
