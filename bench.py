@@ -222,11 +222,14 @@ def run_mk(args, ws, rank, local):
     # would do: H2D of the points first (quantize needs them), then features and weights
     # (fwd), then the output gradient (dgrad) while the coordinates and the map are built;
     # each result goes back D2H as soon as its kernel finished (y during dgrad, grad_in
-    # during wgrad).  The step is PCIe bound: 84 MB cross the link per step.
+    # during wgrad).  Consecutive steps are pipelined like a streaming training loop: step
+    # i+1's uploads overlap step i's downloads (PCIe is full duplex); every step still moves
+    # all of its own inputs and results.  84 MB cross PCIe per step, so e2e is PCIe bound.
     h2d_s, d2h_s = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
 
-    def e2e_step(start):
-        h2d_s.wait_event(start)
+    def e2e_step(start=None):
+        if start is not None:
+            h2d_s.wait_event(start)
         with torch.cuda.stream(h2d_s):
             p = pts_p.to(dev, non_blocking=True)
             ev_p = torch.cuda.Event()
@@ -239,10 +242,12 @@ def run_mk(args, ws, rank, local):
             ev_g.record(h2d_s)
         for t in (p, x, w, g):
             t.record_stream(stream)
+        flush.zero_()  # L2 flush before this step's compute (inside the timed region)
         stream.wait_event(ev_p)
         c, _, _ = mk.coords_quantize(p, synthetic.ROOM_VOXEL, deferred=True)
         m = mk.kmap_build(c, c, region)
         stream.wait_event(ev_x)
+
         def to_host(dev_t, host_t):  # D2H on its own stream as soon as dev_t is ready
             ev = torch.cuda.Event()
             ev.record(stream)
@@ -260,21 +265,27 @@ def run_mk(args, ws, rank, local):
         if ws > 1:
             allreduce_grad(gw)
         to_host(gw, gw_p)
-        stream.wait_stream(d2h_s)
 
-    for _ in range(2):
-        st0 = torch.cuda.Event()
-        st0.record(stream)
-        e2e_step(st0)
+    # warm-up: at least W steps and 0.3 s of transfers (an idle PCIe link trains up to full
+    # speed only under sustained traffic; the first e2e of a fresh process was 3-5x slower)
+    tw, nw = time.time(), 0
+    while nw < max(args.warmup, 3) or time.time() - tw < 0.3:
+        e2e_step()
+        nw += 1
+        if nw % 4 == 0:
+            torch.cuda.synchronize()
+    stream.wait_stream(d2h_s)
     torch.cuda.synchronize()
-    e_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    if ws > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
     for i in range(args.steps):
-        flush.zero_()
-        e_ev[i][0].record(stream)
-        e2e_step(e_ev[i][0])
-        e_ev[i][1].record(stream)
+        e2e_step(e0 if i == 0 else None)
+    stream.wait_stream(d2h_s)  # the last results are on the host
+    e1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = float(sum(a.elapsed_time(b) for a, b in e_ev))
+    e2e_ms = float(e0.elapsed_time(e1))
     if ws > 1:
         t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
