@@ -410,6 +410,24 @@ def run_mk(args, ws, rank, local):
     roof.update({"frac": round(roof["achieved"] / roof["peak"], 4), "traffic": traffic, "kernel": dom,
                  "kernel_us": round(dom_ms * 1e3, 2), "algorithmic_flops": flops_pass,
                  "algorithmic_bytes": bytes_alg, "arith_intensity": round(ai, 1), "peak_source": pk["source"]})
+    # The bound that actually binds the gather-GEMMs: L2 -> SM traffic of the
+    # random row gathers (ncu l1tex__m_xbar2l1tex_read_bytes per launch, profiles/) over the
+    # same live phase time, against the gather ceiling measured by tools/ubench_gather.cu
+    # (cp.async warp-stage gathers of the same 150k x 128 B table, profiles/ubench_gather_r01.txt).
+    gather = None
+    ub = ROOT / "profiles" / "ubench_gather_r01.txt"
+    try:
+        l2sm = json.loads(summ.read_text())["kernels"][dom]["l2_to_sm_bytes"] if summ.exists() else None
+        ceil = max(float(ln.split("TB/s")[0].split()[-1]) for ln in ub.read_text().splitlines()
+                   if ln.startswith("cp.async warp-stage")) if ub.exists() else None
+    except (ValueError, KeyError, AttributeError):
+        l2sm, ceil = None, None
+    if l2sm and ceil:
+        ach = l2sm / (dom_ms * 1e-3) / 1e12
+        gather = {"bound": "l2_gather", "achieved": round(ach, 2), "peak": ceil, "unit": "TB/s",
+                  "frac": round(ach / ceil, 4), "bytes_per_launch": l2sm, "kernel": dom,
+                  "source": "ncu l2->sm bytes (profiles/ncu_summary.json) / live phase time; "
+                            "ceiling tools/ubench_gather.cu"}
 
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -425,6 +443,7 @@ def run_mk(args, ws, rank, local):
         "gpu_launches": int(launches),
         "extras_f1_f4": extras,
         "roofline": roof,
+        "roofline_gather": gather,
         "clocks": clocks,
     }
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
