@@ -676,7 +676,14 @@ constexpr int kMaxSegs = kWgradMaxSegs + 1;  // per-CTA plan capacity (kmap_wpla
 // (M = C_out padded to 128 with a constant zero panel, N = C_in, K = 16 pairs), commits
 // stage slots in groups, and publishes the segment to the epilogue, which writes the fp32
 // partial dW_k tile of the segment's slot.
-__global__ void __launch_bounds__(kThreads, 1) k_wgrad_umma(const __grid_constant__ WgradParams p) {
+// NP producer warps (>= the stage slots in use); NP = 16: one CTA per SM; NP = 8: two CTAs
+// per SM; NP = 4: three (shared memory split accordingly).
+template <int NP>
+__global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
+    k_wgrad_umma(const __grid_constant__ WgradParams p) {
+  constexpr int kEpiWarp0 = NP;                    // epilogue warps (TMEM lane quarters 0-3)
+  constexpr int kMmaWarp = NP + kEpiWarps;         // the MMA issuer
+  constexpr int kThreads = (NP + kEpiWarps + 1) * 32;
   constexpr int PS = kPairsPerStage;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
@@ -1126,9 +1133,17 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   p.a_bytes = (uint32_t)(p.halves * p.mrows) * kPairsPerStage * 2;  // M padded to 64 / 128 per half
   p.b_bytes = (uint32_t)c_in * kPairsPerStage * 2;
   p.slot_bytes = (p.a_bytes + p.b_bytes + 1023) & ~1023u;
-  const int reserve = 1024 + 1024 + kProdWarps * 4 * kPairsPerStage * 4 + (kMaxSegs + 2) * 4 +
+  static const int np_env = [] {  // producer warps: 8 (two CTAs per SM, default), 16 or 4
+    const char* v = std::getenv("MK_WGRAD_NP");
+    const int x = v ? std::atoi(v) : 8;
+    return x == 16 || x == 4 ? x : 8;
+  }();
+  const int np = np_env;
+  const int per_sm = np == 16 ? 1 : np == 8 ? 2 : 3;
+  const int budget = per_sm == 1 ? kMaxSmem : kMaxSmem / per_sm - 1024;
+  const int reserve = 1024 + 1024 + np * 4 * kPairsPerStage * 4 + (kMaxSegs + 2) * 4 +
                       (int)sizeof(int4) * kMaxSegs + 64;
-  p.sa = std::min(kProdWarps, (kMaxSmem - reserve) / (int)p.slot_bytes);
+  p.sa = std::min(np, (budget - reserve) / (int)p.slot_bytes);
   if (p.sa >= 8) p.sa -= p.sa % 4;
   p.ga = p.sa % 4 == 0 ? 4 : p.sa % 2 == 0 ? 2 : 1;
   p.tmem_cols = pow2_cols((uint32_t)(p.halves * c_in));
@@ -1137,12 +1152,17 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   float* part = nullptr;
   if (dev_plan) {
     if (m->n_out > 0 && m->n_in > 0) {
-      const int n_cta = ctx->num_sms;
+      const int n_cta = ctx->num_sms * per_sm;
       part = (float*)dev_alloc(ctx->alloc, sizeof(float) * (n_cta + m->K) * te, s);
       if (!part) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 wgrad: workspace allocation failed");
       p.part = part;
-      set_smem_once(k_wgrad_umma, smem);
-      pdl_launch(k_wgrad_umma, n_cta, kThreads, smem, s, p);
+      auto go = [&](auto kern, int threads) {
+        set_smem_once(kern, smem);
+        pdl_launch(kern, n_cta, threads, smem, s, p);
+      };
+      if (np == 16) go(k_wgrad_umma<16>, (16 + kEpiWarps + 1) * 32);
+      else if (np == 8) go(k_wgrad_umma<8>, (8 + kEpiWarps + 1) * 32);
+      else go(k_wgrad_umma<4>, (4 + kEpiWarps + 1) * 32);
       dim3 rg((unsigned)ceil_div(te, 256), (unsigned)m->K);
       pdl_launch(k_reduce_partials_dev, rg, 256, 0, s, (const int64_t*)m->ptr, n_cta, (const float*)part, te, dW);
     } else {
@@ -1154,8 +1174,8 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
       part = (float*)dev_alloc(ctx->alloc, sizeof(float) * m->n_wslots * te, s);
       if (!part) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 wgrad: workspace allocation failed");
       p.part = part;
-      set_smem_once(k_wgrad_umma, smem);
-      pdl_launch(k_wgrad_umma, m->n_wcta, kThreads, smem, s, p);
+      set_smem_once(k_wgrad_umma<16>, smem);
+      pdl_launch(k_wgrad_umma<16>, m->n_wcta, (16 + kEpiWarps + 1) * 32, smem, s, p);
     }
     dim3 rg((unsigned)ceil_div(te, 256), (unsigned)m->K);
     k_reduce_partials<<<rg, 256, 0, s>>>(m->wslot_begin, part, te, dW);
