@@ -1058,13 +1058,26 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   p.fold = env_fold > 0 ? 1 : 0;
   p.tb = p.fold ? std::max(1, std::min(env_fold, 256 / c_y)) : std::max(1, std::min(2, 256 / c_y));
   p.tmem_cols = pow2_cols((uint32_t)(p.tb * c_y));
+  static const int env_ctas0 = [] {  // CTAs per SM the smem budget aims at: 3 (default) or 2
+    const char* e = std::getenv("MK_FWD_CTAS");
+    return e && std::atoi(e) == 2 ? 2 : 3;
+  }();
+  // Three CTAs per SM (configs[1] fwd 65.4 -> 62.9 us, dgrad 64.3 -> 62.2 us) when two stage
+  // slots and the W ring fit a third of the SM and the registers allow it (the fused-epilogue
+  // instance needs 84 registers: two CTAs).
+  const int env_ctas = env_ctas0 == 3 && !ep.active() && 1024 + 512 + kFwdProd * 3 * kTileM * 4 + (int)sizeof(Plan) +
+                                             nch * 2 * (int)(c_y * CH * 2) + 2 * kTileM * CH * 2 <=
+                                             kMaxSmem / 3 - 1024
+                           ? 3
+                           : 2;
   const int base = 1024 + 512 + kFwdProd * 3 * kTileM * 4 + (int)sizeof(Plan);
   p.sw = nch * 2;
-  if (base + p.sw * (int)p.b_bytes + kFwdProd * (int)p.a_bytes <= kMaxSmem / 2 - 1024 - 2 * nch * (int)p.b_bytes)
+  if (env_ctas == 2 &&
+      base + p.sw * (int)p.b_bytes + kFwdProd * (int)p.a_bytes <= kMaxSmem / 2 - 1024 - 2 * nch * (int)p.b_bytes)
     p.sw = nch * 4;
   const int fixed = base + p.sw * (int)p.b_bytes;
-  p.sa = std::min(kFwdProd, (kMaxSmem - fixed) / (int)p.a_bytes);
-  p.sa -= p.sa % 2;
+  p.sa = std::min(kFwdProd, ((env_ctas == 2 ? kMaxSmem : kMaxSmem / 3 - 1024) - fixed) / (int)p.a_bytes);
+  if (env_ctas == 2) p.sa -= p.sa % 2;
   static const int env_np = [] {
     const char* e = std::getenv("MK_FWD_NP");
     return e ? std::atoi(e) : 0;
