@@ -200,7 +200,8 @@ mk_status mk_context_create(int device, mk_alloc_fn alloc, mk_free_fn free_fn, v
   c->alloc.alloc = alloc;
   c->alloc.free_fn = free_fn;
   c->alloc.user = user;
-  if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess) {
+  if (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess) {
     delete c;
     MK_FAIL(MK_ERR_CUDA, "mk_context_create: stream creation failed");
   }
@@ -219,6 +220,7 @@ void mk_context_destroy(mk_context* ctx) {
   if (ctx->d_bar) cudaFree(ctx->d_bar);
   if (ctx->mb_ring) cudaFreeHost(ctx->mb_ring);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   delete ctx;
 }
 

@@ -21,6 +21,8 @@
 #include <deque>
 #include <map>
 
+#include <cstdlib>
+
 #include "mk_internal.cuh"
 
 namespace mk {
@@ -742,6 +744,23 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     ck(cudaMemsetAsync(m->tile_maskT, 0, sizeof(uint32_t) * ntilesT * mw, s));
   }
   ht.mark("setup");
+  static const bool fork_env = [] {
+    const char* v = std::getenv("MK_KMAP_FORK");
+    return !(v && v[0] == '0');
+  }();
+  const bool fork = fork_env && rm && n_out > 0 && symmetric && ctx->side;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  mk_status fork_st = MK_OK;
+  if (rm && n_out > 0) {  // allocated on s before any fork (stream-ordered)
+    m->perm = (int32_t*)alloc(sizeof(int32_t) * n_pad);
+    if (!m->perm) return oom();
+  }
+  auto sort_and_permute = [&](cudaStream_t ss) {
+    fork_st = radix_sort_perm(m->alloc, rowmask, n_out, K, m->perm, ss, ctx->barrier_slot(), ctx->num_sms);
+    if (fork_st == MK_OK)
+      ck(pdl_launch(k_permute_rm, (unsigned)ntiles, kTileRows, 0, ss, nbr_rm, n_pad, n_out, K, m->perm, m->nbr,
+                    m->tile_mask, symmetric ? m->d_mirror : nullptr, m->tile_maskT));
+  };
   if (n_out > 0) {
     const size_t smem = sizeof(int32_t) * (4 * K + K * D + kRM + kTileRows * kRMPitch);
     if (smem > 48 * 1024) {
@@ -754,6 +773,17 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
     else
       ck(pdl_launch(k_probe<false>, (unsigned)ntiles, kThreads, smem, s, out->keys, n_out, n_pad, in->table.buckets,
                     in->table.bmask, d_offs, K, D, sign, scale4, m->nbr, tile_cnt, ntiles, m->tile_mask, mw, nullptr));
+    // Symmetric row-ordered maps: the row sort and the permuted table depend only on the probe,
+    // the pair lists only on the probe and the scan, so the sort + permute run on the
+    // context's side stream concurrently with scan + emit (joined before the build ends).
+    if (fork) {
+      ck(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+      ck(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+      ck(cudaEventRecord(ev_fork, s));
+      ck(cudaStreamWaitEvent(ctx->side, ev_fork, 0));
+      sort_and_permute(ctx->side);
+      ck(cudaEventRecord(ev_join, ctx->side));
+    }
     ck(pdl_launch(k_scan, K, 1024, 0, s, tile_cnt, ntiles, tile_off, totals));
     ht.mark("probe+scan");
   } else {
@@ -808,14 +838,13 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
   // rows sharing offsets share tiles, so the tensor-core kernels skip empty (tile, k) units.
   // The permutation is internal; the CSR above and all exported row orders are unchanged.
   if (rm && n_out > 0) {
-    m->perm = (int32_t*)alloc(sizeof(int32_t) * n_pad);
-    if (!m->perm) return oom();
-    ht.mark("emit");
-    st = radix_sort_perm(m->alloc, rowmask, n_out, K, m->perm, s, ctx->barrier_slot(), ctx->num_sms);
-    ht.mark("sort");
-    if (st == MK_OK) {
-      ck(pdl_launch(k_permute_rm, (unsigned)ntiles, kTileRows, 0, s, nbr_rm, n_pad, n_out, K, m->perm, m->nbr,
-                    m->tile_mask, symmetric ? m->d_mirror : nullptr, m->tile_maskT));
+    if (fork) {
+      ck(cudaStreamWaitEvent(s, ev_join, 0));
+      st = fork_st;
+    } else {
+      ht.mark("emit");
+      sort_and_permute(s);
+      st = fork_st;
     }
     if (st == MK_OK && !symmetric && n_in > 0) {
       ck(pdl_launch(k_rowmask_T, (unsigned)std::min<int64_t>(ceil_div(n_in, 256), 4096), 256, 0, s, m->nbrT, nT_pad,
@@ -837,6 +866,8 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
                   ntiles, mw, m->d_mirror, K, m->tile_maskT));
   }
   if (symmetric) m->permT = m->perm;  // same row set, mirrored masks: same ordering
+  if (ev_fork) cudaEventDestroy(ev_fork);  // released once complete
+  if (ev_join) cudaEventDestroy(ev_join);
   ck(cudaGetLastError());
   free_scratch();  // stream-ordered: after every kernel above
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&m->done, cudaEventDisableTiming);

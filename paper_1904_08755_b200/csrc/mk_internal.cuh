@@ -260,6 +260,7 @@ struct mk_context {
   int num_sms = 148;
   mk::Alloc alloc;
   cudaStream_t aux = nullptr;  // private non-blocking stream for small lazy read-backs
+  cudaStream_t side = nullptr;  // private non-blocking stream: map-build work forked off the caller's stream
   // Device copies of kernel-region tables (offsets, then mirror indices), uploaded once per
   // region and kept for the context's lifetime (mk::region_device).
   std::mutex region_mu;

@@ -169,6 +169,9 @@ __global__ void __launch_bounds__(kThreads) k_radix_scatter(const uint32_t* __re
 //      also counts its next-pass digit into cnt_{p+1}[d'][pos / T] (global atomics), so
 //      later passes need no H phase                                              | barrier
 constexpr int kCT = 512;
+#ifndef MK_SORT_MINB
+#define MK_SORT_MINB 1
+#endif
 constexpr int kCW = kCT / 32;
 constexpr int kCR = 4;  // chunks of a tile held in registers (tiles up to 2048 keys)
 
@@ -204,7 +207,7 @@ __device__ __forceinline__ void grid_barrier_done(unsigned* bar, unsigned G) {
 }
 
 template <int RB>
-__global__ void __launch_bounds__(kCT, 1) k_radix_sort_coop(uint32_t* __restrict__ keys, uint32_t* __restrict__ k2,
+__global__ void __launch_bounds__(kCT, MK_SORT_MINB) k_radix_sort_coop(uint32_t* __restrict__ keys, uint32_t* __restrict__ k2,
                                                             int32_t* __restrict__ v1, int32_t* __restrict__ v2,
                                                             int32_t* __restrict__ perm, int64_t n, int passes,
                                                             int rb, uint32_t* __restrict__ cnt,
