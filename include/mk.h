@@ -315,6 +315,12 @@ const char* mk_last_error_message(void);
 int64_t mk_last_error_row(void);
 /* Number of library kernels launched by this process so far (bench "gpu_launches"). */
 int64_t mk_kernel_launch_count(void);
+/* The stable radix sort the map builder uses to order rows by neighbour bitmask, exposed
+ * for testing: d_perm (device int32 [n]) receives the permutation that sorts the low `bits`
+ * (1..32) bits of d_keys (device uint32 [n], not modified) stably; ctx's cooperative
+ * one-kernel path unless MK_SORT_COOP=0.  Asynchronous. */
+mk_status mk_debug_sort_perm(mk_context* ctx, const uint32_t* d_keys, int64_t n, int32_t bits, int32_t* d_perm,
+                             void* stream);
 
 #ifdef __cplusplus
 }

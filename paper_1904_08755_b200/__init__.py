@@ -487,3 +487,14 @@ def crf_backward(m: KernelMap, phi_u: torch.Tensor, W: torch.Tensor, n_iters: in
         _check(_L.mk_crf_backward(context(phi.device.index), m._h, _ptr(phi), _ptr(w), C, int(n_iters), _ptr(g),
                                   _ptr(gphi), _ptr(gw), _stream(phi)), "mk_crf_backward")
     return gphi, gw
+
+
+def debug_sort_perm(keys: torch.Tensor, bits: int) -> torch.Tensor:
+    """The map builder's stable radix sort (mk_debug_sort_perm): permutation sorting the low
+    `bits` bits of uint32 keys (given as int32 / int64 tensors of non-negative values)."""
+    k = _cuda(keys, torch.int32, "keys")
+    perm = torch.empty(k.shape[0], dtype=torch.int32, device=k.device)
+    with _on_device(k.device):
+        _check(_L.mk_debug_sort_perm(context(k.device.index), _ptr(k), k.shape[0], int(bits), _ptr(perm),
+                                     _stream(k)), "mk_debug_sort_perm")
+    return perm

@@ -46,7 +46,7 @@ EXPORTS = [
     "mk_kmap_build", "mk_kmap_info", "mk_kmap_export", "mk_kmap_destroy",
     "mk_conv_forward", "mk_conv_forward_fused", "mk_conv_backward", "mk_conv_transpose_forward", "mk_conv_transpose_backward",
     "mk_pool_forward", "mk_pool_backward", "mk_global_pool", "mk_crf_infer", "mk_crf_backward",
-    "mk_last_error_message", "mk_last_error_row", "mk_kernel_launch_count",
+    "mk_last_error_message", "mk_last_error_row", "mk_kernel_launch_count", "mk_debug_sort_perm",
 ]
 
 
@@ -78,6 +78,7 @@ def load() -> ctypes.CDLL:
         "mk_global_pool": [P, P, i32, P, i32, ctypes.c_int, i32, P, P],
         "mk_crf_infer": [P, P, P, P, i32, i32, P, P],
         "mk_crf_backward": [P, P, P, P, i32, i32, P, P, P, P],
+        "mk_debug_sort_perm": [P, P, i64, i32, P, P],
         "mk_conv_transpose_forward": [P, P, P, i32, P, P, i32, ctypes.c_int, ctypes.c_int, P],
         "mk_conv_backward": [P, P, P, P, P, i32, i32, ctypes.c_int, P, P, P],
         "mk_conv_transpose_backward": [P, P, P, P, P, i32, i32, ctypes.c_int, P, P, P],

@@ -468,3 +468,24 @@ mk_status radix_sort_perm(const Alloc& a, uint32_t* keys, int64_t n, int bits, i
 }
 
 }  // namespace mk
+
+extern "C" mk_status mk_debug_sort_perm(mk_context* ctx, const uint32_t* d_keys, int64_t n, int32_t bits,
+                                        int32_t* d_perm, void* stream) {
+  using namespace mk;
+  clear_error();
+  if (!ctx || n < 0 || (n > 0 && (!d_keys || !d_perm)) || bits < 1 || bits > 32)
+    MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_debug_sort_perm: bad argument");
+  if (n == 0) return MK_OK;
+  if (n > INT32_MAX) MK_FAIL(MK_ERR_UNSUPPORTED, "mk_debug_sort_perm: more than 2^31 keys");
+  cudaStream_t s = (cudaStream_t)stream;
+  uint32_t* k = (uint32_t*)dev_alloc(ctx->alloc, sizeof(uint32_t) * n, s);  // the sort clobbers its keys
+  if (!k) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "mk_debug_sort_perm: allocation failed");
+  const cudaError_t e = cudaMemcpyAsync(k, d_keys, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) {
+    dev_free(ctx->alloc, k, s);
+    MK_FAIL(MK_ERR_CUDA, std::string("mk_debug_sort_perm: ") + cudaGetErrorString(e));
+  }
+  const mk_status st = radix_sort_perm(ctx->alloc, k, n, bits, d_perm, s, ctx->barrier_slot(), ctx->num_sms);
+  dev_free(ctx->alloc, k, s);
+  return st;
+}
