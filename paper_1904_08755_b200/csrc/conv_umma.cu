@@ -1158,7 +1158,14 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
                       (int)sizeof(int4) * kMaxSegs + 64;
   p.sa = std::min(np, (budget - reserve) / (int)p.slot_bytes);
   if (p.sa >= 8) p.sa -= p.sa % 4;
-  p.ga = p.sa % 4 == 0 ? 4 : p.sa % 2 == 0 ? 2 : 1;
+  // stage slots released per commit: grouped at one CTA per SM (a commit drains the tensor
+  // pipe), one per commit when another CTA hides the drain (wgrad 85.9 -> 82.4 us, configs[1])
+  p.ga = per_sm >= 2 ? 1 : p.sa % 4 == 0 ? 4 : p.sa % 2 == 0 ? 2 : 1;
+  static const int env_ga = [] {  // development: stage slots released per commit
+    const char* e = std::getenv("MK_WGRAD_GA");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (env_ga > 0 && p.sa % env_ga == 0) p.ga = env_ga;
   p.tmem_cols = pow2_cols((uint32_t)(p.halves * c_in));
   if (p.sa < 2 || p.tmem_cols > 512) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: channel counts too large");
   const int smem = p.sa * (int)p.slot_bytes + reserve;
