@@ -1146,10 +1146,12 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   p.a_bytes = (uint32_t)(p.halves * p.mrows) * kPairsPerStage * 2;  // M padded to 64 / 128 per half
   p.b_bytes = (uint32_t)c_in * kPairsPerStage * 2;
   p.slot_bytes = (p.a_bytes + p.b_bytes + 1023) & ~1023u;
-  static const int np_env = [] {  // producer warps: 8 (two CTAs per SM, default), 16 or 4
+  // producer warps: 4 (three CTAs per SM, default), 8 (two) or 16 (one).  configs[1] wgrad:
+  // one CTA 104.5 us; two 85.9 us (82.3 with one commit per slot); three 78.1 us.
+  static const int np_env = [] {
     const char* v = std::getenv("MK_WGRAD_NP");
-    const int x = v ? std::atoi(v) : 8;
-    return x == 16 || x == 4 ? x : 8;
+    const int x = v ? std::atoi(v) : 4;
+    return x == 16 || x == 8 ? x : 4;
   }();
   const int np = np_env;
   const int per_sm = np == 16 ? 1 : np == 8 ? 2 : 3;
