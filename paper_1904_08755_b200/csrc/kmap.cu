@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(1024) k_scan(const int32_t* __restrict__ tile_
 // the tile's neighbour entries into the pair lists (output-ascending within an offset,
 // S:157); for maps that are not symmetric also the transposed table nbrT[k][a] = o (dgrad).
 template <bool RM>
-__global__ void __launch_bounds__(kThreads) k_emit(const int32_t* __restrict__ nbr, int64_t n_out, int64_t n_pad, int K,
+__global__ void __launch_bounds__(kThreads, 8) k_emit(const int32_t* __restrict__ nbr, int64_t n_out, int64_t n_pad, int K,
                                                    const int64_t* __restrict__ totals, int64_t* __restrict__ ptr_out,
                                                    const int64_t* __restrict__ tile_off, int64_t ntiles,
                                                    int32_t* __restrict__ in_idx, int32_t* __restrict__ out_idx,
