@@ -30,7 +30,7 @@ namespace {
 
 constexpr int kBlock = 256;
 #ifndef MK_RANK_ITEMS
-#define MK_RANK_ITEMS 6
+#define MK_RANK_ITEMS 5
 #endif
 #ifndef MK_RANK_MINB
 #define MK_RANK_MINB 1
