@@ -58,7 +58,7 @@ typedef enum {
   MK_ERR_NONFINITE_INPUT = 4,    /* NaN / Inf point coordinate                   */
   MK_ERR_COORD_RANGE = 5,        /* coordinate outside the representable domain (R19)   */
   MK_ERR_STRIDE = 6,             /* coordinate not a multiple of the tensor stride*/
-  MK_ERR_UNSUPPORTED = 7,        /* D > 4, channel count not a multiple of 8, ...       */
+  MK_ERR_UNSUPPORTED = 7,        /* D > 7, channels > 256, bf16 channels % 16 != 0, ... */
   MK_ERR_OUT_OF_MEMORY = 8,
   MK_ERR_CUDA = 9                /* a CUDA runtime error; message carries its text      */
 } mk_status;
@@ -267,7 +267,10 @@ mk_status mk_crf_backward(mk_context* ctx, const mk_kmap* m, const float* d_phi_
  *   are 0 ("F^o <- 0"; R15).  No bias (R16).
  *   d_fin   [n_in][c_in] of in_dt;  d_w [K][c_out][c_in] of in_dt;  d_fout [n_out][c_out]
  *   of out_dt.  Accumulation is fp32.  MK_BF16 inputs run on the tcgen05 tensor cores;
- *   MK_F32 inputs run exact fp32 FFMA.  c_in, c_out: multiples of 8, <= 256.
+ *   MK_F32 inputs run exact fp32 FFMA.  Channel contract: 1 <= c_in, c_out <= 256 for
+ *   MK_F32; multiples of 16 in 16..256 for MK_BF16 (every such pair is planned: wide
+ *   outputs are split over column slices, wide weight-gradient tiles use fewer, larger CTAs);
+ *   anything else returns MK_ERR_UNSUPPORTED.
  * Works on any map; mk_conv_transpose_forward additionally requires a transposed map. */
 mk_status mk_conv_forward(mk_context* ctx, const mk_kmap* m, const void* d_fin, int32_t c_in,
                           const void* d_w, void* d_fout, int32_t c_out, mk_dtype in_dt,

@@ -37,7 +37,7 @@ def build(force: bool = False) -> Path:
     src = _HERE / "oracle.cpp"
     if force or not _SO.exists() or _SO.stat().st_mtime < max(src.stat().st_mtime, (_HERE / "oracle.h").stat().st_mtime):
         tmp = _SO.with_suffix(f".so.{os.getpid()}")
-        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-fno-fast-math",
+        subprocess.check_call(["g++", "-O2", "-std=c++17", "-fPIC", "-shared", "-fno-fast-math", "-fopenmp",
                                "-o", str(tmp), str(src)])
         os.replace(tmp, _SO)
     return _SO
@@ -69,10 +69,19 @@ def lib():
         L.orc_conv_forward_rows.argtypes = [P, P, P, i32, P, i32, P, i32, P, i64, P]
         L.orc_conv_dgrad.argtypes = [P, P, P, i32, P, i32, P, P, i64, i32]
         L.orc_conv_wgrad.argtypes = [P, P, P, i32, P, i32, P, i32, P]
+        L.orc_kmap_reverse.argtypes = [P, P, P, i32, P, P, P]
+        L.orc_set_threads.argtypes = [i32]
+        L.orc_set_threads.restype = ctypes.c_int
         for f in ("orc_quantize", "orc_create", "orc_stride", "orc_region", "orc_lookup", "orc_kmap"):
             getattr(L, f).restype = ctypes.c_int
         _lib = L
     return _lib
+
+
+def set_threads(n: int = 0) -> int:
+    """Threads of the oracle's OpenMP loops (0 = leave as is); returns the count in effect.
+    Results are bit-identical for any count (only disjoint writes are split)."""
+    return int(lib().orc_set_threads(int(n)))
 
 
 def _p(a: np.ndarray | None):
@@ -201,6 +210,20 @@ def kmap(c_in, c_out, offsets, scale=None, transposed: bool = False):
     L.orc_kmap(_p(ci), ci.shape[0], _p(co), co.shape[0], D, _p(offs), K, _p(sc), int(transposed),
                _p(ptr), _p(ins), _p(outs))
     return ptr, ins[:M].copy(), outs[:M].copy()
+
+
+def kmap_reverse(kmap_csr, n_in: int | None = None):
+    """The map with input and output roles exchanged, output-ascending per offset."""
+    ptr, ins, outs = (np.ascontiguousarray(a) for a in kmap_csr)
+    ptr = _c(ptr, np.int64)
+    ins, outs = _c(ins, np.int32), _c(outs, np.int32)
+    K = ptr.shape[0] - 1
+    M = max(int(ptr[-1]), 1)
+    rptr = np.zeros(K + 1, np.int64)
+    rin = np.zeros(M, np.int32)
+    rout = np.zeros(M, np.int32)
+    lib().orc_kmap_reverse(_p(ptr), _p(ins), _p(outs), K, _p(rptr), _p(rin), _p(rout))
+    return rptr, rin[:int(ptr[-1])].copy(), rout[:int(ptr[-1])].copy()
 
 
 def conv_forward(kmap_csr, f_in, W, n_out: int):

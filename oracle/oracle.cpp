@@ -21,6 +21,10 @@
 #include <unordered_map>
 #include <vector>
 
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
 namespace {
 
 constexpr int kMaxWords = 8;  // D <= 7 spatial axes + batch
@@ -47,6 +51,25 @@ Key row_key(const int32_t* row, int32_t D) {
 }
 
 bool fits_i32(int64_t v) { return v >= INT32_MIN && v <= INT32_MAX; }
+
+// The ABI's coordinate domain (reading R19, mk.h MK_MAX_DIM): int32 components; for D = 4
+// the time axis u_3 in [-2^15, 2^15) and batch b <= 65534; for D = 5..7 axes 0-2 in
+// [-2^19, 2^19), axes 3-5 in [-2^11, 2^11), axis 6 in [-2^15, 2^15) and (D = 7) b <= 65534.
+// Rows outside it are rejected with ORC_COORD_RANGE (the same status the GPU path returns).
+bool in_domain(const int64_t* c, int32_t D, int64_t b) {
+  auto in = [](int64_t v, int64_t lo, int64_t hi) { return v >= lo && v < hi; };
+  for (int d = 0; d < D; ++d)
+    if (!fits_i32(c[d])) return false;
+  if (D == 4) return in(c[3], -32768, 32768) && b <= 65534;
+  if (D >= 5) {
+    for (int d = 0; d < 3; ++d)
+      if (!in(c[d], -(1 << 19), 1 << 19)) return false;
+    for (int d = 3; d < std::min(D, 6); ++d)
+      if (!in(c[d], -(1 << 11), 1 << 11)) return false;
+    if (D == 7) return in(c[6], -32768, 32768) && b <= 65534;
+  }
+  return true;
+}
 
 // floor division toward -infinity (reading R7).  s > 0.
 int64_t floor_div(int64_t u, int64_t s) {
@@ -88,8 +111,13 @@ int orc_quantize(const float* points, const int32_t* batch, int64_t n, int32_t D
       if (!(q >= -2147483648.0f && q < 2147483648.0f)) range = true;
     }
     if (nonfinite) { *err_row = p; return ORC_NONFINITE_INPUT; }
-    if (range) { *err_row = p; return ORC_COORD_RANGE; }
     if (batch && batch[p] < 0) { *err_row = p; return ORC_INVALID_ARGUMENT; }
+    if (!range) {
+      int64_t c[kMaxWords];
+      for (int d = 0; d < D; ++d) c[d] = static_cast<int64_t>(std::floor(points[p * D + d] / voxel));
+      range = !in_domain(c, D, batch ? batch[p] : 0);
+    }
+    if (range) { *err_row = p; return ORC_COORD_RANGE; }
   }
   // Alg. 1, serial form: C_p' <- floor(C_p / v_l); unique keys;
   // the first point of each key is kept (i_x of the reduction f, reading R9); rows are
@@ -132,6 +160,9 @@ int orc_create(const int32_t* coords, int64_t n, int32_t D, const int32_t* tenso
       if (r[d] % s != 0) { *err_row = p; return ORC_STRIDE; }
     }
     if (r[D] < 0) { *err_row = p; return ORC_INVALID_ARGUMENT; }
+    int64_t c[kMaxWords];
+    for (int d = 0; d < D; ++d) c[d] = r[d];
+    if (!in_domain(c, D, r[D])) { *err_row = p; return ORC_COORD_RANGE; }
   }
   CoordMap map;
   map.reserve(static_cast<size_t>(n) * 2 + 1);
@@ -345,9 +376,13 @@ int orc_kmap(const int32_t* c_in, int64_t n_in, const int32_t* c_out, int64_t n_
   // Eq. 3: for u in C_out and i in N^D, u + i in C_in contributes W_i x_{u+i}.
   // Offsets are scaled by the fine tensor stride (reading R14); transposed maps reverse the
   // roles of input and output (reading R13).  Output-ascending inside each offset.
+  // The lookups of one offset are independent (optional OpenMP over o); the pairs are then
+  // appended serially in output order.
   int64_t count = 0;
   ptr[0] = 0;
+  std::vector<int32_t> hit(static_cast<size_t>(n_out));
   for (int32_t k = 0; k < K; ++k) {
+#pragma omp parallel for schedule(static)
     for (int64_t o = 0; o < n_out; ++o) {
       const int32_t* u = c_out + o * (D + 1);
       Key q{};
@@ -357,12 +392,16 @@ int orc_kmap(const int32_t* c_in, int64_t n_in, const int32_t* c_out, int64_t n_
         if (!fits_i32(v)) { ok = false; break; }
         q[d] = static_cast<int32_t>(v);
       }
+      hit[o] = -1;
       if (!ok) continue;
       q[D] = u[D];  // batch index is never offset (reading R18)
       auto it = map.find(q);
-      if (it == map.end()) continue;
+      if (it != map.end()) hit[o] = it->second;
+    }
+    for (int64_t o = 0; o < n_out; ++o) {
+      if (hit[o] < 0) continue;
       if (in_idx) {
-        in_idx[count] = it->second;
+        in_idx[count] = hit[o];
         out_idx[count] = static_cast<int32_t>(o);
       }
       ++count;
@@ -377,9 +416,12 @@ void orc_conv_forward(const int64_t* ptr, const int32_t* in_idx, const int32_t* 
                       int64_t n_out, int32_t c_out) {
   // Alg. 2 line 1: F^o <- 0.
   std::fill(f_out, f_out + n_out * c_out, 0.0);
-  // Alg. 2 lines 2-5: for each offset, gather, multiply by W_i, add-and-scatter.
+  // Alg. 2 lines 2-5: for each offset, gather, multiply by W_i, add-and-scatter.  Within one
+  // offset the outputs O_i are distinct, so the optional OpenMP split over the pairs
+  // of an offset is race-free and gives bit-identical results.
   for (int32_t k = 0; k < K; ++k) {
     const double* Wk = W + (int64_t)k * c_out * c_in;
+#pragma omp parallel for schedule(static)
     for (int64_t p = ptr[k]; p < ptr[k + 1]; ++p) {
       const double* x = f_in + (int64_t)in_idx[p] * c_in;
       double* y = f_out + (int64_t)out_idx[p] * c_out;
@@ -396,6 +438,7 @@ void orc_conv_forward_rows(const int64_t* ptr, const int32_t* in_idx, const int3
                            int32_t K, const double* f_in, int32_t c_in, const double* W,
                            int32_t c_out, const int32_t* rows, int64_t n_rows, double* f_rows) {
   // Eq. 3 evaluated at the selected outputs u: sum over offsets i with u+i in C_in.
+#pragma omp parallel for schedule(dynamic, 64)
   for (int64_t r = 0; r < n_rows; ++r) {
     double* y = f_rows + r * c_out;
     std::fill(y, y + c_out, 0.0);
@@ -420,8 +463,10 @@ void orc_conv_dgrad(const int64_t* ptr, const int32_t* in_idx, const int32_t* ou
                     const double* g_out, int32_t c_out, const double* W, double* g_in,
                     int64_t n_in, int32_t c_in) {
   std::fill(g_in, g_in + n_in * c_in, 0.0);
+  // Within one offset the inputs I_i are distinct: the optional OpenMP split is race-free.
   for (int32_t k = 0; k < K; ++k) {
     const double* Wk = W + (int64_t)k * c_out * c_in;
+#pragma omp parallel for schedule(static)
     for (int64_t p = ptr[k]; p < ptr[k + 1]; ++p) {
       const double* g = g_out + (int64_t)out_idx[p] * c_out;
       double* x = g_in + (int64_t)in_idx[p] * c_in;
@@ -440,13 +485,45 @@ void orc_conv_wgrad(const int64_t* ptr, const int32_t* in_idx, const int32_t* ou
   for (int32_t k = 0; k < K; ++k) {
     double* dWk = dW + (int64_t)k * c_out * c_in;
     std::fill(dWk, dWk + (int64_t)c_out * c_in, 0.0);
-    for (int64_t p = ptr[k]; p < ptr[k + 1]; ++p) {
-      const double* g = g_out + (int64_t)out_idx[p] * c_out;
-      const double* x = f_in + (int64_t)in_idx[p] * c_in;
-      for (int32_t co = 0; co < c_out; ++co)
-        for (int32_t ci = 0; ci < c_in; ++ci) dWk[(int64_t)co * c_in + ci] += g[co] * x[ci];
-    }
+    // Optional OpenMP over the rows co of dW_k: every element still sums the pairs in order.
+#pragma omp parallel for schedule(static)
+    for (int32_t co = 0; co < c_out; ++co)
+      for (int64_t p = ptr[k]; p < ptr[k + 1]; ++p) {
+        const double g = g_out[(int64_t)out_idx[p] * c_out + co];
+        const double* x = f_in + (int64_t)in_idx[p] * c_in;
+        for (int32_t ci = 0; ci < c_in; ++ci) dWk[(int64_t)co * c_in + ci] += g * x[ci];
+      }
   }
+}
+
+int orc_kmap_reverse(const int64_t* ptr, const int32_t* in_idx, const int32_t* out_idx, int32_t K,
+                     int64_t* rptr, int32_t* rin, int32_t* rout) {
+  // the map of the reverse direction has the roles of input and output exchanged:
+  // pair (a, o) of offset k becomes (o, a), listed output-ascending, i.e. by a.
+  rptr[0] = 0;
+  for (int32_t k = 0; k < K; ++k) {
+    std::vector<std::pair<int32_t, int32_t>> pairs;
+    for (int64_t p = ptr[k]; p < ptr[k + 1]; ++p) pairs.emplace_back(in_idx[p], out_idx[p]);
+    std::sort(pairs.begin(), pairs.end());
+    int64_t q = ptr[k];
+    for (const auto& pr : pairs) {
+      rout[q] = pr.first;  // the former input row is the new output
+      rin[q] = pr.second;
+      ++q;
+    }
+    rptr[k + 1] = ptr[k + 1];
+  }
+  return ORC_OK;
+}
+
+int orc_set_threads(int32_t n) {
+#ifdef _OPENMP
+  if (n > 0) omp_set_num_threads(n);
+  return omp_get_max_threads();
+#else
+  (void)n;
+  return 1;
+#endif
 }
 
 }  // extern "C"

@@ -126,6 +126,17 @@ void orc_global_pool(const int32_t* batch, int64_t n, const double* f_in, int32_
 void orc_crf_infer(const int64_t* ptr, const int32_t* in_idx, const int32_t* out_idx, int32_t K,
                    const double* phi_u, int64_t n, int32_t C, const double* W, int32_t n_iters, double* q);
 
+/* The reverse map ("the role of input and output coordinates is reversed"): every pair
+ * (a, o) of offset k becomes (o, a), output-ascending within the offset.  Its forward conv
+ * with W_k^T is the input gradient O7; reverse(kmap(fine -> coarse)) is the transposed map. */
+int orc_kmap_reverse(const int64_t* ptr, const int32_t* in_idx, const int32_t* out_idx, int32_t K,
+                     int64_t* rptr, int32_t* rin, int32_t* rout);
+
+/* Threads of the optional OpenMP loops (n > 0 sets it; returns the count in effect).  The
+ * parallel loops split only work whose writes are disjoint (pairs of one offset, rows of
+ * dW_k, output rows), so every result is bit-identical for any thread count. */
+int orc_set_threads(int32_t n);
+
 #ifdef __cplusplus
 }
 #endif

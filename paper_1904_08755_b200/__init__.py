@@ -154,13 +154,24 @@ def coords_quantize(points: torch.Tensor, voxel: float, batch: Optional[torch.Te
     c = Coords(h, pts.device, deferred=deferred)
     if not return_maps:
         return c
-    return c, p2r, (first if deferred else first[:c.n])
+    if deferred:
+        # capacity N_p, rows >= N undefined: coords_labels cuts it to c.n (collecting the count)
+        first._mk_deferred_coords = c
+        return c, p2r, first
+    return c, p2r, first[:c.n]
 
 
 def coords_labels(point_to_row: torch.Tensor, first_point: torch.Tensor, labels: torch.Tensor,
-                  ignore_label: int = -1) -> torch.Tensor:
+                  ignore_label: int = -1, coords: Optional["Coords"] = None) -> torch.Tensor:
     """Per-voxel labels of Alg. 1: the points' common label, else ignore_label.
-    point_to_row / first_point are the maps returned by coords_quantize."""
+    point_to_row / first_point are the maps returned by coords_quantize.  With a deferred
+    quantize pass its Coords as `coords`: first_point then has capacity N_p and only its
+    first c.n rows are defined, so it is cut to them (rows >= N would index out of bounds)."""
+    coords = coords if coords is not None else getattr(first_point, "_mk_deferred_coords", None)
+    if coords is not None:
+        first_point = first_point[:coords.n]
+    if first_point.shape[0] > point_to_row.shape[0]:
+        raise ValueError("first_point has more rows than there are points")
     p2r = _cuda(point_to_row, torch.int32, "point_to_row")
     first = _cuda(first_point, torch.int32, "first_point")
     lab = _cuda(labels, torch.int32, "labels")
@@ -324,6 +335,16 @@ def _dt(t: torch.Tensor) -> int:
     return _DT[t.dtype]
 
 
+def _out_buf(buf, shape, dtype, device, what):
+    """A caller-supplied output buffer after validation, or a new one."""
+    if buf is None:
+        return torch.empty(shape, dtype=dtype, device=device)
+    if tuple(buf.shape) != tuple(shape) or buf.dtype != dtype or buf.device != device or not buf.is_contiguous():
+        raise ValueError(f"{what}: expected a contiguous {dtype} tensor of shape {tuple(shape)} on {device}, got "
+                         f"{buf.dtype} {tuple(buf.shape)} on {buf.device} (contiguous={buf.is_contiguous()})")
+    return buf
+
+
 def _conv(fn, name, m: KernelMap, f_in, W, out_dtype, out=None):
     if not (f_in.is_cuda and W.is_cuda):
         raise ValueError("conv inputs must be CUDA tensors (no CPU path)")
@@ -331,9 +352,12 @@ def _conv(fn, name, m: KernelMap, f_in, W, out_dtype, out=None):
     if K != m.K or f_in.shape[-1] != c_in or f_in.shape[0] != m.n_in or W.dtype != f_in.dtype:
         raise ValueError(f"{name}: shape/dtype mismatch (K={m.K}, n_in={m.n_in})")
     out_dtype = out_dtype or f_in.dtype
-    y = out if out is not None else torch.empty((m.n_out, c_out), dtype=out_dtype, device=f_in.device)
+    y = _out_buf(out, (m.n_out, c_out), out_dtype, f_in.device, "out")
+    # contiguous copies are bound to locals so they stay alive until the call returns (a
+    # temporary freed early could be reused by the next argument's copy)
+    x, w = f_in.contiguous(), W.contiguous()
     with _on_device(f_in.device):
-        _check(fn(context(f_in.device.index), m._h, _ptr(f_in.contiguous()), c_in, _ptr(W.contiguous()), _ptr(y),
+        _check(fn(context(f_in.device.index), m._h, _ptr(x), c_in, _ptr(w), _ptr(y),
                   c_out, _dt(f_in), _DT[out_dtype], _stream(f_in)), name)
     return y
 
@@ -356,7 +380,7 @@ def _conv_fused(m: KernelMap, f_in, W, out_dtype, out, scale, shift, residual, r
     if K != m.K or f_in.shape[-1] != c_in or f_in.shape[0] != m.n_in or W.dtype != f_in.dtype:
         raise ValueError(f"mk_conv_forward_fused: shape/dtype mismatch (K={m.K}, n_in={m.n_in})")
     out_dtype = out_dtype or f_in.dtype
-    y = out if out is not None else torch.empty((m.n_out, c_out), dtype=out_dtype, device=f_in.device)
+    y = _out_buf(out, (m.n_out, c_out), out_dtype, f_in.device, "out")
     sc = None if scale is None else _cuda(scale, torch.float32, "scale")
     sh = None if shift is None else _cuda(shift, torch.float32, "shift")
     for t, nm in ((sc, "scale"), (sh, "shift")):
@@ -367,9 +391,10 @@ def _conv_fused(m: KernelMap, f_in, W, out_dtype, out, scale, shift, residual, r
         res = _cuda(residual, out_dtype, "residual")
         if tuple(res.shape) != (m.n_out, c_out):
             raise ValueError("residual must be [n_out][C_out]")
+    x, w = f_in.contiguous(), W.contiguous()
     with _on_device(f_in.device):
-        _check(_L.mk_conv_forward_fused(context(f_in.device.index), m._h, _ptr(f_in.contiguous()), c_in,
-                                        _ptr(W.contiguous()), _ptr(y), c_out, _dt(f_in), _DT[out_dtype], _ptr(sc),
+        _check(_L.mk_conv_forward_fused(context(f_in.device.index), m._h, _ptr(x), c_in,
+                                        _ptr(w), _ptr(y), c_out, _dt(f_in), _DT[out_dtype], _ptr(sc),
                                         _ptr(sh), _ptr(res), int(bool(relu)), _stream(f_in)), "mk_conv_forward_fused")
     return y
 
@@ -391,13 +416,14 @@ def _backward(fn, name, m: KernelMap, g_out, f_in, W, need_gin=True, need_gw=Tru
         raise ValueError(f"{name}: shape mismatch")
     if not (g_out.dtype == f_in.dtype == W.dtype):
         raise TypeError(f"{name}: g_out, f_in and W must share a dtype")
-    if need_gin and gin is None:
-        gin = torch.empty((m.n_in, c_in), dtype=f_in.dtype, device=f_in.device)
-    if need_gw and gw is None:
-        gw = torch.empty((K, c_out, c_in), dtype=torch.float32, device=f_in.device)
+    if need_gin:
+        gin = _out_buf(gin, (m.n_in, c_in), f_in.dtype, f_in.device, "gin")
+    if need_gw:
+        gw = _out_buf(gw, (K, c_out, c_in), torch.float32, f_in.device, "gw")
+    g, x, w = g_out.contiguous(), f_in.contiguous(), W.contiguous()  # alive until the call returns
     with _on_device(f_in.device):
-        _check(fn(context(f_in.device.index), m._h, _ptr(g_out.contiguous()), _ptr(f_in.contiguous()),
-                  _ptr(W.contiguous()), c_in, c_out, _dt(f_in), _ptr(gin if need_gin else None),
+        _check(fn(context(f_in.device.index), m._h, _ptr(g), _ptr(x),
+                  _ptr(w), c_in, c_out, _dt(f_in), _ptr(gin if need_gin else None),
                   _ptr(gw if need_gw else None), _stream(f_in)), name)
     return (gin if need_gin else None), (gw if need_gw else None)
 
@@ -422,10 +448,10 @@ def pool_forward(m: KernelMap, f_in: torch.Tensor, mode: int = POOL_MAX, out=Non
         raise ValueError(f"pool_forward: f_in has {f_in.shape[0]} rows, the map has n_in={m.n_in}")
     x = f_in.contiguous()
     C = x.shape[1]
-    y = out if out is not None else torch.empty((m.n_out, C), dtype=x.dtype, device=x.device)
+    y = _out_buf(out, (m.n_out, C), x.dtype, x.device, "out")
     am = None
     if mode == POOL_MAX:
-        am = argmax if argmax is not None else torch.empty((m.n_out, C), dtype=torch.int32, device=x.device)
+        am = _out_buf(argmax, (m.n_out, C), torch.int32, x.device, "argmax")
     with _on_device(x.device):
         _check(_L.mk_pool_forward(context(x.device.index), m._h, int(mode), _ptr(x), C, _dt(x), _ptr(y), _ptr(am),
                                   _stream(x)), "mk_pool_forward")
@@ -438,7 +464,11 @@ def pool_backward(m: KernelMap, g_out: torch.Tensor, mode: int = POOL_MAX, argma
         raise ValueError(f"pool_backward: g_out has {g_out.shape[0]} rows, the map has n_out={m.n_out}")
     g = g_out.contiguous()
     C = g.shape[1]
-    gi = out if out is not None else torch.empty((m.n_in, C), dtype=g.dtype, device=g.device)
+    gi = _out_buf(out, (m.n_in, C), g.dtype, g.device, "out")
+    if mode == POOL_MAX:
+        if argmax is None:
+            raise ValueError("pool_backward: POOL_MAX needs the argmax of pool_forward")
+        argmax = _out_buf(argmax, (m.n_out, C), torch.int32, g.device, "argmax")
     with _on_device(g.device):
         _check(_L.mk_pool_backward(context(g.device.index), m._h, int(mode), _ptr(g), C, _dt(g), _ptr(argmax),
                                    _ptr(gi), _stream(g)), "mk_pool_backward")

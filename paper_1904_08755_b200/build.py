@@ -19,8 +19,11 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-I", str(ROOT / "include"), "-I", str(CSRC)]
 
 
-def _stale(obj: Path, src: Path) -> bool:
-    if not obj.exists():
+def _stale(obj: Path, src: Path, cmd) -> bool:
+    """An object is rebuilt when a source or header is newer, or when its compile command
+    (flags, defines) differs from the one recorded next to it."""
+    stamp = obj.with_suffix(".cmd")
+    if not obj.exists() or not stamp.exists() or stamp.read_text() != " ".join(cmd):
         return True
     deps = [src, *CSRC.glob("*.cuh"), ROOT / "include" / "mk.h"]
     return obj.stat().st_mtime < max(d.stat().st_mtime for d in deps)
@@ -39,9 +42,10 @@ def build(verbose: bool = False, jobs: int = 8, trace: bool = False, variant: st
     for s in SOURCES:
         src, obj = CSRC / s, objdir / (Path(s).stem + ".o")
         objs.append(obj)
-        if _stale(obj, src):
-            cmd = ["nvcc", *ARCH, *FLAGS, *defs, "-Xptxas", "-v" if verbose else "-O3", "-c", str(src), "-o", str(obj)]
-            procs.append((cmd, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
+        cmd = ["nvcc", *ARCH, *FLAGS, *defs, "-c", str(src), "-o", str(obj)]
+        if _stale(obj, src, cmd) or verbose:
+            run = cmd[:-4] + ["-Xptxas", "-v"] + cmd[-4:] if verbose else cmd
+            procs.append((cmd, obj, subprocess.Popen(run, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))
             if len(procs) >= jobs:
                 _drain(procs, verbose)
     _drain(procs, verbose)
@@ -54,11 +58,12 @@ def build(verbose: bool = False, jobs: int = 8, trace: bool = False, variant: st
 
 def _drain(procs, verbose):
     while procs:
-        cmd, p = procs.pop(0)
+        cmd, obj, p = procs.pop(0)
         out, _ = p.communicate()
         if p.returncode != 0:
             sys.stderr.write(out)
             raise RuntimeError("nvcc failed: " + " ".join(cmd))
+        obj.with_suffix(".cmd").write_text(" ".join(cmd))
         if verbose and out.strip():
             print(out)
 

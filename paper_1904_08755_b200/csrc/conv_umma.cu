@@ -210,12 +210,14 @@ struct FwdParams {
   NbrView nb;
   int64_t n_rows, ntiles;
   int c_x, c_y, nch, out_f32;
+  int cw;  // output columns per CTA (the MMA's N): blockIdx.y takes columns [cw*blockIdx.y, +cw) of c_y
+  uint32_t b_img;  // bytes of one full W chunk image (c_y rows); a CTA copies its cw-row slice
   int dbg;  // development switch (env MK_DEBUG_CONV): bit 0 = no MMAs, bit 1 = no gathers; 0 in production
   int sa;  // A stage slots
   int np;  // producer warps (np divides sa)
   int ga;  // stage slots released together by one tcgen05.commit (sa % ga == 0)
   int sw;  // W chunk slots (a ring: W_k chunks are prefetched several offsets ahead)
-  int tb;  // tiles per CTA (one TMEM accumulator each: tb * c_y <= 512 columns)
+  int tb;  // tiles per CTA (one TMEM accumulator each: tb * cw <= 512 columns)
   int fold;  // tile order (see cta_tile)
   uint32_t a_bytes, b_bytes, tmem_cols;
   Epilogue ep;  // fused scale / shift / residual / ReLU (forward only; identity otherwise)
@@ -372,6 +374,9 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
   uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t tile0 = cta_tile0(p);
+  const int y0 = (int)blockIdx.y * p.cw;        // this CTA's output columns [y0, y0 + cwj)
+  const int cwj = min(p.cw, p.c_y - y0);
+  const uint32_t wb = (uint32_t)cwj * RB;       // bytes of this CTA's slice of a W chunk
 
   // prologue that touches no global memory overlaps the predecessor kernel (PDL)
   if (threadIdx.x == 32) {
@@ -495,8 +500,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
           ACCT_WAIT(0, cb + j % kNCB, (uint32_t)(j / kNCB) & 1u);
         }
         for (int c = 0; c < p.nch; ++c) {
-          mbar_arrive_expect_tx(w_full + ws, p.b_bytes);
-          bulk_g2s(w_base + (size_t)ws * p.b_bytes, p.wpack + ((int64_t)pl->k[u] * p.nch + c) * p.b_bytes, p.b_bytes,
+          mbar_arrive_expect_tx(w_full + ws, wb);
+          bulk_g2s(w_base + (size_t)ws * p.b_bytes, p.wpack + ((int64_t)pl->k[u] * p.nch + c) * p.b_img + y0 * RB, wb,
                    w_full + ws);
           if (++ws == (uint32_t)p.sw) ws = 0;
         }
@@ -511,7 +516,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
     // one commit per group of ga stage slots.
     {
       const bool leader = lane == 0;
-      const uint32_t idesc = idesc_bf16(kTileM, p.c_y, 0, 0);
+      const uint32_t idesc = idesc_bf16(kTileM, (uint32_t)cwj, 0, 0);
       const uint64_t dhi = smem_desc(0, 16, 8 * RB, layout_code(RB));
       const uint32_t a0 = __shfl_sync(0xffffffffu, smem_u32(a_base) >> 4, 0), astep = p.a_bytes >> 4;
       const uint32_t w0 = __shfl_sync(0xffffffffu, smem_u32(w_base) >> 4, 0), wstep = p.b_bytes >> 4;
@@ -535,7 +540,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
         tc_fence_after();
         for (uint32_t b = tw; b; b &= b - 1) {
           const int i = __ffs(b) - 1;
-          const uint32_t d = tb0 + (uint32_t)(i * p.c_y);
+          const uint32_t d = tb0 + (uint32_t)(i * p.cw);
           uint32_t acc = (init >> i) & 1u;
           uint32_t x = ws;
           for (int c = 0; c < p.nch; ++c) {
@@ -589,7 +594,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
       const int64_t row = valid ? p.nb.row_of(pos) : 0;
       if (!((act >> i) & 1u)) {  // no offset in this tile: the conv output is 0
         if (valid)
-          for (int col0 = 0; col0 < p.c_y; col0 += 16) {
+          for (int col0 = y0; col0 < y0 + cwj; col0 += 16) {
             uint32_t v[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) v[e] = 0u;
@@ -598,14 +603,14 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
           }
         continue;
       }
-      const uint32_t tl_addr = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(i * p.c_y);
-      for (int col0 = 0; col0 < p.c_y; col0 += 16) {
+      const uint32_t tl_addr = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(i * p.cw);
+      for (int col0 = 0; col0 < cwj; col0 += 16) {
         uint32_t v[16];
         tmem_ld16(tl_addr + col0, v);
         tmem_ld_wait();
         if (valid) {
-          if (EPI) epi16(p, row, col0, v);
-          store16(p, row, col0, v);
+          if (EPI) epi16(p, row, y0 + col0, v);
+          store16(p, row, y0 + col0, v);
         }
       }
     }
@@ -1047,48 +1052,55 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   }();
   p.dbg = dbg;
   p.a_bytes = kTileM * CH * 2;
-  p.b_bytes = (uint32_t)c_y * CH * 2;
-  // Two tiles per CTA (one TMEM accumulator each, <= 256 columns so two CTAs share an SM);
-  // smem ~100 KB per CTA: 4 A stages (16 KB each at CH=64), a ring of 4 W chunks, per-warp
-  // index buffers and the plan (B200 gathers ~9 TB/s at 8 warps/SM, ubench_gather.cu).
+  p.b_img = (uint32_t)c_y * CH * 2;
   static const int env_fold = [] {  // default: 2 tiles per CTA, folded order (measured best)
     const char* e = std::getenv("MK_FWD_FOLD");
     return e ? std::atoi(e) : 2;
   }();
-  p.fold = env_fold > 0 ? 1 : 0;
-  p.tb = p.fold ? std::max(1, std::min(env_fold, 256 / c_y)) : std::max(1, std::min(2, 256 / c_y));
-  p.tmem_cols = pow2_cols((uint32_t)(p.tb * c_y));
   static const int env_ctas0 = [] {  // CTAs per SM the smem budget aims at: 3 (default) or 2
     const char* e = std::getenv("MK_FWD_CTAS");
     return e && std::atoi(e) == 2 ? 2 : 3;
   }();
-  // Three CTAs per SM (configs[1] fwd 65.4 -> 62.9 us, dgrad 64.3 -> 62.2 us) when two stage
-  // slots and the W ring fit a third of the SM and the registers allow it (the fused-epilogue
-  // instance needs 84 registers: two CTAs).
-  const int env_ctas = env_ctas0 == 3 && !ep.active() && 1024 + 512 + kFwdProd * 3 * kTileM * 4 + (int)sizeof(Plan) +
-                                             nch * 2 * (int)(c_y * CH * 2) + 2 * kTileM * CH * 2 <=
-                                             kMaxSmem / 3 - 1024
-                           ? 3
-                           : 2;
-  const int base = 1024 + 512 + kFwdProd * 3 * kTileM * 4 + (int)sizeof(Plan);
-  p.sw = nch * 2;
-  if (env_ctas == 2 &&
-      base + p.sw * (int)p.b_bytes + kFwdProd * (int)p.a_bytes <= kMaxSmem / 2 - 1024 - 2 * nch * (int)p.b_bytes)
-    p.sw = nch * 4;
-  const int fixed = base + p.sw * (int)p.b_bytes;
-  p.sa = std::min(kFwdProd, ((env_ctas == 2 ? kMaxSmem : kMaxSmem / 3 - 1024) - fixed) / (int)p.a_bytes);
-  if (env_ctas == 2) p.sa -= p.sa % 2;
   static const int env_np = [] {
     const char* e = std::getenv("MK_FWD_NP");
     return e ? std::atoi(e) : 0;
   }();
+  p.fold = env_fold > 0 ? 1 : 0;
+  const int base = 1024 + 512 + kFwdProd * 3 * kTileM * 4 + (int)sizeof(Plan);
+  // Output columns per CTA.  All of C_out in one CTA when its W ring (2 units of nch chunks of
+  // cw x CH) and two A stage slots fit the SM; otherwise the columns are split over
+  // blockIdx.y (each CTA gathers the same rows and multiplies by its slice of W_k: e.g. C_in =
+  // C_out = 256 needs 2 x 4 x 32 KB of W alone, over the 227 KB of an SM).
+  int ysplit = 1, fixed = 0;
+  for (;; ++ysplit) {
+    p.cw = 16 * (int)ceil_div(ceil_div(c_y, 16), ysplit);
+    if (ysplit > 1 && (int64_t)(ysplit - 1) * p.cw >= c_y) continue;  // no empty column slice
+    p.b_bytes = (uint32_t)p.cw * CH * 2;
+    p.tb = p.fold ? std::max(1, std::min(env_fold, 256 / p.cw)) : std::max(1, std::min(2, 256 / p.cw));
+    p.tmem_cols = pow2_cols((uint32_t)(p.tb * p.cw));
+    // Three CTAs per SM (configs[1] fwd 65.4 -> 62.9 us, dgrad 64.3 -> 62.2 us) when two stage
+    // slots and the W ring fit a third of the SM and the registers allow it (the fused-epilogue
+    // instance needs 84 registers: two CTAs).
+    const int ctas = env_ctas0 == 3 && !ep.active() && 3 * p.tmem_cols <= 512 &&
+                             base + nch * 2 * (int)p.b_bytes + 2 * (int)p.a_bytes <= kMaxSmem / 3 - 1024
+                         ? 3
+                         : 2;
+    p.sw = nch * 2;
+    if (ctas == 2 &&
+        base + p.sw * (int)p.b_bytes + kFwdProd * (int)p.a_bytes <= kMaxSmem / 2 - 1024 - 2 * nch * (int)p.b_bytes)
+      p.sw = nch * 4;
+    fixed = base + p.sw * (int)p.b_bytes;
+    p.sa = std::min(kFwdProd, ((ctas == 2 ? kMaxSmem : kMaxSmem / 3 - 1024) - fixed) / (int)p.a_bytes);
+    if (ctas == 2) p.sa -= p.sa % 2;
+    if ((p.sa >= 2 && p.tmem_cols <= 512) || p.cw <= 16) break;
+  }
   // one producer warp per slot measured best (fwd 68.6 us vs 73.8 with two slots per warp,
   // configs[1]): more warps issue the gathers faster than fewer warps with deeper queues
   p.np = env_np > 0 ? std::min(env_np, p.sa) : p.sa;
   p.ga = p.sa % 2 == 0 ? 2 : 1;  // the W ring must hold >= ga units: sw / nch >= 2 >= ga
   if (p.sa < 2 || p.tmem_cols > 512)
     MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: channel counts too large for the smem pipeline");
-  const size_t wbytes = (size_t)nb.K * nch * p.b_bytes;
+  const size_t wbytes = (size_t)nb.K * nch * p.b_img;
   uint8_t* wpack = (uint8_t*)dev_alloc(ctx->alloc, wbytes, s);
   if (!wpack) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 conv: weight pack allocation failed");
   {
@@ -1098,11 +1110,12 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   }
   p.wpack = wpack;
   const int smem = fixed + p.sa * (int)p.a_bytes;
-  const int64_t grid = ceil_div(p.ntiles, p.tb);  // one CTA per tb adjacent tiles
+  // one CTA per tb tiles and column slice
+  const dim3 grid((unsigned)ceil_div(p.ntiles, p.tb), (unsigned)ysplit);
   cudaError_t e;
   auto go = [&](auto kern) {
     set_smem_once(kern, smem);
-    return pdl_launch(kern, (unsigned)grid, kFwdThreads, smem, s, p);
+    return pdl_launch(kern, grid, kFwdThreads, smem, s, p);
   };
   const bool epi = ep.active();
   if (CH == 64)
@@ -1153,22 +1166,27 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
     const int x = v ? std::atoi(v) : 4;
     return x == 16 || x == 8 ? x : 4;
   }();
-  const int np = np_env;
-  const int per_sm = np == 16 ? 1 : np == 8 ? 2 : 3;
-  const int budget = per_sm == 1 ? kMaxSmem : kMaxSmem / per_sm - 1024;
-  const int reserve = 1024 + 1024 + np * 4 * kPairsPerStage * 4 + (kMaxSegs + 2) * 4 +
-                      (int)sizeof(int4) * kMaxSegs + 64;
-  p.sa = std::min(np, (budget - reserve) / (int)p.slot_bytes);
-  if (p.sa >= 8) p.sa -= p.sa % 4;
-  // stage slots released per commit: grouped at one CTA per SM (a commit drains the tensor
-  // pipe), one per commit when another CTA hides the drain (wgrad 85.9 -> 82.4 us, configs[1])
-  p.ga = per_sm >= 2 ? 1 : p.sa % 4 == 0 ? 4 : p.sa % 2 == 0 ? 2 : 1;
   static const int env_ga = [] {  // development: stage slots released per commit
     const char* e = std::getenv("MK_WGRAD_GA");
     return e ? std::atoi(e) : 0;
   }();
-  if (env_ga > 0 && p.sa % env_ga == 0) p.ga = env_ga;
   p.tmem_cols = pow2_cols((uint32_t)(p.halves * c_in));
+  // Fewer, larger CTAs when the stage slots of wide channel counts (up to 2 x 32 KB per slot
+  // at 256 x 256) or their TMEM accumulators do not fit three CTAs per SM: np = 8 (two CTAs)
+  // or 16 (one CTA, up to 3 slots of 64 KB).
+  int np = np_env, per_sm = 3, reserve = 0;
+  for (;; np *= 2) {
+    per_sm = np == 16 ? 1 : np == 8 ? 2 : 3;
+    const int budget = per_sm == 1 ? kMaxSmem : kMaxSmem / per_sm - 1024;
+    reserve = 1024 + 1024 + np * 4 * kPairsPerStage * 4 + (kMaxSegs + 2) * 4 + (int)sizeof(int4) * kMaxSegs + 64;
+    p.sa = std::min(np, (budget - reserve) / (int)p.slot_bytes);
+    if ((p.sa >= 2 && per_sm * p.tmem_cols <= 512) || np >= 16) break;
+  }
+  if (p.sa >= 8) p.sa -= p.sa % 4;
+  // stage slots released per commit: grouped at one CTA per SM (a commit drains the tensor
+  // pipe), one per commit when another CTA hides the drain (wgrad 85.9 -> 82.4 us, configs[1])
+  p.ga = per_sm >= 2 ? 1 : p.sa % 4 == 0 ? 4 : p.sa % 2 == 0 ? 2 : 1;
+  if (env_ga > 0 && p.sa % env_ga == 0) p.ga = env_ga;
   if (p.sa < 2 || p.tmem_cols > 512) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: channel counts too large");
   const int smem = p.sa * (int)p.slot_bytes + reserve;
   float* part = nullptr;

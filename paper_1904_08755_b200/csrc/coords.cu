@@ -553,9 +553,11 @@ mk_status coords_resolve(const mk_coords* cc) {
   for (uint32_t it = 1;; ++it) {
     if (*vseq == c->seq) {
       std::atomic_thread_fence(std::memory_order_acquire);
-      err = c->mb->w0;
-      count = c->mb->w1;
-      if (*vseq == c->seq) break;  // not overwritten while reading
+      const volatile Mailbox* vm = c->mb;
+      err = vm->w0;
+      count = vm->w1;
+      std::atomic_thread_fence(std::memory_order_acquire);
+      if (*vseq == c->seq) break;  // not overwritten while reading (the writer zeroes seq first)
     }
     if ((it & 255u) == 0) {
       const cudaError_t q = cudaEventQuery(c->ev);

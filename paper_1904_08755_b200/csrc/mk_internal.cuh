@@ -395,7 +395,13 @@ Mailbox* mailbox_ring_slot(mk_context* ctx, unsigned long long* seq);
 cudaError_t mailbox_wait(const Mailbox* mb, unsigned long long seq, cudaStream_t s);
 __device__ __forceinline__ void mailbox_post(Mailbox* mb, unsigned long long seq, unsigned long long w0,
                                              unsigned long long w1) {
+  // seqlock writer: the slot is marked as being written (seq 0, never a valid sequence
+  // number) before its words change, so a host reader of an older call that checks seq before
+  // and after reading w0 / w1 can never accept a newer call's words (ring slots are reused
+  // every kMbSlots calls)
   volatile Mailbox* v = mb;
+  v->seq = 0ull;
+  __threadfence_system();
   v->w0 = w0;
   v->w1 = w1;
   __threadfence_system();

@@ -29,7 +29,3 @@ def assert_close(y, y64, scale64, tol, what=""):
 def to_np(t: torch.Tensor) -> np.ndarray:
     return t.detach().float().cpu().numpy() if t.dtype == torch.bfloat16 else t.detach().cpu().numpy()
 
-
-def csr_np(m):
-    ptr, ins, outs = m.export()
-    return ptr.cpu().numpy(), ins.cpu().numpy(), outs.cpu().numpy()

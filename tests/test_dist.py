@@ -17,46 +17,63 @@ ROOT = Path(__file__).resolve().parents[1]
 
 
 def _scans(n_scans=5, seed=3):
+    """Small float point clouds, one per batch index, concatenated in ascending scan order
+    (as bench.py's configs[4] batch)."""
     g = np.random.default_rng(seed)
-    rows = []
+    pts, bat = [], []
     for b in range(n_scans):
-        n = int(g.integers(150, 400))
-        c = g.integers(-6, 6, (n, 3))
-        rows.append(np.concatenate([c, np.full((n, 1), b)], axis=1))
-    return np.concatenate(rows).astype(np.int32)
+        n = int(g.integers(300, 700))
+        pts.append(g.uniform(-0.6, 0.6, (n, 3)).astype(np.float32))
+        bat.append(np.full(n, b, np.int32))
+    return np.concatenate(pts), np.concatenate(bat)
+
+
+VOXEL = 0.1
+
+
+def _features(n_rows):
+    g = np.random.default_rng(9)
+    X = g.standard_normal((n_rows, 4))
+    W = g.standard_normal((27, 5, 4))
+    G = g.standard_normal((n_rows, 5))
+    return X, W, G
 
 
 def _worker(rank, world, port, out_dir):
+    # The host side of bench.py's multi-GPU step, driven with the oracle as the per-rank
+    # compute: LPT shard plan on per-scan |M|, the rank's own points (rank_points), its own
+    # coordinates and map, the dW all-reduce (allreduce_grad) and the output all-gather
+    # (RowGather), over gloo instead of NCCL.
     sys.path.insert(0, str(ROOT))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     import oracle
-    from paper_1904_08755_b200.dist import allreduce_grad, gather_rows, lpt_assign
-    rows = _scans()
-    coords, _ = oracle.create(rows)
+    from paper_1904_08755_b200.dist import RowGather, allreduce_grad, lpt_assign, rank_points
+    pts, bat = _scans()
     offs = oracle.region(0, 3, [3, 3, 3])
-    g = np.random.default_rng(9)
-    X = g.standard_normal((coords.shape[0], 4))
-    W = g.standard_normal((27, 5, 4))
-    G = g.standard_normal((coords.shape[0], 5))
-    scans = sorted(set(coords[:, 3].tolist()))
-    costs = []
-    for b in scans:
-        sel = coords[:, 3] == b
-        costs.append(float(oracle.kmap(coords[sel], coords[sel], offs)[0][-1]))
+    n_scans = int(bat.max()) + 1
+    costs = []  # |M| per scan (setup, every rank the same)
+    for b in range(n_scans):
+        cb, _, _ = oracle.quantize(pts[bat == b], VOXEL, bat[bat == b])
+        costs.append(float(oracle.kmap(cb, cb, offs)[0][-1]))
     mine = lpt_assign(costs, world)[rank]
-    y_parts, dW = [], np.zeros_like(W)
-    for b in mine:
-        sel = np.nonzero(coords[:, 3] == b)[0]
-        km = oracle.kmap(coords[sel], coords[sel], offs)
-        y_parts.append(np.concatenate([sel[:, None], oracle.conv_forward(km, X[sel], W, sel.size)], axis=1))
-        dW += oracle.conv_wgrad(km, G[sel], X[sel], 27)
-    y_local = torch.from_numpy(np.concatenate(y_parts) if y_parts else np.zeros((0, 6)))
+    p_r, b_r = rank_points(pts, bat, mine)
+    coords_r, _, _ = oracle.quantize(p_r, VOXEL, b_r)
+    # features are indexed by the batched row (the rows of the rank's scans, in order)
+    coords_all, _, _ = oracle.quantize(pts, VOXEL, bat)
+    sel = np.nonzero(np.isin(coords_all[:, 3], mine))[0]
+    assert np.array_equal(coords_all[sel], coords_r)
+    X, W, G = _features(coords_all.shape[0])
+    km = oracle.kmap(coords_r, coords_r, offs)
+    y = oracle.conv_forward(km, X[sel], W, sel.size)
+    dW = oracle.conv_wgrad(km, G[sel], X[sel], 27)
     dW_t = allreduce_grad(torch.from_numpy(dW.copy()))
-    gathered = gather_rows(y_local)
+    y_rows = torch.from_numpy(np.concatenate([sel[:, None].astype(np.float64), y], axis=1))
+    gather = RowGather(y_rows.shape[0], y_rows.shape[1], y_rows.dtype, y_rows.device)
+    gather(y_rows)
     if rank == 0:
-        full = torch.cat(gathered).numpy()
+        full = torch.cat(gather.views()).numpy()
         np.save(os.path.join(out_dir, "y.npy"), full)
         np.save(os.path.join(out_dir, "dW.npy"), dW_t.numpy())
     dist.barrier()
@@ -81,14 +98,11 @@ def test_sharded_equals_batched_gloo(tmp_path, orc):
     mp.start_processes(_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True, start_method="spawn")
     y = np.load(tmp_path / "y.npy")
     dW = np.load(tmp_path / "dW.npy")
-    rows = _scans()
-    coords, _ = orc.create(rows)
+    pts, bat = _scans()
+    coords, _, _ = orc.quantize(pts, VOXEL, bat)  # the batched scans (all at once)
     offs = orc.region(0, 3, [3, 3, 3])
-    g = np.random.default_rng(9)
-    X = g.standard_normal((coords.shape[0], 4))
-    W = g.standard_normal((27, 5, 4))
-    G = g.standard_normal((coords.shape[0], 5))
-    km = orc.kmap(coords, coords, offs)  # the batched map (all scans at once)
+    X, W, G = _features(coords.shape[0])
+    km = orc.kmap(coords, coords, offs)
     y_all = orc.conv_forward(km, X, W, coords.shape[0])
     dW_all = orc.conv_wgrad(km, G, X, 27)
     order = np.argsort(y[:, 0])

@@ -1,55 +1,40 @@
-"""GPU <-> fp64 oracle parity of the feature path: forward, dgrad, wgrad, transposed conv,
-in fp32 mode (tolerance 1e-5) and bf16 mode (2e-2), at oracle-sized cases spanning many
-128-row tiles with ragged tails, and on sampled rows at full BASELINE sizes."""
+"""GPU <-> fp64 oracle parity of the feature path: forward, dgrad, wgrad and the transposed
+conv, in fp32 mode (tolerance 1e-5) and bf16 mode (2e-2), with every expectation built by the
+oracle alone (tests/parity.py): oracle coordinates, oracle offsets, oracle kernel map.
+
+Sizes: oracle-sized cases spanning many 128-row tiles with ragged tails, a sweep of every
+bf16 channel pair (C_in, C_out) in {16, 32, ..., 256}^2, and BASELINE.json configs[1]-[3] at
+full size in the launch configuration bench.py times (configs[4] is in test_gpu_configs.py).
+"""
 import numpy as np
 import pytest
 import torch
 
 import synthetic
-from gpu_util import BF16_TOL, FP32_TOL, assert_close, csr_np, to_np
+from gpu_util import BF16_TOL, FP32_TOL
+from parity import Spec, check_features, dev, map_pair, oracle_threads, sample
 
 pytestmark = pytest.mark.gpu
 
 
 @pytest.fixture(scope="module")
-def mk():
+def mk(orc):
     assert torch.cuda.is_available(), "GPU tests need a CUDA device"
     import paper_1904_08755_b200 as m
+    oracle_threads(orc)
     return m
-
-
-def dev(a, dtype=None):
-    t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    return t if dtype is None else t.to(dtype)
 
 
 def _sparse(mk, orc, seed, n, span, D=3, ts=1, nb=2):
     g = np.random.default_rng(seed)
     rows = np.concatenate([g.integers(-span, span, (n, D)) * ts, g.integers(0, nb, (n, 1))], axis=1).astype(np.int32)
     oc, _ = orc.create(rows, [ts] * D)
-    return mk.coords_create(dev(oc), [ts] * D), oc
+    c = mk.coords_create(dev(rows), [ts] * D)
+    assert np.array_equal(c.export().cpu().numpy(), oc)
+    return c, oc
 
 
-def _check_all(mk, orc, m, km_np, X, W, G, dt, tol, transposed=False, what=""):
-    tdt = torch.float32 if dt == "f32" else torch.bfloat16
-    # bf16 mode: inputs rounded RNE from the same fp32 samples; compared to the fp64 oracle
-    # on the ORIGINAL fp32 values (DESIGN.md §3 R21).
-    Xd, Wd, Gd = dev(X).to(tdt), dev(W).to(tdt), dev(G).to(tdt)
-    fwd = mk.conv_transpose_forward if transposed else mk.conv_forward
-    bwd = mk.conv_transpose_backward if transposed else mk.conv_backward
-    K, c_out, c_in = W.shape
-    y = fwd(m, Xd, Wd, out_dtype=torch.float32)
-    y64 = orc.conv_forward(km_np, X, W, m.n_out)
-    assert_close(to_np(y), y64, orc.conv_forward(km_np, np.abs(X), np.abs(W), m.n_out), tol, what + " fwd")
-    gin, gw = bwd(m, Gd, Xd, Wd)
-    gin64 = orc.conv_dgrad(km_np, G, W, m.n_in)
-    assert_close(to_np(gin), gin64, orc.conv_dgrad(km_np, np.abs(G), np.abs(W), m.n_in), tol, what + " dgrad")
-    gw64 = orc.conv_wgrad(km_np, G, X, K)
-    assert_close(to_np(gw), gw64, orc.conv_wgrad(km_np, np.abs(G), np.abs(X), K), tol, what + " wgrad")
-    # determinism: bit-identical on repeat (fixed reduction order)
-    y2 = fwd(m, Xd, Wd, out_dtype=torch.float32)
-    gin2, gw2 = bwd(m, Gd, Xd, Wd)
-    assert torch.equal(y, y2) and torch.equal(gin, gin2) and torch.equal(gw, gw2)
+CUBE3 = Spec(0, 3, 3)
 
 
 @pytest.mark.parametrize("dt,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
@@ -57,48 +42,45 @@ def _check_all(mk, orc, m, km_np, X, W, G, dt, tol, transposed=False, what=""):
                                              (96, 96, 5000, 15), (16, 32, 333, 6)])
 def test_submanifold_conv(mk, orc, dt, tol, cin, cout, n, span):
     c, oc = _sparse(mk, orc, cin + n, n, span)
-    r = mk.Region(mk.HYPERCUBE, 3, 3)
-    m = mk.kmap_build(c, c, r)
-    km = csr_np(m)
+    m, okm = map_pair(mk, orc, c, c, oc, oc, CUBE3, [1, 1, 1])
     g = np.random.default_rng(n)
     X = synthetic.features(1, c.n, cin)
     W = synthetic.weights(2, 27, cout, cin)
     G = g.uniform(-1, 1, (c.n, cout)).astype(np.float32)
-    _check_all(mk, orc, m, km, X, W, G, dt, tol, what=f"{dt} {cin}->{cout}")
+    check_features(mk, orc, m, okm, X, W, G, dt, tol, what=f"{dt} {cin}->{cout}")
 
 
 @pytest.mark.parametrize("dt,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
 def test_hybrid_4d_conv(mk, orc, dt, tol):
     c, oc = _sparse(mk, orc, 44, 12000, 14, D=4)
-    m = mk.kmap_build(c, c, mk.Region(mk.HYBRID, 4, 3))
-    km = csr_np(m)
+    m, okm = map_pair(mk, orc, c, c, oc, oc, Spec(2, 4, 3), [1] * 4)
     X = synthetic.features(3, c.n, 32)
     W = synthetic.weights(4, 29, 64, 32)
     G = synthetic.features(5, c.n, 64)
-    _check_all(mk, orc, m, km, X, W, G, dt, tol, what="hybrid")
+    check_features(mk, orc, m, okm, X, W, G, dt, tol, what="hybrid")
 
 
 @pytest.mark.parametrize("dt,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
-@pytest.mark.parametrize("K", [2, 3])
-def test_strided_conv_and_transpose(mk, orc, dt, tol, K):
-    fine, ofine = _sparse(mk, orc, 70 + K, 15000, 24)
+@pytest.mark.parametrize("K,ts", [(2, 1), (3, 1), (2, 2), (3, 2)])
+def test_strided_conv_and_transpose(mk, orc, dt, tol, K, ts):
+    # input tensor stride ts: offsets are scaled by ts (R14); coarse stride 2 ts
+    fine, ofine = _sparse(mk, orc, 70 + K + 10 * ts, 15000, 24, ts=ts)
     coarse = mk.coords_stride(fine, [2, 2, 2])
-    r = mk.Region(mk.HYPERCUBE, 3, K)
-    m = mk.kmap_build(fine, coarse, r)
-    km = csr_np(m)
-    Kv = m.K
+    ocoarse = orc.stride(ofine, [2, 2, 2], [ts] * 3)
+    assert np.array_equal(coarse.export().cpu().numpy(), ocoarse)
+    spec = Spec(0, 3, K)
+    m, okm = map_pair(mk, orc, fine, coarse, ofine, ocoarse, spec, [ts] * 3, what=f"down K={K}")
     cin, cout = 32, 48
     X = synthetic.features(6, fine.n, cin)
-    W = synthetic.weights(7, Kv, cout, cin)
+    W = synthetic.weights(7, m.K, cout, cin)
     G = synthetic.features(8, coarse.n, cout)
-    _check_all(mk, orc, m, km, X, W, G, dt, tol, what=f"down K={K}")
-    # transposed conv coarse -> fine
-    mt = mk.kmap_build(coarse, fine, r, transposed=True)
-    kmt = csr_np(mt)
+    check_features(mk, orc, m, okm, X, W, G, dt, tol, what=f"down K={K} ts={ts}")
+    # transposed conv coarse -> fine, probing v - i*ts in the coarse table
+    mt, okmt = map_pair(mk, orc, coarse, fine, ocoarse, ofine, spec, [ts] * 3, transposed=True, what=f"up K={K}")
     Y = synthetic.features(9, coarse.n, cout)
-    WT = synthetic.weights(10, Kv, cin, cout)
+    WT = synthetic.weights(10, m.K, cin, cout)
     GT = synthetic.features(11, fine.n, cin)
-    _check_all(mk, orc, mt, kmt, Y, WT, GT, dt, tol, transposed=True, what=f"up K={K}")
+    check_features(mk, orc, mt, okmt, Y, WT, GT, dt, tol, transposed=True, what=f"up K={K} ts={ts}")
 
 
 def test_adjoint_identity_fp32(mk, orc):
@@ -117,36 +99,97 @@ def test_adjoint_identity_fp32(mk, orc):
 
 
 @pytest.mark.parametrize("dt,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
-def test_room_full_size_sampled(mk, orc, dt, tol):
-    # BASELINE configs[1] at full size in the bench launch configuration; the oracle
-    # evaluates Eq. 3 on sampled output rows (O6 row by row).
-    pts = synthetic.room_points(2003)
-    c, _, _ = mk.coords_quantize(dev(pts), synthetic.ROOM_VOXEL)
-    m = mk.kmap_build(c, c, mk.Region(mk.HYPERCUBE, 3, 3))
-    km = csr_np(m)
-    X = synthetic.features(1, c.n, 64)
-    W = synthetic.weights(2, 27, 64, 64)
-    tdt = torch.float32 if dt == "f32" else torch.bfloat16
-    y = to_np(mk.conv_forward(m, dev(X).to(tdt), dev(W).to(tdt), out_dtype=torch.float32))
-    rows = np.random.default_rng(0).choice(c.n, 2000, replace=False).astype(np.int32)
-    rows = np.concatenate([rows, [0, c.n - 1]]).astype(np.int32)
-    y64 = orc.conv_forward_rows(km, X, W, rows)
-    s64 = orc.conv_forward_rows(km, np.abs(X), np.abs(W), rows)
-    assert_close(y[rows], y64, s64, tol, f"room {dt}")
-
-
-@pytest.mark.parametrize("dt,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
 def test_tesseract_4d_conv(mk, orc, dt, tol):
-    # K = 3^4 = 81 offsets (the 4D hypercube of P:253): exercises the K > 32 kernel-map path
-    # (k-major table, identity row order, exact pair lists) and the conv kernels' multi-word
-    # offset masks.
+    # K = 3^4 = 81 offsets (the 4D hypercube of P:253): the K > 32 kernel-map path (k-major
+    # table, identity row order, host split-K plan) and multi-word offset masks.
     c, oc = _sparse(mk, orc, 81, 6000, 7, D=4)
-    m = mk.kmap_build(c, c, mk.Region(mk.HYPERCUBE, 4, 3))
+    m, okm = map_pair(mk, orc, c, c, oc, oc, Spec(0, 4, 3), [1] * 4)
     assert m.K == 81
-    km = csr_np(m)
-    optr, oin, oout = orc.kmap(oc, oc, mk.region_offsets(mk.Region(mk.HYPERCUBE, 4, 3)))
-    assert np.array_equal(km[0], optr) and np.array_equal(km[1], oin) and np.array_equal(km[2], oout)
     X = synthetic.features(12, c.n, 16)
     W = synthetic.weights(13, 81, 32, 16)
     G = synthetic.features(14, c.n, 32)
-    _check_all(mk, orc, m, km, X, W, G, dt, tol, what="tesseract")
+    check_features(mk, orc, m, okm, X, W, G, dt, tol, what="tesseract")
+
+
+# ------------------------------------------------------------------ channel contract
+@pytest.fixture(scope="module")
+def sweep_map(mk, orc):
+    c, oc = _sparse(mk, orc, 777, 1500, 9)
+    m, okm = map_pair(mk, orc, c, c, oc, oc, CUBE3, [1, 1, 1])
+    return c, m, okm
+
+
+@pytest.mark.parametrize("cin", list(range(16, 257, 16)))
+def test_bf16_channel_sweep(mk, orc, sweep_map, cin):
+    # mk.h's bf16 channel contract: every (C_in, C_out) in {16, ..., 256}^2 plans (no
+    # MK_ERR_UNSUPPORTED) and matches the oracle in fwd, dgrad and wgrad.
+    c, m, okm = sweep_map
+    for cout in range(16, 257, 16):
+        X = synthetic.features(cin, c.n, cin)
+        W = synthetic.weights(cout, 27, cout, cin)
+        G = synthetic.features(cin + cout, c.n, cout)
+        check_features(mk, orc, m, okm, X, W, G, "bf16", BF16_TOL, what=f"sweep {cin}->{cout}", repeat=False)
+
+
+# ------------------------------------------------------------------ BASELINE configs at full size
+@pytest.fixture(scope="module")
+def room(mk, orc):
+    # configs[1]: the bench's ScanNet-shaped room (seed 2000), quantized on both sides
+    pts = synthetic.room_points(2000)
+    c, _, _ = mk.coords_quantize(dev(pts), synthetic.ROOM_VOXEL)
+    oc, _, _ = orc.quantize(pts, synthetic.ROOM_VOXEL)
+    assert np.array_equal(c.export().cpu().numpy(), oc)
+    m, okm = map_pair(mk, orc, c, c, oc, oc, CUBE3, [1, 1, 1], what="room")
+    return c, oc, m, okm
+
+
+@pytest.mark.parametrize("dt,tol", [("bf16", BF16_TOL), ("f32", FP32_TOL)])
+def test_config1_room_full_size_all_rows(mk, orc, room, dt, tol):
+    # configs[1] at full size (150k voxels, 1.39M pairs, C 64 -> 64): every row of fwd and
+    # dgrad and all of dW, element by element.  The weight-gradient split-K gives each of its
+    # 444 CTAs ~49 stages of 64 pairs, so its 4-slot stage ring wraps ~12 times.
+    c, oc, m, okm = room
+    assert m.n_pairs > 444 * 64 * 8
+    X = synthetic.features(1, c.n, 64)
+    W = synthetic.weights(2, 27, 64, 64)
+    G = synthetic.features(3, c.n, 64)
+    check_features(mk, orc, m, okm, X, W, G, dt, tol, what=f"configs[1] {dt}")
+
+
+def test_config2_video_hybrid_full_size(mk, orc):
+    # configs[2]: 3-frame Synthia-like video, 4D (x, y, z, t), hybrid kernel (29 offsets),
+    # C 32 -> 64, full size, all rows.
+    pts, fr = synthetic.video_points(3000)
+    c3, _, _ = mk.coords_quantize(dev(pts), synthetic.VIDEO_VOXEL, dev(fr))
+    o3, _, _ = orc.quantize(pts, synthetic.VIDEO_VOXEL, fr)
+    assert np.array_equal(c3.export().cpu().numpy(), o3)
+    o4 = np.concatenate([o3, np.zeros((o3.shape[0], 1), np.int32)], axis=1)  # frame -> t, b = 0
+    c4 = mk.coords_create(dev(o4))
+    m, okm = map_pair(mk, orc, c4, c4, o4, o4, Spec(2, 4, 3), [1] * 4, what="video")
+    assert m.K == 29 and c4.n > 200000
+    X = synthetic.features(31, c4.n, 32)
+    W = synthetic.weights(32, 29, 64, 32)
+    G = synthetic.features(33, c4.n, 64)
+    check_features(mk, orc, m, okm, X, W, G, "bf16", BF16_TOL, what="configs[2]")
+
+
+def test_config3_unet_pair_full_size(mk, orc, room):
+    # configs[3]: the encoder / decoder layer pair on the room: output coordinates of the
+    # stride-2 conv, 2x2x2 conv 128 -> 256 (fwd, dgrad, wgrad), and the transposed
+    # 2x2x2 conv 256 -> 128 back onto the cached fine set (fwd, dgrad, wgrad).
+    c, oc, _, _ = room
+    coarse = mk.coords_stride(c, [2, 2, 2])
+    ocoarse = orc.stride(oc, [2, 2, 2])
+    assert np.array_equal(coarse.export().cpu().numpy(), ocoarse)
+    spec = Spec(0, 3, 2)
+    md, okd = map_pair(mk, orc, c, coarse, oc, ocoarse, spec, [1, 1, 1], what="down")
+    assert md.n_pairs == c.n  # R3: with K = sigma = 2 every fine row is in exactly one pair
+    X = synthetic.features(41, c.n, 128)
+    W = synthetic.weights(42, 8, 256, 128)
+    G = synthetic.features(43, coarse.n, 256)
+    check_features(mk, orc, md, okd, X, W, G, "bf16", BF16_TOL, what="configs[3] down 128->256")
+    mu, oku = map_pair(mk, orc, coarse, c, ocoarse, oc, spec, [1, 1, 1], transposed=True, what="up")
+    Y = synthetic.features(44, coarse.n, 256)
+    WT = synthetic.weights(45, 8, 128, 256)
+    GT = synthetic.features(46, c.n, 128)
+    check_features(mk, orc, mu, oku, Y, WT, GT, "bf16", BF16_TOL, transposed=True, what="configs[3] up 256->128")

@@ -6,7 +6,7 @@ import torch
 
 import synthetic
 from conftest import full_grid
-from gpu_util import csr_np
+from parity import Spec, csr_host, map_pair
 
 pytestmark = pytest.mark.gpu
 
@@ -132,14 +132,11 @@ def test_lookup_matches_oracle(mk, orc):
 
 
 # ------------------------------------------------------------------ kernel maps
-def _check_map(mk, orc, cin_np, cout_np, region, scale, transposed, ci, co):
-    m = mk.kmap_build(ci, co, region, transposed=transposed)
-    offs = mk.region_offsets(region)
-    optr, oin, oout = orc.kmap(cin_np, cout_np, offs, scale, transposed)
-    ptr, ins, outs = csr_np(m)
-    assert np.array_equal(ptr, optr)
-    assert np.array_equal(ins, oin) and np.array_equal(outs, oout)
-    return m
+def _check_map(mk, orc, cin_np, cout_np, spec, scale, transposed, ci, co):
+    """GPU map of the GPU coordinate handles vs the oracle's map of the oracle's coordinates
+    and offsets (byte-identical); the region tables of both sides agree too."""
+    assert np.array_equal(mk.region_offsets(spec.mk(mk)), spec.orc(orc))
+    return map_pair(mk, orc, ci, co, cin_np, cout_np, spec, scale, transposed)[0]
 
 
 @pytest.mark.parametrize("kind,D,size,dil", [(0, 3, 3, 1), (0, 3, 5, 1), (1, 3, 3, 1), (2, 4, 3, 1), (0, 4, 3, 1),
@@ -149,7 +146,7 @@ def test_kmap_submanifold_matches_oracle(mk, orc, kind, D, size, dil):
     rows = np.concatenate([g.integers(-25, 25, (40000, D)), g.integers(0, 2, (40000, 1))], axis=1).astype(np.int32)
     c = mk.coords_create(dev(rows))
     oc, _ = orc.create(rows)
-    _check_map(mk, orc, oc, oc, mk.Region(kind, D, size, dil), [1] * D, False, c, c)
+    _check_map(mk, orc, oc, oc, Spec(kind, D, size, dil), [1] * D, False, c, c)
 
 
 def test_kmap_worked_examples(mk):
@@ -157,7 +154,7 @@ def test_kmap_worked_examples(mk):
     assert mk.kmap_build(c, c, mk.Region(mk.HYPERCUBE, 2, 3)).n_pairs == 100
     c1 = mk.coords_create(dev(np.array([[5, 5, 5, 0]], np.int32)))
     m = mk.kmap_build(c1, c1, mk.Region(mk.HYPERCUBE, 3, 3))
-    ptr, ins, outs = csr_np(m)
+    ptr, ins, outs = csr_host(m)
     assert m.n_pairs == 1 and ptr[14] - ptr[13] == 1  # one pair at offset 0
 
 
@@ -169,7 +166,8 @@ def test_kmap_strided_and_transposed_match_oracle(mk, orc, K, ts):
     coarse = mk.coords_stride(fine, [2, 2, 2])
     ofine, _ = orc.create(rows, [ts] * 3)
     ocoarse = orc.stride(ofine, [2, 2, 2], [ts] * 3)
-    r = mk.Region(mk.HYPERCUBE, 3, K)
+    assert np.array_equal(coarse.export().cpu().numpy(), ocoarse)
+    r = Spec(0, 3, K)
     m = _check_map(mk, orc, ofine, ocoarse, r, [ts] * 3, False, fine, coarse)
     if K == 2:
         assert m.n_pairs == fine.n  # R3 partition pin
@@ -181,7 +179,8 @@ def test_kmap_room_full_size(mk, orc):
     pts = synthetic.room_points(2002)
     c, _, _ = mk.coords_quantize(dev(pts), synthetic.ROOM_VOXEL)
     oc, _, _ = orc.quantize(pts, synthetic.ROOM_VOXEL)
-    _check_map(mk, orc, oc, oc, mk.Region(mk.HYPERCUBE, 3, 3), [1, 1, 1], False, c, c)
+    assert np.array_equal(c.export().cpu().numpy(), oc)
+    _check_map(mk, orc, oc, oc, Spec(0, 3, 3), [1, 1, 1], False, c, c)
 
 
 def test_kmap_video_hybrid_full_size(mk, orc):
@@ -194,7 +193,7 @@ def test_kmap_video_hybrid_full_size(mk, orc):
     o3, _, _ = orc.quantize(pts, synthetic.VIDEO_VOXEL, fr)
     o4 = np.concatenate([o3, np.zeros((o3.shape[0], 1), np.int32)], axis=1)
     assert np.array_equal(c4.export().cpu().numpy(), o4)
-    m = _check_map(mk, orc, o4, o4, mk.Region(mk.HYBRID, 4, 3), [1] * 4, False, c4, c4)
+    m = _check_map(mk, orc, o4, o4, Spec(2, 4, 3), [1] * 4, False, c4, c4)
     assert m.K == 29
 
 
@@ -230,20 +229,16 @@ def test_expand_and_generative_transposed_conv(mk, orc, K):
     g = np.random.default_rng(40 + K)
     rows = np.concatenate([g.integers(-40, 40, (20000, 3)), g.integers(0, 2, (20000, 1))], axis=1).astype(np.int32)
     oc, _ = orc.create(rows)
-    fine = mk.coords_create(dev(oc))
+    fine = mk.coords_create(dev(rows))
     coarse = mk.coords_stride(fine, [2, 2, 2])
-    region = mk.Region(mk.HYPERCUBE, 3, K)
+    spec = Spec(0, 3, K)
+    region = spec.mk(mk)
     up = mk.coords_expand(coarse, region, [1, 1, 1])
     ocoarse = orc.stride(oc, [2, 2, 2])
-    offs = mk.region_offsets(region)
-    oup = orc.expand(ocoarse, offs, [1, 1, 1])
+    oup = orc.expand(ocoarse, spec.orc(orc), [1, 1, 1])
     assert np.array_equal(up.export().cpu().numpy(), oup)
     assert up.tensor_stride == [1, 1, 1]
-    m = mk.kmap_build(coarse, up, region, transposed=True)
-    km = csr_np(m)
-    okm = orc.kmap(ocoarse, oup, offs, [1, 1, 1], transposed=True)
-    for a, b in zip(km, okm):
-        assert np.array_equal(a, b)
+    m, okm = map_pair(mk, orc, coarse, up, ocoarse, oup, spec, [1, 1, 1], transposed=True)
     Y = g.standard_normal((coarse.n, 32)).astype(np.float32)
     W = (g.standard_normal((m.K, 16, 32)) * 0.1).astype(np.float32)
     z = mk.conv_transpose_forward(m, dev(Y), dev(W)).cpu().numpy()

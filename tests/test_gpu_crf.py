@@ -5,7 +5,8 @@ import numpy as np
 import pytest
 import torch
 
-from gpu_util import FP32_TOL, assert_close, csr_np
+from gpu_util import FP32_TOL, assert_close
+from parity import Spec, map_pair
 
 pytestmark = pytest.mark.gpu
 D = 7
@@ -53,13 +54,8 @@ def test_kmap7_hypercross_matches_oracle(mk, orc):
     rows = _lattice7(2)
     oc, _ = orc.create(rows)
     c = mk.coords_create(dev(oc))
-    r = mk.Region(mk.HYPERCROSS, D, 3)
-    m = mk.kmap_build(c, c, r)
+    m, _ = map_pair(mk, orc, c, c, oc, oc, Spec(1, D, 3), [1] * D, what="7D hypercross")
     assert m.K == 15
-    km = csr_np(m)
-    okm = orc.kmap(oc, oc, mk.region_offsets(r))
-    for a, b in zip(km, okm):
-        assert np.array_equal(a, b)
 
 
 @pytest.mark.parametrize("C,n_iters", [(8, 3), (20, 1)])
@@ -67,9 +63,7 @@ def test_crf_infer_matches_oracle(mk, orc, C, n_iters):
     rows = _lattice7(3)
     oc, _ = orc.create(rows)
     c = mk.coords_create(dev(oc))
-    r = mk.Region(mk.HYPERCROSS, D, 3)
-    m = mk.kmap_build(c, c, r)
-    km = csr_np(m)
+    m, km = map_pair(mk, orc, c, c, oc, oc, Spec(1, D, 3), [1] * D)
     g = np.random.default_rng(C)
     phi = g.standard_normal((c.n, C)).astype(np.float32)
     W = (g.standard_normal((15, C, C)) * 0.5).astype(np.float32)
@@ -89,8 +83,7 @@ def test_crf_backward_matches_oracle(mk, orc, C, n_iters):
     rows = _lattice7(5, n=12000)
     oc, _ = orc.create(rows)
     c = mk.coords_create(dev(oc))
-    m = mk.kmap_build(c, c, mk.Region(mk.HYPERCROSS, D, 3))
-    km = csr_np(m)
+    m, km = map_pair(mk, orc, c, c, oc, oc, Spec(1, D, 3), [1] * D)
     g = np.random.default_rng(100 + C)
     phi = g.standard_normal((c.n, C)).astype(np.float32)
     W = (g.standard_normal((15, C, C)) * 0.5).astype(np.float32)

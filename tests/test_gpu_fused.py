@@ -8,7 +8,8 @@ import pytest
 import torch
 
 import synthetic
-from gpu_util import BF16_TOL, FP32_TOL, assert_close, csr_np, to_np
+from gpu_util import BF16_TOL, FP32_TOL, assert_close, to_np
+from parity import Spec, map_pair
 
 pytestmark = pytest.mark.gpu
 
@@ -29,7 +30,9 @@ def _coords(mk, orc, seed, n, span, D=3, ts=1):
     g = np.random.default_rng(seed)
     rows = np.concatenate([g.integers(-span, span, (n, D)) * ts, g.integers(0, 2, (n, 1))], axis=1).astype(np.int32)
     oc, _ = orc.create(rows, [ts] * D)
-    return mk.coords_create(dev(oc), [ts] * D)
+    c = mk.coords_create(dev(rows), [ts] * D)
+    assert np.array_equal(c.export().cpu().numpy(), oc)
+    return c, oc
 
 
 def _epi_params(seed, c_out, n_out):
@@ -39,7 +42,7 @@ def _epi_params(seed, c_out, n_out):
     return gamma, beta, mean, var, g.uniform(-1, 1, (n_out, c_out)).astype(np.float32)
 
 
-def _check(mk, orc, m, X, W, dt, out_dt, tol, opts, seed, transposed=False):
+def _check(mk, orc, m, km, X, W, dt, out_dt, tol, opts, seed, transposed=False):
     tdt = torch.float32 if dt == "f32" else torch.bfloat16
     odt = torch.float32 if out_dt == "f32" else torch.bfloat16
     K, c_out, c_in = W.shape
@@ -52,7 +55,6 @@ def _check(mk, orc, m, X, W, dt, out_dt, tol, opts, seed, transposed=False):
         kw["residual"] = dev(R).to(odt)
     relu = "relu" in opts
     y = mk.conv_forward(m, dev(X).to(tdt), dev(W).to(tdt), out_dtype=odt, relu=relu, **kw)
-    km = csr_np(m)
     # the oracle sees the fp32-folded scale / shift and the residual as the GPU stores it
     sc = scale.astype(np.float32).astype(np.float64) if "bn" in opts else None
     sh = shift.astype(np.float32).astype(np.float64) if "bn" in opts else None
@@ -75,40 +77,40 @@ def _check(mk, orc, m, X, W, dt, out_dt, tol, opts, seed, transposed=False):
 @pytest.mark.parametrize("out_dt", ["f32", "bf16"])
 @pytest.mark.parametrize("opts", [("bn", "res", "relu"), ("relu",), ("bn",), ("res",)])
 def test_fused_submanifold(mk, orc, dt, tol, out_dt, opts):
-    c = _coords(mk, orc, 5, 9000, 20)
-    m = mk.kmap_build(c, c, mk.Region(mk.HYPERCUBE, 3, 3))
+    c, oc = _coords(mk, orc, 5, 9000, 20)
+    m, km = map_pair(mk, orc, c, c, oc, oc, Spec(0, 3, 3), [1] * 3)
     X = synthetic.features(11, c.n, 32)
     W = synthetic.weights(12, 27, 64, 32)
-    _check(mk, orc, m, X, W, dt, out_dt, tol, opts, 13)
+    _check(mk, orc, m, km, X, W, dt, out_dt, tol, opts, 13)
 
 
 @pytest.mark.parametrize("dt,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
 def test_fused_rows_without_pairs(mk, orc, dt, tol):
-    cin = _coords(mk, orc, 21, 3000, 25)
-    cout = _coords(mk, orc, 22, 2500, 25)  # a different set: many output rows have no pair
-    m = mk.kmap_build(cin, cout, mk.Region(mk.HYPERCUBE, 3, 3))
+    cin, ocin = _coords(mk, orc, 21, 3000, 25)
+    cout, ocout = _coords(mk, orc, 22, 2500, 25)  # a different set: many output rows have no pair
+    m, km = map_pair(mk, orc, cin, cout, ocin, ocout, Spec(0, 3, 3), [1] * 3)
     assert m.n_pairs > 0
     X = synthetic.features(23, cin.n, 16)
     W = synthetic.weights(24, 27, 48, 16)
-    _check(mk, orc, m, X, W, dt, "f32", tol, ("bn", "res", "relu"), 25)
+    _check(mk, orc, m, km, X, W, dt, "f32", tol, ("bn", "res", "relu"), 25)
 
 
 @pytest.mark.parametrize("dt,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
 def test_fused_transposed(mk, orc, dt, tol):
-    c = _coords(mk, orc, 31, 8000, 24)
+    c, oc = _coords(mk, orc, 31, 8000, 24)
     cs = mk.coords_stride(c, [2, 2, 2])
-    m = mk.kmap_build(cs, c, mk.Region(mk.HYPERCUBE, 3, 2), transposed=True)
+    ocs = orc.stride(oc, [2, 2, 2])
+    m, km = map_pair(mk, orc, cs, c, ocs, oc, Spec(0, 3, 2), [1] * 3, transposed=True)
     X = synthetic.features(32, cs.n, 64)
     W = synthetic.weights(33, 8, 32, 64)
-    _check(mk, orc, m, X, W, dt, "f32", tol, ("bn", "relu"), 34)
+    _check(mk, orc, m, km, X, W, dt, "f32", tol, ("bn", "relu"), 34)
 
 
 def test_residual_block_chain_fp32(mk, orc):
     """MinkowskiNet basic block: relu(bn2(conv2(relu(bn1(conv1 x)))) + x), both
     convs with fused epilogues, against the oracle chain in fp64."""
-    c = _coords(mk, orc, 41, 12000, 22)
-    m = mk.kmap_build(c, c, mk.Region(mk.HYPERCUBE, 3, 3))
-    km = csr_np(m)
+    c, oc = _coords(mk, orc, 41, 12000, 22)
+    m, km = map_pair(mk, orc, c, c, oc, oc, Spec(0, 3, 3), [1] * 3)
     C = 32
     X = synthetic.features(42, c.n, C)
     W1, W2 = synthetic.weights(43, 27, C, C), synthetic.weights(44, 27, C, C)

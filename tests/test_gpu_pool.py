@@ -6,7 +6,8 @@ import numpy as np
 import pytest
 import torch
 
-from gpu_util import FP32_TOL, assert_close, csr_np
+from gpu_util import FP32_TOL, assert_close
+from parity import Spec, map_pair
 
 pytestmark = pytest.mark.gpu
 
@@ -27,23 +28,23 @@ def _sets(mk, orc, seed, n=20000, span=30):
     g = np.random.default_rng(seed)
     rows = np.concatenate([g.integers(-span, span, (n, 3)), g.integers(0, 2, (n, 1))], axis=1).astype(np.int32)
     oc, _ = orc.create(rows)
-    fine = mk.coords_create(dev(oc))
+    fine = mk.coords_create(dev(rows))
+    assert np.array_equal(fine.export().cpu().numpy(), oc)
     coarse = mk.coords_stride(fine, [2, 2, 2])
-    return fine, coarse, oc
+    return fine, coarse, oc, orc.stride(oc, [2, 2, 2])
 
 
 @pytest.mark.parametrize("dt", ["f32", "bf16"])
 @pytest.mark.parametrize("K,kind", [(2, "strided"), (3, "strided"), (3, "submanifold"), (2, "transposed")])
 def test_pool_matches_oracle(mk, orc, dt, K, kind):
-    fine, coarse, _ = _sets(mk, orc, 10 * K + len(kind))
-    r = mk.Region(mk.HYPERCUBE, 3, K)
+    fine, coarse, ofine, ocoarse = _sets(mk, orc, 10 * K + len(kind))
+    spec = Spec(0, 3, K)
     if kind == "strided":
-        m = mk.kmap_build(fine, coarse, r)
+        m, km = map_pair(mk, orc, fine, coarse, ofine, ocoarse, spec, [1] * 3)
     elif kind == "submanifold":
-        m = mk.kmap_build(fine, fine, r)
+        m, km = map_pair(mk, orc, fine, fine, ofine, ofine, spec, [1] * 3)
     else:  # unpooling: coarse -> fine on the transposed map ("transposed pooling")
-        m = mk.kmap_build(coarse, fine, r, transposed=True)
-    km = csr_np(m)
+        m, km = map_pair(mk, orc, coarse, fine, ocoarse, ofine, spec, [1] * 3, transposed=True)
     g = np.random.default_rng(K)
     C = 40
     tdt = torch.float32 if dt == "f32" else torch.bfloat16

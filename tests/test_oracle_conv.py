@@ -181,3 +181,82 @@ def test_forward_rows_and_equivariance(orc):
     X2 = g.standard_normal(X.shape)
     np.testing.assert_allclose(orc.conv_forward(km, 2 * X - 3 * X2, W, c.shape[0]),
                                2 * y - 3 * orc.conv_forward(km, X2, W, c.shape[0]), rtol=1e-11, atol=1e-11)
+
+
+# ---------------------------------------------------------------- tensor stride > 1 (R14)
+# "stride size of the input sparse tensor": a sparse tensor of tensor stride s has
+# coordinates on the lattice sZ^D, and its neighbours at offset i are u + i*s.  A fully
+# occupied stride-2 lattice is therefore the dense grid with every index doubled (P:159's
+# dense special case on the compacted grid), so F.conv3d on the compacted grid pins the
+# offset scaling of orc_kmap: a dropped scale (u + i) finds no neighbour on 2Z^3, a doubled
+# one (u + 4i) skips the nearest ones — both change every output.
+def _stride2_grid(G, base=-4):
+    c = full_grid(G, 3)
+    c[:, :3] = 2 * c[:, :3] + base  # the lattice 2Z^3 shifted to negative coordinates
+    return c
+
+
+def _compact(c, base=-4, s=2):
+    return (c[:, :3] - base) // s
+
+
+@pytest.mark.parametrize("G,cin,cout", [(5, 3, 4), (4, 5, 2)])
+def test_tensor_stride2_submanifold_equals_conv3d(orc, G, cin, cout):
+    g = np.random.default_rng(40 + G)
+    c, _ = orc.create(_stride2_grid(G), tensor_stride=[2, 2, 2])
+    offs = orc.region(0, 3, [3, 3, 3])
+    km = orc.kmap(c, c, offs, scale=[2, 2, 2])
+    X = g.standard_normal((c.shape[0], cin))
+    W = g.standard_normal((27, cout, cin))
+    Gout = g.standard_normal((c.shape[0], cout))
+    cc = _compact(c)
+    xd = torch.zeros(1, cin, G, G, G, dtype=torch.float64)
+    xd[0][:, cc[:, 0], cc[:, 1], cc[:, 2]] = torch.from_numpy(X.T)
+    xd.requires_grad_(True)
+    wt = _w_to_torch(W, offs, 3).requires_grad_(True)
+    yd = F.conv3d(xd, wt, padding=1)
+    np.testing.assert_allclose(orc.conv_forward(km, X, W, c.shape[0]), _dense_to_rows(yd[0].detach().numpy(), cc),
+                               rtol=1e-12, atol=1e-12)
+    gd = torch.zeros_like(yd)
+    gd[0][:, cc[:, 0], cc[:, 1], cc[:, 2]] = torch.from_numpy(Gout.T)
+    (yd * gd).sum().backward()
+    np.testing.assert_allclose(orc.conv_dgrad(km, Gout, W, c.shape[0]), _dense_to_rows(xd.grad[0].numpy(), cc),
+                               rtol=1e-12, atol=1e-12)
+    dW = orc.conv_wgrad(km, Gout, X, 27)
+    for k, (a, b, e) in enumerate(offs.tolist()):
+        np.testing.assert_allclose(dW[k], wt.grad[:, :, a + 1, b + 1, e + 1].numpy(), rtol=1e-12, atol=1e-12)
+    # |M| on the full lattice is the closed form (3G - 2)^3 only with the scaled offsets
+    assert km[0][-1] == (3 * G - 2) ** 3
+
+
+@pytest.mark.parametrize("K", [2, 3])
+def test_tensor_stride2_to_4_and_transpose_equal_conv3d(orc, K):
+    # stride-2 input -> stride-4 output (s_out = s_in * sigma), offsets scaled by s_in = 2;
+    # the transposed map probes the fine (stride 2) set at v - i*2 (R13/R14).
+    G, cin, cout = 6, 3, 4
+    g = np.random.default_rng(50 + K)
+    fine, _ = orc.create(_stride2_grid(G), tensor_stride=[2, 2, 2])
+    coarse = orc.stride(fine, [2, 2, 2], [2, 2, 2])
+    assert np.all(coarse[:, :3] % 4 == 0)
+    offs = orc.region(0, 3, [K] * 3)
+    km = orc.kmap(fine, coarse, offs, scale=[2, 2, 2])
+    X = g.standard_normal((fine.shape[0], cin))
+    W = g.standard_normal((offs.shape[0], cout, cin))
+    y = orc.conv_forward(km, X, W, coarse.shape[0])
+    cf = _compact(fine)
+    xd = torch.zeros(1, cin, G, G, G, dtype=torch.float64)
+    xd[0][:, cf[:, 0], cf[:, 1], cf[:, 2]] = torch.from_numpy(X.T)
+    wt = _w_to_torch(W, offs, K)
+    # base -4 is a multiple of 4, so the coarse lattice point 4j + base sits at compact 2j
+    yd = F.conv3d(xd, wt, stride=2, padding=1 if K == 3 else 0)[0].numpy()
+    np.testing.assert_allclose(y, _dense_to_rows(yd, _compact(coarse) // 2), rtol=1e-12, atol=1e-12)
+    if K == 2:
+        kmT = orc.kmap(coarse, fine, offs, scale=[2, 2, 2], transposed=True)
+        Y = g.standard_normal((coarse.shape[0], cout))
+        WT = np.transpose(W, (0, 2, 1)).copy()
+        z = orc.conv_forward(kmT, Y, WT, fine.shape[0])
+        cc = _compact(coarse) // 2
+        yd2 = torch.zeros(1, cout, G // 2, G // 2, G // 2, dtype=torch.float64)
+        yd2[0][:, cc[:, 0], cc[:, 1], cc[:, 2]] = torch.from_numpy(Y.T)
+        zd = F.conv_transpose3d(yd2, wt, stride=2)[0].numpy()
+        np.testing.assert_allclose(z, _dense_to_rows(zd, cf), rtol=1e-12, atol=1e-12)

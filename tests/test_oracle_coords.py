@@ -191,3 +191,36 @@ def test_expand_pins(orc):
     assert sorted(map(tuple, up.tolist())) == sorted(map(tuple, fine.tolist()))
     # (4) batch indices never move (R18)
     assert set(got[:, 3].tolist()) == set(c[:, 3].tolist())
+
+
+def test_packed_key_domain(orc):
+    # Reading R19 (the ABI domain of mk.h): D = 4 keeps t in [-2^15, 2^15) and b <= 65534;
+    # D = 5..7 keeps axes 0-2 in [-2^19, 2^19), axes 3-5 in [-2^11, 2^11), axis 6 in
+    # [-2^15, 2^15).  The first row outside the domain is reported with COORD_RANGE.
+    r4 = np.zeros((10, 5), np.int32)
+    r4[6, 3] = -32768            # the lowest representable t: accepted
+    orc.create(r4.copy())
+    for row, col, v in ((4, 3, 40000), (2, 3, -32769), (7, 4, 65535)):
+        bad = r4.copy()
+        bad[row, col] = v
+        with pytest.raises(orc.OracleError) as e:
+            orc.create(bad)
+        assert e.value.status == orc.COORD_RANGE and e.value.row == row
+    r7 = np.zeros((6, 8), np.int32)
+    r7[1, 0], r7[2, 3], r7[3, 6] = (1 << 19) - 1, -(1 << 11), 32767  # edges: accepted
+    orc.create(r7.copy())
+    for row, col, v in ((3, 0, 1 << 19), (5, 4, 1 << 11), (1, 6, -32769)):
+        bad = r7.copy()
+        bad[row, col] = v
+        with pytest.raises(orc.OracleError) as e:
+            orc.create(bad)
+        assert e.value.status == orc.COORD_RANGE and e.value.row == row
+    # quantize applies the same domain to floor(p / v): t = 40000.5 / 1.0 -> 40000
+    pts = np.zeros((5, 4), np.float32)
+    pts[3, 3] = 40000.5
+    with pytest.raises(orc.OracleError) as e:
+        orc.quantize(pts, 1.0)
+    assert e.value.status == orc.COORD_RANGE and e.value.row == 3
+    # D <= 3: any int32 component
+    big = np.array([[2**31 - 1, -2**31, 0, 0]], np.int32)
+    assert np.array_equal(orc.create(big)[0], big)

@@ -148,3 +148,27 @@ def test_lookup(orc):
     miss = rows.copy()
     miss[:, 3] = 5
     assert np.all(orc.lookup(rows, miss) == -1)
+
+
+@pytest.mark.parametrize("K", [2, 3])
+def test_kmap_reverse_is_transposed_map_and_involution(orc, K):
+    # P:202 (roles reversed): reverse(map fine -> coarse) is the transposed map coarse -> fine,
+    # which is built by independent probing (v - i*s); reversing twice gives the map back.
+    g = np.random.default_rng(21 + K)
+    fine = np.concatenate([g.integers(-6, 6, (300, 3)) * 2, g.integers(0, 2, (300, 1))], axis=1).astype(np.int32)
+    fine, _ = orc.create(fine, tensor_stride=[2, 2, 2])
+    coarse = orc.stride(fine, [2, 2, 2], [2, 2, 2])
+    offs = orc.region(0, 3, [K] * 3)
+    fwd = orc.kmap(fine, coarse, offs, scale=[2, 2, 2])
+    tr = orc.kmap(coarse, fine, offs, scale=[2, 2, 2], transposed=True)
+    rev = orc.kmap_reverse(fwd)
+    for a, b in zip(rev, tr):
+        assert np.array_equal(a, b)
+    for a, b in zip(orc.kmap_reverse(rev), fwd):
+        assert np.array_equal(a, b)
+    # O7 = O6 on the reverse map with W_k^T, element by element
+    X = g.standard_normal((coarse.shape[0], 3))
+    W = g.standard_normal((offs.shape[0], 3, 4))
+    rows = np.arange(fine.shape[0], dtype=np.int32)
+    np.testing.assert_allclose(orc.conv_forward_rows(rev, X, np.transpose(W, (0, 2, 1)).copy(), rows),
+                               orc.conv_dgrad(fwd, X, W, fine.shape[0]), rtol=1e-13, atol=1e-13)
