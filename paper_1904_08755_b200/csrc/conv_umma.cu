@@ -219,6 +219,7 @@ struct FwdParams {
   int sw;  // W chunk slots (a ring: W_k chunks are prefetched several offsets ahead)
   int tb;  // tiles per CTA (one TMEM accumulator each: tb * cw <= 512 columns)
   int fold;  // tile order (see cta_tile)
+  int ncb;   // commit barriers in the ring (power of two)
   uint32_t a_bytes, b_bytes, tmem_cols;
   Epilogue ep;  // fused scale / shift / residual / ReLU (forward only; identity otherwise)
 };
@@ -274,10 +275,12 @@ __device__ __forceinline__ void store16(const FwdParams& p, int64_t row, int col
 
 constexpr int kMaxK = 128;  // offsets supported by the tensor-core conv (4 mask words)
 // Ring of commit barriers: the MMA thread's j-th group commit (covering steps up to
-// (j+1)*ga - 1) arrives on cb[j % kNCB]; anyone needing "all MMAs of step <= x done" waits
-// for commit x / ga at parity (j / kNCB) & 1.  kNCB >> the MMA's possible run-ahead, so a
+// (j+1)*ga - 1) arrives on cb[j % ncb]; anyone needing "all MMAs of step <= x done" waits
+// for commit x / ga at parity (j / ncb) & 1.  ncb (a power of two, sized by the host) exceeds
+// the number of commits the MMA can issue past any awaited one — the W stager waits for the
+// commit of the unit upr units back, so ncb > upr * tb * nch / ga + sa — so a
 // waiter can never confuse phases.
-constexpr int kNCB = 16;
+constexpr int kNCB = 16;  // minimum commit-ring size
 
 // Per-CTA plan, built once in shared memory by warp 0: the CTA's tiles are
 // blockIdx.x * tb + i (adjacent in the map's bitmask-sorted row order, so they share most
@@ -368,8 +371,8 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
   int32_t* nbr_s = (int32_t*)(w_base + (size_t)p.sw * p.b_bytes);  // [kFwdProd][3][128] index buffers
   Plan* pl = (Plan*)(nbr_s + kFwdProd * 3 * kTileM);
   uint64_t* a_full = (uint64_t*)(((uintptr_t)(pl + 1) + 15) & ~(uintptr_t)15);
-  uint64_t* cb = a_full + p.sa;  // [kNCB] commit ring (stage slots and W slots are released by it)
-  uint64_t* w_full = cb + kNCB;
+  uint64_t* cb = a_full + p.sa;  // [ncb] commit ring (stage slots and W slots are released by it)
+  uint64_t* w_full = cb + p.ncb;
   uint64_t* tfull = w_full + p.sw;
   uint32_t* tmem_slot = (uint32_t*)(tfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -381,7 +384,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
   // prologue that touches no global memory overlaps the predecessor kernel (PDL)
   if (threadIdx.x == 32) {
     for (int s = 0; s < p.sa; ++s) mbar_init(a_full + s, 32);  // one cp.async arrival per lane
-    for (int j = 0; j < kNCB; ++j) mbar_init(cb + j, 1);
+    for (int j = 0; j < p.ncb; ++j) mbar_init(cb + j, 1);
     for (int s = 0; s < p.sw; ++s) mbar_init(w_full + s, 1);
     mbar_init(tfull, 1);
     fence_mbar_init();
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
       const int slot = g % p.sa;
       if (g >= p.sa) {  // slot reuse: all MMAs of step g - sa done
         const int j = (g - p.sa) / p.ga;
-        ACCT_WAIT(0, cb + j % kNCB, (uint32_t)(j / kNCB) & 1u);
+        ACCT_WAIT(0, cb + (j & (p.ncb - 1)), (uint32_t)(j / p.ncb) & 1u);
       }
       const uint32_t a_s = smem_u32(a_base + (size_t)slot * p.a_bytes);
       const int32_t* ix = ibuf + b * kTileM;
@@ -497,7 +500,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
         const int uo = u - upr;
         if (uo >= 0) {
           const int j = (pl->g0[uo + 1] - 1) / p.ga;  // commit covering uo's last step
-          ACCT_WAIT(0, cb + j % kNCB, (uint32_t)(j / kNCB) & 1u);
+          ACCT_WAIT(0, cb + (j & (p.ncb - 1)), (uint32_t)(j / p.ncb) & 1u);
         }
         for (int c = 0; c < p.nch; ++c) {
           mbar_arrive_expect_tx(w_full + ws, wb);
@@ -557,7 +560,7 @@ __global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_const
             __syncwarp();
             // a commit stalls the next MMAs ~250 cycles (tools/ubench_umma.cu): one per ga steps
             if (++gq == (uint32_t)p.ga) {
-              if (leader) umma_commit(cb + (ncommit % kNCB));
+              if (leader) umma_commit(cb + (ncommit & (uint32_t)(p.ncb - 1)));
               ++ncommit;
               gq = 0;
             }
@@ -1066,7 +1069,15 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
     return e ? std::atoi(e) : 0;
   }();
   p.fold = env_fold > 0 ? 1 : 0;
-  const int base = 1024 + 512 + kFwdProd * 3 * kTileM * 4 + (int)sizeof(Plan);
+  // alignment + index buffers + plan + TMEM slot; the barriers (a_full, commit ring, W ring,
+  // tfull) are added per plan below
+  const int base0 = 1024 + kFwdProd * 3 * kTileM * 4 + (int)sizeof(Plan) + 16;
+  // commit-ring size for a plan (an upper bound over sa <= 4, ga >= 1; see kNCB)
+  auto ring = [&](int sw, int tb) {
+    int n = kNCB;
+    while (n <= (sw / nch) * tb * nch + kFwdProd + 4) n *= 2;
+    return n;
+  };
   // Output columns per CTA.  All of C_out in one CTA when its W ring (2 units of nch chunks of
   // cw x CH) and two A stage slots fit the SM; otherwise the columns are split over
   // blockIdx.y (each CTA gathers the same rows and multiplies by its slice of W_k: e.g. C_in =
@@ -1078,6 +1089,7 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
     p.b_bytes = (uint32_t)p.cw * CH * 2;
     p.tb = p.fold ? std::max(1, std::min(env_fold, 256 / p.cw)) : std::max(1, std::min(2, 256 / p.cw));
     p.tmem_cols = pow2_cols((uint32_t)(p.tb * p.cw));
+    const int base = base0 + 8 * (kFwdProd + ring(nch * 4, p.tb) + nch * 4 + 2);
     // Three CTAs per SM (configs[1] fwd 65.4 -> 62.9 us, dgrad 64.3 -> 62.2 us) when two stage
     // slots and the W ring fit a third of the SM and the registers allow it (the fused-epilogue
     // instance needs 84 registers: two CTAs).
@@ -1098,6 +1110,7 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   // configs[1]): more warps issue the gathers faster than fewer warps with deeper queues
   p.np = env_np > 0 ? std::min(env_np, p.sa) : p.sa;
   p.ga = p.sa % 2 == 0 ? 2 : 1;  // the W ring must hold >= ga units: sw / nch >= 2 >= ga
+  p.ncb = ring(p.sw, p.tb);
   if (p.sa < 2 || p.tmem_cols > 512)
     MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: channel counts too large for the smem pipeline");
   const size_t wbytes = (size_t)nb.K * nch * p.b_img;

@@ -125,6 +125,7 @@ def test_bf16_channel_sweep(mk, orc, sweep_map, cin):
     # MK_ERR_UNSUPPORTED) and matches the oracle in fwd, dgrad and wgrad.
     c, m, okm = sweep_map
     for cout in range(16, 257, 16):
+        print(f"sweep {cin}->{cout}", flush=True)
         X = synthetic.features(cin, c.n, cin)
         W = synthetic.weights(cout, 27, cout, cin)
         G = synthetic.features(cin + cout, c.n, cout)
