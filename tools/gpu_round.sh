@@ -1,19 +1,11 @@
 #!/bin/bash
-# One GPU round trip: parity tests, smoke, bench, launch list (+ optional ncu full captures).
-# usage: tools/gpu_round.sh [tag] [full-capture-kernel-regex ...]
-set -u
-TAG=${1:-run}; shift || true
-OUT=gpurun_out/$TAG
+# One GPU call: GPU tests, smoke, default bench line (outputs under gpurun_out/$1).
+set -x
+OUT=gpurun_out/${1:-run}
 mkdir -p $OUT
-timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest.txt 2>&1; echo "pytest rc=$?" >> $OUT/pytest.txt
-tail -3 $OUT/pytest.txt
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.txt 2>&1; echo "smoke rc=$?" >> $OUT/smoke.txt
-tail -2 $OUT/smoke.txt
-timeout 600 python bench.py > $OUT/bench.json 2> $OUT/bench.err; tail -2 $OUT/bench.err; cat $OUT/bench.json
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $OUT/launches.csv \
-    python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
-for K in "$@"; do
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s 2 -c 1 -o $OUT/prof_$K \
-      python bench.py --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
-done
-ls $OUT
+nvidia-smi > $OUT/nvsmi.txt 2>&1
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -x -q --durations=25 > $OUT/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" >> $OUT/smoke.log
+timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench rc=$?" >> $OUT/bench.err
+tail -3 $OUT/pytest_gpu.log; tail -2 $OUT/smoke.log; cat $OUT/bench.json | head -c 3000
