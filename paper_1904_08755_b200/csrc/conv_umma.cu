@@ -53,8 +53,15 @@ constexpr int kFwdStage = 9;
 constexpr int kFwdThreads = 10 * 32;
 constexpr int kMaxSmem = 227 * 1024;
 
+// Rounds a dynamic shared-memory pointer up to 1024 bytes.  The offset is added to the
+// pointer itself (no integer round trip), so the compiler keeps the shared state space
+// and every access derived from it is an LDS/STS, not a generic load.
 __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
-  return (uint8_t*)(((uintptr_t)p + 1023) & ~(uintptr_t)1023);
+  return p + ((1024u - (smem_u32(p) & 1023u)) & 1023u);
+}
+template <class T>
+__device__ __forceinline__ T* align16(void* p) {
+  return (T*)((uint8_t*)p + ((16u - (smem_u32(p) & 15u)) & 15u));
 }
 
 // ------------------------------------------------------------------ weight packing
@@ -170,7 +177,15 @@ __device__ unsigned long long g_cta[4096][4];  // per-CTA [start ns, end ns, smi
     mbar_wait(bar, par);                                       \
     acct[slot] += clock64() - _t0;                             \
   } while (0)
+#define ACCT_WAIT_SLEEP(slot, bar, par)                        \
+  do {                                                         \
+    const long long _t0 = clock64();                           \
+    mbar_wait_sleep(bar, par);                                 \
+    acct[slot] += clock64() - _t0;                             \
+  } while (0)
 #define ACCT_DECL long long acct[8] = {0, 0, 0, 0, 0, 0, 0, 0}; const long long acct_t0 = clock64();
+#define ACCT_NOW(v) const long long v = clock64()
+#define ACCT_ADD(slot, t0) (acct[slot] += clock64() - (t0))
 #define ACCT_DUMP                                                                             \
   do {                                                                                        \
     if (blockIdx.x == 100 && lane == 0) {                                                     \
@@ -180,6 +195,9 @@ __device__ unsigned long long g_cta[4096][4];  // per-CTA [start ns, end ns, smi
   } while (0)
 #else
 #define ACCT_WAIT(slot, bar, par) mbar_wait(bar, par)
+#define ACCT_WAIT_SLEEP(slot, bar, par) mbar_wait_sleep(bar, par)
+#define ACCT_NOW(v)
+#define ACCT_ADD(slot, t0)
 #define ACCT_DECL
 #define ACCT_DUMP \
   do {            \
@@ -637,8 +655,10 @@ struct WgradParams {
   const int32_t* out_idx;
   const int4* segs;          // (k, begin, end, slot), grouped by CTA
   const int32_t* seg_begin;  // [n_cta + 1]
-  const int64_t* ptr;        // [K + 1] device CSR offsets (device-side plan when segs == NULL)
+  const int64_t* ptr;        // [K + 1] device CSR offsets (device-side plans)
+  int32_t* jtab;             // strided plan: [2K] (first CTA, CTAs) of every offset, written by CTA 0
   int K;
+  int mode;                  // plan: 0 contiguous ranges, 1 host segments, 2 strided per-offset chunks
   float* part;               // [n_slots][c_out][c_in]
   int c_out, c_in, halves;
   int mrows;                 // UMMA M: 64 when C_out <= 64 (no zero panel), else 128 per half
@@ -673,6 +693,19 @@ __global__ void k_reduce_partials_dev(const int64_t* __restrict__ ptr, int n_cta
     for (int64_t c = b / L; c <= (en - 1) / L; ++c) s += part[(c + k) * tile_elems + e];
   dW[(int64_t)k * tile_elems + e] = s;
 }
+// Strided plan (mode 2): dW_k = sum of the partials of offset k's CTAs jtab[k] ..
+// jtab[k] + jtab[K + k] - 1 in CTA order (deterministic).
+__global__ void k_reduce_partials_jtab(const int32_t* __restrict__ jtab, int K, const float* __restrict__ part,
+                                       int64_t tile_elems, float* __restrict__ dW) {
+  pdl_enter();
+  const int k = blockIdx.y;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= tile_elems) return;
+  const int c0 = __ldg(jtab + k), n = __ldg(jtab + K + k);
+  float s = 0.f;
+  for (int c = c0; c < c0 + n; ++c) s += part[(int64_t)c * tile_elems + e];
+  dW[(int64_t)k * tile_elems + e] = s;
+}
 constexpr int kMaxSegs = kWgradMaxSegs + 1;  // per-CTA plan capacity (kmap_wplan cuts ranges to fit)
 
 // Weight gradient: split-K over the pairs.  Step g = 64 pairs of one segment (k, range) of
@@ -697,8 +730,10 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
   uint8_t* smem = align1024(smem_raw);
   int32_t* ibuf_all = (int32_t*)(smem + (size_t)p.sa * p.slot_bytes);  // [sa][2][2][64]
   int32_t* seg_g0 = ibuf_all + p.sa * 4 * PS;                          // [kMaxSegs + 1]
-  uint64_t* a_full =
-      (uint64_t*)(((uintptr_t)(seg_g0 + kMaxSegs + 2) + 15 + sizeof(int4) * kMaxSegs + 16 + 15) & ~(uintptr_t)15);
+  int4* s_segs = align16<int4>(seg_g0 + kMaxSegs + 2);  // [kMaxSegs]
+  int* s_nseg = (int*)(s_segs + kMaxSegs);
+  int64_t* s_rng = align16<int64_t>(s_nseg + 1);  // strided plan: [ptr_k, ptr_k+1, j, J]
+  uint64_t* a_full = align16<uint64_t>(s_rng + 4);
   uint64_t* a_empty = a_full + p.sa;
   uint64_t* tfull = a_empty + p.sa;
   uint64_t* tempty = tfull + 1;
@@ -707,13 +742,74 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
   const int rba = p.pwa * 2, rbb = p.pwb * 2;             // panel row bytes
   const int npa = p.c_out / p.pwa, npb = p.c_in / p.pwb;  // real panels
   const uint32_t panel_a = PS * rba, panel_b = PS * rbb;  // panel strides (LBO)
-  int4* s_segs = (int4*)(((uintptr_t)(seg_g0 + kMaxSegs + 2) + 15) & ~(uintptr_t)15);  // [kMaxSegs]
-  int* s_nseg = (int*)(s_segs + kMaxSegs);
 
   pdl_enter();
   if (warp == 0) {  // plan: this CTA's segments and the first step of every segment
     int nseg = 0;
-    if (p.segs) {  // host plan (kmap_wplan)
+    if (p.mode == 2) {
+      // Strided per-offset plan: offset k gets J_k CTAs (one more than its share of the
+      // 64-pair chunks beyond one per non-empty offset, largest remainder first); CTA j of
+      // offset k takes chunks j, j + J_k, j + 2 J_k, ... of k's output-sorted pair list and
+      // accumulates all of them into ONE partial.  Every offset then advances through its
+      // pairs at the same relative speed, so the CTAs running at any moment all read the
+      // same window of output rows (and their neighbours): the G and X rows they gather stay
+      // in L2 even when the features are far larger than L2 (configs[4]).  K <= 32.
+      const int k = lane;
+      const int64_t b = k < p.K ? __ldg(p.ptr + k) : 0, en = k < p.K ? __ldg(p.ptr + k + 1) : 0;
+      const int64_t ck = (en - b + PS - 1) / PS;
+      int64_t C = ck;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) C += __shfl_xor_sync(0xffffffffu, C, o);
+      const int nz = __popc(__ballot_sync(0xffffffffu, ck > 0));
+      const int64_t spare = (int64_t)gridDim.x - nz;
+      int J = 0;
+      int64_t rem = -1;
+      if (ck > 0 && C > 0) {
+        J = 1 + (int)(spare * ck / C);
+        rem = spare * ck % C;
+      }
+      int given = J;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) given += __shfl_xor_sync(0xffffffffu, given, o);
+      const int extra = (int)gridDim.x - given;  // < nz
+      int rank = 0;  // lanes with a larger remainder (ties: lower offset first)
+      for (int l = 0; l < 32; ++l) {
+        const int64_t rl = __shfl_sync(0xffffffffu, rem, l);
+        rank += (rl > rem) || (rl == rem && l < lane);
+      }
+      if (rem >= 0 && rank < extra) ++J;
+      int c0 = J;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, c0, o);
+        if (lane >= o) c0 += y;
+      }
+      c0 -= J;
+      if (blockIdx.x == 0 && k < p.K) {  // for the reduction: CTAs c0 .. c0 + min(J, ck) - 1
+        p.jtab[k] = c0;
+        p.jtab[p.K + k] = (int)min((int64_t)J, ck);
+      }
+      const int c = (int)blockIdx.x;
+      // the CTA's offset; CTAs j >= ck of an offset (more CTAs than chunks) stay idle
+      const unsigned mine = __ballot_sync(0xffffffffu, J > 0 && c >= c0 && c < c0 + J && c - c0 < ck);
+      if (lane == 0) seg_g0[0] = 0;
+      __syncwarp();
+      if (mine) {
+        const int km = __ffs(mine) - 1;
+        if (lane == km) {
+          const int j = c - c0;
+          s_rng[0] = b;
+          s_rng[1] = en;
+          s_rng[2] = j;
+          s_rng[3] = J;
+          s_segs[0] = make_int4(k, 0, 0, c);
+          seg_g0[1] = (int)((ck - j + J - 1) / J);
+        }
+        nseg = 1;
+      }
+      __syncwarp();
+      if (lane == 0) *s_nseg = nseg;
+    } else if (p.segs) {  // host plan (kmap_wplan)
       const int sb = p.seg_begin[blockIdx.x], se = min(p.seg_begin[blockIdx.x + 1], sb + kMaxSegs);
       nseg = se - sb;
       for (int i = lane; i < nseg; i += 32) s_segs[i] = p.segs[sb + i];
@@ -735,7 +831,7 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
     }
     __syncwarp();
     int base = 0;
-    for (int i0 = 0; i0 < nseg; i0 += 32) {
+    for (int i0 = 0; i0 < nseg && p.mode != 2; i0 += 32) {
       const int i = i0 + lane;
       const int4 sg = i < nseg ? s_segs[i] : make_int4(0, 0, 0, 0);
       const int st = i < nseg ? (sg.z - sg.y + PS - 1) / PS : 0;
@@ -748,7 +844,7 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
       if (i < nseg) seg_g0[i] = base + incl - st;
       base += __shfl_sync(0xffffffffu, incl, 31);
     }
-    if (lane == 0) {
+    if (lane == 0 && p.mode != 2) {
       seg_g0[nseg] = base;
       *s_nseg = nseg;
     }
@@ -785,7 +881,13 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
     // ------------------------------------------------------------ gather producers
     int32_t* ib_w = ibuf_all + warp * 4 * PS;  // [2][out, in][64]
     int si = 0;
+    const int64_t r_b = s_rng[0], r_e = s_rng[1], r_j = s_rng[2], r_J = s_rng[3];
     auto locate = [&](int g, int* b0, int* e) {
+      if (p.mode == 2) {  // chunk j + g J of the offset
+        *b0 = (int)(r_b + (r_j + (int64_t)g * r_J) * PS);
+        *e = (int)r_e;
+        return;
+      }
       while (seg_g0[si + 1] <= g) ++si;
       const int4 sg = s_segs[si];
       *b0 = sg.y + (g - seg_g0[si]) * PS;
@@ -821,6 +923,7 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
         fetch_idx(b0n, en, ib ^ 1);
       }
       ACCT_WAIT(0, a_empty + warp / p.ga, (my & 1) ^ 1);
+      ACCT_NOW(t_issue);
       const uint32_t a_s = smem_u32(smem + (size_t)warp * p.slot_bytes), b_s = a_s + p.a_bytes;
       const int32_t* oi = ib_w + ib * 2 * PS;
       const int32_t* ii = oi + PS;
@@ -836,13 +939,20 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
           if (b0 + pr < e) cp_async16(dst, src + (int64_t)oi[pr] * p.c_out, 16u);
           else st_shared_zero16(dst);
         }
-      } else {
-        for (int idx = lane; idx < PS * ca; idx += 32) {
-          const int pr = idx / ca, ch = idx - pr * ca;
+      } else {  // consecutive lanes take consecutive 16-byte chunks (whole sectors per row)
+        int pr = lane / ca, ch = lane - (lane / ca) * ca;
+        const int dpr = 32 / ca, dch = 32 - dpr * ca;
+        for (; pr < PS;) {
           const int pa = ch / ja, j = ch - pa * ja;
           const uint32_t dst = a_s + pa * panel_a + swz(pr, j, rba);
           if (b0 + pr < e) cp_async16(dst, p.g + (int64_t)oi[pr] * p.c_out + ch * 8, 16u);
           else st_shared_zero16(dst);
+          pr += dpr;
+          ch += dch;
+          if (ch >= ca) {
+            ch -= ca;
+            ++pr;
+          }
         }
       }
       if ((32 % cb) == 0) {
@@ -856,20 +966,33 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
           else st_shared_zero16(dst);
         }
       } else {
-        for (int idx = lane; idx < PS * cb; idx += 32) {
-          const int pr = idx / cb, ch = idx - pr * cb;
+        int pr = lane / cb, ch = lane - (lane / cb) * cb;
+        const int dpr = 32 / cb, dch = 32 - dpr * cb;
+        for (; pr < PS;) {
           const int pb = ch / jb, j = ch - pb * jb;
           const uint32_t dst = b_s + pb * panel_b + swz(pr, j, rbb);
           if (b0 + pr < e) cp_async16(dst, p.x + (int64_t)ii[pr] * p.c_in + ch * 8, 16u);
           else st_shared_zero16(dst);
+          pr += dpr;
+          ch += dch;
+          if (ch >= cb) {
+            ch -= cb;
+            ++pr;
+          }
         }
       }
       cp_async_commit();
+      ACCT_ADD(1, t_issue);
+      ACCT_NOW(t_land);
       cp_async_wait_n(0);
       fence_proxy_async_smem();
       __syncwarp();
+      ACCT_ADD(2, t_land);
       if (lane == 0) mbar_arrive(a_full + warp);
       ++my;
+#ifdef MK_TRACE
+      acct[3] += 1;
+#endif
       ib ^= 1;
       b0 = b0n;
       e = en;
@@ -892,6 +1015,7 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
         const int q0 = __shfl_sync(0xffffffffu, seg_g0[i], 0), q1 = __shfl_sync(0xffffffffu, seg_g0[i + 1], 0);
         for (int q = q0; q < q1; ++q) {
           ACCT_WAIT(2, a_full + s, sph);
+          ACCT_NOW(t_mma);
           tc_fence_after();
           const uint32_t alo = s0 + s * sstep, blo = alo + boff;
           if (leader) {
@@ -907,6 +1031,10 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
             if (leader) umma_commit(a_empty + s / p.ga);
             gq = 0;
           }
+          ACCT_ADD(3, t_mma);
+#ifdef MK_TRACE
+          acct[4] += 1;
+#endif
           if (++s == (uint32_t)p.sa) {
             s = 0;
             sph ^= 1;
@@ -1161,6 +1289,7 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   p.segs = dev_plan ? nullptr : m->wseg;
   p.seg_begin = dev_plan ? nullptr : m->wseg_begin;
   p.ptr = m->ptr;
+  p.jtab = nullptr;
   p.K = m->K;
   p.c_out = c_out;
   p.c_in = c_in;
@@ -1191,7 +1320,7 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   for (;; np *= 2) {
     per_sm = np == 16 ? 1 : np == 8 ? 2 : 3;
     const int budget = per_sm == 1 ? kMaxSmem : kMaxSmem / per_sm - 1024;
-    reserve = 1024 + 1024 + np * 4 * kPairsPerStage * 4 + (kMaxSegs + 2) * 4 + (int)sizeof(int4) * kMaxSegs + 64;
+    reserve = 1024 + 1024 + np * 4 * kPairsPerStage * 4 + (kMaxSegs + 2) * 4 + (int)sizeof(int4) * kMaxSegs + 128;
     p.sa = std::min(np, (budget - reserve) / (int)p.slot_bytes);
     if ((p.sa >= 2 && per_sm * p.tmem_cols <= 512) || np >= 16) break;
   }
@@ -1203,12 +1332,22 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   if (p.sa < 2 || p.tmem_cols > 512) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: channel counts too large");
   const int smem = p.sa * (int)p.slot_bytes + reserve;
   float* part = nullptr;
+  static const int env_mode = [] {  // development: MK_WGRAD_PLAN=0 contiguous ranges, 2 strided
+    const char* e = std::getenv("MK_WGRAD_PLAN");
+    return e ? std::atoi(e) : 2;
+  }();
+  p.mode = dev_plan ? (m->K <= 32 && env_mode == 2 ? 2 : 0) : 1;
   if (dev_plan) {
     if (m->n_out > 0 && m->n_in > 0) {
       const int n_cta = ctx->num_sms * per_sm;
-      part = (float*)dev_alloc(ctx->alloc, sizeof(float) * (n_cta + m->K) * te, s);
+      // partial slots: one per CTA (strided plan) or per (CTA, offset) segment; then the
+      // (first CTA, CTAs) table of the strided plan
+      const int64_t slots = p.mode == 2 ? n_cta : n_cta + m->K;
+      const size_t pbytes = ((sizeof(float) * slots * te + 255) & ~size_t(255));
+      part = (float*)dev_alloc(ctx->alloc, pbytes + sizeof(int32_t) * 2 * m->K, s);
       if (!part) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 wgrad: workspace allocation failed");
       p.part = part;
+      p.jtab = (int32_t*)((uint8_t*)part + pbytes);
       auto go = [&](auto kern, int threads) {
         set_smem_once(kern, smem);
         pdl_launch(kern, n_cta, threads, smem, s, p);
@@ -1217,7 +1356,10 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
       else if (np == 8) go(k_wgrad_umma<8>, (8 + kEpiWarps + 1) * 32);
       else go(k_wgrad_umma<4>, (4 + kEpiWarps + 1) * 32);
       dim3 rg((unsigned)ceil_div(te, 256), (unsigned)m->K);
-      pdl_launch(k_reduce_partials_dev, rg, 256, 0, s, (const int64_t*)m->ptr, n_cta, (const float*)part, te, dW);
+      if (p.mode == 2)
+        pdl_launch(k_reduce_partials_jtab, rg, 256, 0, s, (const int32_t*)p.jtab, m->K, (const float*)part, te, dW);
+      else
+        pdl_launch(k_reduce_partials_dev, rg, 256, 0, s, (const int64_t*)m->ptr, n_cta, (const float*)part, te, dW);
     } else {
       const cudaError_t z = cudaMemsetAsync(dW, 0, sizeof(float) * m->K * te, s);
       if (z != cudaSuccess) MK_FAIL(MK_ERR_CUDA, "bf16 wgrad: memset failed");

@@ -48,6 +48,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }
 }
+// Blocking wait that suspends the thread (suspend-time hint) instead of spinning: for warps
+// off the critical path, so that their polling does not take issue slots from the warps
+// that share their SM sub-partition (a hot try_wait loop is one instruction stream per
+// waiting warp).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+        : "memory");
+  } while (!ok);
+}
 
 // ------------------------------------------------------------------ copies
 // 16-byte cp.async, L2 only; src_bytes = 0 zero-fills the destination.

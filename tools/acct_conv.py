@@ -1,4 +1,5 @@
-"""Per-warp cycle accounting of CTA 0 of the forward conv kernel (MK_TRACE build)."""
+"""Per-warp cycle accounting of CTA 100 of the forward conv kernel (MK_TRACE build).
+usage: python tools/acct_conv.py [1|4]"""
 import ctypes
 import os
 import sys
@@ -14,20 +15,26 @@ import torch  # noqa: E402
 import paper_1904_08755_b200 as mk  # noqa: E402
 import synthetic  # noqa: E402
 
-pts = torch.from_numpy(synthetic.room_points(2000)).cuda()
-c, _, _ = mk.coords_quantize(pts, 0.02)
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 1
+if cfg == 4:
+    p, b = synthetic.rooms_batch(5000, 16)
+    c, _, _ = mk.coords_quantize(torch.from_numpy(p).cuda(), synthetic.ROOM_VOXEL, torch.from_numpy(b).cuda())
+    C = 96
+else:
+    c, _, _ = mk.coords_quantize(torch.from_numpy(synthetic.room_points(2000)).cuda(), synthetic.ROOM_VOXEL)
+    C = 64
 m = mk.kmap_build(c, c, mk.Region(mk.HYPERCUBE, 3, 3))
-X = torch.randn(c.n, 64, device="cuda").bfloat16()
-W = (torch.randn(27, 64, 64, device="cuda") * 0.02).bfloat16()
+X = torch.randn(c.n, C, device="cuda").bfloat16()
+W = (torch.randn(27, C, C, device="cuda") * 0.02).bfloat16()
 for _ in range(3):
     mk.conv_forward(m, X, W)
 torch.cuda.synchronize()
 a = np.zeros((32, 8), np.uint64)
 mk._L.mk_debug_acct.argtypes = [ctypes.c_void_p]
 mk._L.mk_debug_acct(a.ctypes.data)
-print("warp: [slot0 .. slot6 cycles, total cycles]   producers: 0=a_empty wait 1=issue 2=data wait 3=steps")
-print("      stager(21): 0=w_empty  mma(20): 0=tempty 1=w_full 2=a_full 3=steps  epi(16-19): 0=tfull")
-for w in range(22):
-    print(w, a[w].tolist())
-import torch.cuda
-print("smem/occupancy check done via ncu; CTA 300 shown")
+print(f"configs[{cfg}] C={C}; cycles of CTA 100 per warp; last col = total")
+print("producers 1-3,5-7,9-10: 0=slot-free wait 1=fnext 2=issue 3=wait_group 4=steps 5=item switch | epi 12-15: 0=acc_full wait | mma(0): 1=W wait 2=A full "
+      "wait 3=acc_empty wait 4=steps 5=fence 6=mma+commit | stager(4): 0=ring wait")
+for w in range(16):
+    if a[w].any():
+        print(w, a[w].tolist())

@@ -1,14 +1,16 @@
 #!/bin/bash
-# Quick GPU check: parity tests + bench (no cpu baseline) + launch list.
-TAG=${1:-quick}
-OUT=gpurun_out/$TAG
-mkdir -p $OUT
-timeout 900 python -m pytest tests -m gpu -x -q > $OUT/pytest.txt 2>&1; echo "pytest rc=$?" >> $OUT/pytest.txt
-tail -15 $OUT/pytest.txt
-timeout 600 python bench.py --no-cpu-baseline > $OUT/bench.json 2> $OUT/bench.err; tail -3 $OUT/bench.err
-python -c "import json; d=json.load(open('$OUT/bench.json')); print(d['ms_per_step'], d['phases_us'], d['value'])"
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none -c 400 --csv --log-file $OUT/launches.csv \
-    python bench.py --steps 2 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
-python tools/launches.py $OUT/launches.csv | head -25
-python tools/host_overhead.py
-MK_HOST_TIMING=1 python tools/host_overhead.py 2>&1 | grep "mk host" | tail -6
+# Quick GPU iteration: conv parity tests + short bench lines (configs[4] and [1]).
+# usage: tools/quick.sh TAG [pytest -k expr] [extra env assignments for an A/B line]
+TAG=${1:-quick}; KEXPR=${2:-conv or configs}; AB=${3:-}
+OUT=gpurun_out/$TAG; mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { tail $OUT/build.log; exit 1; }
+timeout 900 python -m pytest tests -m gpu -x -q -k "$KEXPR" > $OUT/pytest.log 2>&1; echo "pytest rc=$?" >> $OUT/pytest.log
+tail -3 $OUT/pytest.log
+for cfg in 4 1; do
+  timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-extras --no-cpu-baseline --no-e2e > $OUT/bench_c$cfg.json 2> $OUT/bench_c$cfg.err
+  python -c "import json;d=json.load(open('$OUT/bench_c$cfg.json'));print('cfg$cfg',d['value'],d['ms_per_step'],d['phases_us'])"
+  if [ -n "$AB" ]; then
+    env $AB timeout 300 python bench.py --config $cfg --steps 10 --warmup 3 --no-extras --no-cpu-baseline --no-e2e > $OUT/bench_c${cfg}_ab.json 2>/dev/null
+    python -c "import json;d=json.load(open('$OUT/bench_c${cfg}_ab.json'));print('cfg$cfg AB($AB)',d['value'],d['ms_per_step'],d['phases_us'])"
+  fi
+done

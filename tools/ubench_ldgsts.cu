@@ -1,0 +1,103 @@
+// ubench_ldgsts.cu — does cp.async.mbarrier.arrive.noinc serialise a warp's cp.async
+// stream?  Each warp gathers 16 KB stages (128 random 128-byte rows of a 19 MB table) into
+// its own ring of D+1 smem slots, keeping D stages in flight (wait_group D), optionally
+// with one noinc arrival per stage on a per-warp mbarrier.  Development tool.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_1904_08755_b200/csrc ubench_ldgsts.cu
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "sm100.cuh"
+
+using namespace mk::sm100;
+
+__global__ void k_g(const uint4* __restrict__ tab, const int* __restrict__ idx, int stages_per_warp, int D, int noinc,
+                    long long* issue_cycles, uint4* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (lane == 0) mbar_init(&bar[warp], 32);
+  fence_mbar_init();
+  __syncthreads();
+  const int slots = D + 1;
+  const uint32_t base = smem_u32(sm) + warp * slots * 16384;
+  long long t_issue = 0;
+  uint32_t ph = 0;
+  const int gw = blockIdx.x * nw + warp;
+  for (int st = 0; st < stages_per_warp; ++st) {
+    const uint32_t dst = base + (st % slots) * 16384;
+    const int* ix = idx + ((size_t)gw * stages_per_warp + st) * 128;
+    int rows[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) rows[i] = __ldg(ix + i * 4 + lane / 8);
+    if (rows[0] == -7) out[1] = make_uint4(0, 0, 0, 0);  // indices resident before the timer
+    long long t0 = clock64();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int r = i * 4 + lane / 8;
+      cp_async16(dst + r * 128 + (lane & 7) * 16, tab + (size_t)rows[i] * 8 + (lane & 7), 16);
+    }
+    if (noinc) cp_async_arrive_noinc(&bar[warp]);
+    cp_async_commit();
+    t_issue += clock64() - t0;
+    (void)rows;
+    cp_async_wait_n(D);
+    if (noinc && st >= D) {  // the arrival of stage st - D
+      mbar_wait(&bar[warp], ph);
+      ph ^= 1;
+    }
+  }
+  cp_async_wait_n(0);
+  __syncthreads();
+  if (lane == 0) issue_cycles[blockIdx.x * nw + warp] = t_issue;
+  if (((uint32_t*)sm)[threadIdx.x] == 0x12345678) out[0] = make_uint4(1, 1, 1, 1);
+}
+
+int main() {
+  const int n_rows = 150000, sm = 148;
+  uint4* tab;
+  cudaMalloc(&tab, (size_t)n_rows * 128);
+  cudaMemset(tab, 1, (size_t)n_rows * 128);
+  const int max_idx = 148 * 32 * 64 * 128;
+  std::vector<int> h(max_idx);
+  srand(1);
+  for (auto& v : h) v = rand() % n_rows;
+  int* idx;
+  cudaMalloc(&idx, sizeof(int) * max_idx);
+  cudaMemcpy(idx, h.data(), sizeof(int) * max_idx, cudaMemcpyHostToDevice);
+  long long* ic;
+  cudaMalloc(&ic, 148 * 32 * 8);
+  uint4* out;
+  cudaMalloc(&out, 16);
+  cudaFuncSetAttribute(k_g, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int W : {4, 8, 12, 16}) {
+    for (int D : {0, 1, 2, 3}) {
+      if ((D + 1) * W * 16 > 220) continue;
+      for (int noinc = 0; noinc < 2; ++noinc) {
+        const int spw = 1400000 / 128 / (sm * W);  // ~1.4M rows in total (a configs[1] conv)
+        const int smem = (D + 1) * W * 16384;
+        k_g<<<sm, W * 32, smem>>>(tab, idx, spw, D, noinc, ic, out);
+        cudaEventRecord(e0);
+        k_g<<<sm, W * 32, smem>>>(tab, idx, spw, D, noinc, ic, out);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        std::vector<long long> hc(sm * W);
+        cudaMemcpy(hc.data(), ic, 8 * sm * W, cudaMemcpyDeviceToHost);
+        double mi = 0;
+        for (auto v : hc) mi += v;
+        mi /= hc.size() * spw;
+        const double bytes = (double)sm * W * spw * 16384;
+        printf("warps/SM=%2d depth=%d noinc=%d: %7.1f us %6.2f TB/s  issue %6.0f cycles/stage (%s)\n", W, D, noinc,
+               ms * 1e3, bytes / (ms * 1e-3) / 1e12, mi, cudaGetErrorString(cudaGetLastError()));
+      }
+    }
+  }
+  return 0;
+}

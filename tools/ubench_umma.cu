@@ -258,7 +258,7 @@ int main() {
   long long h[148];
   cudaFuncSetAttribute(k_umma, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
   cudaFuncSetAttribute(k_umma_nowait, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
-  for (int nowait = 0; nowait < 0; ++nowait)
+  for (int nowait = 0; nowait < 2; ++nowait)
     for (int N : {64, 128, 256})
       for (int per : {1, 4, 16}) {
         const int iters = 2048 / per;
