@@ -29,6 +29,13 @@ namespace mk {
 namespace {
 
 constexpr int kBlock = 256;
+#ifndef MK_TABLE_SLOTS_X2
+#define MK_TABLE_SLOTS_X2 4
+#endif
+// Tables of at least this many buckets (64 MB, half of L2) get per-batch regions (TableRef).
+#ifndef MK_SUB_MIN_BUCKETS
+#define MK_SUB_MIN_BUCKETS (1u << 20)
+#endif
 #ifndef MK_RANK_ITEMS
 #define MK_RANK_ITEMS 5
 #endif
@@ -140,35 +147,110 @@ struct ExpandSrc {  // f4: expanded row p = (input row p / K, offset p % K) -> u
 };
 
 // ---------------------------------------------------------------- kernels
+// Per-batch region layout (TableRef): histogram of the rows' batch indices (block-local in
+// shared memory, then one global add per non-empty bin), then one block sizes the regions
+// (buckets for >= MK_TABLE_SLOTS_X2 / 2 slots per row, like the flat table, at least 32)
+// and lays them out by an exclusive scan.  A batch index outside [0, kMaxSub) or a layout
+// larger than the allocation falls back to the flat table (nsub = 0).
+// cnt[kMaxSub] counts, cnt[kMaxSub] = largest batch + 1, cnt[kMaxSub + 1] = overflow flag.
 template <class Src>
-__global__ void __launch_bounds__(kBlock) k_insert(Src src, int64_t n, int4* __restrict__ buckets,
-                                                   int32_t* __restrict__ first, uint32_t bmask,
+__global__ void __launch_bounds__(kBlock) k_bhist(Src src, int64_t n, int D, int32_t* __restrict__ cnt) {
+  pdl_enter();
+  __shared__ int32_t h[kMaxSub];
+  __shared__ int32_t s_max, s_over;
+  for (int i = threadIdx.x; i < kMaxSub; i += kBlock) h[i] = 0;
+  if (threadIdx.x == 0) s_max = 0, s_over = 0;
+  __syncthreads();
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+    int4 k;
+    if (src.key(p, &k) != E_NONE) continue;  // reported by k_insert
+    const uint32_t b = (uint32_t)key_batch(k, D);
+    if (b < (uint32_t)kMaxSub) {
+      atomicAdd(&h[b], 1);
+      atomicMax(&s_max, (int32_t)b + 1);
+    } else {
+      s_over = 1;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < kMaxSub; i += kBlock)
+    if (h[i]) atomicAdd(cnt + i, h[i]);
+  if (threadIdx.x == 0) {
+    if (s_max) atomicMax(cnt + kMaxSub, s_max);
+    if (s_over) atomicOr(cnt + kMaxSub + 1, 1);
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_blayout(const int32_t* __restrict__ cnt, int64_t cap_buckets,
+                                                  int2* __restrict__ sub) {
+  pdl_enter();
+  __shared__ int64_t s_part[1024 / 32];
+  constexpr int kPer = kMaxSub / 1024;
+  const int nsub = cnt[kMaxSub];
+  int64_t size[kPer], tot = 0;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int b = threadIdx.x * kPer + j;
+    int64_t want = b < nsub ? ((int64_t)MK_TABLE_SLOTS_X2 * cnt[b] + 2 * kSlotsPerBucket - 1) / (2 * kSlotsPerBucket) : 0;
+    size[j] = b < nsub ? (want > 32 ? want : 32) : 0;
+    tot += size[j];
+  }
+  // block exclusive scan of the per-thread totals
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int64_t incl = tot;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int64_t y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane == 31) s_part[warp] = incl;
+  __syncthreads();
+  int64_t off = incl - tot, all = 0;
+  for (int w = 0; w < 1024 / 32; ++w) {
+    if (w < warp) off += s_part[w];
+    all += s_part[w];
+  }
+  const bool flat = cnt[kMaxSub + 1] != 0 || nsub == 0 || all > cap_buckets || all > (int64_t)UINT32_MAX;
+#pragma unroll
+  for (int j = 0; j < kPer; ++j) {
+    const int b = threadIdx.x * kPer + j;
+    if (!flat && b < nsub) sub[1 + b] = make_int2((int32_t)off, (int32_t)size[j]);
+    off += size[j];
+  }
+  if (threadIdx.x == 0) sub[0] = make_int2(flat ? 0 : nsub, flat ? -1 : (int32_t)all);
+}
+
+template <class Src>
+__global__ void __launch_bounds__(kBlock) k_insert(Src src, int64_t n, TableRef t, int32_t* __restrict__ first,
                                                    int32_t* __restrict__ slot_of, unsigned long long* err) {
   pdl_enter();
   // Claim-or-find in one 128-bit atomicCAS of the key itself (sm_90+): the slot is ours or
   // already holds the key -> record the smallest point index of the key (atomicMin).
   const unsigned __int128 kEmpty = ~(unsigned __int128)0;
-  const uint32_t nslots = (bmask + 1u) * kSlotsPerBucket;
+  int4* buckets = const_cast<int4*>(t.buckets);
   for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
        p += (int64_t)gridDim.x * blockDim.x) {
     int4 k;
     const uint32_t code = src.key(p, &k);
-    if (code != E_NONE) {
-      report(err, p, code);
+    uint32_t base = 0, size = 0;
+    if (code != E_NONE || !t.region(k, &base, &size)) {
+      if (code != E_NONE) report(err, p, code);
       slot_of[p] = -1;  // no slot: k_rank skips the row (the call fails anyway)
       continue;
     }
     unsigned __int128 kv;
     memcpy(&kv, &k, sizeof(kv));
-    uint32_t h = (hash_key(k) & bmask) * kSlotsPerBucket;  // first slot of the key's bucket
+    // slots of the region: [3 base, 3 (base + size)); first slot of the key's bucket
+    const uint32_t s0 = base * kSlotsPerBucket, ns = size * kSlotsPerBucket;
+    uint32_t h = hash_bucket(hash_key(k), size) * kSlotsPerBucket;
     while (true) {
-      const unsigned __int128 old = atomicCAS((unsigned __int128*)slot_key(buckets, h), kEmpty, kv);
+      const unsigned __int128 old = atomicCAS((unsigned __int128*)slot_key(buckets, s0 + h), kEmpty, kv);
       if (old == kEmpty || old == kv) {
-        atomicMin(first + h, (int32_t)p);
-        slot_of[p] = (int32_t)h;
+        atomicMin(first + s0 + h, (int32_t)p);
+        slot_of[p] = (int32_t)(s0 + h);
         break;
       }
-      h = h + 1 == nslots ? 0u : h + 1;
+      h = h + 1 == ns ? 0u : h + 1;
     }
   }
 }
@@ -301,10 +383,11 @@ __global__ void __launch_bounds__(kBlock, MK_RANK_MINB) k_rank(Src src, int64_t 
 // Table init in one launch: bucket words to the empty sentinel (all ones: empty keys, rows
 // -1), first-point words to INT32_MAX, look-back status words / ticket / count to 0, the
 // error word to all ones.
-__global__ void k_init(int4* __restrict__ buckets, int32_t* __restrict__ first, uint32_t nb,
+__global__ void k_init(int4* __restrict__ buckets, int32_t* __restrict__ first, uint32_t nb, const int2* sub,
                        unsigned long long* __restrict__ small, int64_t n_small, unsigned long long* err) {
   pdl_enter();
   const int4 e = make_int4(-1, -1, -1, -1);
+  if (sub && sub[0].x > 0) nb = (uint32_t)sub[0].y;  // per-batch regions: the buckets in use
   const int64_t words = (int64_t)nb * 4, slots = (int64_t)nb * kSlotsPerBucket;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x) {
     buckets[i] = e;
@@ -335,15 +418,14 @@ __global__ void k_labels_mark(const int32_t* __restrict__ p2r, const int32_t* __
   }
 }
 
-__global__ void k_lookup(const int32_t* __restrict__ q, int64_t nq, int D, const int4* __restrict__ buckets,
-                         uint32_t bmask, int32_t* __restrict__ rows) {
+__global__ void k_lookup(const int32_t* __restrict__ q, int64_t nq, int D, TableRef t, int32_t* __restrict__ rows) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nq; i += (int64_t)gridDim.x * blockDim.x) {
     int64_t c[kMaxD] = {0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
     for (int d = 0; d < kMaxD; ++d)
       if (d < D) c[d] = q[i * (D + 1) + d];
     int4 k;
-    rows[i] = pack_key(c, D, q[i * (D + 1) + D], &k) ? probe(buckets, bmask, k) : -1;
+    rows[i] = pack_key(c, D, q[i * (D + 1) + D], &k) ? probe(t, k) : -1;
   }
 }
 
@@ -394,12 +476,17 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
   HostTimer ht("build_coords");
   if (n < 0 || n > INT32_MAX) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "row count out of range [0, 2^31)");
   // buckets of 3 slots, >= MK_TABLE_SLOTS_X2 * n / 2 slots in total (default 4: load <= 1/2)
-#ifndef MK_TABLE_SLOTS_X2
-#define MK_TABLE_SLOTS_X2 4
-#endif
   const uint32_t nb =
       next_pow2(std::max<int64_t>(ceil_div(MK_TABLE_SLOTS_X2 * n, 2 * kSlotsPerBucket), 32));
-  const uint32_t nslots = nb * kSlotsPerBucket;
+  // Per-batch regions for tables that outgrow L2 (see TableRef): a region holds its batch's
+  // share (at least 32 buckets), so the regions together fit in nb + 33 kMaxSub buckets.
+  static const bool no_sub = [] {
+    const char* e = std::getenv("MK_NO_SUBTABLES");
+    return e && e[0] && e[0] != '0';
+  }();
+  const bool use_sub = !no_sub && nb >= MK_SUB_MIN_BUCKETS && (int64_t)nb + 33 * kMaxSub <= (int64_t)UINT32_MAX / 4;
+  const int64_t cap = use_sub ? (int64_t)nb + 33 * kMaxSub : nb;  // buckets allocated
+  const int64_t nslots = cap * kSlotsPerBucket;
   const int64_t ntiles = std::max<int64_t>(1, ceil_div(n, kTile));
 
   mk_coords* c = new mk_coords();
@@ -410,8 +497,9 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
 
   // persistent: table keys, table values, row keys
   Carver pc;
-  const size_t o_tk = pc.take<int4>((size_t)nb * 4), o_rk = pc.take<int4>(std::max<int64_t>(n, 1)),
-               o_res = pc.take<unsigned long long>(2);  // (error word, count) for a deferred count
+  const size_t o_tk = pc.take<int4>((size_t)cap * 4), o_rk = pc.take<int4>(std::max<int64_t>(n, 1)),
+               o_res = pc.take<unsigned long long>(2),  // (error word, count) for a deferred count
+      o_sub = use_sub ? pc.take<int2>(1 + kMaxSub) : 0;
   char* pbase = (char*)dev_alloc(c->alloc, pc.off, s);
   if (!pbase) {
     delete c;
@@ -420,13 +508,15 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
   c->owned.push_back(pbase);
   c->table.buckets = (int4*)(pbase + o_tk);
   c->table.bmask = nb - 1;
+  c->table.sub = use_sub ? (int2*)(pbase + o_sub) : nullptr;
   c->keys = (int4*)(pbase + o_rk);
 
   // scratch: first point per slot, slot per row, look-back status, ticket, error word, count
   Carver sc;
   const size_t o_cl = sc.take<int32_t>(nslots), o_sl = sc.take<int32_t>(std::max<int64_t>(n, 1)),
                o_st = sc.take<unsigned long long>(ntiles), o_ti = sc.take<unsigned int>(1),
-               o_er = sc.take<unsigned long long>(2);  // error word, then the row count
+               o_er = sc.take<unsigned long long>(2),  // error word, then the row count
+      o_hi = use_sub ? sc.take<int32_t>(kMaxSub + 2) : 0;
   char* sbase = (char*)dev_alloc(c->alloc, sc.off, s);
   if (!sbase) {
     mk_coords_destroy(c);
@@ -448,12 +538,24 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
 
   cudaError_t e;
   ht.mark("alloc");
+  if (use_sub && n > 0) {  // per-batch region layout (device side, before the table init)
+    int32_t* hist = (int32_t*)(sbase + o_hi);
+    if ((e = cudaMemsetAsync(hist, 0, sizeof(int32_t) * (kMaxSub + 2), s)) != cudaSuccess)
+      return fail_cuda(e, "memset");
+    pdl_launch(k_bhist<Src>, grid_for(n, kBlock, ctx->num_sms / 4 > 0 ? ctx->num_sms / 4 : 1), kBlock, 0, s, src, n, D,
+               hist);
+    pdl_launch(k_blayout, 1, 1024, 0, s, (const int32_t*)hist, cap, c->table.sub);
+  } else if (use_sub) {
+    const int2 flat = make_int2(0, -1);
+    if ((e = cudaMemcpyAsync(c->table.sub, &flat, sizeof(flat), cudaMemcpyHostToDevice, s)) != cudaSuccess)
+      return fail_cuda(e, "layout");
+  }
   {
     // status[ntiles], ticket, count are contiguous 8-byte words from o_st; err follows.
     unsigned long long* small = (unsigned long long*)(sbase + o_st);
     const int64_t n_small = (int64_t)((o_er - o_st) / 8);
     pdl_launch(k_init, grid_for(std::max<int64_t>((int64_t)nb * 4, n_small), 256, ctx->num_sms), 256, 0, s,
-               c->table.buckets, first, nb, small, n_small, err);
+               c->table.buckets, first, nb, (const int2*)c->table.sub, small, n_small, err);
   }
   static const bool no_mailbox = [] {  // MK_NO_MAILBOX=1: D2H copy + stream sync (A/B measurement)
     const char* v = std::getenv("MK_NO_MAILBOX");
@@ -468,8 +570,8 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
   if (!deferred && n > 0 && !no_mailbox) mb = mailbox(&seq);
   if (n > 0) {
     ht.mark("init");
-    pdl_launch(k_insert<Src>, grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s, src, n, c->table.buckets, first,
-               nb - 1, slot_of, err);
+    pdl_launch(k_insert<Src>, grid_for(n, kBlock, ctx->num_sms), kBlock, 0, s, src, n, c->table.ref(D), first,
+               slot_of, err);
     ht.mark("insert");
     pdl_launch(k_rank<Src>, (int)ntiles, kBlock, 0, s, src, n, (const int32_t*)first, (const int32_t*)slot_of,
                c->table.buckets, c->keys, d_first, d_p2r, status, ticket, count, (const unsigned long long*)err, mb,
@@ -752,8 +854,7 @@ mk_status mk_coords_lookup(const mk_coords* c, const int32_t* d_queries, int64_t
   clear_error();
   if (!c || q < 0 || (q > 0 && (!d_queries || !d_rows))) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "mk_coords_lookup: bad argument");
   if (q == 0) return MK_OK;
-  k_lookup<<<grid_for(q, 256, 148), 256, 0, (cudaStream_t)stream>>>(d_queries, q, c->D, c->table.buckets,
-                                                                      c->table.bmask, d_rows);
+  k_lookup<<<grid_for(q, 256, 148), 256, 0, (cudaStream_t)stream>>>(d_queries, q, c->D, c->table.ref(c->D), d_rows);
   MK_LAUNCH_CHECK();
   return MK_OK;
 }

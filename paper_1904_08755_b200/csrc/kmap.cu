@@ -78,7 +78,7 @@ constexpr int kPB = MK_PROBE_PB;
 
 template <bool RM>
 __global__ void __launch_bounds__(kThreads, MK_PROBE_MINB) k_probe(const int4* __restrict__ okeys, int64_t n_out, int64_t n_pad,
-                                                    const int4* __restrict__ buckets, uint32_t bmask,
+                                                    const TableRef tref,
                                                     const int32_t* __restrict__ offs, int K, int D, int sign,
                                                     Scale scale4, int32_t* __restrict__ nbr,
                                                     int32_t* __restrict__ tile_cnt, int64_t ntiles,
@@ -116,6 +116,11 @@ __global__ void __launch_bounds__(kThreads, MK_PROBE_MINB) k_probe(const int4* _
   const int64_t o = tile * kTileRows + r;
   const bool valid = o < n_out;
   const int4 u = valid ? __ldg(okeys + o) : make_int4(0, 0, 0, 0);
+  // the region of the input table that holds the row's batch (offsets never change the
+  // batch, R18): one lookup per row instead of per query
+  const int4* __restrict__ buckets = tref.buckets;
+  uint32_t rbase = 0, rsize = 0;
+  const bool in_tab = valid && tref.region(u, &rbase, &rsize);
   auto small = [](int32_t v, int32_t lim) { return v > -lim && v < lim; };
   // block-uniform: one row outside the fast-path range sends the whole tile down the slow path
   const bool fast = __syncthreads_and(!s_slow && D <= 4 && small(u.x, 1 << 30) && small(u.y, 1 << 30) &&
@@ -138,7 +143,8 @@ __global__ void __launch_bounds__(kThreads, MK_PROBE_MINB) k_probe(const int4* _
         }
         // unconditional loads of the first sector (bucket 0 for masked queries): no
         // divergent regions, all kPB loads of the thread are issued back to back
-        hb[b] = ok[b] ? hash_key(q[b]) & bmask : 0u;
+        ok[b] = ok[b] && in_tab;
+        hb[b] = ok[b] ? rbase + hash_bucket(hash_key(q[b]), rsize) : 0u;
         load_sector(buckets + (size_t)hb[b] * 4u, &k0[b], &v[b]);
       }
 #pragma unroll
@@ -151,7 +157,7 @@ __global__ void __launch_bounds__(kThreads, MK_PROBE_MINB) k_probe(const int4* _
               a = v[b].x;
             } else if (k0[b].w != kEmptyWord && v[b].y >= 0) {  // slot 1 occupied (rare)
               a = bucket_rest(buckets + (size_t)hb[b] * 4u, q[b], k0[b], v[b]);
-              if (a == -2) a = probe_next(buckets, bmask, q[b], hb[b]);  // bucket full of other keys
+              if (a == -2) a = probe_next(buckets, rbase, rsize, q[b], hb[b]);  // bucket full of other keys
             }
           }
           s_tab[r * kRMPitch + k] = a;
@@ -768,11 +774,11 @@ mk_status mk_kmap_build(mk_context* ctx, const mk_coords* in, const mk_coords* o
       cudaFuncSetAttribute(k_probe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     }
     if (rm)
-      ck(pdl_launch(k_probe<true>, (unsigned)ntiles, kThreads, smem, s, out->keys, n_out, n_pad, in->table.buckets,
-                    in->table.bmask, d_offs, K, D, sign, scale4, nbr_rm, tile_cnt, ntiles, m->tile_mask, mw, rowmask));
+      ck(pdl_launch(k_probe<true>, (unsigned)ntiles, kThreads, smem, s, out->keys, n_out, n_pad, in->table.ref(D),
+                    d_offs, K, D, sign, scale4, nbr_rm, tile_cnt, ntiles, m->tile_mask, mw, rowmask));
     else
-      ck(pdl_launch(k_probe<false>, (unsigned)ntiles, kThreads, smem, s, out->keys, n_out, n_pad, in->table.buckets,
-                    in->table.bmask, d_offs, K, D, sign, scale4, m->nbr, tile_cnt, ntiles, m->tile_mask, mw, nullptr));
+      ck(pdl_launch(k_probe<false>, (unsigned)ntiles, kThreads, smem, s, out->keys, n_out, n_pad, in->table.ref(D),
+                    d_offs, K, D, sign, scale4, m->nbr, tile_cnt, ntiles, m->tile_mask, mw, nullptr));
     // Symmetric row-ordered maps: the row sort and the permuted table depend only on the probe,
     // the pair lists only on the probe and the scan, so the sort + permute run on the
     // context's side stream concurrently with scan + emit (joined before the build ends).

@@ -178,7 +178,7 @@ __host__ __device__ __forceinline__ bool pack_key(const int64_t* c, int D, int64
 // and one 16-byte word holding the three slots' row values, laid out so that the first
 // 32-byte sector holds key slot 0 and the rows:
 //   bucket b = { key[0], (row[0], row[1], row[2], unused), key[1], key[2] }
-// A key hashes to bucket hash & bmask and is stored in the first free slot of the
+// A key hashes to bucket hash_bucket(hash, buckets) and is stored in the first free slot of the
 // linear-probing sequence of slots 3b, 3b+1, ... (wrapping), so the occupied slots of a
 // bucket are a prefix and, once the table is built, row[j] >= 0 exactly when slot j is
 // occupied.  A lookup reads the first sector (key 0 + rows) and stops there unless key 0
@@ -215,32 +215,75 @@ __device__ __forceinline__ int32_t bucket_rest(const int4* B, int4 q, int4 k0, i
   return -2;
 }
 
-// Continues the lookup of q after bucket b0 (which was full of other keys).
-static __device__ __noinline__ int32_t probe_next(const int4* __restrict__ buckets, uint32_t bmask, int4 q,
-                                                  uint32_t b0) {
-  uint32_t b = (b0 + 1) & bmask;
+// Bucket of hash h in a region of `size` buckets: the high bits of h scaled to the size
+// (multiply-shift; the regions need not be powers of two).
+__host__ __device__ __forceinline__ uint32_t hash_bucket(uint32_t h, uint32_t size) {
+  return (uint32_t)(((uint64_t)h * size) >> 32);
+}
+
+// Per-batch regions.  A large table (many scans in one batch, configs[4]) is split into one
+// region per batch index, each sized from that batch's rows, so that the inserts and the
+// kernel-map probes of one scan — issued in row order, i.e. scan after scan — touch one
+// L2-sized region instead of a table far larger than L2.  The layout lives on the device
+// (computed from a histogram of the batch indices, no host round trip):
+//   sub[0] = (nsub, used buckets), sub[1 + b] = (first bucket, buckets) of batch b;
+// nsub = 0 means one flat region (the table's nb buckets).  Within a region the probing
+// sequence wraps inside the region.  Keys of a batch >= nsub are absent by construction.
+struct TableRef {
+  const int4* buckets;
+  uint32_t nb;       // flat table: buckets
+  const int2* sub;   // per-batch layout (see above) or null
+  int D;             // key layout (for the batch field)
+  // region of key q: false when q cannot be in the table (its batch has no region)
+  __device__ __forceinline__ bool region(int4 q, uint32_t* base, uint32_t* size) const {
+    if (sub) {
+      const int nsub = __ldg(&sub[0].x);
+      if (nsub > 0) {
+        const uint32_t b = (uint32_t)key_batch(q, D);
+        if (b >= (uint32_t)nsub) return false;
+        const int2 r = __ldg(sub + 1 + b);
+        *base = (uint32_t)r.x;
+        *size = (uint32_t)r.y;
+        return true;
+      }
+    }
+    *base = 0;
+    *size = nb;
+    return true;
+  }
+};
+
+// Continues the lookup of q after bucket b0 (which was full of other keys) in its region.
+static __device__ __noinline__ int32_t probe_next(const int4* __restrict__ buckets, uint32_t base, uint32_t size,
+                                                  int4 q, uint32_t b0) {
+  uint32_t j = b0 - base;
   while (true) {
-    const int4* B = buckets + (size_t)b * 4u;
+    j = j + 1 == size ? 0u : j + 1;
+    const int4* B = buckets + (size_t)(base + j) * 4u;
     const int32_t r = bucket_rest(B, q, __ldg(B), __ldg(B + 1));
     if (r != -2) return r;
-    b = (b + 1) & bmask;
   }
 }
 
 // Thread-level lookup of key q; row or -1.
-__device__ __forceinline__ int32_t probe(const int4* __restrict__ buckets, uint32_t bmask, int4 q) {
-  const uint32_t b = hash_key(q) & bmask;
-  const int4* B = buckets + (size_t)b * 4u;
+__device__ __forceinline__ int32_t probe(const TableRef& t, int4 q) {
+  uint32_t base, size;
+  if (!t.region(q, &base, &size)) return -1;
+  const uint32_t b = base + hash_bucket(hash_key(q), size);
+  const int4* B = t.buckets + (size_t)b * 4u;
   int4 k0, v;
   load_sector(B, &k0, &v);
   const int32_t r = bucket_rest(B, q, k0, v);
-  return r != -2 ? r : probe_next(buckets, bmask, q, b);
+  return r != -2 ? r : probe_next(t.buckets, base, size, q, b);
 }
 
 // ------------------------------------------------------------------ handles
+constexpr int kMaxSub = 4096;  // batches with their own region (larger batch indices: flat table)
 struct Table {
   int4* buckets = nullptr;  // [nb][4] (see "hash table" above)
-  uint32_t bmask = 0;       // nb - 1 (nb is a power of two; 3 nb >= 2n slots)
+  uint32_t bmask = 0;       // nb - 1 of the flat table (nb is a power of two; 3 nb >= 2n slots)
+  int2* sub = nullptr;      // per-batch region layout [1 + kMaxSub] (device) or null
+  TableRef ref(int D) const { return TableRef{buckets, bmask + 1u, sub, D}; }
 };
 
 struct Alloc {

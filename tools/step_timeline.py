@@ -1,6 +1,6 @@
-"""GPU timeline of the configs[1] bench step (development tool): kernel start/end times from
+"""GPU timeline of a bench step (configs[cfg]) (development tool): kernel start/end times from
 torch.profiler (CUPTI), printed relative to the step start with the idle gaps between them.
-Usage: python tools/step_timeline.py [n_steps]"""
+Usage: python tools/step_timeline.py [n_steps] [cfg]"""
 import sys
 from pathlib import Path
 
@@ -12,22 +12,19 @@ from torch.profiler import ProfilerActivity, profile  # noqa: E402
 import paper_1904_08755_b200 as mk  # noqa: E402
 import synthetic  # noqa: E402
 
-n_steps = int(sys.argv[1]) if len(sys.argv) > 1 else 3
-pts = torch.from_numpy(synthetic.room_points(2000)).cuda()
-region = mk.Region(mk.HYPERCUBE, 3, 3)
-c, _, _ = mk.coords_quantize(pts, synthetic.ROOM_VOXEL)
-X = torch.randn(c.n, 64, device="cuda").bfloat16()
-W = (torch.randn(27, 64, 64, device="cuda") * 0.02).bfloat16()
-G = torch.randn(c.n, 64, device="cuda").bfloat16()
+n_steps = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+cfg = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+import types  # noqa: E402
+
+import bench  # noqa: E402
+
+args = types.SimpleNamespace(seed=None)
+w = bench.Workload(cfg, args, torch.device("cuda", 0), 0, 1, "bf16")
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
 
 def step():
-    c, _, _ = mk.coords_quantize(pts, synthetic.ROOM_VOXEL, return_maps=True, deferred=True)
-    m = mk.kmap_build(c, c, region)
-    mk.conv_forward(m, X, W)
-    mk.conv_backward(m, G, X, W, need_gin=True, need_gw=False)
-    mk.conv_backward(m, G, X, W, need_gin=False, need_gw=True)
+    w.step(lambda i: None)
 
 
 for _ in range(5):
