@@ -79,6 +79,8 @@ struct QuantSrc {  // Alg. 1 line 1: C_p' <- floor(C_p / v_l)   (R6: fp32 divisi
     if (b < 0) return E_BATCH;
     return pack_key(c, D, b, k) ? E_NONE : E_RANGE;
   }
+  // batch index of row p as the key will hold it (-1 or out of range: the key is invalid)
+  __device__ __forceinline__ int64_t batch_of(int64_t p) const { return batch ? batch[p] : 0; }
 };
 
 struct IntSrc {  // integer rows [n][D+1], batch last (Eq. 1); multiples of the tensor stride
@@ -100,6 +102,7 @@ struct IntSrc {  // integer rows [n][D+1], batch last (Eq. 1); multiples of the 
     if (b < 0) return E_BATCH;
     return pack_key(c, D, b, k) ? E_NONE : E_RANGE;
   }
+  __device__ __forceinline__ int64_t batch_of(int64_t p) const { return rows[p * (D + 1) + D]; }
 };
 
 struct StrideSrc {  // u' = floor_div(u, s_out) * s_out per spatial axis (R7, R11)
@@ -122,6 +125,7 @@ struct StrideSrc {  // u' = floor_div(u, s_out) * s_out per spatial axis (R7, R1
     }
     return pack_key(c, D, key_batch(in, D), k) ? E_NONE : E_RANGE;
   }
+  __device__ __forceinline__ int64_t batch_of(int64_t p) const { return key_batch(keys[p], D); }
 };
 
 struct ExpandSrc {  // f4: expanded row p = (input row p / K, offset p % K) -> u + i_k * s (R18)
@@ -144,6 +148,7 @@ struct ExpandSrc {  // f4: expanded row p = (input row p / K, offset p % K) -> u
     }
     return pack_key(c, D, key_batch(in, D), k) ? E_NONE : E_RANGE;
   }
+  __device__ __forceinline__ int64_t batch_of(int64_t p) const { return key_batch(keys[p / K], D); }
 };
 
 // ---------------------------------------------------------------- kernels
@@ -154,24 +159,33 @@ struct ExpandSrc {  // f4: expanded row p = (input row p / K, offset p % K) -> u
 // larger than the allocation falls back to the flat table (nsub = 0).
 // cnt[kMaxSub] counts, cnt[kMaxSub] = largest batch + 1, cnt[kMaxSub + 1] = overflow flag.
 template <class Src>
-__global__ void __launch_bounds__(kBlock) k_bhist(Src src, int64_t n, int D, int32_t* __restrict__ cnt) {
+__global__ void __launch_bounds__(kBlock) k_bhist(Src src, int64_t n, int32_t* __restrict__ cnt) {
   pdl_enter();
   __shared__ int32_t h[kMaxSub];
   __shared__ int32_t s_max, s_over;
   for (int i = threadIdx.x; i < kMaxSub; i += kBlock) h[i] = 0;
   if (threadIdx.x == 0) s_max = 0, s_over = 0;
   __syncthreads();
-  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
-    int4 k;
-    if (src.key(p, &k) != E_NONE) continue;  // reported by k_insert
-    const uint32_t b = (uint32_t)key_batch(k, D);
-    if (b < (uint32_t)kMaxSub) {
-      atomicAdd(&h[b], 1);
-      atomicMax(&s_max, (int32_t)b + 1);
-    } else {
+  const int lane = threadIdx.x & 31;
+  int32_t bmax = 0;
+  const int64_t n_round = (n + 31) & ~(int64_t)31;  // whole warps in the loop (warp-aggregated adds)
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n_round; p += (int64_t)gridDim.x * blockDim.x) {
+    // the batch field alone (rows with an input error are reported by k_insert; a batch
+    // index that no valid key can hold only makes the layout fall back to the flat table)
+    const int64_t bb = p < n ? src.batch_of(p) : -1;
+    uint32_t b = bb < 0 ? 0xFFFFFFFFu : bb < kMaxSub ? (uint32_t)bb : (uint32_t)kMaxSub;
+    if (b == (uint32_t)kMaxSub) {
       s_over = 1;
+      b = 0xFFFFFFFFu;
+    }
+    // rows are usually batch-major: one shared-memory add per distinct batch of the warp
+    const unsigned same = __match_any_sync(0xffffffffu, b);
+    if (b != 0xFFFFFFFFu && lane == __ffs(same) - 1) {
+      atomicAdd(&h[b], __popc(same));
+      bmax = max(bmax, (int32_t)b + 1);
     }
   }
+  if (bmax) atomicMax(&s_max, bmax);
   __syncthreads();
   for (int i = threadIdx.x; i < kMaxSub; i += kBlock)
     if (h[i]) atomicAdd(cnt + i, h[i]);
@@ -542,7 +556,7 @@ mk_status build_coords(mk_context* ctx, const Src& src, int64_t n, int D, const 
     int32_t* hist = (int32_t*)(sbase + o_hi);
     if ((e = cudaMemsetAsync(hist, 0, sizeof(int32_t) * (kMaxSub + 2), s)) != cudaSuccess)
       return fail_cuda(e, "memset");
-    pdl_launch(k_bhist<Src>, grid_for(n, kBlock, ctx->num_sms / 4 > 0 ? ctx->num_sms / 4 : 1), kBlock, 0, s, src, n, D,
+    pdl_launch(k_bhist<Src>, grid_for(n, kBlock, ctx->num_sms / 4 > 0 ? ctx->num_sms / 4 : 1), kBlock, 0, s, src, n,
                hist);
     pdl_launch(k_blayout, 1, 1024, 0, s, (const int32_t*)hist, cap, c->table.sub);
   } else if (use_sub) {

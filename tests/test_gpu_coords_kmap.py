@@ -131,6 +131,31 @@ def test_lookup_matches_oracle(mk, orc):
     assert np.array_equal(c.lookup(dev(q)).cpu().numpy(), orc.lookup(oc, q))
 
 
+@pytest.mark.parametrize("batches", [[0, 1, 2, 7, 9], [3, 5000]])
+def test_per_batch_regions_match_oracle(mk, orc, batches):
+    # >= 1.6M rows: the table gets per-batch regions (mk_internal.cuh TableRef); uneven
+    # batch sizes, batch indices with no rows (lookups of them are absent), and a batch
+    # index >= kMaxSub (4096), which falls back to the flat table.  Rows, lookups and a
+    # 3x3x3 map are byte-identical to the oracle's.
+    g = np.random.default_rng(sum(batches))
+    sizes = g.dirichlet(np.ones(len(batches))) * 1_700_000 + 20_000
+    parts = []
+    for b, n in zip(batches, sizes.astype(int)):
+        xyz = g.integers(-120, 120, (n, 3))
+        parts.append(np.concatenate([xyz, np.full((n, 1), b)], axis=1))
+    rows = np.concatenate(parts).astype(np.int32)
+    c = mk.coords_create(dev(rows))
+    oc, _ = orc.create(rows)
+    assert np.array_equal(c.export().cpu().numpy(), oc)
+    q = np.concatenate([g.integers(-121, 121, (200000, 3)), g.choice(batches + [4, 8, 4095], (200000, 1))],
+                       axis=1).astype(np.int32)
+    assert np.array_equal(c.lookup(dev(q)).cpu().numpy(), orc.lookup(oc, q))
+    sel = np.isin(oc[:, 3], batches[:2])  # a map on a slice of the rows (oracle time)
+    sub = np.ascontiguousarray(oc[sel][::8])
+    cs = mk.coords_create(dev(sub))
+    map_pair(mk, orc, c, cs, oc, sub, Spec(0, 3, 3), [1, 1, 1], what="regions map")
+
+
 # ------------------------------------------------------------------ kernel maps
 def _check_map(mk, orc, cin_np, cout_np, spec, scale, transposed, ci, co):
     """GPU map of the GPU coordinate handles vs the oracle's map of the oracle's coordinates

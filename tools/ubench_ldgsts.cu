@@ -13,10 +13,13 @@
 
 using namespace mk::sm100;
 
+// mode bits: 1 = indices from shared memory (LDS.128, 4 per lane group) instead of registers,
+// 2 = swizzled destination, 4 = zero-fill form (src-size operand), 8 = runtime row stride
 __global__ void k_g(const uint4* __restrict__ tab, const int* __restrict__ idx, int stages_per_warp, int D, int noinc,
-                    long long* issue_cycles, uint4* out) {
+                    int mode, int stride16, long long* issue_cycles, uint4* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   __shared__ uint64_t bar[32];
+  __shared__ __align__(16) int sidx[16][128];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   if (lane == 0) mbar_init(&bar[warp], 32);
   fence_mbar_init();
@@ -26,23 +29,46 @@ __global__ void k_g(const uint4* __restrict__ tab, const int* __restrict__ idx, 
   long long t_issue = 0;
   uint32_t ph = 0;
   const int gw = blockIdx.x * nw + warp;
+  const int q4 = lane >> 3, jj = lane & 7;
   for (int st = 0; st < stages_per_warp; ++st) {
     const uint32_t dst = base + (st % slots) * 16384;
     const int* ix = idx + ((size_t)gw * stages_per_warp + st) * 128;
     int rows[32];
+    if (mode & 1) {
+      reinterpret_cast<int4*>(sidx[warp])[lane] = __ldg(reinterpret_cast<const int4*>(ix) + lane);
+      __syncwarp();
+    } else {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) rows[i] = __ldg(ix + i * 4 + lane / 8);
-    if (rows[0] == -7) out[1] = make_uint4(0, 0, 0, 0);  // indices resident before the timer
+      for (int i = 0; i < 32; ++i) rows[i] = __ldg(ix + i * 4 + lane / 8);
+      if (rows[0] == -7) out[1] = make_uint4(0, 0, 0, 0);
+    }
     long long t0 = clock64();
+    if (mode & 1) {
+#pragma unroll 2
+      for (int i = 0; i < 32; i += 4) {
+        const int4 a4 = *(const int4*)(&sidx[warp][q4 * 32 + i]);
+        const int av[4] = {a4.x, a4.y, a4.z, a4.w};
 #pragma unroll
-    for (int i = 0; i < 32; ++i) {
-      const int r = i * 4 + lane / 8;
-      cp_async16(dst + r * 128 + (lane & 7) * 16, tab + (size_t)rows[i] * 8 + (lane & 7), 16);
+        for (int e = 0; e < 4; ++e) {
+          const int r = q4 * 32 + i + e;
+          const uint32_t d = (mode & 2) ? dst + swz(r, jj, 128) : dst + r * 128 + jj * 16;
+          const uint4* src = (mode & 8) ? tab + (int64_t)max(av[e], 0) * stride16 + jj : tab + (size_t)av[e] * 8 + jj;
+          if (mode & 4) cp_async16(d, src, av[e] >= 0 ? 16u : 0u);
+          else cp_async16(d, src, 16u);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int r = i * 4 + lane / 8;
+        const uint32_t d = (mode & 2) ? dst + swz(r, jj, 128) : dst + r * 128 + jj * 16;
+        if (mode & 4) cp_async16(d, tab + (size_t)rows[i] * 8 + jj, rows[i] >= 0 ? 16u : 0u);
+        else cp_async16(d, tab + (size_t)rows[i] * 8 + jj, 16u);
+      }
     }
     if (noinc) cp_async_arrive_noinc(&bar[warp]);
     cp_async_commit();
     t_issue += clock64() - t0;
-    (void)rows;
     cp_async_wait_n(D);
     if (noinc && st >= D) {  // the arrival of stage st - D
       mbar_wait(&bar[warp], ph);
@@ -71,19 +97,20 @@ int main() {
   cudaMalloc(&ic, 148 * 32 * 8);
   uint4* out;
   cudaMalloc(&out, 16);
-  cudaFuncSetAttribute(k_g, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  cudaFuncSetAttribute(k_g, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int W : {4, 8, 12, 16}) {
-    for (int D : {0, 1, 2, 3}) {
-      if ((D + 1) * W * 16 > 220) continue;
+  for (int W : {4, 8, 12}) {
+    for (int mode : {0, 4, 2, 6}) {
+      const int D = 1;
+      if ((D + 1) * W * 16 > 200) continue;
       for (int noinc = 0; noinc < 2; ++noinc) {
         const int spw = 1400000 / 128 / (sm * W);  // ~1.4M rows in total (a configs[1] conv)
         const int smem = (D + 1) * W * 16384;
-        k_g<<<sm, W * 32, smem>>>(tab, idx, spw, D, noinc, ic, out);
+        k_g<<<sm, W * 32, smem>>>(tab, idx, spw, D, noinc, mode, 8, ic, out);
         cudaEventRecord(e0);
-        k_g<<<sm, W * 32, smem>>>(tab, idx, spw, D, noinc, ic, out);
+        k_g<<<sm, W * 32, smem>>>(tab, idx, spw, D, noinc, mode, 8, ic, out);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         float ms;
@@ -94,7 +121,7 @@ int main() {
         for (auto v : hc) mi += v;
         mi /= hc.size() * spw;
         const double bytes = (double)sm * W * spw * 16384;
-        printf("warps/SM=%2d depth=%d noinc=%d: %7.1f us %6.2f TB/s  issue %6.0f cycles/stage (%s)\n", W, D, noinc,
+        printf("warps/SM=%2d mode=%2d noinc=%d: %7.1f us %6.2f TB/s  issue %6.0f cycles/stage (%s)\n", W, mode, noinc,
                ms * 1e3, bytes / (ms * 1e-3) / 1e12, mi, cudaGetErrorString(cudaGetLastError()));
       }
     }
