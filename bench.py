@@ -493,15 +493,25 @@ def summarize(w, ph, pk, dtype):
     }
 
 
+NCU_SUMMARY = {4: "ncu_summary_r02.json", 1: "ncu_summary_r02_c1.json"}
+MAP_KERNELS = ("quant_insert", "quant_rank", "kmap_probe", "kmap_emit", "kmap_sort")
+
+
 def ncu_traffic(cfg, kernel):
-    """DRAM bytes per launch of a kernel from the committed ncu capture (cold L2:
-    --cache-control all), or None."""
-    p = ROOT / "profiles" / "ncu_summary_r02.json"
-    if not p.exists():
+    """DRAM bytes (read + write) per launch of a kernel of this workload from the committed
+    ncu capture (tools/ncu_profile.sh: --set full --cache-control all, i.e. cold L2 as in the
+    flushed bench step), or None.  "map_build" sums the map-build kernels' captures."""
+    name = NCU_SUMMARY.get(cfg)
+    p = ROOT / "profiles" / name if name else None
+    if p is None or not p.exists():
         return None
     try:
-        d = json.loads(p.read_text())
-        return d.get(f"configs[{cfg}]", {}).get(kernel, {}).get("dram_bytes")
+        d = json.loads(p.read_text()).get("dram_bytes_per_launch", {})
+        if kernel == "map_build":
+            v = [d.get(k) for k in MAP_KERNELS]
+            return None if any(x is None for x in v) else int(sum(v))
+        x = d.get(kernel)
+        return None if x is None else int(x)
     except (ValueError, AttributeError):
         return None
 

@@ -60,8 +60,9 @@ for rep in sorted(src.glob("*.ncu-rep")):
     if "dram_read_bytes" in d and "dram_write_bytes" in d:
         d["dram_bytes"] = d["dram_read_bytes"] + d["dram_write_bytes"]
     res[rep.stem] = d
-summary = {"source": str(src), "note": "ncu --set full --clock-control none --cache-control none, one launch of the "
-           "bench step (bench.py --steps 1 --warmup 1); bytes are per launch",
+summary = {"source": str(src), "note": "ncu --set full --clock-control none --cache-control all (L2 flushed before "
+           "every replay pass: cold-cache DRAM bytes, as in the flushed bench step), one launch of the bench step "
+           "(tools/ncu_profile.sh); bytes are per launch",
            "kernels": res,
            "dram_bytes_per_launch": {k: v.get("dram_bytes") for k, v in res.items()}}
 out_json.write_text(json.dumps(summary, indent=1))
