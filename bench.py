@@ -524,10 +524,17 @@ def run_mk(args, ws, rank, local):
     import paper_1904_08755_b200 as mk
     from paper_1904_08755_b200.dist import RowGather
 
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # MK_DIST_BACKEND=gloo (development): ranks may share GPUs (device = local rank modulo the
+    # visible devices) to exercise the multi-rank path where only one GPU is available
+    backend = os.environ.get("MK_DIST_BACKEND", "nccl")
+    local_dev = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     # configs[0]-[3] are single-scan workloads: under N > 1 every rank runs its own replica
     # (weak scaling, no collective other than the dW all-reduce); configs[4] is sharded
     stream = torch.cuda.current_stream()
@@ -536,7 +543,7 @@ def run_mk(args, ws, rank, local):
     pk = peaks()
 
     w = Workload(args.config, args, dev, rank, ws, args.dtype)
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local_dev)
     sampler.start()
     time.sleep(0.3)
     t0 = time.time()
@@ -557,6 +564,9 @@ def run_mk(args, ws, rank, local):
     ms_per_step = total_ms / args.steps
     value = flops_all / (ms_per_step * 1e-3) / 1e12
     summ = summarize(w, ph, pk, args.dtype)
+    if ws > 1:  # the committed ncu captures are of the one-GPU workload
+        summ["roofline"]["traffic"] = None
+        summ["roofline_map_build"]["traffic"] = None
 
     # ---- output all-gather (configs[4]; north star: "NCCL all-gather of outputs"), timed
     #      separately from the compute phase with events, max over ranks
