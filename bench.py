@@ -348,11 +348,20 @@ class Workload:
         flops = 2.0 * cin * cout * self.M
         byts = n_in * cin * s + n_out * cout * s + 8 * self.M + self.K * cin * cout * s
         ai = flops / byts
-        if dtype == "f32":  # exact FFMA path: FP32 ALU bound (148 SMs x 128 lanes x 2 flop x clock)
+        if dtype == "f32" and (cin % 16 or cout % 16 or os.environ.get("MK_F32_MODE") == "exact"):
+            # exact FFMA path: FP32 ALU bound (148 SMs x 128 lanes x 2 flop x clock)
             peak = 148 * 128 * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
             ach = flops / (t_ms * 1e-3) / 1e12
             return {"bound": "alu", "achieved": round(ach, 2), "peak": round(peak, 1), "unit": "TFLOP/s",
                     "frac": round(ach / peak, 4), "peak_source": "derived: 148 SM x 128 FP32 lanes x 2 x max clock"}
+        if dtype == "f32":
+            # fp32 on the bf16 tensor cores by three-way operand splitting (conv_split.cu): six
+            # bf16 products per fp32 product, so the fp32 peak is the bf16 peak / 6
+            peak = pk["bf16_tflops_sustained"] / 6.0
+            ach = flops / (t_ms * 1e-3) / 1e12
+            return {"bound": "tensor", "achieved": round(ach, 2), "peak": round(peak, 1), "unit": "TFLOP/s",
+                    "frac": round(ach / peak, 4), "algorithmic_flops": flops,
+                    "peak_source": pk["source"] + " sustained bf16 / 6 (bf16x3 split: 6 bf16 products per fp32 product)"}
         ridge = pk["bf16_tflops_sustained"] * 1e12 / (pk["hbm_gbs"] * 1e9)
         if ai >= ridge:
             ach = flops / (t_ms * 1e-3) / 1e12

@@ -266,8 +266,12 @@ mk_status mk_crf_backward(mk_context* ctx, const mk_kmap* m, const float* d_phi_
  *   F_out[o] = sum over pairs (a, o) of offset k of W_k F_in[a];  rows without any pair
  *   are 0 ("F^o <- 0"; R15).  No bias (R16).
  *   d_fin   [n_in][c_in] of in_dt;  d_w [K][c_out][c_in] of in_dt;  d_fout [n_out][c_out]
- *   of out_dt.  Accumulation is fp32.  MK_BF16 inputs run on the tcgen05 tensor cores;
- *   MK_F32 inputs run exact fp32 FFMA.  Channel contract: 1 <= c_in, c_out <= 256 for
+ *   of out_dt.  Accumulation is fp32.  MK_BF16 inputs run on the tcgen05 tensor cores.
+ *   MK_F32 inputs run on the same tensor cores as six bf16 convolutions of three-way bf16
+ *   splits of the operands (x = x1 + x2 + x3; the dropped products are below 2^-24 relative,
+ *   fp32-level accuracy) when c_in and c_out are multiples of 16 and no epilogue is fused;
+ *   otherwise, or with the environment variable MK_F32_MODE=exact, exact fp32 FFMA kernels.
+ *   Both are deterministic.  Channel contract: 1 <= c_in, c_out <= 256 for
  *   MK_F32; multiples of 16 in 16..256 for MK_BF16 (every such pair is planned: wide
  *   outputs are split over column slices, wide weight-gradient tiles use fewer, larger CTAs);
  *   anything else returns MK_ERR_UNSUPPORTED.

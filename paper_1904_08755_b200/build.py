@@ -13,7 +13,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 SO = PKG / "libmk.so"
-SOURCES = ["context.cu", "region.cu", "coords.cu", "kmap.cu", "conv.cu", "conv_simt.cu", "conv_umma.cu", "pool.cu", "crf.cu", "sort.cu"]
+SOURCES = ["context.cu", "region.cu", "coords.cu", "kmap.cu", "conv.cu", "conv_simt.cu", "conv_umma.cu", "conv_split.cu", "pool.cu", "crf.cu", "sort.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", str(ROOT / "include"), "-I", str(CSRC)]

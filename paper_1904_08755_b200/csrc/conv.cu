@@ -1,6 +1,8 @@
 // conv.cu — entry points of the generalized sparse convolution (Alg. 2), its
 // reverse mode, and the transposed convolution.  Validation and dispatch only:
-// fp32 -> exact FFMA kernels (conv_simt.cu); bf16 -> tcgen05 tensor cores (conv_umma.cu).
+// bf16 -> tcgen05 tensor cores (conv_umma.cu); fp32 -> the same tensor cores on three-way
+// bf16 splits of the operands (conv_split.cu) when the channel counts suit them, else (and
+// with MK_F32_MODE=exact) exact FFMA kernels (conv_simt.cu).
 #include <algorithm>
 
 #include "conv.cuh"
@@ -28,6 +30,9 @@ mk_status forward_impl(mk_context* ctx, const mk_kmap* m, const void* d_fin, int
   if (m->n_in > 0 && m->n_out > 0 && (!d_fin || !d_w)) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv: null input or weights");
   if (m->n_out == 0) return MK_OK;
   const NbrView v = forward_view(m);
+  if (in_dt == MK_F32 && split_f32_enabled(c_in, c_out, m->K, ep))
+    return launch_conv_f32_split(ctx, v, (const float*)d_fin, m->n_in, c_in, (const float*)d_w, c_in, c_out, d_fout,
+                                 c_out, out_dt, m->n_out, false, s);
   if (in_dt == MK_F32)
     return launch_conv_f32(v, (const float*)d_fin, c_in, (const float*)d_w, c_in, c_out, d_fout, c_out, out_dt,
                            m->n_out, false, s, ep);
@@ -43,7 +48,10 @@ mk_status backward_impl(mk_context* ctx, const mk_kmap* m, const void* d_gout, c
   if (d_gin && m->n_in > 0) {
     if (m->n_out > 0 && !d_w) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv backward: null weights");
     const NbrView v = dgrad_view(m);
-    if (dt == MK_F32)
+    if (dt == MK_F32 && split_f32_enabled(c_in, c_out, m->K, Epilogue()))
+      st = launch_conv_f32_split(ctx, v, (const float*)d_gout, m->n_out, c_out, (const float*)d_w, c_in, c_out, d_gin,
+                                 c_in, MK_F32, m->n_in, true, s);
+    else if (dt == MK_F32)
       st = launch_conv_f32(v, (const float*)d_gout, c_out, (const float*)d_w, c_in, c_out, d_gin, c_in, MK_F32,
                            m->n_in, true, s);
     else
@@ -52,7 +60,9 @@ mk_status backward_impl(mk_context* ctx, const mk_kmap* m, const void* d_gout, c
   }
   if (d_gw) {
     if (m->n_out > 0 && m->n_in > 0 && !d_fin) MK_FAIL(MK_ERR_INVALID_ARGUMENT, "conv backward: null input features");
-    if (dt == MK_F32) {
+    if (dt == MK_F32 && split_f32_enabled(c_in, c_out, m->K, Epilogue())) {
+      st = launch_wgrad_f32_split(ctx, m, (const float*)d_gout, c_out, (const float*)d_fin, c_in, d_gw, s);
+    } else if (dt == MK_F32) {
       st = kmap_host(m);  // per-offset pair counts on the host (waits for the build only)
       if (st != MK_OK) return st;
       // split-K plan: chunks of <= P pairs per offset, P = 4096 or smaller so that the grid has

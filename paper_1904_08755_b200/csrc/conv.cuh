@@ -94,6 +94,13 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
                            cudaStream_t s, const Epilogue& ep = Epilogue());
 mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, int c_out, const void* x, int c_in,
                             float* dW, cudaStream_t s);
+// fp32 on the bf16 tensor cores by three-way operand splitting (conv_split.cu)
+bool split_f32_enabled(int c_in, int c_out, int K, const Epilogue& ep);
+mk_status launch_conv_f32_split(mk_context* ctx, const NbrView& nb, const float* x, int64_t n_src, int c_x,
+                                const float* W, int c_in_w, int c_out_w, void* y, int c_y, mk_dtype out_dt,
+                                int64_t n_rows, bool trans, cudaStream_t s);
+mk_status launch_wgrad_f32_split(mk_context* ctx, const mk_kmap* m, const float* g, int c_out, const float* x,
+                                 int c_in, float* dW, cudaStream_t s);
 __global__ void k_reduce_partials(const int32_t* __restrict__ chunk_begin, const float* __restrict__ part,
                                   int64_t tile_elems, float* __restrict__ dW);
 
