@@ -50,6 +50,19 @@ def test_submanifold_conv(mk, orc, dt, tol, cin, cout, n, span):
     check_features(mk, orc, m, okm, X, W, G, dt, tol, what=f"{dt} {cin}->{cout}")
 
 
+@pytest.mark.parametrize("cin,cout", [(12, 20), (3, 40), (64, 24), (40, 64)])
+def test_fp32_channel_counts_off_the_tensor_core_grid(mk, orc, cin, cout):
+    # fp32 with a channel count that is not a multiple of 16 (on either side) runs the
+    # exact-FFMA kernels and must match the oracle at the fp32 tolerance, like the bf16x3
+    # split path (R28) that the multiples-of-16 cases above take
+    c, oc = _sparse(mk, orc, cin * 7 + cout, 4000, 14)
+    m, okm = map_pair(mk, orc, c, c, oc, oc, CUBE3, [1, 1, 1])
+    X = synthetic.features(21, c.n, cin)
+    W = synthetic.weights(22, 27, cout, cin)
+    G = synthetic.features(23, c.n, cout)
+    check_features(mk, orc, m, okm, X, W, G, "f32", FP32_TOL, what=f"f32 {cin}->{cout}")
+
+
 @pytest.mark.parametrize("dt,tol", [("f32", FP32_TOL), ("bf16", BF16_TOL)])
 def test_hybrid_4d_conv(mk, orc, dt, tol):
     c, oc = _sparse(mk, orc, 44, 12000, 14, D=4)
