@@ -67,12 +67,14 @@ __device__ __forceinline__ bool shift_key(int4 u, int D, const int32_t* off, int
 // over the staged block.
 // Queries in flight per thread and CTAs per SM: the probe is latency bound, so occupancy
 // pays more than per-thread ILP (configs[1] kmap phase: PB 4 / 2 CTAs 153 us, PB 4 / 3 CTAs
-// 145 us, PB 2 / 4 CTAs 134 us, PB 2 / 5 CTAs 136 us).
+// 145 us, PB 2 / 4 CTAs 134 us, PB 2 / 5 CTAs 136 us; round 2, configs[4] map phase: PB 2 /
+// 4 CTAs 1107 us, PB 1 / 6 CTAs 1006 us, PB 1 / 8 CTAs 1041 us, PB 4 / 3 CTAs 1250 us, with
+// configs[1] within 3 us of the best).
 #ifndef MK_PROBE_PB
-#define MK_PROBE_PB 2
+#define MK_PROBE_PB 1
 #endif
 #ifndef MK_PROBE_MINB
-#define MK_PROBE_MINB 4
+#define MK_PROBE_MINB 6
 #endif
 constexpr int kPB = MK_PROBE_PB;
 
