@@ -492,6 +492,18 @@ def summarize(w, ph, pk, dtype):
                 "stride + kmap", "time_us": round(build_ms * 1e3, 2), "traffic": ncu_traffic(w.cfg, "map_build"),
                 "peak_source": pk["source"]}
     conv_total = sum(conv_ms.values())
+    # the gather bound of the dominant conv kernel: rows gathered per pair (fwd: C_in, dgrad:
+    # C_out, wgrad: both) against the random 128-byte-row gather ceiling measured on this GPU
+    # (tools/ubench_ldgsts.cu, profiles/ubench_ldgsts_r02.txt: 10.64 TB/s with 12 warps/SM)
+    (_, cin, cout, _n_in, _n_out) = [L for L in w.layers if L[0] == nm][0]
+    esz = 2 if dtype == "bf16" else 4
+    per_pair = {"conv_fwd": cin, "conv_dgrad": cout, "conv_wgrad": cin + cout}[dom.split("_", 2)[0] + "_" +
+                                                                               dom.split("_", 2)[1]] * esz
+    gb = per_pair * w.M
+    gach = gb / (conv_ms[dom] * 1e-3) / 1e12
+    gather = {"bound": "l2_gather", "achieved": round(gach, 2), "peak": GATHER_PEAK_TBS, "unit": "TB/s",
+              "frac": round(gach / GATHER_PEAK_TBS, 4), "gathered_bytes": int(gb), "kernel": dom,
+              "peak_source": "builder-measured random 128-byte row gather ceiling (tools/ubench_ldgsts.cu)"}
     return {
         "phases_us": phases,
         "conv_tflops": round(w.flops_step / (conv_total * 1e-3) / 1e12, 3),
@@ -499,10 +511,12 @@ def summarize(w, ph, pk, dtype):
         "gprobes_per_s": round(w.N * w.K / (build_ms * 1e-3) / 1e9, 2),
         "roofline": roof,
         "roofline_map_build": map_roof,
+        "roofline_gather": gather,
     }
 
 
 NCU_SUMMARY = {4: "ncu_summary_r02.json", 1: "ncu_summary_r02_c1.json"}
+GATHER_PEAK_TBS = 10.64
 MAP_KERNELS = ("quant_insert", "quant_rank", "kmap_probe", "kmap_emit", "kmap_sort")
 
 

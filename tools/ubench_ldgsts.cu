@@ -1,5 +1,7 @@
-// ubench_ldgsts.cu — does cp.async.mbarrier.arrive.noinc serialise a warp's cp.async
-// stream?  Each warp gathers 16 KB stages (128 random 128-byte rows of a 19 MB table) into
+// ubench_ldgsts.cu — random 128-byte row gathers by warps issuing 16 KB cp.async stages with
+// the row indices already in registers: bandwidth vs issuing warps per SM, and the cost of
+// the zero-fill (src-size) form (mode bit 4), the SW128 destination swizzle (mode bit 2) and
+// a cp.async.mbarrier.arrive.noinc per stage.  Each warp gathers 16 KB stages (128 random 128-byte rows of a 19 MB table) into
 // its own ring of D+1 smem slots, keeping D stages in flight (wait_group D), optionally
 // with one noinc arrival per stage on a per-warp mbarrier.  Development tool.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_1904_08755_b200/csrc ubench_ldgsts.cu
@@ -101,29 +103,30 @@ int main() {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  for (int W : {4, 8, 12}) {
-    for (int mode : {0, 4, 2, 6}) {
-      const int D = 1;
-      if ((D + 1) * W * 16 > 200) continue;
-      for (int noinc = 0; noinc < 2; ++noinc) {
-        const int spw = 1400000 / 128 / (sm * W);  // ~1.4M rows in total (a configs[1] conv)
-        const int smem = (D + 1) * W * 16384;
-        k_g<<<sm, W * 32, smem>>>(tab, idx, spw, D, noinc, mode, 8, ic, out);
-        cudaEventRecord(e0);
-        k_g<<<sm, W * 32, smem>>>(tab, idx, spw, D, noinc, mode, 8, ic, out);
-        cudaEventRecord(e1);
-        cudaEventSynchronize(e1);
-        float ms;
-        cudaEventElapsedTime(&ms, e0, e1);
-        std::vector<long long> hc(sm * W);
-        cudaMemcpy(hc.data(), ic, 8 * sm * W, cudaMemcpyDeviceToHost);
-        double mi = 0;
-        for (auto v : hc) mi += v;
-        mi /= hc.size() * spw;
-        const double bytes = (double)sm * W * spw * 16384;
-        printf("warps/SM=%2d mode=%2d noinc=%d: %7.1f us %6.2f TB/s  issue %6.0f cycles/stage (%s)\n", W, mode, noinc,
-               ms * 1e3, bytes / (ms * 1e-3) / 1e12, mi, cudaGetErrorString(cudaGetLastError()));
-      }
+  struct Case {
+    int W, D, mode;
+  };
+  const Case cases[] = {{4, 0, 0}, {8, 0, 0}, {12, 0, 0}, {4, 1, 0}, {4, 1, 4}, {4, 1, 2}, {4, 1, 6}};
+  for (const Case& cs : cases) {
+    const int W = cs.W, D = cs.D, mode = cs.mode;
+    for (int noinc = 0; noinc < 2; ++noinc) {
+      const int spw = 1400000 / 128 / (sm * W);  // ~1.4M rows in total (a configs[1] conv)
+      const int smem = (D + 1) * W * 16384;
+      k_g<<<sm, W * 32, smem>>>(tab, idx, spw, D, noinc, mode, 8, ic, out);
+      cudaEventRecord(e0);
+      k_g<<<sm, W * 32, smem>>>(tab, idx, spw, D, noinc, mode, 8, ic, out);
+      cudaEventRecord(e1);
+      cudaEventSynchronize(e1);
+      float ms;
+      cudaEventElapsedTime(&ms, e0, e1);
+      std::vector<long long> hc(sm * W);
+      cudaMemcpy(hc.data(), ic, 8 * sm * W, cudaMemcpyDeviceToHost);
+      double mi = 0;
+      for (auto v : hc) mi += v;
+      mi /= hc.size() * spw;
+      const double bytes = (double)sm * W * spw * 16384;
+      printf("warps/SM=%2d depth=%d mode=%d noinc=%d: %7.1f us %6.2f TB/s  issue %6.0f cycles/stage (%s)\n", W, D,
+             mode, noinc, ms * 1e3, bytes / (ms * 1e-3) / 1e12, mi, cudaGetErrorString(cudaGetLastError()));
     }
   }
   return 0;
