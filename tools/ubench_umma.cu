@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <vector>
 
 #include "sm100.cuh"
 
@@ -252,7 +253,74 @@ __global__ void __launch_bounds__(128, 1) k_commit(int rounds, int nmma, long lo
   if (warp == 0) tmem_dealloc(tbase, 512);
 }
 
+// several CTAs per SM, each: 4 UMMAs (M=128, N=64, K=16) + commit per step, waiting only for
+// the commit 8 steps back.  Do commits from different CTAs drain each other's MMAs?
+__global__ void __launch_bounds__(128) k_multi(int steps, int commit_every, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  __shared__ uint64_t bar[8];
+  __shared__ uint32_t tslot;
+  const int warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < 32768 / 4; i += 128) ((uint32_t*)sm)[i] = 0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 8; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tmem_alloc_dyn(&tslot, 128);
+  fence_proxy_async_smem();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = tslot;
+  if (threadIdx.x == 0) {
+    const uint32_t idesc = idesc_bf16(128, 64, 0, 0);
+    const uint64_t dhi = smem_desc(0, 16, 1024, 2);
+    const uint32_t a0 = smem_u32(sm) >> 4, b0 = a0 + 1024;
+    long long t0 = clock64();
+    int nc = 0;
+    for (int st = 0; st < steps; ++st) {
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) umma_f16(tbase, dhi | (uint64_t)(a0 + kk * 2), dhi | (uint64_t)(b0 + kk * 2), idesc, 1u);
+      if ((st + 1) % commit_every == 0) {
+        if (nc >= 8) mbar_wait(&bar[nc & 7], ((nc >> 3) - 1) & 1);
+        umma_commit(&bar[nc & 7]);
+        ++nc;
+      }
+    }
+    for (int j = nc > 8 ? nc - 8 : 0; j < nc; ++j) mbar_wait(&bar[j & 7], (j >> 3) & 1);
+    out[blockIdx.x] = clock64() - t0;
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 0) tmem_dealloc(tbase, 128);
+}
+
 int main() {
+  {
+    long long* dm;
+    cudaMalloc(&dm, 148 * 4 * 8);
+    std::vector<long long> hm(148 * 4);
+    cudaFuncSetAttribute(k_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, 60 * 1024);
+    for (int per_sm : {1, 2, 3}) {
+      for (int ce : {1, 2, 4}) {
+        const int steps = 2048;
+        const int smem = (227 * 1024) / per_sm - 4096;  // forces per_sm CTAs per SM at most
+        cudaFuncSetAttribute(k_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a);
+        k_multi<<<148 * per_sm, 128, smem>>>(steps, ce, dm);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        const double mmas_per_sm = (double)per_sm * steps * 4;
+        printf("CTAs/SM=%d commit every %d steps: %8.1f us  %6.1f cycles per UMMA per SM (%s)\n", per_sm, ce, ms * 1e3,
+               ms * 1e-3 * 1.965e9 / mmas_per_sm, cudaGetErrorString(cudaGetLastError()));
+      }
+    }
+  }
   long long* d;
   cudaMalloc(&d, 148 * 8);
   long long h[148];
