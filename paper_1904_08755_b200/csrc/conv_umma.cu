@@ -1325,8 +1325,8 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
     if ((p.sa >= 2 && per_sm * p.tmem_cols <= 512) || np >= 16) break;
   }
   if (p.sa >= 8) p.sa -= p.sa % 4;
-  // stage slots released per commit: grouped at one CTA per SM (a commit drains the tensor
-  // pipe), one per commit when another CTA hides the drain (wgrad 85.9 -> 82.4 us, configs[1])
+  // stage slots released per commit: grouped at one CTA per SM, one per commit when other CTAs
+  // share the SM (wgrad 85.9 -> 82.4 us, configs[1]; grouping at three CTAs: slower)
   p.ga = per_sm >= 2 ? 1 : p.sa % 4 == 0 ? 4 : p.sa % 2 == 0 ? 2 : 1;
   if (env_ga > 0 && p.sa % env_ga == 0) p.ga = env_ga;
   if (p.sa < 2 || p.tmem_cols > 512) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: channel counts too large");
