@@ -662,7 +662,8 @@ struct WgradParams {
   float* part;               // [n_slots][c_out][c_in]
   int c_out, c_in, halves;
   int mrows;                 // UMMA M: 64 when C_out <= 64 (no zero panel), else 128 per half
-  int sa, ga;                // stage slots (== producer warps), slots per commit group
+  int sa, ga;                // stage slots, slots per commit group
+  int wps;                   // producer warps per stage slot (each gathers 64 / wps pairs of a step)
   int pwa, pwb;              // panel widths (channels) of A (G) and B (X)
   uint32_t a_bytes, b_bytes, slot_bytes, tmem_cols;
 };
@@ -851,7 +852,7 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
   }
   if (threadIdx.x == 32) {
     for (int s = 0; s < p.sa; ++s) {
-      mbar_init(a_full + s, 1);
+      mbar_init(a_full + s, p.wps);
       mbar_init(a_empty + s, 1);
     }
     mbar_init(tfull, 1);
@@ -877,8 +878,12 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
   const int n_steps = seg_g0[nseg];
   ACCT_DECL
 
-  if (warp < p.sa) {
+  if (warp < p.sa * p.wps) {
     // ------------------------------------------------------------ gather producers
+    // Warp w fills stage slot w / wps with pairs [PW part, PW part + PW) of the slot's steps
+    // (PW = 64 / wps, part = w % wps): when the channel counts leave fewer slots than
+    // producer warps, every warp still gathers (more warps issuing = more gathers in flight).
+    const int slot = warp / p.wps, part = warp - slot * p.wps, PW = PS / p.wps, pr0 = part * PW, pr1 = pr0 + PW;
     int32_t* ib_w = ibuf_all + warp * 4 * PS;  // [2][out, in][64]
     int si = 0;
     const int64_t r_b = s_rng[0], r_e = s_rng[1], r_j = s_rng[2], r_J = s_rng[3];
@@ -897,15 +902,15 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
       int32_t* d = ib_w + buf * 2 * PS;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int i = lane + 32 * h;
-        if (b0 + i < e) {
+        const int i = pr0 + lane + 32 * h;
+        if (i < pr1 && b0 + i < e) {
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(d + i)), "l"(p.out_idx + b0 + i) : "memory");
           asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(d + PS + i)), "l"(p.in_idx + b0 + i)
                        : "memory");
         }
       }
     };
-    int g = warp, b0 = 0, e = 0, b0n = 0, en = 0;
+    int g = slot, b0 = 0, e = 0, b0n = 0, en = 0;
     if (g < n_steps) {
       locate(g, &b0, &e);
       fetch_idx(b0, e, 0);
@@ -922,9 +927,9 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
         locate(g + p.sa, &b0n, &en);
         fetch_idx(b0n, en, ib ^ 1);
       }
-      ACCT_WAIT(0, a_empty + warp / p.ga, (my & 1) ^ 1);
+      ACCT_WAIT(0, a_empty + slot / p.ga, (my & 1) ^ 1);
       ACCT_NOW(t_issue);
-      const uint32_t a_s = smem_u32(smem + (size_t)warp * p.slot_bytes), b_s = a_s + p.a_bytes;
+      const uint32_t a_s = smem_u32(smem + (size_t)slot * p.slot_bytes), b_s = a_s + p.a_bytes;
       const int32_t* oi = ib_w + ib * 2 * PS;
       const int32_t* ii = oi + PS;
       // G rows -> A panels, X rows -> B panels.  Fast path when a row's chunk count divides
@@ -934,15 +939,15 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
         const __nv_bfloat16* src = p.g + ch * 8;
         const uint32_t dst0 = a_s + pa * panel_a;
 #pragma unroll 4
-        for (int pr = lane / ca; pr < PS; pr += 32 / ca) {
+        for (int pr = pr0 + lane / ca; pr < pr1; pr += 32 / ca) {
           const uint32_t dst = dst0 + swz(pr, j, rba);
           if (b0 + pr < e) cp_async16(dst, src + (int64_t)oi[pr] * p.c_out, 16u);
           else st_shared_zero16(dst);
         }
       } else {  // consecutive lanes take consecutive 16-byte chunks (whole sectors per row)
-        int pr = lane / ca, ch = lane - (lane / ca) * ca;
+        int pr = pr0 + lane / ca, ch = lane - (lane / ca) * ca;
         const int dpr = 32 / ca, dch = 32 - dpr * ca;
-        for (; pr < PS;) {
+        for (; pr < pr1;) {
           const int pa = ch / ja, j = ch - pa * ja;
           const uint32_t dst = a_s + pa * panel_a + swz(pr, j, rba);
           if (b0 + pr < e) cp_async16(dst, p.g + (int64_t)oi[pr] * p.c_out + ch * 8, 16u);
@@ -960,15 +965,15 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
         const __nv_bfloat16* src = p.x + ch * 8;
         const uint32_t dst0 = b_s + pb * panel_b;
 #pragma unroll 4
-        for (int pr = lane / cb; pr < PS; pr += 32 / cb) {
+        for (int pr = pr0 + lane / cb; pr < pr1; pr += 32 / cb) {
           const uint32_t dst = dst0 + swz(pr, j, rbb);
           if (b0 + pr < e) cp_async16(dst, src + (int64_t)ii[pr] * p.c_in, 16u);
           else st_shared_zero16(dst);
         }
       } else {
-        int pr = lane / cb, ch = lane - (lane / cb) * cb;
+        int pr = pr0 + lane / cb, ch = lane - (lane / cb) * cb;
         const int dpr = 32 / cb, dch = 32 - dpr * cb;
-        for (; pr < PS;) {
+        for (; pr < pr1;) {
           const int pb = ch / jb, j = ch - pb * jb;
           const uint32_t dst = b_s + pb * panel_b + swz(pr, j, rbb);
           if (b0 + pr < e) cp_async16(dst, p.x + (int64_t)ii[pr] * p.c_in + ch * 8, 16u);
@@ -988,7 +993,7 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
       fence_proxy_async_smem();
       __syncwarp();
       ACCT_ADD(2, t_land);
-      if (lane == 0) mbar_arrive(a_full + warp);
+      if (lane == 0) mbar_arrive(a_full + slot);
       ++my;
 #ifdef MK_TRACE
       acct[3] += 1;
@@ -1325,6 +1330,13 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
     if ((p.sa >= 2 && per_sm * p.tmem_cols <= 512) || np >= 16) break;
   }
   if (p.sa >= 8) p.sa -= p.sa % 4;
+  static const int env_wps = [] {  // development: MK_WGRAD_WPS=1 one producer warp per slot
+    const char* e = std::getenv("MK_WGRAD_WPS");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.wps = 1;  // producer warps per slot: the spare warps when fewer slots than warps fit
+  while (p.sa * p.wps * 2 <= np && p.wps < 4) p.wps *= 2;
+  if (env_wps == 1) p.wps = 1;
   // stage slots released per commit: grouped at one CTA per SM, one per commit when other CTAs
   // share the SM (wgrad 85.9 -> 82.4 us, configs[1]; grouping at three CTAs: slower)
   p.ga = per_sm >= 2 ? 1 : p.sa % 4 == 0 ? 4 : p.sa % 2 == 0 ? 2 : 1;
