@@ -1335,7 +1335,7 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
     return e ? std::atoi(e) : 0;
   }();
   p.wps = 1;  // producer warps per slot: the spare warps when fewer slots than warps fit
-  while (p.sa * p.wps * 2 <= np && p.wps < 4) p.wps *= 2;
+  while (dev_plan && p.sa * p.wps * 2 <= np && p.wps < 4) p.wps *= 2;  // (the host-plan kernel: one)
   if (env_wps == 1) p.wps = 1;
   // stage slots released per commit: grouped at one CTA per SM, one per commit when other CTAs
   // share the SM (wgrad 85.9 -> 82.4 us, configs[1]; grouping at three CTAs: slower)
