@@ -47,10 +47,8 @@ constexpr int kThreads = (kMmaWarp + 1) * 32;     // 672 (weight-gradient kernel
 // the bitmask-sorted tiles, whose work varies ~4x): 4 gather warps, 4 epilogue warps, the
 // MMA warp and the W stager.
 constexpr int kFwdProd = 4;
-constexpr int kFwdEpi0 = 4;                       // epilogue warps 4-7 (TMEM lane quarters)
-constexpr int kFwdMma = 8;
-constexpr int kFwdStage = 9;
-constexpr int kFwdThreads = 10 * 32;
+// (epilogue warps 4-7 on the TMEM lane quarters, then the MMA warp and the W stager; the
+// two-CTA instance has 8 producer warps, see k_conv_umma)
 constexpr int kMaxSmem = 227 * 1024;
 
 // Rounds a dynamic shared-memory pointer up to 1024 bytes.  The offset is added to the
@@ -378,16 +376,18 @@ __device__ void build_plan(const FwdParams& p, Plan* pl) {
 }
 
 // Output-stationary gather-GEMM over the CTA's tb tiles, offset-outer (see file header).
-template <int CH, bool EPI>  // EPI: the fused epilogue is compiled in (plain convs keep the lean kernel)
-__global__ void __launch_bounds__(kFwdThreads, 2) k_conv_umma(const __grid_constant__ FwdParams p) {
+// NPW: gather producer warps (4: up to three CTAs per SM; 8: two CTAs per SM, 16 issuing warps).
+template <int CH, bool EPI, int NPW>  // EPI: the fused epilogue is compiled in (plain convs keep the lean kernel)
+__global__ void __launch_bounds__((NPW + 6) * 32, 2) k_conv_umma(const __grid_constant__ FwdParams p) {
+  constexpr int kFwdEpi0 = NPW, kFwdMma = NPW + 4, kFwdStage = NPW + 5;
   constexpr int J = CH / 8;    // 16-byte chunks per gathered row
   constexpr int RB = CH * 2;   // bytes per gathered row (= swizzle span)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
   uint8_t* a_base = smem;
   uint8_t* w_base = a_base + (size_t)p.sa * p.a_bytes;
-  int32_t* nbr_s = (int32_t*)(w_base + (size_t)p.sw * p.b_bytes);  // [kFwdProd][3][128] index buffers
-  Plan* pl = (Plan*)(nbr_s + kFwdProd * 3 * kTileM);
+  int32_t* nbr_s = (int32_t*)(w_base + (size_t)p.sw * p.b_bytes);  // [NPW][3][128] index buffers
+  Plan* pl = (Plan*)(nbr_s + NPW * 3 * kTileM);
   uint64_t* a_full = (uint64_t*)(((uintptr_t)(pl + 1) + 15) & ~(uintptr_t)15);
   uint64_t* cb = a_full + p.sa;  // [ncb] commit ring (stage slots and W slots are released by it)
   uint64_t* w_full = cb + p.ncb;
@@ -664,6 +664,7 @@ struct WgradParams {
   int mrows;                 // UMMA M: 64 when C_out <= 64 (no zero panel), else 128 per half
   int sa, ga;                // stage slots, slots per commit group
   int wps;                   // producer warps per stage slot (each gathers 64 / wps pairs of a step)
+  int a_pad;                 // A holds zeroed padding panels (else a_bytes = the real panels only)
   int pwa, pwb;              // panel widths (channels) of A (G) and B (X)
   uint32_t a_bytes, b_bytes, slot_bytes, tmem_cols;
 };
@@ -729,8 +730,8 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
   constexpr int PS = kPairsPerStage;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = align1024(smem_raw);
-  int32_t* ibuf_all = (int32_t*)(smem + (size_t)p.sa * p.slot_bytes);  // [sa][2][2][64]
-  int32_t* seg_g0 = ibuf_all + p.sa * 4 * PS;                          // [kMaxSegs + 1]
+  int32_t* ibuf_all = (int32_t*)(smem + (size_t)p.sa * p.slot_bytes);  // [sa * wps][2][2][64] (one per producer warp)
+  int32_t* seg_g0 = ibuf_all + p.sa * p.wps * 4 * PS;                  // [kMaxSegs + 1]
   int4* s_segs = align16<int4>(seg_g0 + kMaxSegs + 2);  // [kMaxSegs]
   int* s_nseg = (int*)(s_segs + kMaxSegs);
   int64_t* s_rng = align16<int64_t>(s_nseg + 1);  // strided plan: [ptr_k, ptr_k+1, j, J]
@@ -859,8 +860,11 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
     mbar_init(tempty, kEpiWarps * 32);
     fence_mbar_init();
   }
-  // zero the padding panels of A (M padded to 128 per half) once; never overwritten
-  {
+  // zero the padding panels of A (M padded to 128 per half) once; never overwritten.  Without
+  // them (a_pad = 0, default) the padding rows of the UMMA read whatever follows the real
+  // panels (the slot's B panels or the next slot): they only feed accumulator rows >= C_out,
+  // which are never stored.
+  if (p.a_pad) {
     const int tot_pa = (int)(p.a_bytes / panel_a);
     for (int s = 0; s < p.sa; ++s)
       for (int pa = npa; pa < tot_pa; ++pa) {
@@ -1201,49 +1205,70 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
     const char* e = std::getenv("MK_FWD_NP");
     return e ? std::atoi(e) : 0;
   }();
+  static const int env_npw = [] {  // producer warps of the two-CTA instance: 8 (default) or 4
+    const char* e = std::getenv("MK_FWD_NPW");
+    return e && std::atoi(e) == 4 ? 4 : 8;
+  }();
+  static const int env_samax = [] {  // development: stage slots per two-CTA CTA (default: one per producer warp)
+    const char* e = std::getenv("MK_FWD_SAMAX");
+    return e ? std::max(2, std::min(16, std::atoi(e))) : 0;
+  }();
   p.fold = env_fold > 0 ? 1 : 0;
-  // alignment + index buffers + plan + TMEM slot; the barriers (a_full, commit ring, W ring,
-  // tfull) are added per plan below
-  const int base0 = 1024 + kFwdProd * 3 * kTileM * 4 + (int)sizeof(Plan) + 16;
-  // commit-ring size for a plan (an upper bound over sa <= 4, ga >= 1; see kNCB)
-  auto ring = [&](int sw, int tb) {
+  // alignment + index buffers (3 per producer warp) + plan + TMEM slot; the barriers (a_full,
+  // commit ring, W ring, tfull) are added per plan below
+  auto base0 = [&](int npw) { return 1024 + npw * 3 * kTileM * 4 + (int)sizeof(Plan) + 16; };
+  // commit-ring size for a plan (an upper bound over sa <= samax, ga >= 1; see kNCB)
+  auto ring = [&](int sw, int tb, int samax) {
     int n = kNCB;
-    while (n <= (sw / nch) * tb * nch + kFwdProd + 4) n *= 2;
+    while (n <= (sw / nch) * tb * nch + samax + 4) n *= 2;
     return n;
   };
   // Output columns per CTA.  All of C_out in one CTA when its W ring (2 units of nch chunks of
   // cw x CH) and two A stage slots fit the SM; otherwise the columns are split over
   // blockIdx.y (each CTA gathers the same rows and multiplies by its slice of W_k: e.g. C_in =
   // C_out = 256 needs 2 x 4 x 32 KB of W alone, over the 227 KB of an SM).
-  int ysplit = 1, fixed = 0;
+  // Producer warps: three CTAs per SM run the 4-warp instance (one stage slot per warp); two
+  // CTAs per SM the 8-warp instance with up to 8 slots (16 issuing warps per SM: configs[4]
+  // fwd 1239 -> 1113 us, dgrad 1229 -> 1098 us; gathers are latency bound per warp,
+  // tools/ubench_ldgsts.cu), except the fused-epilogue instance (84 registers).
+  int ysplit = 1, fixed = 0, ctas = 2, npw = kFwdProd, samax = kFwdProd;
   for (;; ++ysplit) {
     p.cw = 16 * (int)ceil_div(ceil_div(c_y, 16), ysplit);
     if (ysplit > 1 && (int64_t)(ysplit - 1) * p.cw >= c_y) continue;  // no empty column slice
     p.b_bytes = (uint32_t)p.cw * CH * 2;
     p.tb = p.fold ? std::max(1, std::min(env_fold, 256 / p.cw)) : std::max(1, std::min(2, 256 / p.cw));
     p.tmem_cols = pow2_cols((uint32_t)(p.tb * p.cw));
-    const int base = base0 + 8 * (kFwdProd + ring(nch * 4, p.tb) + nch * 4 + 2);
+    const int base3 = base0(kFwdProd) + 8 * (kFwdProd + ring(nch * 4, p.tb, kFwdProd) + nch * 4 + 2);
     // Three CTAs per SM (configs[1] fwd 65.4 -> 62.9 us, dgrad 64.3 -> 62.2 us) when two stage
     // slots and the W ring fit a third of the SM and the registers allow it (the fused-epilogue
     // instance needs 84 registers: two CTAs).
-    const int ctas = env_ctas0 == 3 && !ep.active() && 3 * p.tmem_cols <= 512 &&
-                             base + nch * 2 * (int)p.b_bytes + 2 * (int)p.a_bytes <= kMaxSmem / 3 - 1024
-                         ? 3
-                         : 2;
-    p.sw = nch * 2;
-    if (ctas == 2 &&
-        base + p.sw * (int)p.b_bytes + kFwdProd * (int)p.a_bytes <= kMaxSmem / 2 - 1024 - 2 * nch * (int)p.b_bytes)
-      p.sw = nch * 4;
-    fixed = base + p.sw * (int)p.b_bytes;
-    p.sa = std::min(kFwdProd, ((ctas == 2 ? kMaxSmem : kMaxSmem / 3 - 1024) - fixed) / (int)p.a_bytes);
-    if (ctas == 2) p.sa -= p.sa % 2;
+    ctas = env_ctas0 == 3 && !ep.active() && 3 * p.tmem_cols <= 512 &&
+                   base3 + nch * 2 * (int)p.b_bytes + 2 * (int)p.a_bytes <= kMaxSmem / 3 - 1024
+               ? 3
+               : 2;
+    // two CTAs: the 8-warp plan when it gets at least 6 slots in half an SM, else the 4-warp one
+    for (int w = ctas == 2 && !ep.active() ? env_npw : kFwdProd;; w = kFwdProd) {
+      npw = w;
+      samax = npw == kFwdProd ? kFwdProd : env_samax > 0 ? env_samax : npw;
+      const int base = ctas == 3 ? base3 : base0(npw) + 8 * (samax + ring(nch * 4, p.tb, samax) + nch * 4 + 2);
+      // per-CTA budget: a third of the SM, half of it (8-warp instance), or the 4-slot cap
+      const int budget = ctas == 3 ? kMaxSmem / 3 - 1024 : samax > kFwdProd ? kMaxSmem / 2 - 1024 : kMaxSmem;
+      p.sw = nch * 2;
+      if (ctas == 2 && samax == kFwdProd &&
+          base + p.sw * (int)p.b_bytes + kFwdProd * (int)p.a_bytes <= kMaxSmem / 2 - 1024 - 2 * nch * (int)p.b_bytes)
+        p.sw = nch * 4;
+      fixed = base + p.sw * (int)p.b_bytes;
+      p.sa = std::min(samax, (budget - fixed) / (int)p.a_bytes);
+      if (ctas == 2) p.sa -= p.sa % 2;
+      if (npw == kFwdProd || p.sa >= 6) break;
+    }
     if ((p.sa >= 2 && p.tmem_cols <= 512) || p.cw <= 16) break;
   }
   // one producer warp per slot measured best (fwd 68.6 us vs 73.8 with two slots per warp,
   // configs[1]): more warps issue the gathers faster than fewer warps with deeper queues
-  p.np = env_np > 0 ? std::min(env_np, p.sa) : p.sa;
+  p.np = std::min(npw, env_np > 0 ? std::min(env_np, p.sa) : p.sa);
   p.ga = p.sa % 2 == 0 ? 2 : 1;  // the W ring must hold >= ga units: sw / nch >= 2 >= ga
-  p.ncb = ring(p.sw, p.tb);
+  p.ncb = ring(p.sw, p.tb, samax);
   if (p.sa < 2 || p.tmem_cols > 512)
     MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: channel counts too large for the smem pipeline");
   const size_t wbytes = (size_t)nb.K * nch * p.b_img;
@@ -1259,17 +1284,17 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   // one CTA per tb tiles and column slice
   const dim3 grid((unsigned)ceil_div(p.ntiles, p.tb), (unsigned)ysplit);
   cudaError_t e;
-  auto go = [&](auto kern) {
+  auto go = [&](auto kern, int nw) {
     set_smem_once(kern, smem);
-    return pdl_launch(kern, grid, kFwdThreads, smem, s, p);
+    return pdl_launch(kern, grid, (nw + 6) * 32, smem, s, p);
   };
   const bool epi = ep.active();
-  if (CH == 64)
-    e = epi ? go(k_conv_umma<64, true>) : go(k_conv_umma<64, false>);
-  else if (CH == 32)
-    e = epi ? go(k_conv_umma<32, true>) : go(k_conv_umma<32, false>);
+  if (epi)
+    e = CH == 64 ? go(k_conv_umma<64, true, 4>, 4) : CH == 32 ? go(k_conv_umma<32, true, 4>, 4) : go(k_conv_umma<16, true, 4>, 4);
+  else if (npw == 8)
+    e = CH == 64 ? go(k_conv_umma<64, false, 8>, 8) : CH == 32 ? go(k_conv_umma<32, false, 8>, 8) : go(k_conv_umma<16, false, 8>, 8);
   else
-    e = epi ? go(k_conv_umma<16, true>) : go(k_conv_umma<16, false>);
+    e = CH == 64 ? go(k_conv_umma<64, false, 4>, 4) : CH == 32 ? go(k_conv_umma<32, false, 4>, 4) : go(k_conv_umma<16, false, 4>, 4);
   if (e == cudaSuccess) e = cudaGetLastError();
   dev_free(ctx->alloc, wpack, s);
   if (e != cudaSuccess) MK_FAIL(MK_ERR_CUDA, std::string("bf16 conv launch: ") + cudaGetErrorString(e));
@@ -1303,15 +1328,21 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   p.halves = c_out > 128 ? 2 : 1;
   p.mrows = c_out <= 64 ? 64 : 128;
   if (c_out > 256) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: C_out above 256");
-  p.a_bytes = (uint32_t)(p.halves * p.mrows) * kPairsPerStage * 2;  // M padded to 64 / 128 per half
+  static const int env_apad = [] {  // development: MK_WGRAD_APAD=1 zeroed padding panels in every slot
+    const char* e = std::getenv("MK_WGRAD_APAD");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.a_pad = env_apad;
+  const uint32_t a_padded = (uint32_t)(p.halves * p.mrows) * kPairsPerStage * 2;  // M padded to 64 / 128 per half
+  p.a_bytes = p.a_pad ? a_padded : (uint32_t)c_out * kPairsPerStage * 2;
   p.b_bytes = (uint32_t)c_in * kPairsPerStage * 2;
   p.slot_bytes = (p.a_bytes + p.b_bytes + 1023) & ~1023u;
   // producer warps: 4 (three CTAs per SM, default), 8 (two) or 16 (one).  configs[1] wgrad:
   // one CTA 104.5 us; two 85.9 us (82.3 with one commit per slot); three 78.1 us.
-  static const int np_env = [] {
+  static const int np_env = [] {  // 0: automatic
     const char* v = std::getenv("MK_WGRAD_NP");
-    const int x = v ? std::atoi(v) : 4;
-    return x == 16 || x == 8 ? x : 4;
+    const int x = v ? std::atoi(v) : 0;
+    return x == 16 || x == 8 || x == 4 ? x : 0;
   }();
   static const int env_ga = [] {  // development: stage slots released per commit
     const char* e = std::getenv("MK_WGRAD_GA");
@@ -1321,13 +1352,30 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   // Fewer, larger CTAs when the stage slots of wide channel counts (up to 2 x 32 KB per slot
   // at 256 x 256) or their TMEM accumulators do not fit three CTAs per SM: np = 8 (two CTAs)
   // or 16 (one CTA, up to 3 slots of 64 KB).
-  int np = np_env, per_sm = 3, reserve = 0;
-  for (;; np *= 2) {
-    per_sm = np == 16 ? 1 : np == 8 ? 2 : 3;
+  // Automatic: three CTAs unless they get fewer than three stage slots each and two CTAs get
+  // at least four (configs[4], C = 96: 2 vs 4 slots, wgrad 1797 -> 1633 us; configs[1], C = 64:
+  // 4 vs 8 slots, 74 us with three CTAs vs 82 with two).
+  int np = np_env > 0 ? np_env : 4, per_sm = 3, reserve = 0;
+  auto plan = [&](int n) {
+    per_sm = n == 16 ? 1 : n == 8 ? 2 : 3;
     const int budget = per_sm == 1 ? kMaxSmem : kMaxSmem / per_sm - 1024;
-    reserve = 1024 + 1024 + np * 4 * kPairsPerStage * 4 + (kMaxSegs + 2) * 4 + (int)sizeof(int4) * kMaxSegs + 128;
-    p.sa = std::min(np, (budget - reserve) / (int)p.slot_bytes);
+    // (+ room for the last slot's padding rows to read past it, when A has no padding panels)
+    reserve = 1024 + 1024 + n * 4 * kPairsPerStage * 4 + (kMaxSegs + 2) * 4 + (int)sizeof(int4) * kMaxSegs + 128 +
+              std::max(0, (int)a_padded - (int)p.slot_bytes);
+    return std::min(n, (budget - reserve) / (int)p.slot_bytes);
+  };
+  for (;; np *= 2) {
+    p.sa = plan(np);
     if ((p.sa >= 2 && per_sm * p.tmem_cols <= 512) || np >= 16) break;
+  }
+  if (np_env == 0 && np == 4 && p.sa < 3) {
+    const int sa8 = plan(8);
+    if (sa8 >= 4 && 2 * p.tmem_cols <= 512) {
+      np = 8;
+      p.sa = sa8;
+    } else {
+      p.sa = plan(4);
+    }
   }
   if (p.sa >= 8) p.sa -= p.sa % 4;
   static const int env_wps = [] {  // development: MK_WGRAD_WPS=1 one producer warp per slot

@@ -36,3 +36,13 @@ def full_grid(G, D, batch=0):
     """Every cell of a G^D grid (fully occupied: C = Z^D restricted to the box)."""
     idx = np.stack(np.meshgrid(*[np.arange(G)] * D, indexing="ij"), axis=-1).reshape(-1, D)
     return np.concatenate([idx, np.full((idx.shape[0], 1), batch)], axis=1).astype(np.int32)
+
+
+def pytest_collection_modifyitems(config, items):
+    """GPU tests get a per-test timeout (pytest-timeout, thread method): a kernel that hangs
+    ends the run with a stack dump instead of blocking it until an outer limit."""
+    if not config.pluginmanager.hasplugin("timeout"):
+        return
+    for item in items:
+        if item.get_closest_marker("gpu") and not item.get_closest_marker("timeout"):
+            item.add_marker(pytest.mark.timeout(600, method="thread"))
