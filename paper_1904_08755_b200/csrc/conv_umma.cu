@@ -234,6 +234,7 @@ struct FwdParams {
   int ga;  // stage slots released together by one tcgen05.commit (sa % ga == 0)
   int sw;  // W chunk slots (a ring: W_k chunks are prefetched several offsets ahead)
   int tb;  // tiles per CTA (one TMEM accumulator each: tb * cw <= 512 columns)
+  int grp;  // MMA steps cover all nch chunks of a (unit, tile)
   int fold;  // tile order (see cta_tile)
   int ncb;   // commit barriers in the ring (power of two)
   uint32_t a_bytes, b_bytes, tmem_cols;
@@ -476,6 +477,7 @@ __global__ void __launch_bounds__((NPW + 6) * 32, 2) k_conv_umma(const __grid_co
         const int j = (g - p.sa) / p.ga;
         ACCT_WAIT(0, cb + (j & (p.ncb - 1)), (uint32_t)(j / p.ncb) & 1u);
       }
+      ACCT_NOW(t_issue);
       const uint32_t a_s = smem_u32(a_base + (size_t)slot * p.a_bytes);
       const int32_t* ix = ibuf + b * kTileM;
       const __nv_bfloat16* xc = p.x + c * CH;
@@ -501,8 +503,14 @@ __global__ void __launch_bounds__((NPW + 6) * 32, 2) k_conv_umma(const __grid_co
       }
       cp_async_arrive_noinc(a_full + slot);
       cp_async_commit();
+      ACCT_ADD(1, t_issue);
+      ACCT_NOW(t_wg);
       cp_async_wait_n(1);  // group of step g - np done: the index buffer of step g + np is complete
       __syncwarp();
+      ACCT_ADD(3, t_wg);
+#ifdef MK_TRACE
+      acct[4] += 1;
+#endif
     }
     cp_async_wait_n(0);
   } else if (warp == kFwdStage) {
@@ -564,11 +572,55 @@ __global__ void __launch_bounds__((NPW + 6) * 32, 2) k_conv_umma(const __grid_co
           const uint32_t d = tb0 + (uint32_t)(i * p.cw);
           uint32_t acc = (init >> i) & 1u;
           uint32_t x = ws;
+          if (p.grp) {
+            // grouped: the nch chunk steps of this (unit, tile) as one MMA step — one fence,
+            // one elected block of nch * CH / 16 UMMAs and one commit (ga == nch) instead of
+            // nch of each (the MMA warp's per-step overhead bounds the C = 96 kernel)
+            uint32_t s2 = s, ph2 = sph;
+            for (int c = 0; c < p.nch; ++c) {
+              ACCT_WAIT(2, a_full + s2, ph2);
+              if (++s2 == (uint32_t)p.sa) {
+                s2 = 0;
+                ph2 ^= 1;
+              }
+            }
+            ACCT_NOW(t_f);
+            fence_proxy_async_smem();
+            tc_fence_after();
+            ACCT_ADD(3, t_f);
+            ACCT_NOW(t_i);
+            if (leader && !(p.dbg & 1)) {
+              uint32_t sc = s, xc = x;
+              for (int c = 0; c < p.nch; ++c) {
+                const uint32_t alo = a0 + sc * astep, blo = w0 + xc * wstep;
+#pragma unroll
+                for (int kk = 0; kk < CH / 16; ++kk)
+                  umma_f16(d, dhi | (uint64_t)(alo + kk * 2), dhi | (uint64_t)(blo + kk * 2), idesc,
+                           acc | (uint32_t)c | (uint32_t)kk);
+                if (++sc == (uint32_t)p.sa) sc = 0;
+                if (++xc == (uint32_t)p.sw) xc = 0;
+              }
+              umma_commit(cb + (ncommit & (uint32_t)(p.ncb - 1)));
+            }
+            ++ncommit;
+            __syncwarp();
+            ACCT_ADD(4, t_i);
+#ifdef MK_TRACE
+            acct[6] += p.nch;
+#endif
+            s = s2;
+            sph = ph2;
+            init |= 1u << i;
+            continue;
+          }
           for (int c = 0; c < p.nch; ++c) {
             ACCT_WAIT(2, a_full + s, sph);
+            ACCT_NOW(t_f);
             fence_proxy_async_smem();  // the cp.async (generic proxy) rows -> tcgen05 (async proxy)
             tc_fence_after();
             const uint32_t alo = a0 + s * astep, blo = w0 + x * wstep;
+            ACCT_ADD(3, t_f);
+            ACCT_NOW(t_i);
             if (leader && !(p.dbg & 1)) {
 #pragma unroll
               for (int kk = 0; kk < CH / 16; ++kk)
@@ -576,12 +628,19 @@ __global__ void __launch_bounds__((NPW + 6) * 32, 2) k_conv_umma(const __grid_co
             }
             acc = 1;
             __syncwarp();
+            ACCT_ADD(4, t_i);
+            ACCT_NOW(t_c);
             // a commit stalls the next MMAs ~250 cycles (tools/ubench_umma.cu): one per ga steps
             if (++gq == (uint32_t)p.ga) {
               if (leader) umma_commit(cb + (ncommit & (uint32_t)(p.ncb - 1)));
               ++ncommit;
               gq = 0;
             }
+            __syncwarp();
+            ACCT_ADD(5, t_c);
+#ifdef MK_TRACE
+            acct[6] += 1;
+#endif
             if (++s == (uint32_t)p.sa) {
               s = 0;
               sph ^= 1;
@@ -665,6 +724,7 @@ struct WgradParams {
   int sa, ga;                // stage slots, slots per commit group
   int wps;                   // producer warps per stage slot (each gathers 64 / wps pairs of a step)
   int a_pad;                 // A holds zeroed padding panels (else a_bytes = the real panels only)
+  int nacc;                  // TMEM accumulators per half the K steps alternate between (1 or 2)
   int pwa, pwb;              // panel widths (channels) of A (G) and B (X)
   uint32_t a_bytes, b_bytes, slot_bytes, tmem_cols;
 };
@@ -1027,20 +1087,29 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
           ACCT_NOW(t_mma);
           tc_fence_after();
           const uint32_t alo = s0 + s * sstep, blo = alo + boff;
+          ACCT_ADD(5, t_mma);
+          ACCT_NOW(t_iss);
+          // nacc = 2: the K steps alternate between two accumulators (summed by the epilogue),
+          // so consecutive UMMAs do not wait on each other's accumulator (tools/ubench_umma.cu)
           if (leader) {
 #pragma unroll
-            for (int kk = 0; kk < PS / 16; ++kk)
+            for (int kk = 0; kk < PS / 16; ++kk) {
+              const uint32_t a = p.nacc == 2 ? (uint32_t)(kk & 1) : 0u;
               for (int h = 0; h < p.halves; ++h)
-                umma_f16(tb0 + h * (uint32_t)p.c_in, ahi | (uint64_t)(alo + h * hstep + kk * ka),
-                         bhi | (uint64_t)(blo + kk * kb), idesc, acc | (uint32_t)kk);
+                umma_f16(tb0 + (a * p.halves + h) * (uint32_t)p.c_in, ahi | (uint64_t)(alo + h * hstep + kk * ka),
+                         bhi | (uint64_t)(blo + kk * kb), idesc, acc | (uint32_t)(kk >= p.nacc));
+            }
           }
           acc = 1;
           __syncwarp();
+          ACCT_ADD(3, t_iss);
+          ACCT_NOW(t_cm);
           if (++gq == (uint32_t)p.ga) {
             if (leader) umma_commit(a_empty + s / p.ga);
             gq = 0;
           }
-          ACCT_ADD(3, t_mma);
+          __syncwarp();
+          ACCT_ADD(6, t_cm);
 #ifdef MK_TRACE
           acct[4] += 1;
 #endif
@@ -1069,6 +1138,13 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
           uint32_t v[16];
           tmem_ld16(ta + col0, v);
           tmem_ld_wait();
+          if (p.nacc == 2) {  // second accumulator (odd K steps)
+            uint32_t v2[16];
+            tmem_ld16(ta + (uint32_t)(p.halves * p.c_in) + col0, v2);
+            tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = __float_as_uint(__uint_as_float(v[e]) + __uint_as_float(v2[e]));
+          }
           if (co < p.c_out) {
             float4* d4 = (float4*)(dst + col0);
 #pragma unroll
@@ -1268,6 +1344,14 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   // configs[1]): more warps issue the gathers faster than fewer warps with deeper queues
   p.np = std::min(npw, env_np > 0 ? std::min(env_np, p.sa) : p.sa);
   p.ga = p.sa % 2 == 0 ? 2 : 1;  // the W ring must hold >= ga units: sw / nch >= 2 >= ga
+  // several channel chunks: one MMA step (and commit) per (unit, tile), ga = nch (a commit then
+  // never covers steps of a later unit, so the W ring needs no more than two units)
+  static const int env_grp = [] {
+    const char* e = std::getenv("MK_FWD_GROUP");
+    return e ? std::atoi(e) : 1;
+  }();
+  p.grp = env_grp && nch > 1 && p.sa >= nch ? 1 : 0;
+  if (p.grp) p.ga = nch;
   p.ncb = ring(p.sw, p.tb, samax);
   if (p.sa < 2 || p.tmem_cols > 512)
     MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: channel counts too large for the smem pipeline");
@@ -1378,6 +1462,12 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
     }
   }
   if (p.sa >= 8) p.sa -= p.sa % 4;
+  static const int env_nacc = [] {  // development: MK_WGRAD_NACC=1 one accumulator
+    const char* e = std::getenv("MK_WGRAD_NACC");
+    return e ? std::atoi(e) : 2;
+  }();
+  p.nacc = env_nacc == 2 && per_sm * pow2_cols((uint32_t)(2 * p.halves * c_in)) <= 512 ? 2 : 1;
+  p.tmem_cols = pow2_cols((uint32_t)(p.nacc * p.halves * c_in));
   static const int env_wps = [] {  // development: MK_WGRAD_WPS=1 one producer warp per slot
     const char* e = std::getenv("MK_WGRAD_WPS");
     return e ? std::atoi(e) : 0;

@@ -33,8 +33,8 @@ a = np.zeros((32, 8), np.uint64)
 mk._L.mk_debug_acct.argtypes = [ctypes.c_void_p]
 mk._L.mk_debug_acct(a.ctypes.data)
 print(f"configs[{cfg}] C={C}; cycles of CTA 100 per warp; last col = total")
-print("producers 1-3,5-7,9-10: 0=slot-free wait 1=fnext 2=issue 3=wait_group 4=steps 5=item switch | epi 12-15: 0=acc_full wait | mma(0): 1=W wait 2=A full "
-      "wait 3=acc_empty wait 4=steps 5=fence 6=mma+commit | stager(4): 0=ring wait")
-for w in range(16):
+print("producers (warps < np): 0=slot-free wait 1=gather issue 3=wait_group 4=steps | epilogue: 0=tfull wait | "
+      "mma: 1=W wait 2=A full wait 3=fences 4=umma issue 5=commit 6=steps | stager: 0=ring wait")
+for w in range(32):
     if a[w].any():
         print(w, a[w].tolist())

@@ -34,7 +34,7 @@ a = np.zeros((32, 8), np.uint64)
 mk._L.mk_debug_acct.argtypes = [ctypes.c_void_p]
 mk._L.mk_debug_acct(a.ctypes.data)
 print(f"configs[{cfg}] C={C}; cycles of CTA 100 per warp; last col = total")
-print("producers: 0=slot-free wait 1=gather issue 2=own-data wait 3=steps | mma: 2=full wait 3=issue+commit 4=steps "
+print("producers: 0=slot-free wait 1=gather issue 2=own-data wait 3=steps | mma: 2=full wait 3=umma issue 4=steps 5=fence 6=commit "
       "| epi: 0=tfull wait")
 for w in range(21):
     if a[w].any():
