@@ -385,6 +385,9 @@ def time_steps(w, steps, warmup, stream, flush, sync_ranks=None):
     torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ph + 1)] for _ in range(steps)]
     launches0 = w.mk.kernel_launch_count()
+    import gc
+    gc.collect()
+    gc.disable()  # a collector pass inside a step would stall the host while the GPU drains
     if sync_ranks:
         sync_ranks()
     torch.cuda.synchronize()
@@ -392,10 +395,14 @@ def time_steps(w, steps, warmup, stream, flush, sync_ranks=None):
         flush.zero_()
         w.step(lambda i, e=evs[s]: e[i].record(stream))
     torch.cuda.synchronize()
+    gc.enable()
     if sync_ranks:
         sync_ranks()
     launches = w.mk.kernel_launch_count() - launches0
     ph = np.array([[evs[s][j].elapsed_time(evs[s][j + 1]) for j in range(n_ph)] for s in range(steps)])
+    if os.environ.get("MK_BENCH_STEPS"):  # development: per-step phase times (us) on stderr
+        for s in range(steps):
+            print("step", s, " ".join(f"{v * 1e3:.0f}" for v in ph[s]), file=sys.stderr)
     return ph, launches
 
 

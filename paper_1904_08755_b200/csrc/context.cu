@@ -197,6 +197,7 @@ mk_status mk_context_create(int device, mk_alloc_fn alloc, mk_free_fn free_fn, v
   mk_context* c = new mk_context();
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
+  c->l2_bytes = prop.l2CacheSize;
   c->alloc.alloc = alloc;
   c->alloc.free_fn = free_fn;
   c->alloc.user = user;

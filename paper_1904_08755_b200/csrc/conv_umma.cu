@@ -235,6 +235,7 @@ struct FwdParams {
   int sw;  // W chunk slots (a ring: W_k chunks are prefetched several offsets ahead)
   int tb;  // tiles per CTA (one TMEM accumulator each: tb * cw <= 512 columns)
   int grp;  // MMA steps cover all nch chunks of a (unit, tile)
+  int off32;  // n_src * c_x < 2^31: 32-bit element offsets in the gathers
   int fold;  // tile order (see cta_tile)
   int ncb;   // commit barriers in the ring (power of two)
   uint32_t a_bytes, b_bytes, tmem_cols;
@@ -459,7 +460,9 @@ __global__ void __launch_bounds__((NPW + 6) * 32, 2) k_conv_umma(const __grid_co
       return c;
     };
     const int np = p.np;
-    const int q4 = lane >> 3, jj = lane & (J - 1);
+    constexpr int RG = kTileM / (32 / J);  // rows per lane group (32 / J groups of J lanes)
+    const int q4 = lane / J, jj = lane & (J - 1);
+    const int c_x = p.c_x;
     // indices of the warp's first two steps
     int cq[3] = {0, 0, 0};  // channel chunk of the step whose indices sit in buffer i
     if (warp < n_steps) cq[0] = fetch_idx(warp, 0);
@@ -482,6 +485,19 @@ __global__ void __launch_bounds__((NPW + 6) * 32, 2) k_conv_umma(const __grid_co
       const int32_t* ix = ibuf + b * kTileM;
       const __nv_bfloat16* xc = p.x + c * CH;
       if (p.dbg & 2) {
+      } else if (p.off32) {
+        // lane group q4 = lane / J owns rows [q4 RG, q4 RG + RG), lane jj its 16-byte column:
+        // one 16-byte index load per 4 rows, 32-bit element offsets, ignore-src zero fill
+#pragma unroll 2
+        for (int i = 0; i < RG; i += 4) {
+          const int4 a4 = *(const int4*)(ix + q4 * RG + i);
+          const int av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int r = q4 * RG + i + e;
+            cp_async16_z(a_s + swz(r, jj, RB), xc + ((uint32_t)max(av[e], 0) * (uint32_t)c_x + jj * 8), av[e] < 0);
+          }
+        }
       } else if (J == 8) {
 #pragma unroll 2
         for (int i = 0; i < 32; i += 4) {
@@ -725,6 +741,9 @@ struct WgradParams {
   int wps;                   // producer warps per stage slot (each gathers 64 / wps pairs of a step)
   int a_pad;                 // A holds zeroed padding panels (else a_bytes = the real panels only)
   int nacc;                  // TMEM accumulators per half the K steps alternate between (1 or 2)
+  int off32;                 // n_out * c_out and n_in * c_in < 2^31: 32-bit element offsets
+  unsigned* gsync;           // strided plan: per-epoch arrival counters (zeroed), or nullptr
+  int sync_b, sync_s, sync_emax;  // rounds per epoch, epochs of slack, counter capacity
   int pwa, pwb;              // panel widths (channels) of A (G) and B (X)
   uint32_t a_bytes, b_bytes, slot_bytes, tmem_cols;
 };
@@ -781,7 +800,7 @@ constexpr int kMaxSegs = kWgradMaxSegs + 1;  // per-CTA plan capacity (kmap_wpla
 // partial dW_k tile of the segment's slot.
 // NP producer warps (>= the stage slots in use); NP = 16: one CTA per SM; NP = 8: two CTAs
 // per SM; NP = 4: three (shared memory split accordingly).
-template <int NP>
+template <int NP, bool P3>  // P3: the period-3 gather path is compiled in (C = 48 / 96 operands)
 __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
     k_wgrad_umma(const __grid_constant__ WgradParams p) {
   constexpr int kEpiWarp0 = NP;                    // epilogue warps (TMEM lane quarters 0-3)
@@ -800,6 +819,7 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
   uint64_t* tfull = a_empty + p.sa;
   uint64_t* tempty = tfull + 1;
   uint32_t* tmem_slot = (uint32_t*)(tempty + 1);
+  volatile int* s_sync = (volatile int*)(tmem_slot + 1);  // [epochs, allowed epochs, MMA steps done]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rba = p.pwa * 2, rbb = p.pwb * 2;             // panel row bytes
   const int npa = p.c_out / p.pwa, npb = p.c_in / p.pwb;  // real panels
@@ -871,6 +891,18 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
       }
       __syncwarp();
       if (lane == 0) *s_nseg = nseg;
+      // Epoch throttle: the CTAs drift apart over ~1000 rounds (one chunk each), which widens
+      // the window of rows read at once beyond L2.  With gsync, every CTA arrives at a global
+      // counter after each epoch of sync_b rounds and its producers stay within sync_s epochs of
+      // the last epoch all CTAs completed (all CTAs are co-resident: grid = CTAs per SM x SMs).
+      int rounds = J > 0 ? (int)((ck + J - 1) / J) : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) rounds = max(rounds, __shfl_xor_sync(0xffffffffu, rounds, o));
+      if (lane == 0) {
+        s_sync[0] = p.gsync ? min((rounds + p.sync_b - 1) / p.sync_b, p.sync_emax) : 0;
+        s_sync[1] = p.gsync ? p.sync_s + 1 : INT_MAX;
+        s_sync[2] = 0;
+      }
     } else if (p.segs) {  // host plan (kmap_wplan)
       const int sb = p.seg_begin[blockIdx.x], se = min(p.seg_begin[blockIdx.x + 1], sb + kMaxSegs);
       nseg = se - sb;
@@ -912,6 +944,11 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
     }
   }
   if (threadIdx.x == 32) {
+    if (p.mode != 2) {
+      s_sync[0] = 0;
+      s_sync[1] = INT_MAX;
+      s_sync[2] = 0;
+    }
     for (int s = 0; s < p.sa; ++s) {
       mbar_init(a_full + s, p.wps);
       mbar_init(a_empty + s, 1);
@@ -984,12 +1021,43 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
     }
     uint32_t my = 0, ib = 0;
     const int ca = p.c_out / 8, cb = p.c_in / 8;  // 16-byte chunks per G row / X row
-    const int ja = rba / 16, jb = rbb / 16;       // chunks per panel row
+    const __nv_bfloat16* const g_base = p.g;
+    const __nv_bfloat16* const x_base = p.x;
+    const int c_out_r = p.c_out, c_in_r = p.c_in;
+    const int ja = rba / 16, jb = rbb / 16;       // chunks per panel row (2, 4 or 8)
+    const int lja = __ffs(ja) - 1, ljb = __ffs(jb) - 1;  // (panel = chunk >> l: no integer division)
+    // Period-3 path (96 % c8 == 0, 96 / c8 rows a multiple of 8: C = 48, 96): three warp
+    // instructions cover 96 / c8 whole rows, and since the swizzle pattern repeats every 8 rows
+    // each lane's (row, smem offset, source offset) triple per instruction is fixed: ~6
+    // instructions per 16-byte copy instead of ~30 with the running (row, chunk) carry.
+    struct Per3 {
+      int r[3], d[3], c[3];
+      int rows;
+    };
+    auto per3 = [&](int c8, int jx, int ljx, uint32_t panel, int rbx) {
+      Per3 t;
+      t.rows = 0;
+      if (P3 && p.off32 && c8 > 0 && (32 % c8) != 0 && 96 % c8 == 0 && (96 / c8) % 8 == 0) {
+        t.rows = 96 / c8;
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          const int q = lane + 32 * i, r = q / c8, ch = q - r * c8;
+          t.r[i] = r;
+          t.c[i] = ch * 8;
+          t.d[i] = (int)((uint32_t)(ch >> ljx) * panel + swz((uint32_t)r, (uint32_t)(ch & (jx - 1)), (uint32_t)rbx));
+        }
+      }
+      return t;
+    };
+    const Per3 pa3 = per3(c_out_r / 8, ja, lja, panel_a, rba), pb3 = per3(c_in_r / 8, jb, ljb, panel_b, rbb);
     for (; g < n_steps; g += p.sa) {
       const bool have_n = g + p.sa < n_steps;
       if (have_n) {
         locate(g + p.sa, &b0n, &en);
         fetch_idx(b0n, en, ib ^ 1);
+      }
+      if (g / p.sync_b >= s_sync[1]) {  // epoch throttle (strided plan)
+        while (g / p.sync_b >= s_sync[1]) __nanosleep(128);
       }
       ACCT_WAIT(0, a_empty + slot / p.ga, (my & 1) ^ 1);
       ACCT_NOW(t_issue);
@@ -998,7 +1066,17 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
       const int32_t* ii = oi + PS;
       // G rows -> A panels, X rows -> B panels.  Fast path when a row's chunk count divides
       // the warp: each lane keeps one chunk column (no per-element divisions).
-      if ((32 % ca) == 0) {
+      if (P3 && pa3.rows) {
+        for (int R0 = pr0; R0 < pr1; R0 += pa3.rows) {
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            const int pr = R0 + pa3.r[i];
+            const bool v = b0 + pr < e;
+            const uint32_t row = v ? (uint32_t)oi[pr] : 0u;  // (32-bit element offsets: host-checked)
+            cp_async16_z(a_s + (uint32_t)(R0 * rba + pa3.d[i]), g_base + (row * (uint32_t)c_out_r + pa3.c[i]), !v);
+          }
+        }
+      } else if ((32 % ca) == 0) {
         const int ch = lane % ca, pa = ch / ja, j = ch - pa * ja;
         const __nv_bfloat16* src = p.g + ch * 8;
         const uint32_t dst0 = a_s + pa * panel_a;
@@ -1011,10 +1089,13 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
       } else {  // consecutive lanes take consecutive 16-byte chunks (whole sectors per row)
         int pr = pr0 + lane / ca, ch = lane - (lane / ca) * ca;
         const int dpr = 32 / ca, dch = 32 - dpr * ca;
+        const __nv_bfloat16* const gsrc = g_base;  // registers: the asm memory clobbers would reload params
+        const int cst = c_out_r;
+#pragma unroll 2
         for (; pr < pr1;) {
-          const int pa = ch / ja, j = ch - pa * ja;
+          const int pa = ch >> lja, j = ch & (ja - 1);
           const uint32_t dst = a_s + pa * panel_a + swz(pr, j, rba);
-          if (b0 + pr < e) cp_async16(dst, p.g + (int64_t)oi[pr] * p.c_out + ch * 8, 16u);
+          if (b0 + pr < e) cp_async16(dst, gsrc + (int64_t)oi[pr] * cst + ch * 8, 16u);
           else st_shared_zero16(dst);
           pr += dpr;
           ch += dch;
@@ -1024,7 +1105,17 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
           }
         }
       }
-      if ((32 % cb) == 0) {
+      if (P3 && pb3.rows) {
+        for (int R0 = pr0; R0 < pr1; R0 += pb3.rows) {
+#pragma unroll
+          for (int i = 0; i < 3; ++i) {
+            const int pr = R0 + pb3.r[i];
+            const bool v = b0 + pr < e;
+            const uint32_t row = v ? (uint32_t)ii[pr] : 0u;
+            cp_async16_z(b_s + (uint32_t)(R0 * rbb + pb3.d[i]), x_base + (row * (uint32_t)c_in_r + pb3.c[i]), !v);
+          }
+        }
+      } else if ((32 % cb) == 0) {
         const int ch = lane % cb, pb = ch / jb, j = ch - pb * jb;
         const __nv_bfloat16* src = p.x + ch * 8;
         const uint32_t dst0 = b_s + pb * panel_b;
@@ -1037,10 +1128,13 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
       } else {
         int pr = pr0 + lane / cb, ch = lane - (lane / cb) * cb;
         const int dpr = 32 / cb, dch = 32 - dpr * cb;
+        const __nv_bfloat16* const xsrc = x_base;
+        const int cst = c_in_r;
+#pragma unroll 2
         for (; pr < pr1;) {
-          const int pb = ch / jb, j = ch - pb * jb;
+          const int pb = ch >> ljb, j = ch & (jb - 1);
           const uint32_t dst = b_s + pb * panel_b + swz(pr, j, rbb);
-          if (b0 + pr < e) cp_async16(dst, p.x + (int64_t)ii[pr] * p.c_in + ch * 8, 16u);
+          if (b0 + pr < e) cp_async16(dst, xsrc + (int64_t)ii[pr] * cst + ch * 8, 16u);
           else st_shared_zero16(dst);
           pr += dpr;
           ch += dch;
@@ -1108,6 +1202,7 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
             if (leader) umma_commit(a_empty + s / p.ga);
             gq = 0;
           }
+          if (leader) s_sync[2] = q + 1;  // steps consumed (the epoch throttle's progress)
           __syncwarp();
           ACCT_ADD(6, t_cm);
 #ifdef MK_TRACE
@@ -1124,6 +1219,30 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
     }
   } else if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kEpiWarps) {
     const int q = warp & 3;
+    if (warp == kEpiWarp0 && lane == 0 && s_sync[0] > 0) {
+      // epoch throttle: arrive after each local epoch, open the next epochs once all CTAs
+      // arrived; bounded spins (a wait that never ends disables the throttle instead)
+      const int E = s_sync[0];
+      long long spins = 0;
+      for (int e = 0; e < E; ++e) {
+        const int target = min((e + 1) * p.sync_b, n_steps);
+        while (s_sync[2] < target) __nanosleep(256);
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.gsync + e) : "memory");
+        unsigned v;
+        for (;;) {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.gsync + e) : "memory");
+          if (v >= gridDim.x || ++spins > (1LL << 22)) break;
+          __nanosleep(128);
+        }
+        if (v < gridDim.x) {
+          s_sync[1] = INT_MAX;
+          break;
+        }
+        s_sync[1] = e + 2 + p.sync_s;
+      }
+      s_sync[1] = INT_MAX;
+    }
+    __syncwarp();
     for (int i = 0; i < nseg; ++i) {
       const int4 sg = s_segs[i];
       ACCT_WAIT(0, tfull, i & 1);
@@ -1247,7 +1366,6 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
                             int c_in_w, int c_out_w, void* y, int c_y, mk_dtype out_dt, int64_t n_rows, bool trans,
                             cudaStream_t s, const Epilogue& ep) {
   if (n_rows == 0) return MK_OK;
-  (void)n_src;
   if (nb.K > kMaxK) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 conv: more than 128 kernel offsets");
   const int CH = c_x % 64 == 0 ? 64 : c_x % 32 == 0 ? 32 : 16;
   const int nch = c_x / CH;
@@ -1261,6 +1379,7 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   p.c_y = c_y;
   p.nch = nch;
   p.out_f32 = out_dt == MK_F32;
+  p.off32 = n_src * (int64_t)c_x < INT32_MAX;
   p.ep = ep;
   static const int dbg = [] {
     const char* e = std::getenv("MK_DEBUG_CONV");
@@ -1396,6 +1515,11 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   }
   const int64_t te = (int64_t)c_out * c_in;
   WgradParams p;
+  p.off32 = (int64_t)m->n_out * c_out < INT32_MAX && (int64_t)m->n_in * c_in < INT32_MAX;
+  p.gsync = nullptr;  // (epoch throttle off unless the strided plan sets it up below)
+  p.sync_b = 1;
+  p.sync_s = 0;
+  p.sync_emax = 0;
   p.g = (const __nv_bfloat16*)g;
   p.x = (const __nv_bfloat16*)x;
   p.in_idx = m->in_idx;
@@ -1494,17 +1618,43 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
       // (first CTA, CTAs) table of the strided plan
       const int64_t slots = p.mode == 2 ? n_cta : n_cta + m->K;
       const size_t pbytes = ((sizeof(float) * slots * te + 255) & ~size_t(255));
-      part = (float*)dev_alloc(ctx->alloc, pbytes + sizeof(int32_t) * 2 * m->K, s);
+      // epoch throttle of the strided plan (rounds per epoch, slack in epochs): counters for
+      // an upper bound of the epochs (rounds <= chunks / spare CTAs + 2)
+      static const int env_sync[3] = {
+          [] { const char* e = std::getenv("MK_WGRAD_SYNC"); return e ? std::atoi(e) : 1; }(),
+          [] { const char* e = std::getenv("MK_WGRAD_SYNCB"); return e ? std::max(1, std::atoi(e)) : 8; }(),
+          [] { const char* e = std::getenv("MK_WGRAD_SYNCS"); return e ? std::max(0, std::atoi(e)) : 2; }()};
+      const int64_t spare = (int64_t)n_cta - m->K;
+      int emax = 0;
+      // only when the gathered features exceed L2 (configs[4]: cold-L2 DRAM reads 4.8 -> 2.5 GB
+      // per launch, time unchanged; on L2-resident maps it costs a few us)
+      const bool big = ((int64_t)m->n_in * c_in + (int64_t)m->n_out * c_out) * 2 > (int64_t)ctx->l2_bytes / 2;
+      if (p.mode == 2 && env_sync[0] && spare > 0 && (big || env_sync[0] == 2)) {
+        const int64_t chunks = (int64_t)m->K * m->n_out / kPairsPerStage + m->K;
+        emax = (int)std::min<int64_t>(1 << 20, (chunks / spare + 2) / env_sync[1] + 2);
+      }
+      const size_t jbytes = ((sizeof(int32_t) * 2 * m->K + 255) & ~size_t(255));
+      part = (float*)dev_alloc(ctx->alloc, pbytes + jbytes + sizeof(unsigned) * emax, s);
       if (!part) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 wgrad: workspace allocation failed");
       p.part = part;
       p.jtab = (int32_t*)((uint8_t*)part + pbytes);
+      p.gsync = emax > 0 ? (unsigned*)((uint8_t*)part + pbytes + jbytes) : nullptr;
+      p.sync_b = env_sync[1];
+      p.sync_s = env_sync[2];
+      p.sync_emax = emax;
+      if (emax > 0) {
+        const cudaError_t z = cudaMemsetAsync(p.gsync, 0, sizeof(unsigned) * emax, s);
+        if (z != cudaSuccess) MK_FAIL(MK_ERR_CUDA, "bf16 wgrad: memset failed");
+      }
       auto go = [&](auto kern, int threads) {
         set_smem_once(kern, smem);
         pdl_launch(kern, n_cta, threads, smem, s, p);
       };
-      if (np == 16) go(k_wgrad_umma<16>, (16 + kEpiWarps + 1) * 32);
-      else if (np == 8) go(k_wgrad_umma<8>, (8 + kEpiWarps + 1) * 32);
-      else go(k_wgrad_umma<4>, (4 + kEpiWarps + 1) * 32);
+      auto per3 = [](int c) { const int c8 = c / 8; return c8 > 0 && 32 % c8 != 0 && 96 % c8 == 0 && (96 / c8) % 8 == 0; };
+      const bool p3 = p.off32 && (per3(c_out) || per3(c_in));
+      if (np == 16) p3 ? go(k_wgrad_umma<16, true>, (16 + kEpiWarps + 1) * 32) : go(k_wgrad_umma<16, false>, (16 + kEpiWarps + 1) * 32);
+      else if (np == 8) p3 ? go(k_wgrad_umma<8, true>, (8 + kEpiWarps + 1) * 32) : go(k_wgrad_umma<8, false>, (8 + kEpiWarps + 1) * 32);
+      else p3 ? go(k_wgrad_umma<4, true>, (4 + kEpiWarps + 1) * 32) : go(k_wgrad_umma<4, false>, (4 + kEpiWarps + 1) * 32);
       dim3 rg((unsigned)ceil_div(te, 256), (unsigned)m->K);
       if (p.mode == 2)
         pdl_launch(k_reduce_partials_jtab, rg, 256, 0, s, (const int32_t*)p.jtab, m->K, (const float*)part, te, dW);
@@ -1519,8 +1669,8 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
       part = (float*)dev_alloc(ctx->alloc, sizeof(float) * m->n_wslots * te, s);
       if (!part) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 wgrad: workspace allocation failed");
       p.part = part;
-      set_smem_once(k_wgrad_umma<16>, smem);
-      pdl_launch(k_wgrad_umma<16>, m->n_wcta, (16 + kEpiWarps + 1) * 32, smem, s, p);
+      set_smem_once(k_wgrad_umma<16, false>, smem);
+      pdl_launch(k_wgrad_umma<16, false>, m->n_wcta, (16 + kEpiWarps + 1) * 32, smem, s, p);
     }
     dim3 rg((unsigned)ceil_div(te, 256), (unsigned)m->K);
     k_reduce_partials<<<rg, 256, 0, s>>>(m->wslot_begin, part, te, dW);

@@ -301,6 +301,7 @@ struct Mailbox;  // host-mapped result slot (below)
 struct mk_context {
   int device = 0;
   int num_sms = 148;
+  int64_t l2_bytes = 126 << 20;  // device L2 size (cudaDeviceProp::l2CacheSize)
   mk::Alloc alloc;
   cudaStream_t aux = nullptr;  // private non-blocking stream for small lazy read-backs
   cudaStream_t side = nullptr;  // private non-blocking stream: map-build work forked off the caller's stream
