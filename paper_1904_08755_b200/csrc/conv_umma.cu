@@ -560,7 +560,6 @@ __global__ void __launch_bounds__((NPW + 6) * 32, 2) k_conv_umma(const __grid_co
     // a constant high part | (smem address >> 4); slot / phase counters are incremental;
     // one commit per group of ga stage slots.
     {
-      const bool leader = lane == 0;
       const uint32_t idesc = idesc_bf16(kTileM, (uint32_t)cwj, 0, 0);
       const uint64_t dhi = smem_desc(0, 16, 8 * RB, layout_code(RB));
       const uint32_t a0 = __shfl_sync(0xffffffffu, smem_u32(a_base) >> 4, 0), astep = p.a_bytes >> 4;
@@ -605,7 +604,7 @@ __global__ void __launch_bounds__((NPW + 6) * 32, 2) k_conv_umma(const __grid_co
             tc_fence_after();
             ACCT_ADD(3, t_f);
             ACCT_NOW(t_i);
-            if (leader && !(p.dbg & 1)) {
+            if (elect_one() && !(p.dbg & 1)) {
               uint32_t sc = s, xc = x;
               for (int c = 0; c < p.nch; ++c) {
                 const uint32_t alo = a0 + sc * astep, blo = w0 + xc * wstep;
@@ -637,7 +636,7 @@ __global__ void __launch_bounds__((NPW + 6) * 32, 2) k_conv_umma(const __grid_co
             const uint32_t alo = a0 + s * astep, blo = w0 + x * wstep;
             ACCT_ADD(3, t_f);
             ACCT_NOW(t_i);
-            if (leader && !(p.dbg & 1)) {
+            if (elect_one() && !(p.dbg & 1)) {
 #pragma unroll
               for (int kk = 0; kk < CH / 16; ++kk)
                 umma_f16(d, dhi | (uint64_t)(alo + kk * 2), dhi | (uint64_t)(blo + kk * 2), idesc, acc | (uint32_t)kk);
@@ -648,7 +647,7 @@ __global__ void __launch_bounds__((NPW + 6) * 32, 2) k_conv_umma(const __grid_co
             ACCT_NOW(t_c);
             // a commit stalls the next MMAs ~250 cycles (tools/ubench_umma.cu): one per ga steps
             if (++gq == (uint32_t)p.ga) {
-              if (leader) umma_commit(cb + (ncommit & (uint32_t)(p.ncb - 1)));
+              if (elect_one()) umma_commit(cb + (ncommit & (uint32_t)(p.ncb - 1)));
               ++ncommit;
               gq = 0;
             }
@@ -671,7 +670,7 @@ __global__ void __launch_bounds__((NPW + 6) * 32, 2) k_conv_umma(const __grid_co
             wph ^= 1;
           }
       }
-      if (leader && n_steps > 0) umma_commit(tfull);
+      if (n_steps > 0 && elect_one()) umma_commit(tfull);
       __syncwarp();
     }
   } else if (warp >= kFwdEpi0 && warp < kFwdEpi0 + 4) {
@@ -1185,7 +1184,7 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
           ACCT_NOW(t_iss);
           // nacc = 2: the K steps alternate between two accumulators (summed by the epilogue),
           // so consecutive UMMAs do not wait on each other's accumulator (tools/ubench_umma.cu)
-          if (leader) {
+          if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < PS / 16; ++kk) {
               const uint32_t a = p.nacc == 2 ? (uint32_t)(kk & 1) : 0u;
@@ -1199,7 +1198,7 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
           ACCT_ADD(3, t_iss);
           ACCT_NOW(t_cm);
           if (++gq == (uint32_t)p.ga) {
-            if (leader) umma_commit(a_empty + s / p.ga);
+            if (elect_one()) umma_commit(a_empty + s / p.ga);
             gq = 0;
           }
           if (leader) s_sync[2] = q + 1;  // steps consumed (the epoch throttle's progress)
@@ -1213,7 +1212,7 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
             sph ^= 1;
           }
         }
-        if (leader) umma_commit(tfull);
+        if (elect_one()) umma_commit(tfull);
         __syncwarp();
       }
     }
