@@ -36,6 +36,31 @@ void* dev_alloc(const Alloc& a, size_t bytes, cudaStream_t s) {
   return p;
 }
 
+void* scratch_acquire(mk_context* ctx, size_t bytes, cudaStream_t s) {
+  ctx->scratch_mu.lock();
+  if (ctx->scratch_cap < bytes) {
+    if (ctx->scratch) dev_free(ctx->alloc, ctx->scratch, ctx->scratch_stream ? ctx->scratch_stream : s);
+    const size_t cap = bytes + bytes / 4;
+    ctx->scratch = dev_alloc(ctx->alloc, cap, s);
+    ctx->scratch_cap = ctx->scratch ? cap : 0;
+    ctx->scratch_stream = s;
+    if (!ctx->scratch) {
+      ctx->scratch_mu.unlock();
+      return nullptr;
+    }
+  } else if (ctx->scratch_stream && ctx->scratch_stream != s) {
+    cudaStreamWaitEvent(s, ctx->scratch_ev, 0);  // the previous user's kernels are done with it
+  }
+  return ctx->scratch;
+}
+
+void scratch_release(mk_context* ctx, cudaStream_t s) {
+  if (!ctx->scratch_ev) cudaEventCreateWithFlags(&ctx->scratch_ev, cudaEventDisableTiming);
+  cudaEventRecord(ctx->scratch_ev, s);
+  ctx->scratch_stream = s;
+  ctx->scratch_mu.unlock();
+}
+
 void dev_free(const Alloc& a, void* p, cudaStream_t s) {
   if (!p) return;
   if (a.free_fn) {
@@ -193,6 +218,21 @@ mk_status mk_context_create(int device, mk_alloc_fn alloc, mk_free_fn free_fn, v
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
     uint64_t thr = UINT64_MAX;
     cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    // Reserve pool memory up front (allocate + free once; the threshold keeps it mapped): the
+    // per-call handles and temporaries of a step (tables, maps, partials: ~2-3 GB at configs[4])
+    // then never make the pool map new memory inside a step, which stalled the host for
+    // 0.3-66 ms when sizes and lifetimes fragmented it.  MK_POOL_RESERVE_MB overrides (0: off).
+    const char* e = std::getenv("MK_POOL_RESERVE_MB");
+    const size_t mb = e ? (size_t)std::atoll(e) : (size_t)8192;
+    if (mb > 0 && (size_t)prop.totalGlobalMem > 4 * (mb << 20)) {
+      void* p = nullptr;
+      if (cudaMallocAsync(&p, mb << 20, 0) == cudaSuccess) {
+        cudaFreeAsync(p, 0);
+        cudaStreamSynchronize(0);
+      } else {
+        cudaGetLastError();
+      }
+    }
   }
   mk_context* c = new mk_context();
   c->device = device;
@@ -222,6 +262,11 @@ void mk_context_destroy(mk_context* ctx) {
   if (ctx->mb_ring) cudaFreeHost(ctx->mb_ring);
   if (ctx->aux) cudaStreamDestroy(ctx->aux);
   if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->scratch) {
+    cudaDeviceSynchronize();
+    mk::dev_free(ctx->alloc, ctx->scratch, nullptr);
+  }
+  if (ctx->scratch_ev) cudaEventDestroy(ctx->scratch_ev);
   delete ctx;
 }
 

@@ -134,7 +134,10 @@ mk_status mk_conv_backward(mk_context* ctx, const mk_kmap* m, const void* d_gout
                            const void* d_w, int32_t c_in, int32_t c_out, mk_dtype dt, void* d_gin, float* d_gw,
                            void* stream) {
   clear_error();
-  return backward_impl(ctx, m, d_gout, d_fin, d_w, c_in, c_out, dt, d_gin, d_gw, (cudaStream_t)stream);
+  HostTimer ht("conv_backward");
+  const mk_status st = backward_impl(ctx, m, d_gout, d_fin, d_w, c_in, c_out, dt, d_gin, d_gw, (cudaStream_t)stream);
+  ht.mark("impl");
+  return st;
 }
 
 mk_status mk_conv_transpose_forward(mk_context* ctx, const mk_kmap* m, const void* d_fin, int32_t c_in,

@@ -35,14 +35,7 @@ namespace {
 using namespace sm100;
 
 constexpr int kTileM = 128;
-// Random 128-byte row gathers are latency bound per warp: B200 reaches ~5 TB/s with 8
-// issuing warps per SM and >12 TB/s with 32 (tools/ubench_gather.cu), so the gather
-// producers are 16 warps.
-constexpr int kProdWarps = 16;                    // wgrad producers
-constexpr int kEpiWarps = 4;
-constexpr int kEpiWarp0 = 16;                     // epilogue warps 16-19 (TMEM lane quarters 0-3)
-constexpr int kMmaWarp = kEpiWarp0 + kEpiWarps;   // warp 20
-constexpr int kThreads = (kMmaWarp + 1) * 32;     // 672 (weight-gradient kernel)
+constexpr int kEpiWarps = 4;  // epilogue warps (TMEM lane quarters 0-3) of both kernels
 // Forward / dgrad kernel: small CTAs (2 per SM co-reside, the hardware scheduler balances
 // the bitmask-sorted tiles, whose work varies ~4x): 4 gather warps, 4 epilogue warps, the
 // MMA warp and the W stager.
@@ -91,71 +84,6 @@ __global__ void k_pack_w(const __nv_bfloat16* __restrict__ W, int K, int c_out, 
 }
 
 // ------------------------------------------------------------------ forward / dgrad
-__device__ __forceinline__ int tile_active_count(const NbrView& nb, int64_t tile) {
-  int n = 0;
-  for (int w = 0; w < nb.mw; ++w) n += __popc(__ldg(nb.mask + tile * nb.mw + w));
-  return n;
-}
-
-__device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t n) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-
-// Enumerates the (tile, mask word) units of a CTA in processing order: tiles blockIdx.x,
-// blockIdx.x + gridDim.x, ...; inside a tile the words with at least one active offset.
-struct UnitIter {
-  const uint32_t* mask;
-  int64_t ntiles;
-  int mw;
-  int64_t tile;
-  int w;
-  uint32_t bits;
-  __device__ UnitIter(const NbrView& nb, int64_t ntiles_) : mask(nb.mask), ntiles(ntiles_), mw(nb.mw) {
-    tile = blockIdx.x;
-    w = -1;
-    bits = 0;
-  }
-  __device__ __forceinline__ bool next() {
-    while (true) {
-      if (++w >= mw) {
-        w = 0;
-        tile += gridDim.x;
-      }
-      if (tile >= ntiles) return false;
-      bits = __ldg(mask + tile * mw + w);
-      if (bits) return true;
-    }
-  }
-};
-
-// Per-warp completion signalling for cp.async stages: every stage a warp issues is one
-// cp.async group; once `lag` newer groups exist, the oldest is waited for, made visible to
-// the async proxy (the tensor cores read it) and announced with ONE arrival per warp on the
-// stage's full barrier (instead of one arrival per thread).
-struct StageSignal {
-  int lag, pending;
-  uint32_t s, S;
-  __device__ StageSignal(int lag_, uint32_t S_) : lag(lag_), pending(0), s(0), S(S_) {}
-  __device__ __forceinline__ void arrive_oldest(uint64_t* full) {
-    fence_proxy_async_smem();
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(full + s);
-    if (++s == S) s = 0;
-    --pending;
-  }
-  __device__ __forceinline__ void issued(uint64_t* full) {
-    cp_async_commit();
-    if (++pending > lag) {
-      cp_async_wait_n(lag);
-      arrive_oldest(full);
-    }
-  }
-  __device__ __forceinline__ void drain(uint64_t* full) {
-    cp_async_wait_n(0);
-    while (pending > 0) arrive_oldest(full);
-  }
-};
-
 #ifdef MK_TRACE
 __device__ unsigned long long g_trace[4][8192];
 __device__ __forceinline__ unsigned long long gtime() {
@@ -204,20 +132,6 @@ __device__ unsigned long long g_cta[4096][4];  // per-CTA [start ns, end ns, smi
   do {                    \
   } while (0)
 #endif
-
-constexpr int kNbrBuf = 32 * kTileM;  // int32 entries per staging buffer (32 offsets x 128 rows)
-
-// Bulk-copies (TMA engine) the neighbour indices of unit `u` — 128 rows per active offset,
-// one 512-byte row segment each — into a staging buffer; completion on `bar`.
-__device__ __forceinline__ void stage_nbr(const NbrView& nb, const UnitIter& u, int32_t* buf, uint64_t* bar) {
-  mbar_arrive_expect_tx(bar, (uint32_t)__popc(u.bits) * kTileM * 4);
-  uint32_t bits = u.bits;
-  for (int j = 0; bits; ++j) {
-    const int k = u.w * 32 + __ffs(bits) - 1;
-    bits &= bits - 1;
-    bulk_g2s(buf + j * kTileM, nb.tab + (int64_t)nb.kk(k) * nb.n + u.tile * kTileM, kTileM * 4, bar);
-  }
-}
 
 struct FwdParams {
   const __nv_bfloat16* x;  // [n_src][c_x]
@@ -821,7 +735,7 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
   volatile int* s_sync = (volatile int*)(tmem_slot + 1);  // [epochs, allowed epochs, MMA steps done]
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int rba = p.pwa * 2, rbb = p.pwb * 2;             // panel row bytes
-  const int npa = p.c_out / p.pwa, npb = p.c_in / p.pwb;  // real panels
+  const int npa = p.c_out / p.pwa;  // real A panels
   const uint32_t panel_a = PS * rba, panel_b = PS * rbb;  // panel strides (LBO)
 
   pdl_enter();
@@ -1283,40 +1197,6 @@ __global__ void __launch_bounds__((NP + 5) * 32, NP >= 16 ? 1 : NP >= 8 ? 2 : 3)
   if (warp == kMmaWarp) tmem_dealloc(tbase, p.tmem_cols);
 }
 
-// ------------------------------------------------------------------ host: tensor maps
-typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
-                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
-                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiledFn encode_fn() {
-  static EncodeTiledFn fn = [] {
-    void* f = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      f = nullptr;
-    return (EncodeTiledFn)f;
-  }();
-  return fn;
-}
-
-// A [rows][cols] bf16 row-major tensor viewed for row gathers: box {box_cols, 1}, swizzle
-// matching a K-major / MN-major UMMA panel of box_cols * 2 bytes; out-of-range rows
-// (index -1) are zero-filled by the TMA unit.
-bool make_row_map(CUtensorMap* m, const void* base, int64_t rows, int cols, int box_cols) {
-  EncodeTiledFn fn = encode_fn();
-  if (!fn || ((uintptr_t)base & 15) || rows < 1) return false;
-  const cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  const cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
-  const cuuint32_t box[2] = {(cuuint32_t)box_cols, 1};
-  const cuuint32_t es[2] = {1, 1};
-  const CUtensorMapSwizzle sw = box_cols * 2 == 128 ? CU_TENSOR_MAP_SWIZZLE_128B
-                                : box_cols * 2 == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
-                                                     : CU_TENSOR_MAP_SWIZZLE_32B;
-  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
 
 uint32_t pow2_cols(uint32_t c) {
   uint32_t r = 32;
@@ -1507,6 +1387,7 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
                             float* dW, cudaStream_t s) {
   // K <= 63: the split-K plan is computed by the kernel from the device CSR offsets (no host
   // read-back, fully asynchronous); larger K: the host plan caps the segments per CTA.
+  HostTimer ht("wgrad_bf16");
   const bool dev_plan = m->K <= kWgradMaxSegs;
   if (!dev_plan) {
     const mk_status pst = kmap_wplan(m, s);  // built once per map, on first use
@@ -1605,6 +1486,7 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
   if (p.sa < 2 || p.tmem_cols > 512) MK_FAIL(MK_ERR_UNSUPPORTED, "bf16 wgrad: channel counts too large");
   const int smem = p.sa * (int)p.slot_bytes + reserve;
   float* part = nullptr;
+  bool scratch = false;  // part is the context's scratch buffer (held until released below)
   static const int env_mode = [] {  // development: MK_WGRAD_PLAN=0 contiguous ranges, 2 strided
     const char* e = std::getenv("MK_WGRAD_PLAN");
     return e ? std::atoi(e) : 2;
@@ -1633,8 +1515,11 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
         emax = (int)std::min<int64_t>(1 << 20, (chunks / spare + 2) / env_sync[1] + 2);
       }
       const size_t jbytes = ((sizeof(int32_t) * 2 * m->K + 255) & ~size_t(255));
-      part = (float*)dev_alloc(ctx->alloc, pbytes + jbytes + sizeof(unsigned) * emax, s);
+      ht.mark("plan");
+      part = (float*)scratch_acquire(ctx, pbytes + jbytes + sizeof(unsigned) * emax, s);
+      ht.mark("alloc");
       if (!part) MK_FAIL(MK_ERR_OUT_OF_MEMORY, "bf16 wgrad: workspace allocation failed");
+      scratch = true;
       p.part = part;
       p.jtab = (int32_t*)((uint8_t*)part + pbytes);
       p.gsync = emax > 0 ? (unsigned*)((uint8_t*)part + pbytes + jbytes) : nullptr;
@@ -1643,7 +1528,10 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
       p.sync_emax = emax;
       if (emax > 0) {
         const cudaError_t z = cudaMemsetAsync(p.gsync, 0, sizeof(unsigned) * emax, s);
-        if (z != cudaSuccess) MK_FAIL(MK_ERR_CUDA, "bf16 wgrad: memset failed");
+        if (z != cudaSuccess) {
+          scratch_release(ctx, s);
+          MK_FAIL(MK_ERR_CUDA, "bf16 wgrad: memset failed");
+        }
       }
       auto go = [&](auto kern, int threads) {
         set_smem_once(kern, smem);
@@ -1654,6 +1542,7 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
       if (np == 16) p3 ? go(k_wgrad_umma<16, true>, (16 + kEpiWarps + 1) * 32) : go(k_wgrad_umma<16, false>, (16 + kEpiWarps + 1) * 32);
       else if (np == 8) p3 ? go(k_wgrad_umma<8, true>, (8 + kEpiWarps + 1) * 32) : go(k_wgrad_umma<8, false>, (8 + kEpiWarps + 1) * 32);
       else p3 ? go(k_wgrad_umma<4, true>, (4 + kEpiWarps + 1) * 32) : go(k_wgrad_umma<4, false>, (4 + kEpiWarps + 1) * 32);
+      ht.mark("launch");
       dim3 rg((unsigned)ceil_div(te, 256), (unsigned)m->K);
       if (p.mode == 2)
         pdl_launch(k_reduce_partials_jtab, rg, 256, 0, s, (const int32_t*)p.jtab, m->K, (const float*)part, te, dW);
@@ -1675,8 +1564,11 @@ mk_status launch_wgrad_bf16(mk_context* ctx, const mk_kmap* m, const void* g, in
     k_reduce_partials<<<rg, 256, 0, s>>>(m->wslot_begin, part, te, dW);
     g_launches++;
   }
+  ht.mark("reduce");
   cudaError_t e = cudaGetLastError();
-  if (part) dev_free(ctx->alloc, part, s);
+  if (scratch) scratch_release(ctx, s);
+  else if (part) dev_free(ctx->alloc, part, s);
+  ht.mark("free");
   if (e != cudaSuccess) MK_FAIL(MK_ERR_CUDA, std::string("bf16 wgrad launch: ") + cudaGetErrorString(e));
   return MK_OK;
 }

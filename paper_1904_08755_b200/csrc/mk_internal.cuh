@@ -305,6 +305,15 @@ struct mk_context {
   mk::Alloc alloc;
   cudaStream_t aux = nullptr;  // private non-blocking stream for small lazy read-backs
   cudaStream_t side = nullptr;  // private non-blocking stream: map-build work forked off the caller's stream
+  // Grow-only scratch buffer for the per-call weight-gradient partials (tens of MB, allocated
+  // and freed every call otherwise: the stream-ordered pool then maps new memory every few
+  // calls, a 0.3-2.5 ms host stall).  scratch_acquire() holds scratch_mu until
+  // scratch_release(); a call on another stream than the last user first waits for its event.
+  std::mutex scratch_mu;
+  void* scratch = nullptr;
+  size_t scratch_cap = 0;
+  cudaStream_t scratch_stream = nullptr;
+  cudaEvent_t scratch_ev = nullptr;
   // Device copies of kernel-region tables (offsets, then mirror indices), uploaded once per
   // region and kept for the context's lifetime (mk::region_device).
   std::mutex region_mu;
@@ -414,6 +423,8 @@ struct HostTimer {
   ~HostTimer();
 };
 void* dev_alloc(const Alloc& a, size_t bytes, cudaStream_t s);
+void* scratch_acquire(mk_context* ctx, size_t bytes, cudaStream_t s);  // nullptr on failure (lock released)
+void scratch_release(mk_context* ctx, cudaStream_t s);
 void dev_free(const Alloc& a, void* p, cudaStream_t s);
 inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 uint32_t next_pow2(uint64_t v);
