@@ -99,7 +99,11 @@ typedef void (*mk_free_fn)(void* ptr, void* stream, void* user);
 
 /* ---------------------------------------------------------------- context ---------- */
 /* Binds the library to a CUDA device.  Fails with MK_ERR_UNSUPPORTED on devices older
- * than sm_100 (the kernels are compiled for sm_100a only). */
+ * than sm_100 (the kernels are compiled for sm_100a only).  With the default allocator (NULL
+ * callbacks) it sets the device's default stream-ordered pool to keep freed memory and
+ * reserves 8 GB in it once (MK_POOL_RESERVE_MB overrides, 0 disables), so a call never
+ * maps new pool memory in steady state.  The context keeps one grow-only scratch buffer
+ * (weight-gradient partial sums); it is freed by mk_context_destroy. */
 mk_status mk_context_create(int device, mk_alloc_fn alloc, mk_free_fn free_fn, void* user,
                             mk_context** out);
 void mk_context_destroy(mk_context* ctx);
