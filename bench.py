@@ -522,7 +522,7 @@ def summarize(w, ph, pk, dtype):
     }
 
 
-NCU_SUMMARY = {4: "ncu_summary_r02s3.json", 1: "ncu_summary_r02s3_c1.json"}
+NCU_SUMMARY = {4: "ncu_summary_r02s3b.json", 1: "ncu_summary_r02s3b_c1.json"}
 GATHER_PEAK_TBS = 10.64
 MAP_KERNELS = ("quant_insert", "quant_rank", "kmap_probe", "kmap_emit", "kmap_sort")
 
