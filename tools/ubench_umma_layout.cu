@@ -1,7 +1,8 @@
 // ubench_umma_layout.cu — tcgen05.mma (kind::f16, M = 128, K = 16) throughput by operand
 // layout: K-major SW128 / SW64 (the forward kernel at C = 64 / C = 96) and MN-major SW64 /
 // SW128 panels (the weight gradient).  One CTA per SM, one thread issues UMMAs into 4
-// rotating accumulators (no dependency between consecutive UMMAs), a commit + wait every 8.
+// rotating accumulators (no dependency between consecutive UMMAs), issued by warp 0 under
+// elect.sync, a commit + wait every 8 or every 512 UMMAs.
 // Development tool.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../paper_1904_08755_b200/csrc ubench_umma_layout.cu
 #include <cuda_runtime.h>
@@ -20,7 +21,7 @@ struct Case {
   int N;
 };
 
-__global__ void __launch_bounds__(128, 1) k_umma(Case c, int iters, long long* out) {
+__global__ void __launch_bounds__(128, 1) k_umma(Case c, int iters, int per, long long* out) {
   extern __shared__ __align__(1024) uint8_t smraw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t bar;
@@ -37,7 +38,7 @@ __global__ void __launch_bounds__(128, 1) k_umma(Case c, int iters, long long* o
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = tslot;
-  if (threadIdx.x == 0) {
+  if (warp == 0) {  // the whole warp runs the loop; elect.sync picks the issuing lane
     const uint32_t a = smem_u32(sm), b = a + 32768;
     const uint32_t code = c.rb == 128 ? 2u : c.rb == 64 ? 4u : 6u;
     uint64_t ad, bd;
@@ -56,14 +57,20 @@ __global__ void __launch_bounds__(128, 1) k_umma(Case c, int iters, long long* o
     const long long t0 = clock64();
     uint32_t ph = 0;
     for (int it = 0; it < iters; ++it) {
+      if (elect_one()) {
 #pragma unroll
-      for (int q = 0; q < 8; ++q)
-        umma_f16(tbase + (uint32_t)((q & 3) * c.N), ad + (q & 3) * kstep, bd + (q & 3) * kstep, idesc, it > 0 || q >= 4);
-      umma_commit(&bar);
-      mbar_wait(&bar, ph);
-      ph ^= 1;
+        for (int q = 0; q < 8; ++q)
+          umma_f16(tbase + (uint32_t)((q & 3) * c.N), ad + (q & 3) * kstep, bd + (q & 3) * kstep, idesc, it > 0 || q >= 4);
+      }
+      __syncwarp();
+      if ((it + 1) % per == 0 || it + 1 == iters) {  // commit + wait every `per` batches of 8
+        if (elect_one()) umma_commit(&bar);
+        __syncwarp();
+        mbar_wait(&bar, ph);
+        ph ^= 1;
+      }
     }
-    out[blockIdx.x] = clock64() - t0;
+    if (threadIdx.x == 0) out[blockIdx.x] = clock64() - t0;
   }
   tc_fence_before();
   __syncthreads();
@@ -79,15 +86,18 @@ int main() {
                         {"MN-major SW64 ", 1, 64, 96}, {"MN-major SW128", 1, 128, 96}, {"MN-major SW128 N=128", 1, 128, 128},
                         {"K-major SW128 N=64", 0, 128, 64}, {"MN-major SW64 N=64", 1, 64, 64}};
   const int iters = 2000;
-  for (const Case& c : cases) {
-    k_umma<<<148, 128, 100 * 1024>>>(c, iters, d);
-    cudaError_t e = cudaDeviceSynchronize();
-    std::vector<long long> h(148);
-    cudaMemcpy(h.data(), d, 148 * 8, cudaMemcpyDeviceToHost);
-    double m = 0;
-    for (auto v : h) m += v;
-    m /= 148.0 * iters * 8;
-    printf("%-22s N=%3d: %6.1f cycles per UMMA (%s)\n", c.name, c.N, m, cudaGetErrorString(e));
+  for (int per : {1, 64}) {
+    printf("-- commit + wait every %d x 8 UMMAs\n", per);
+    for (const Case& c : cases) {
+      k_umma<<<148, 128, 100 * 1024>>>(c, iters, per, d);
+      cudaError_t e = cudaDeviceSynchronize();
+      std::vector<long long> h(148);
+      cudaMemcpy(h.data(), d, 148 * 8, cudaMemcpyDeviceToHost);
+      double m = 0;
+      for (auto v : h) m += v;
+      m /= 148.0 * iters * 8;
+      printf("%-22s N=%3d: %6.1f cycles per UMMA (%s)\n", c.name, c.N, m, cudaGetErrorString(e));
+    }
   }
   return 0;
 }
