@@ -150,6 +150,7 @@ struct FwdParams {
   int tb;  // tiles per CTA (one TMEM accumulator each: tb * cw <= 512 columns)
   int grp;  // MMA steps cover all nch chunks of a (unit, tile)
   int off32;  // n_src * c_x < 2^31: 32-bit element offsets in the gathers
+  int accum;  // fp32 output accumulated in place (y += conv) instead of overwritten
   int fold;  // tile order (see cta_tile)
   int ncb;   // commit barriers in the ring (power of two)
   uint32_t a_bytes, b_bytes, tmem_cols;
@@ -188,6 +189,15 @@ __device__ __forceinline__ void epi16(const FwdParams& p, int64_t row, int col0,
 __device__ __forceinline__ void store16(const FwdParams& p, int64_t row, int col0, const uint32_t (&v)[16]) {
   if (p.out_f32) {
     float4* yr = (float4*)((float*)p.y + row * p.c_y + col0);
+    if (p.accum) {  // y += conv (fp32 running sum: the bf16x3 split terms, conv_split.cu)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float4 o = yr[e];
+        yr[e] = make_float4(o.x + __uint_as_float(v[4 * e]), o.y + __uint_as_float(v[4 * e + 1]),
+                            o.z + __uint_as_float(v[4 * e + 2]), o.w + __uint_as_float(v[4 * e + 3]));
+      }
+      return;
+    }
 #pragma unroll
     for (int e = 0; e < 4; ++e)
       yr[e] = make_float4(__uint_as_float(v[4 * e]), __uint_as_float(v[4 * e + 1]), __uint_as_float(v[4 * e + 2]),
@@ -1259,7 +1269,11 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
   p.nch = nch;
   p.out_f32 = out_dt == MK_F32;
   p.off32 = n_src * (int64_t)c_x < INT32_MAX;
-  p.ep = ep;
+  // An epilogue that only adds the fp32 output itself (y = conv + y, the bf16x3 split's running
+  // sum) is an in-place accumulate: the plain instance (8 producer warps) instead of the fused
+  // one (84 registers, 4 producer warps); the same fp32 additions, so bit-identical.
+  p.accum = p.out_f32 && ep.residual == y && !ep.scale && !ep.shift && !ep.relu ? 1 : 0;
+  p.ep = p.accum ? Epilogue() : ep;
   static const int dbg = [] {
     const char* e = std::getenv("MK_DEBUG_CONV");
     return e ? std::atoi(e) : 0;
@@ -1316,12 +1330,12 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
     // Three CTAs per SM (configs[1] fwd 65.4 -> 62.9 us, dgrad 64.3 -> 62.2 us) when two stage
     // slots and the W ring fit a third of the SM and the registers allow it (the fused-epilogue
     // instance needs 84 registers: two CTAs).
-    ctas = env_ctas0 == 3 && !ep.active() && 3 * p.tmem_cols <= 512 &&
+    ctas = env_ctas0 == 3 && !p.ep.active() && 3 * p.tmem_cols <= 512 &&
                    base3 + nch * 2 * (int)p.b_bytes + 2 * (int)p.a_bytes <= kMaxSmem / 3 - 1024
                ? 3
                : 2;
     // two CTAs: the 8-warp plan when it gets at least 6 slots in half an SM, else the 4-warp one
-    for (int w = ctas == 2 && !ep.active() ? env_npw : kFwdProd;; w = kFwdProd) {
+    for (int w = ctas == 2 && !p.ep.active() ? env_npw : kFwdProd;; w = kFwdProd) {
       npw = w;
       samax = npw == kFwdProd ? kFwdProd : env_samax > 0 ? env_samax : npw;
       const int base = ctas == 3 ? base3 : base0(npw) + 8 * (samax + ring(nch * 4, p.tb, samax) + nch * 4 + 2);
@@ -1370,7 +1384,7 @@ mk_status launch_conv_bf16(mk_context* ctx, const NbrView& nb, const void* x, in
     set_smem_once(kern, smem);
     return pdl_launch(kern, grid, (nw + 6) * 32, smem, s, p);
   };
-  const bool epi = ep.active();
+  const bool epi = p.ep.active();
   if (epi)
     e = CH == 64 ? go(k_conv_umma<64, true, 4>, 4) : CH == 32 ? go(k_conv_umma<32, true, 4>, 4) : go(k_conv_umma<16, true, 4>, 4);
   else if (npw == 8)
