@@ -346,12 +346,21 @@ __global__ void __launch_bounds__(kCT, MK_SORT_MINB) k_radix_sort_coop(uint32_t*
       const int64_t b0 = tb + (int64_t)i * kCT;
       if (b0 < te) chunk(b0 + t, kr[i], vr[i]);  // block-uniform condition
     }
-    for (int64_t b0 = tb + (int64_t)kCR * kCT; b0 < te; b0 += kCT) {
-      const int64_t e = b0 + t;
+    {  // the rest of the tile, one chunk ahead: the next chunk's key and value are in flight
+       // while this chunk is ranked (just-in-time loads left every chunk waiting on memory)
+      int64_t b0 = tb + (int64_t)kCR * kCT;
       uint32_t key = 0;
       int32_t val = 0;
-      if (e < te) fetch(e, &key, &val);
-      chunk(e, key, val);
+      if (b0 + t < te) fetch(b0 + t, &key, &val);
+      for (; b0 < te; b0 += kCT) {
+        const int64_t e = b0 + t, en = e + kCT;
+        uint32_t kn = 0;
+        int32_t vn = 0;
+        if (en < te) fetch(en, &kn, &vn);
+        chunk(e, key, val);
+        key = kn;
+        val = vn;
+      }
     }
     SORT_MARK(5 + 4 * p)
     if (!last) grid_barrier(bar, ++nbar * G);
