@@ -207,3 +207,37 @@ def test_config3_unet_pair_full_size(mk, orc, room):
     WT = synthetic.weights(45, 8, 128, 256)
     GT = synthetic.features(46, c.n, 128)
     check_features(mk, orc, mu, oku, Y, WT, GT, "bf16", BF16_TOL, transposed=True, what="configs[3] up 256->128")
+
+
+def test_wgrad_two_streams_share_the_scratch(mk, orc):
+    # The bf16 weight gradient keeps its partial sums in one per-context scratch buffer; calls
+    # on two streams alternate on it (the second waits for the first one's event).  Launch
+    # interleaved weight gradients of two different maps / channel counts on two streams and
+    # compare both with the oracle.
+    cases = []
+    for j, (cin, cout, n, span) in enumerate([(96, 96, 6000, 16), (64, 128, 9000, 20)]):
+        c, oc = _sparse(mk, orc, 700 + j, n, span)
+        m, okm = map_pair(mk, orc, c, c, oc, oc, CUBE3, [1, 1, 1])
+        X = synthetic.features(31 + j, c.n, cin)
+        G = synthetic.features(41 + j, c.n, cout)
+        W = synthetic.weights(51 + j, 27, cout, cin)
+        want = orc.conv_wgrad(okm, G, X, 27)
+        cases.append((m, X, G, W, want))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    outs = [[], []]
+    dev_in = [(dev(X).bfloat16(), dev(G).bfloat16(), dev(W).bfloat16()) for (_, X, G, W, _) in cases]
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for j in (0, 1):
+            with torch.cuda.stream(streams[j]):
+                Xd, Gd, Wd = dev_in[j]
+                _, gw = mk.conv_backward(cases[j][0], Gd, Xd, Wd, need_gin=False, need_gw=True)
+                outs[j].append(gw)
+    torch.cuda.synchronize()
+    for j in (0, 1):
+        want = cases[j][4]
+        for gw in outs[j]:
+            got = gw.cpu().numpy()
+            err = np.abs(got - want).max() / np.abs(want).max()
+            assert err <= BF16_TOL, f"stream {j}: normwise error {err:.3e}"
+        assert all(torch.equal(outs[j][0], o) for o in outs[j][1:]), "not deterministic across streams"
