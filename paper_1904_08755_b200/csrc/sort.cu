@@ -425,8 +425,12 @@ mk_status radix_sort_perm(const Alloc& a, uint32_t* keys, int64_t n, int bits, i
       const char* v = std::getenv("MK_SORT_G");  // development: CTA count cap
       return v ? std::atoi(v) : 0;
     }();
+    // Large sorts run beside the pair-list emit on the other stream (the map builder forks
+    // them) and this kernel takes a whole SM's registers per CTA: two thirds of the SMs leave
+    // room for the emit (configs[4] map phase 993 -> 939 us; small maps keep every SM).
+    const int g_def = n >= (1 << 20) ? std::max(1, num_sms * 2 / 3) : num_sms;
     const int G = (int)std::max<int64_t>(
-        1, std::min<int64_t>(g_cap > 0 ? std::min(g_cap, num_sms) : num_sms, ceil_div(n, kCT)));
+        1, std::min<int64_t>(g_cap > 0 ? std::min(g_cap, num_sms) : g_def, ceil_div(n, kCT)));
     const size_t smem = sizeof(uint32_t) * (2 * kCW * dig + dig);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(G);
